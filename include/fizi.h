@@ -1,0 +1,199 @@
+/*
+ * include/fizi.h -- C ABI of libfizi.so, the B200 (sm_100a) implementation of
+ * the per-frame FIZI + Mouse pixel path of arXiv 1907.04393.
+ *
+ * Citations: P:<n> = PAPER.md line n (/root/reference, read-only), S:<n> =
+ * SPEC.md line n.  DESIGN.md lists every reading (L1..L31) of a passage that is
+ * silent, garbled or contradictory.
+ *
+ * Conventions shared by every entry point
+ *   - Return value: fizi_status (0 = FIZI_OK, < 0 = error).  No entry point
+ *     throws, aborts or prints; fizi_last_error(ctx) describes the last error.
+ *   - Device pointers ("_dev") are plain CUDA device addresses on the
+ *     context's device (e.g. torch.Tensor.data_ptr()); host pointers ("_host")
+ *     are ordinary (preferably pinned) host memory.  The caller owns every
+ *     frame, mask and result buffer; the library owns envelopes, tracker
+ *     states, the LUT table and all scratch, sized once at fizi_create.
+ *   - Inputs are const and never modified.
+ *   - Work is stream-ordered on the caller's CUDA stream (fizi_stream_t is a
+ *     cudaStream_t; NULL = legacy default stream).  Outputs are valid once that
+ *     stream is synchronised.  Calls on one context must be externally
+ *     serialised (one logical consumer).
+ *   - Frame layout (a0): row-major, top row first, interleaved
+ *     (r,g,b) u8, tightly packed: frame i of a batch starts at byte
+ *     i * width * height * 3.  Mask layout: u8 {0,1}, one byte per pixel,
+ *     row-major, frame i at byte i * width * height.
+ *   - A CUDA failure is sticky (FIZI_E_CUDA): the context must be destroyed.
+ */
+#ifndef FIZI_H
+#define FIZI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *fizi_stream_t;   /* == cudaStream_t */
+typedef struct fizi_ctx fizi_ctx;
+
+typedef enum {
+    FIZI_OK = 0,
+    FIZI_E_ARG = -1,      /* parameter out of range or NULL pointer   */
+    FIZI_E_EMPTY = -2,    /* learn with n_frames = 0: "empty sequence"          */
+    FIZI_E_DIMS = -3,     /* width/height differ from the context       */
+    FIZI_E_NOMODEL = -4,  /* process before fizi_learn_background for that stream       */
+    FIZI_E_TIME = -5,     /* decreasing timestamps within a stream (pre of S:292)       */
+    FIZI_E_CUDA = -6,     /* CUDA error (sticky)                                        */
+    FIZI_E_OOM = -7,      /* device allocation failed at fizi_create                    */
+    FIZI_E_CAPACITY = -8  /* batch larger than max_batch, or stream id >= n_streams     */
+} fizi_status;
+
+/* Immutable parameter snapshot.  Defaults (fizi_params_default):
+ * S:187 segmentation, S:285 tracker, S:169 margin is passed to learn. */
+typedef struct fizi_params {
+    uint32_t width, height;        /* fixed per context; 1..65535                          */
+    uint32_t gray_tol_S;           /* 30: keep iff max-min >= S (reading L5); <=255  */
+    uint32_t hue_lo_deg;           /* 340: alpha_1 in degrees [0,360) (reading L7)  */
+    uint32_t hue_hi_deg;           /* 25:  alpha_2; alpha_1 > alpha_2 = band through 0 deg */
+    uint32_t se_radius;            /* 1: square SE side 2r+1; 1..8            */
+    uint32_t min_blob_ppm;         /* 5000: drop components with area*1e6 < ppm*W*H (L13)  */
+    uint32_t luma_target;          /* 128                                          */
+    uint32_t luma_lo, luma_hi;     /* 60, 190: identity iff lo <= mean <= hi       */
+    double   gamma_min, gamma_max; /* 0.4, 2.5; 0 < min <= max                    */
+    double   beta;                 /* 0.5: EMA weight of the new centroid, [0,1]   */
+    double   dwell_radius_px;      /* 15, >= 0                                     */
+    int64_t  dwell_time_ms;        /* 800, >= 0                                    */
+    int64_t  lost_timeout_ms;      /* 500, >= 0                                    */
+    uint32_t debug;                /* 1 = keep per-stage state for fizi_debug_stage        */
+    uint32_t _reserved;
+} fizi_params;
+
+/* One record per processed frame (128 bytes), written to device memory. */
+typedef struct fizi_result {
+    int64_t  t_ms;                 /* the caller's timestamp                               */
+    uint32_t stream;               /* camera stream id                                     */
+    uint32_t frame_idx;            /* index of the frame within its call                   */
+    uint8_t  mean_luma;            /* a2: floor((sum Y + 500N)/(1000N)), Y = 299r+587g+114b */
+    uint8_t  corrected;            /* 1 iff a non-identity gamma LUT was applied           */
+    uint8_t  visible, clicked;     /* a8 (fizi_track / fizi_process_frames only)           */
+    uint32_t fg_merged;            /* popcount of A = R1 & R2 & R3 (a3)                    */
+    uint32_t fg_final;             /* popcount of the final mask (a6)                      */
+    uint32_t n_comp_total;         /* 8-connected components of the open-close mask (a5)   */
+    uint32_t n_comp_kept;          /* components passing the area filter (a6)              */
+    uint32_t blob_area;            /* a7: largest kept component (0 if none)               */
+    uint32_t blob_label;           /*     its label = 1 + min raster index y*W+x (L15)     */
+    uint32_t bbox[4];              /*     x_min, y_min, x_max, y_max                       */
+    uint32_t _pad;
+    uint64_t sum_x, sum_y;         /*     exact moments: sum of x (column), sum of y (row) */
+    double   gamma;                /* a2: 1.0 when not corrected                           */
+    double   cx, cy;               /* a7: centroid sum/area (L17); 0 if no blob            */
+    double   px, py;               /* a8: smoothed pointer                                 */
+    int64_t  dwell_ms;             /* a8: dwell time at the anchor                         */
+} fizi_result;
+
+/* Stages for fizi_debug_stage (SPEC S:265 stage dumps). */
+typedef enum {
+    FIZI_STAGE_R1 = 0,        /* I_R1 background branch, u8 {0,1}         */
+    FIZI_STAGE_R2 = 1,        /* I_R2 gray branch         */
+    FIZI_STAGE_R3 = 2,        /* I_R3 hue branch         */
+    FIZI_STAGE_MERGED = 3,    /* A = R1 & R2 & R3         */
+    FIZI_STAGE_OPENCLOSE = 4, /* O = E(D(D(E(A))))         */
+    FIZI_STAGE_LABELS = 5,    /* u32 canonical labels of O, 0 = background (L15)        */
+    FIZI_STAGE_FINAL = 6,     /* I_FIZI: O restricted to kept components        */
+    FIZI_STAGE_CONTOUR = 7    /* inner boundary FINAL & !erode_1(FINAL) (L30)           */
+} fizi_stage;
+
+/* Fill *p with the defaults above for a width x height context. */
+int fizi_params_default(fizi_params *p, uint32_t width, uint32_t height);
+
+/* Create a context on CUDA device `cuda_device` for n_streams camera streams
+ * (each with its own envelope and tracker state) and batches of at most
+ * max_batch frames (<= 65535).  Validates params (FIZI_E_ARG), allocates all
+ * device memory (FIZI_E_OOM) and builds the 256x256 gamma-LUT table on the
+ * device.  *out is NULL on error. */
+int fizi_create(const fizi_params *params, int cuda_device, uint32_t n_streams,
+                uint32_t max_batch, fizi_ctx **out);
+
+/* a1: learn stream `stream`'s envelope from n_frames
+ * frames (device, frame layout above) -- per pixel and channel
+ * lo = sat(min_k F_k - margin), hi = sat(max_k F_k + margin).  Replaces any
+ * previous model and resets the stream's tracker.  n_frames = 0 ->
+ * FIZI_E_EMPTY; width/height != context -> FIZI_E_DIMS. */
+int fizi_learn_background(fizi_ctx *ctx, uint32_t stream, const uint8_t *frames_dev,
+                          uint32_t n_frames, uint32_t width, uint32_t height,
+                          uint8_t margin, fizi_stream_t cuda_stream);
+
+/* The whole per-frame path (§3.1, §3.2) for a batch of n frames:
+ * frame i belongs to stream stream_of_frame_host[i] and carries timestamp
+ * t_ms_host[i] (both host arrays of n entries).  Frames of one stream are
+ * processed in index order; timestamps must be non-decreasing per stream,
+ * also across calls (FIZI_E_TIME).  Writes masks_dev (n*W*H u8 {0,1}, may be
+ * NULL) and results_dev (n records).  = fizi_segment_frames + fizi_track. */
+int fizi_process_frames(fizi_ctx *ctx, const uint32_t *stream_of_frame_host,
+                        const uint8_t *frames_dev, uint32_t n, uint32_t width,
+                        uint32_t height, const int64_t *t_ms_host, uint8_t *masks_dev,
+                        fizi_result *results_dev, fizi_stream_t cuda_stream);
+
+/* Stateless part a2..a7: like fizi_process_frames but leaves every stream's
+ * tracker untouched and writes visible = clicked = 0, px = py = 0,
+ * dwell_ms = 0 (for sharded multi-GPU runs, §8(e)); no timestamp check. */
+int fizi_segment_frames(fizi_ctx *ctx, const uint32_t *stream_of_frame_host,
+                        const uint8_t *frames_dev, uint32_t n, uint32_t width,
+                        uint32_t height, const int64_t *t_ms_host, uint8_t *masks_dev,
+                        fizi_result *results_dev, fizi_stream_t cuda_stream);
+
+/* a8: fold n records of stream `stream`, in
+ * order, through the stream's tracker state; reads t_ms, blob_area, cx, cy and
+ * writes visible, clicked, px, py, dwell_ms in place.  Used after gathering
+ * the records of a sharded stream. */
+int fizi_track(fizi_ctx *ctx, uint32_t stream, fizi_result *results_dev, uint32_t n,
+               fizi_stream_t cuda_stream);
+
+/* End-to-end variant of fizi_process_frames on HOST buffers: copies frames
+ * (n*W*H*3 bytes) host->device, runs the path, copies masks (may be NULL) and
+ * results back device->host, all on cuda_stream; returns after the stream has
+ * completed (results are valid on return). */
+int fizi_process_frames_host(fizi_ctx *ctx, const uint32_t *stream_of_frame_host,
+                             const uint8_t *frames_host, uint32_t n, uint32_t width,
+                             uint32_t height, const int64_t *t_ms_host, uint8_t *masks_host,
+                             fizi_result *results_host, fizi_stream_t cuda_stream);
+
+/* Reset stream `stream`'s tracker to its initial state (invisible). */
+int fizi_reset_tracker(fizi_ctx *ctx, uint32_t stream);
+
+/* Parity/debug: write stage `stage` of frame `frame_in_last_batch` of the last
+ * fizi_process_frames / fizi_segment_frames call to out_dev (u8 per pixel;
+ * u32 per pixel for FIZI_STAGE_LABELS).  Needs params.debug = 1 and, for
+ * R1/R2/R3, the last call's frames still resident. */
+int fizi_debug_stage(fizi_ctx *ctx, int stage, uint32_t frame_in_last_batch, void *out_dev,
+                     fizi_stream_t cuda_stream);
+
+/* Copy stream `stream`'s envelope out as two interleaved-RGB planes
+ * (W*H*3 u8 each, the S:174 plane layout) to device memory. */
+int fizi_get_background(fizi_ctx *ctx, uint32_t stream, uint8_t *lo_dev, uint8_t *hi_dev,
+                        fizi_stream_t cuda_stream);
+
+/* Install an envelope (same layout as fizi_get_background; lo <= hi is not
+ * required) for stream `stream`, e.g. one broadcast from another rank. */
+int fizi_set_background(fizi_ctx *ctx, uint32_t stream, const uint8_t *lo_dev,
+                        const uint8_t *hi_dev, fizi_stream_t cuda_stream);
+
+/* Number of kernels this context has launched so far (evidence for the
+ * bench's gpu_launches count). */
+uint64_t fizi_kernel_launches(const fizi_ctx *ctx);
+
+/* Human-readable description of the last error on ctx (never NULL). */
+const char *fizi_last_error(const fizi_ctx *ctx);
+
+/* Static name of a status code. */
+const char *fizi_status_string(int status);
+
+/* Free every device and host resource of ctx (NULL is a no-op). */
+void fizi_destroy(fizi_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FIZI_H */

@@ -1,0 +1,10 @@
+"""B200-native (sm_100a) FIZI + Mouse per-frame pixel path of arXiv 1907.04393.
+
+The compute path is libfizi.so (hand-written CUDA behind the C ABI in
+include/fizi.h); this package is its ctypes binding.  See DESIGN.md.
+"""
+from .fizi import (RESULT_BYTES, RESULT_DTYPE, STAGES, Fizi, FiziError, Params, default_params,
+                   lib, results_numpy)
+
+__all__ = ["Fizi", "FiziError", "Params", "RESULT_BYTES", "RESULT_DTYPE", "STAGES",
+           "default_params", "lib", "results_numpy"]

@@ -1,0 +1,504 @@
+// fizi_api.cu -- the C ABI of libfizi.so (include/fizi.h): argument
+// validation, context / memory management and the per-call launch sequence
+//   segment (a2+a3) -> morphology (a4) -> labelling + filter + blob (a5-a7)
+//   -> final u8 mask (a6 output) -> Mouse fold (a8)
+// on the caller's CUDA stream.  No pixel is touched on the host.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "fizi_internal.cuh"
+
+namespace fizi {
+uint32_t morph_tile_rows(const Ctx& c, size_t smem_budget);
+cudaError_t init_morph(Ctx& c);
+cudaError_t init_segment(Ctx& c);
+}  // namespace fizi
+
+struct fizi_ctx {
+  fizi::Ctx c;
+};
+
+using fizi::Ctx;
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int fail(Ctx& c, int code, const std::string& msg) {
+  c.err = msg;
+  return code;
+}
+
+int cuda_fail(Ctx& c, cudaError_t e, const char* where) {
+  c.sticky = true;
+  c.err = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return FIZI_E_CUDA;
+}
+
+int validate_params(const fizi_params* p, std::string& why) {
+  auto bad = [&](const char* m) { why = m; return FIZI_E_ARG; };
+  if (!p) return bad("params is NULL");
+  if (p->width < 1 || p->width > 65535 || p->height < 1 || p->height > 65535)
+    return bad("width/height must be in [1, 65535]");
+  if (p->gray_tol_S > 255) return bad("gray_tol_S must be <= 255");
+  if (p->hue_lo_deg >= 360 || p->hue_hi_deg >= 360) return bad("hue bounds must be in [0, 360)");
+  if (p->se_radius < 1 || p->se_radius > (uint32_t)fizi::kMaxRadius)
+    return bad("se_radius must be in [1, 8]");
+  if (p->min_blob_ppm > 1000000) return bad("min_blob_ppm must be <= 1e6");
+  if (p->luma_target > 255 || p->luma_hi > 255 || !(p->luma_lo < p->luma_target) ||
+      !(p->luma_target < p->luma_hi))
+    return bad("need luma_lo < luma_target < luma_hi <= 255 (S:189)");
+  if (!(std::isfinite(p->gamma_min) && std::isfinite(p->gamma_max)) || !(p->gamma_min > 0.0) ||
+      !(p->gamma_min <= p->gamma_max))
+    return bad("need 0 < gamma_min <= gamma_max");
+  if (!(p->beta >= 0.0 && p->beta <= 1.0)) return bad("beta must be in [0, 1]");
+  if (!(p->dwell_radius_px >= 0.0) || !std::isfinite(p->dwell_radius_px))
+    return bad("dwell_radius_px must be >= 0");
+  if (p->dwell_time_ms < 0 || p->lost_timeout_ms < 0) return bad("times must be >= 0");
+  return FIZI_OK;
+}
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t bytes) {
+  return cudaMalloc(reinterpret_cast<void**>(p), bytes ? bytes : 16);
+}
+
+void free_all(Ctx& c) {
+  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.luma, c.fg, c.bitA, c.bitO, c.bitOC,
+                  c.row_cnt, c.row_off, c.runs, c.parent, c.stats, c.frame_t, c.fix_count,
+                  c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c.pinned) cudaFreeHost(c.pinned);
+  if (c.pinned_ev) cudaEventDestroy(c.pinned_ev);
+}
+
+// Upload the per-call frame table (timestamps, streams, same-stream groups).
+int upload_call(Ctx& c, const uint32_t* sof, const int64_t* t, uint32_t n, uint32_t* n_groups,
+                cudaStream_t st) {
+  const uint32_t mb = c.max_batch;
+  cudaError_t e = cudaEventSynchronize(c.pinned_ev);      // previous upload consumed
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventSynchronize");
+  int64_t* ht = reinterpret_cast<int64_t*>(c.pinned);
+  uint32_t* hs = reinterpret_cast<uint32_t*>(ht + mb);
+  uint32_t* hg = hs + mb;
+  uint32_t* ho = hg + mb;
+  for (uint32_t i = 0; i < n; i++) {
+    ht[i] = t ? t[i] : 0;
+    hs[i] = sof[i];
+  }
+  // groups: streams in order of first appearance, frames in index order,
+  // split every kFrameGroup frames
+  std::vector<uint8_t> seen(c.n_streams, 0);
+  uint32_t pos = 0, g = 0;
+  for (uint32_t i = 0; i < n; i++) {
+    const uint32_t s = sof[i];
+    if (seen[s]) continue;
+    seen[s] = 1;
+    uint32_t in_group = 0;
+    for (uint32_t j = i; j < n; j++) {
+      if (sof[j] != s) continue;
+      if (in_group == 0) ho[g++] = pos;
+      hg[pos++] = j;
+      if (++in_group == (uint32_t)fizi::kFrameGroup) in_group = 0;
+    }
+  }
+  ho[g] = pos;
+  *n_groups = g;
+  const size_t bytes = (size_t)mb * 8 + (size_t)mb * 4 * 2 + (size_t)(mb + 1) * 4;
+  e = cudaMemcpyAsync(c.frame_t, c.pinned, bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemcpyAsync(call table)");
+  e = cudaEventRecord(c.pinned_ev, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
+  return FIZI_OK;
+}
+
+int check_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, uint32_t w,
+               uint32_t h, fizi_result* results) {
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
+  if (w != c.W || h != c.H) return fail(c, FIZI_E_DIMS, "frame dimensions differ from the context");
+  if (n > c.max_batch) return fail(c, FIZI_E_CAPACITY, "n exceeds max_batch");
+  if (n == 0) return FIZI_OK;
+  if (!sof || !frames || !results) return fail(c, FIZI_E_ARG, "NULL pointer argument");
+  if (c.fast && (reinterpret_cast<uintptr_t>(frames) & 15u))
+    return fail(c, FIZI_E_ARG, "frames_dev must be 16-byte aligned");
+  for (uint32_t i = 0; i < n; i++) {
+    if (sof[i] >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+    if (!c.env_valid[sof[i]])
+      return fail(c, FIZI_E_NOMODEL, "stream " + std::to_string(sof[i]) + " has no background model");
+  }
+  return FIZI_OK;
+}
+
+int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, const int64_t* t,
+             uint8_t* masks, fizi_result* res, bool track, cudaStream_t st) {
+  uint32_t n_groups = 0;
+  int rc = upload_call(c, sof, t, n, &n_groups, st);
+  if (rc) return rc;
+  cudaError_t e = fizi::launch_segment(c, frames, n, n_groups, res, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "segment");
+  e = fizi::launch_morph(c, n, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "morph");
+  if (c.p.debug) {
+    e = cudaMemcpyAsync(c.bitOC, c.bitO, (size_t)n * c.H * c.P * 4, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "debug copy");
+  }
+  e = fizi::launch_ccl(c, n, res, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "ccl");
+  if (masks) {
+    e = fizi::launch_expand(c, n, masks, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "expand");
+  }
+  if (track) {
+    e = fizi::launch_track_batch(c, n, res, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "track");
+  }
+  c.last_frames = frames;
+  c.last_n = n;
+  return FIZI_OK;
+}
+
+int check_times(Ctx& c, const uint32_t* sof, const int64_t* t, uint32_t n) {
+  if (!t) return fail(c, FIZI_E_ARG, "t_ms_host is NULL");
+  std::vector<int64_t> last(c.last_t);
+  std::vector<uint8_t> has(c.has_t);
+  for (uint32_t i = 0; i < n; i++) {
+    const uint32_t s = sof[i];
+    if (has[s] && t[i] < last[s])
+      return fail(c, FIZI_E_TIME, "decreasing timestamp in stream " + std::to_string(s));
+    last[s] = t[i];
+    has[s] = 1;
+  }
+  return FIZI_OK;
+}
+
+void commit_times(Ctx& c, const uint32_t* sof, const int64_t* t, uint32_t n) {
+  for (uint32_t i = 0; i < n; i++) {
+    c.last_t[sof[i]] = t[i];
+    c.has_t[sof[i]] = 1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int fizi_params_default(fizi_params* p, uint32_t width, uint32_t height) {
+  if (!p) return FIZI_E_ARG;
+  std::memset(p, 0, sizeof(*p));
+  p->width = width;
+  p->height = height;
+  p->gray_tol_S = 30;
+  p->hue_lo_deg = 340;
+  p->hue_hi_deg = 25;
+  p->se_radius = 1;
+  p->min_blob_ppm = 5000;
+  p->luma_target = 128;
+  p->luma_lo = 60;
+  p->luma_hi = 190;
+  p->gamma_min = 0.4;
+  p->gamma_max = 2.5;
+  p->beta = 0.5;
+  p->dwell_radius_px = 15.0;
+  p->dwell_time_ms = 800;
+  p->lost_timeout_ms = 500;
+  p->debug = 0;
+  return FIZI_OK;
+}
+
+int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
+                uint32_t max_batch, fizi_ctx** out) {
+  if (!out) return FIZI_E_ARG;
+  *out = nullptr;
+  std::string why;
+  int rc = validate_params(params, why);
+  if (rc) return rc;
+  if (n_streams < 1 || max_batch < 1 || max_batch > 65535) return FIZI_E_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) {
+    cudaGetLastError();
+    return FIZI_E_CUDA;
+  }
+  DeviceGuard guard(cuda_device);
+  fizi_ctx* x = new (std::nothrow) fizi_ctx();
+  if (!x) return FIZI_E_OOM;
+  Ctx& c = x->c;
+  c.p = *params;
+  c.device = cuda_device;
+  c.n_streams = n_streams;
+  c.max_batch = max_batch;
+  c.W = params->width;
+  c.H = params->height;
+  c.P = (c.W + 31) / 32;
+  c.N = (uint64_t)c.W * c.H;
+  c.fast = (c.W % 32) == 0;
+  c.nchunks = (uint32_t)((c.N + fizi::kChunkPx - 1) / fizi::kChunkPx);
+  c.env_plane = c.fast ? (uint64_t)c.nchunks * fizi::kChunkBytes : c.N * 3;
+  c.cap_runs = (uint64_t)c.H * ((c.W + 1) / 2);
+  cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  c.morph_tr = fizi::morph_tile_rows(c, fizi::kMorphSmem);
+  if (c.morph_tr == 0) {
+    delete x;
+    return FIZI_E_ARG;
+  }
+  const uint64_t mb = max_batch;
+  const uint64_t wpf = (uint64_t)c.H * c.P;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  A(dalloc(&c.env, (uint64_t)n_streams * 2 * c.env_plane));
+  A(dalloc(&c.lut, 256 * 256));
+  A(dalloc(&c.gamma_tab, 256 * sizeof(double)));
+  A(dalloc(&c.corr_tab, 256));
+  A(dalloc(&c.luma, mb * 8));
+  A(dalloc(&c.fg, mb * 4));
+  A(dalloc(&c.bitA, mb * wpf * 4));
+  A(dalloc(&c.bitO, mb * wpf * 4));
+  if (c.p.debug) A(dalloc(&c.bitOC, mb * wpf * 4));
+  A(dalloc(&c.row_cnt, mb * c.H * 4));
+  A(dalloc(&c.row_off, mb * (c.H + 1) * 4));
+  A(dalloc(&c.runs, mb * c.cap_runs * sizeof(fizi::Run)));
+  A(dalloc(&c.parent, mb * c.cap_runs * 4));
+  A(dalloc(&c.stats, mb * c.cap_runs * sizeof(fizi::RootStats)));
+  const size_t table_bytes = mb * 8 + mb * 4 * 2 + (mb + 1) * 4;
+  A(dalloc(&c.frame_t, table_bytes));
+  A(dalloc(&c.fix_count, (mb + 1) * 4));
+  A(dalloc(&c.tstate, (uint64_t)n_streams * sizeof(fizi::TrackState)));
+  if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned), table_bytes);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.pinned_ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    free_all(c);
+    delete x;
+    return FIZI_E_OOM;
+  }
+  c.frame_stream = reinterpret_cast<uint32_t*>(c.frame_t + mb);
+  c.group_frames = c.frame_stream + mb;
+  c.group_off = c.group_frames + mb;
+  c.pinned_bytes = table_bytes;
+  c.env_valid.assign(n_streams, 0);
+  c.last_t.assign(n_streams, 0);
+  c.has_t.assign(n_streams, 0);
+  e = fizi::init_segment(c);
+  if (e == cudaSuccess) e = fizi::init_morph(c);
+  if (e == cudaSuccess) e = cudaMemset(c.env, 0, (uint64_t)n_streams * 2 * c.env_plane);
+  if (e == cudaSuccess) e = fizi::launch_lut_table(c, 0);
+  if (e == cudaSuccess) e = fizi::launch_tstate_reset(c, 0, n_streams, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    free_all(c);
+    delete x;
+    return FIZI_E_CUDA;
+  }
+  *out = x;
+  return FIZI_OK;
+}
+
+int fizi_learn_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* frames_dev,
+                          uint32_t n_frames, uint32_t width, uint32_t height, uint8_t margin,
+                          fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (n_frames == 0) return fail(c, FIZI_E_EMPTY, "learning needs at least one frame (S:139)");
+  if (width != c.W || height != c.H) return fail(c, FIZI_E_DIMS, "frame dimensions differ from the context");
+  if (!frames_dev) return fail(c, FIZI_E_ARG, "frames_dev is NULL");
+  if (c.fast && (reinterpret_cast<uintptr_t>(frames_dev) & 15u))
+    return fail(c, FIZI_E_ARG, "frames_dev must be 16-byte aligned");
+  DeviceGuard guard(c.device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  cudaError_t e = fizi::launch_learn(c, stream, frames_dev, n_frames, margin, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "learn");
+  e = fizi::launch_tstate_reset(c, stream, 1, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "tracker reset");
+  c.env_valid[stream] = 1;
+  c.has_t[stream] = 0;
+  return FIZI_OK;
+}
+
+int fizi_segment_frames(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* frames_dev, uint32_t n,
+                        uint32_t width, uint32_t height, const int64_t* t_ms, uint8_t* masks_dev,
+                        fizi_result* results_dev, fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  int rc = check_call(c, sof, frames_dev, n, width, height, results_dev);
+  if (rc || n == 0) return rc;
+  DeviceGuard guard(c.device);
+  return run_call(c, sof, frames_dev, n, t_ms, masks_dev, results_dev, false,
+                  reinterpret_cast<cudaStream_t>(cuda_stream));
+}
+
+int fizi_process_frames(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* frames_dev, uint32_t n,
+                        uint32_t width, uint32_t height, const int64_t* t_ms, uint8_t* masks_dev,
+                        fizi_result* results_dev, fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  int rc = check_call(c, sof, frames_dev, n, width, height, results_dev);
+  if (rc || n == 0) return rc;
+  rc = check_times(c, sof, t_ms, n);
+  if (rc) return rc;
+  DeviceGuard guard(c.device);
+  rc = run_call(c, sof, frames_dev, n, t_ms, masks_dev, results_dev, true,
+                reinterpret_cast<cudaStream_t>(cuda_stream));
+  if (rc == FIZI_OK) commit_times(c, sof, t_ms, n);
+  return rc;
+}
+
+int fizi_track(fizi_ctx* ctx, uint32_t stream, fizi_result* results_dev, uint32_t n,
+               fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (n == 0) return FIZI_OK;
+  if (!results_dev) return fail(c, FIZI_E_ARG, "results_dev is NULL");
+  DeviceGuard guard(c.device);
+  cudaError_t e = fizi::launch_track_stream(c, stream, results_dev, n,
+                                            reinterpret_cast<cudaStream_t>(cuda_stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "track");
+  return FIZI_OK;
+}
+
+int fizi_process_frames_host(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* frames_host,
+                             uint32_t n, uint32_t width, uint32_t height, const int64_t* t_ms,
+                             uint8_t* masks_host, fizi_result* results_host,
+                             fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
+  if (n == 0) return FIZI_OK;
+  if (!frames_host || !results_host) return fail(c, FIZI_E_ARG, "NULL pointer argument");
+  if (n > c.max_batch) return fail(c, FIZI_E_CAPACITY, "n exceeds max_batch");
+  DeviceGuard guard(c.device);
+  cudaError_t e = cudaSuccess;
+  if (!c.stage_frames) {
+    e = dalloc(&c.stage_frames, (uint64_t)c.max_batch * c.N * 3);
+    if (e == cudaSuccess) e = dalloc(&c.stage_masks, (uint64_t)c.max_batch * c.N);
+    if (e == cudaSuccess) e = dalloc(&c.stage_results, (uint64_t)c.max_batch * sizeof(fizi_result));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, FIZI_E_OOM, "staging allocation failed");
+    }
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  e = cudaMemcpyAsync(c.stage_frames, frames_host, (size_t)n * c.N * 3, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "H2D frames");
+  int rc = fizi_process_frames(ctx, sof, c.stage_frames, n, width, height, t_ms,
+                               masks_host ? c.stage_masks : nullptr, c.stage_results, cuda_stream);
+  if (rc) return rc;
+  if (masks_host) {
+    e = cudaMemcpyAsync(masks_host, c.stage_masks, (size_t)n * c.N, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "D2H masks");
+  }
+  e = cudaMemcpyAsync(results_host, c.stage_results, (size_t)n * sizeof(fizi_result),
+                      cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "D2H results");
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamSynchronize");
+  return FIZI_OK;
+}
+
+int fizi_reset_tracker(fizi_ctx* ctx, uint32_t stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  DeviceGuard guard(c.device);
+  cudaError_t e = fizi::launch_tstate_reset(c, stream, 1, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(c, e, "tracker reset");
+  c.has_t[stream] = 0;
+  return FIZI_OK;
+}
+
+int fizi_debug_stage(fizi_ctx* ctx, int stage, uint32_t frame, void* out_dev,
+                     fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (!c.p.debug) return fail(c, FIZI_E_ARG, "context was created with debug = 0");
+  if (!out_dev) return fail(c, FIZI_E_ARG, "out_dev is NULL");
+  if (frame >= c.last_n) return fail(c, FIZI_E_ARG, "frame index beyond the last call");
+  if (stage < FIZI_STAGE_R1 || stage > FIZI_STAGE_CONTOUR) return fail(c, FIZI_E_ARG, "bad stage");
+  DeviceGuard guard(c.device);
+  cudaError_t e = fizi::launch_debug_stage(c, stage, frame, out_dev,
+                                           reinterpret_cast<cudaStream_t>(cuda_stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "debug stage");
+  return FIZI_OK;
+}
+
+int fizi_get_background(fizi_ctx* ctx, uint32_t stream, uint8_t* lo_dev, uint8_t* hi_dev,
+                        fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (!c.env_valid[stream]) return fail(c, FIZI_E_NOMODEL, "stream has no background model");
+  if (!lo_dev || !hi_dev) return fail(c, FIZI_E_ARG, "NULL pointer argument");
+  DeviceGuard guard(c.device);
+  cudaError_t e = fizi::launch_env_export(c, stream, lo_dev, hi_dev, false, nullptr, nullptr,
+                                          reinterpret_cast<cudaStream_t>(cuda_stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "get_background");
+  return FIZI_OK;
+}
+
+int fizi_set_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* lo_dev,
+                        const uint8_t* hi_dev, fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (!lo_dev || !hi_dev) return fail(c, FIZI_E_ARG, "NULL pointer argument");
+  DeviceGuard guard(c.device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  cudaError_t e = fizi::launch_env_export(c, stream, nullptr, nullptr, true, lo_dev, hi_dev, st);
+  if (e == cudaSuccess) e = fizi::launch_tstate_reset(c, stream, 1, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "set_background");
+  c.env_valid[stream] = 1;
+  c.has_t[stream] = 0;
+  return FIZI_OK;
+}
+
+uint64_t fizi_kernel_launches(const fizi_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+const char* fizi_last_error(const fizi_ctx* ctx) {
+  if (!ctx) return "NULL context";
+  return ctx->c.err.c_str();
+}
+
+const char* fizi_status_string(int s) {
+  switch (s) {
+    case FIZI_OK: return "FIZI_OK";
+    case FIZI_E_ARG: return "FIZI_E_ARG";
+    case FIZI_E_EMPTY: return "FIZI_E_EMPTY";
+    case FIZI_E_DIMS: return "FIZI_E_DIMS";
+    case FIZI_E_NOMODEL: return "FIZI_E_NOMODEL";
+    case FIZI_E_TIME: return "FIZI_E_TIME";
+    case FIZI_E_CUDA: return "FIZI_E_CUDA";
+    case FIZI_E_OOM: return "FIZI_E_OOM";
+    case FIZI_E_CAPACITY: return "FIZI_E_CAPACITY";
+    default: return "FIZI_E_UNKNOWN";
+  }
+}
+
+void fizi_destroy(fizi_ctx* ctx) {
+  if (!ctx) return;
+  DeviceGuard guard(ctx->c.device);
+  cudaDeviceSynchronize();
+  free_all(ctx->c);
+  delete ctx;
+}
+
+}  // extern "C"

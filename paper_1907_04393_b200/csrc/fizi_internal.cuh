@@ -1,0 +1,133 @@
+// fizi_internal.cuh -- context layout and kernel launchers of libfizi.so.
+//
+// Device data layout:
+//   envelope   per stream: two planes (lo, hi), each nchunks*1536 bytes, in the
+//              chunk-permuted order the fused segmentation kernel reads with
+//              coalesced 16-byte loads (see k_segment.cu: env_perm_index).
+//   bit masks  per frame: H rows x P = ceil(W/32) u32 words, bit i of word k
+//              = pixel x = 32k + i (LSB first); padding bits are always 0.
+//   runs       per frame: a region of cap_runs records (x0, x1, y) in raster
+//              order + union-find parent + per-root statistics.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "fizi.h"
+
+namespace fizi {
+
+constexpr int kChunkPx = 512;            // pixels per warp-chunk in the fused kernel
+constexpr int kChunkBytes = 3 * kChunkPx;
+constexpr int kWarpsPerCta = 8;          // chunks per CTA tile
+constexpr int kTileBytes = kChunkBytes * kWarpsPerCta;   // 12 KiB frame bytes per tile
+constexpr int kFrameGroup = 16;          // frames sharing one envelope load
+constexpr int kStages = 4;               // bulk-copy pipeline depth (frames)
+constexpr int kMaxRadius = 8;
+constexpr size_t kMorphSmem = 200 * 1024;  // dynamic smem budget of the morphology CTA
+
+struct Run {                             // one horizontal run of foreground pixels
+  uint16_t x0, x1, y, pad;
+};
+
+struct RootStats {                       // per component (indexed by its root run)
+  uint32_t area;
+  uint32_t xmin, xmax, ymin, ymax;
+  uint32_t pad;
+  unsigned long long sx, sy;
+};
+
+struct Ctx {
+  fizi_params p{};
+  int device = 0;
+  uint32_t n_streams = 0, max_batch = 0;
+  uint32_t W = 0, H = 0, P = 0;          // P = words per bit-mask row
+  uint64_t N = 0;                        // pixels per frame
+  uint32_t nchunks = 0;                  // ceil(N / 512)
+  uint64_t env_plane = 0;                // bytes per envelope plane (nchunks*1536)
+  uint64_t cap_runs = 0;                 // run capacity per frame
+  bool fast = false;                     // W % 32 == 0: fused bulk-copy kernels
+  int sms = 148;
+  uint32_t morph_tr = 0;                 // output rows per morphology CTA
+  uint64_t launches = 0;
+  std::string err;
+  bool sticky = false;
+
+  // device
+  uint8_t* env = nullptr;                // n_streams * 2 * env_plane
+  uint8_t* lut = nullptr;                // 256 means x 256 entries
+  double* gamma_tab = nullptr;           // 256
+  uint8_t* corr_tab = nullptr;           // 256
+  unsigned long long* luma = nullptr;    // max_batch
+  uint32_t* fg = nullptr;                // max_batch (fg_merged)
+  uint32_t* bitA = nullptr;              // max_batch * H * P
+  uint32_t* bitO = nullptr;              // max_batch * H * P
+  uint32_t* bitOC = nullptr;             // debug copy of O
+  uint32_t* row_cnt = nullptr;           // max_batch * H   (runs per row)
+  uint32_t* row_off = nullptr;           // max_batch * (H+1)
+  Run* runs = nullptr;                   // max_batch * cap_runs
+  uint32_t* parent = nullptr;            // max_batch * cap_runs
+  RootStats* stats = nullptr;            // max_batch * cap_runs
+  uint32_t* frame_stream = nullptr;      // max_batch
+  int64_t* frame_t = nullptr;            // max_batch (start of the per-call table)
+  uint32_t* group_frames = nullptr;      // max_batch (frame ids ordered by group)
+  uint32_t* group_off = nullptr;         // max_batch + 1
+  uint32_t* fix_count = nullptr;         // 1 + max_batch (count, list of corrected frames)
+  uint8_t* tstate = nullptr;             // n_streams tracker states
+  uint8_t* stage_frames = nullptr;       // device staging for fizi_process_frames_host
+  uint8_t* stage_masks = nullptr;
+  fizi_result* stage_results = nullptr;
+
+  // host
+  std::vector<uint8_t> env_valid;
+  std::vector<int64_t> last_t;
+  std::vector<uint8_t> has_t;
+  uint8_t* pinned = nullptr;             // staging for the per-call upload
+  size_t pinned_bytes = 0;
+  cudaEvent_t pinned_ev = nullptr;
+  // last call (debug)
+  const uint8_t* last_frames = nullptr;
+  uint32_t last_n = 0;
+};
+
+struct TrackState {                      // Mouse fold state (c1 step 11)
+  int32_t vis, fired;
+  double px, py, ax, ay;
+  int64_t last_t, anchor_t, dwell;
+};
+
+// ------------------------------------------------------------ envelope layout
+// Fast path: linear frame byte b -> chunk c = b/1536, lane l = (b%1536)/48,
+// piece k = (b%48)/16, byte j = b%16 -> c*1536 + 512k + 16l + j, so that warp
+// lane l reads its 48 frame bytes' envelope with three coalesced 16-byte
+// loads at 512k + 16l.  Generic path: identity.
+__host__ __device__ __forceinline__ uint64_t env_perm_index(uint64_t b, bool fast) {
+  if (!fast) return b;
+  uint64_t c = b / kChunkBytes, o = b % kChunkBytes;
+  uint32_t l = (uint32_t)(o / 48), q = (uint32_t)(o % 48);
+  return c * kChunkBytes + 512u * (q / 16) + 16u * l + (q % 16);
+}
+
+// ----------------------------------------------------------------- launchers
+// All return cudaGetLastError() of their launches; each increments
+// ctx.launches by the number of kernels launched.
+cudaError_t launch_lut_table(Ctx& c, cudaStream_t st);
+cudaError_t launch_learn(Ctx& c, uint32_t stream, const uint8_t* frames, uint32_t n,
+                         uint32_t margin, cudaStream_t st);
+cudaError_t launch_env_export(Ctx& c, uint32_t stream, uint8_t* lo, uint8_t* hi, bool import,
+                              const uint8_t* ilo, const uint8_t* ihi, cudaStream_t st);
+cudaError_t launch_segment(Ctx& c, const uint8_t* frames, uint32_t n, uint32_t n_groups,
+                           fizi_result* res, cudaStream_t st);
+cudaError_t launch_morph(Ctx& c, uint32_t n, cudaStream_t st);
+cudaError_t launch_ccl(Ctx& c, uint32_t n, fizi_result* res, cudaStream_t st);
+cudaError_t launch_expand(Ctx& c, uint32_t n, uint8_t* masks, cudaStream_t st);
+cudaError_t launch_track_batch(Ctx& c, uint32_t n, fizi_result* res, cudaStream_t st);
+cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,
+                                cudaStream_t st);
+cudaError_t launch_tstate_reset(Ctx& c, uint32_t first, uint32_t count, cudaStream_t st);
+cudaError_t launch_debug_stage(Ctx& c, int stage, uint32_t frame, void* out, cudaStream_t st);
+
+}  // namespace fizi

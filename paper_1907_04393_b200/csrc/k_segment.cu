@@ -1,0 +1,434 @@
+// k_segment.cu -- K2+K3: brightness statistics and the three-branch test.
+//
+// a2 (§3.2): exact luma sum per frame -> integer mean -> gamma LUT.
+// a3 (§3.1): R1 background envelope test, R2 gray-spread test,
+//     R3 hue-band test, AND-merged into a bit-packed mask (bit = pixel).
+//
+// Fast path (W % 32 == 0): one CTA = 8 warps = 8 chunks of 512 pixels (a
+// 12 KiB tile of interleaved RGB bytes) x a group of up to 16 frames of one
+// stream.  The tile of each frame is fetched by the TMA engine
+// (cp.async.bulk, 4-stage mbarrier ring) into shared memory, so every frame
+// byte is read from HBM exactly once; the stream's envelope for the tile is
+// loaded once into registers and reused for all frames of the group.
+// The luma sum is computed in the same pass (IDP.4A); the mask is computed
+// speculatively with the identity LUT, which is exact for every frame whose
+// mean lands in [luma_lo, luma_hi] (the common case).  The few frames outside
+// are recomputed by fix_fast_kernel with their LUT after finalize_kernel has
+// the means -- same arithmetic, same result as the two-pass definition.
+//
+// Per thread: 16 pixels = 48 bytes = 12 words.  The common case is a warp
+// whose 512 pixels are all inside the envelope (background): R1 = 0, the
+// AND is 0, and the warp only runs the SWAR envelope test (16-bit lanes,
+// IADD3 + LOP3) and the luma dot products.  Warps with any pixel outside the
+// envelope evaluate R1/R2/R3 per pixel in exact integer arithmetic (the hue is
+// compared by cross-multiplication, reading L8).
+#include "dev_util.cuh"
+#include "fizi_internal.cuh"
+
+namespace fizi {
+
+struct SegArgs {
+  const uint8_t* frames;
+  uint64_t frame_bytes;         // 3N
+  uint64_t N;
+  uint32_t nchunks, tiles, words_per_frame;
+  const uint8_t* env;
+  uint64_t env_plane;
+  const uint32_t* frame_stream;
+  const uint32_t* group_frames;
+  const uint32_t* group_off;
+  uint32_t* bitA;
+  unsigned long long* luma;
+  uint32_t* fg;
+  const uint8_t* lut_table;
+  const uint32_t* fix;          // [0] = count, [1..] = frame ids needing a LUT
+  uint32_t S, a1, a2;
+};
+
+// Rec.601 weights split so every dp4a weight fits a byte:
+// 299 r + 587 g + 114 b = 256 (r + 2 g) + (43 r + 75 g + 114 b).
+// Word i of an interleaved run starting at a pixel boundary holds channels
+// (i%3 = 0: r g b r), (1: g b r g), (2: b r g b).
+__constant__ uint32_t kWlo[3] = {0x2B724B2Bu, 0x4B2B724Bu, 0x724B2B72u};
+__constant__ uint32_t kWhi[3] = {0x01000201u, 0x02010002u, 0x00020100u};
+
+__device__ __forceinline__ uint32_t byte_of(const uint32_t (&w)[12], int b) {
+  return (w[b >> 2] >> (8 * (b & 3))) & 0xFFu;
+}
+
+// Exact R2 & R3 for one corrected pixel (readings L5, L7, L8, L9).
+__device__ __forceinline__ uint32_t gray_and_skin(int r, int g, int b, int S, int a1, int a2) {
+  const int M = max(r, max(g, b));
+  const int m = min(r, min(g, b));
+  const int C = M - m;
+  int d, base;
+  if (M == r) { d = g - b; base = g < b ? 360 : 0; }
+  else if (M == g) { d = b - r; base = 120; }
+  else { d = r - g; base = 240; }
+  const int Hn = 60 * d + base * C;            // hue = Hn / C degrees
+  const int lo = a1 * C, hi = a2 * C;
+  const bool band = (a1 <= a2) ? (Hn >= lo && Hn <= hi) : (Hn >= lo || Hn <= hi);
+  return (uint32_t)((C >= S) & (C > 0) & band);
+}
+
+struct EnvRegs {
+  uint32_t loE[12], loO[12], hiE[12], hiO[12];   // even / odd bytes in 16-bit lanes
+};
+
+__device__ __forceinline__ void load_env(EnvRegs& e, const uint8_t* elo, const uint8_t* ehi) {
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    const uint4 l = __ldg(reinterpret_cast<const uint4*>(elo + 512 * k));
+    const uint4 h = __ldg(reinterpret_cast<const uint4*>(ehi + 512 * k));
+    const uint32_t lw[4] = {l.x, l.y, l.z, l.w}, hw[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      e.loE[4 * k + j] = lw[j] & 0x00FF00FFu;
+      e.loO[4 * k + j] = (lw[j] >> 8) & 0x00FF00FFu;
+      e.hiE[4 * k + j] = hw[j] & 0x00FF00FFu;
+      e.hiO[4 * k + j] = (hw[j] >> 8) & 0x00FF00FFu;
+    }
+  }
+}
+
+// Process this thread's 16 pixels of one frame.  Returns the 16 merged bits
+// (bit p = pixel p); adds the pixels' luma to *luma_acc when !kLut.
+template <bool kLut>
+__device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e, bool valid,
+                                          const uint8_t* lut_s, int S, int a1, int a2,
+                                          uint32_t& luma_acc) {
+  uint32_t fr[12];
+  {
+    const uint4* q = reinterpret_cast<const uint4*>(px48);
+    const uint4 q0 = q[0], q1 = q[1], q2 = q[2];
+    fr[0] = q0.x; fr[1] = q0.y; fr[2] = q0.z; fr[3] = q0.w;
+    fr[4] = q1.x; fr[5] = q1.y; fr[6] = q1.z; fr[7] = q1.w;
+    fr[8] = q2.x; fr[9] = q2.y; fr[10] = q2.z; fr[11] = q2.w;
+  }
+  if (!valid) {
+#pragma unroll
+    for (int i = 0; i < 12; i++) fr[i] = 0;
+  }
+  if (kLut) {
+#pragma unroll
+    for (int i = 0; i < 12; i++) {
+      const uint32_t w = fr[i];
+      fr[i] = (uint32_t)lut_s[w & 0xFF] | ((uint32_t)lut_s[(w >> 8) & 0xFF] << 8) |
+              ((uint32_t)lut_s[(w >> 16) & 0xFF] << 16) | ((uint32_t)lut_s[w >> 24] << 24);
+    }
+  } else {
+    uint32_t alo = 0, ahi = 0;
+#pragma unroll
+    for (int i = 0; i < 12; i++) {
+      alo = __dp4a(fr[i], kWlo[i % 3], alo);
+      ahi = __dp4a(fr[i], kWhi[i % 3], ahi);
+    }
+    luma_acc += (ahi << 8) + alo;
+  }
+  // R1 envelope test on all 48 bytes, two bytes per 32-bit op: in each 16-bit
+  // lane, v + 256 - lo has bit 8 set iff v >= lo; hi + 256 - v iff v <= hi.
+  uint32_t ok = 0xFFFFFFFFu;
+#pragma unroll
+  for (int i = 0; i < 12; i++) {
+    const uint32_t vE = fr[i] & 0x00FF00FFu, vO = (fr[i] >> 8) & 0x00FF00FFu;
+    ok &= (vE + 0x01000100u - e.loE[i]) & (e.hiE[i] + 0x01000100u - vE);
+    ok &= (vO + 0x01000100u - e.loO[i]) & (e.hiO[i] + 0x01000100u - vO);
+  }
+  const bool all_inside = !valid || (ok & 0x01000100u) == 0x01000100u;
+  if (!__any_sync(0xFFFFFFFFu, !all_inside)) return 0u;   // whole warp is background
+
+  // Per-pixel path: per-byte inside flags, then R1 & R2 & R3 per pixel.
+  uint64_t inside = 0;
+#pragma unroll
+  for (int i = 0; i < 12; i++) {
+    const uint32_t vE = fr[i] & 0x00FF00FFu, vO = (fr[i] >> 8) & 0x00FF00FFu;
+    const uint32_t tE = (vE + 0x01000100u - e.loE[i]) & (e.hiE[i] + 0x01000100u - vE);
+    const uint32_t tO = (vO + 0x01000100u - e.loO[i]) & (e.hiO[i] + 0x01000100u - vO);
+    const uint32_t f4 = ((tE >> 8) & 1u) | ((tO >> 7) & 2u) | ((tE >> 22) & 4u) | ((tO >> 21) & 8u);
+    inside |= (uint64_t)f4 << (4 * i);
+  }
+  uint32_t bits = 0;
+#pragma unroll
+  for (int p = 0; p < 16; p++) {
+    const uint32_t r1 = ((uint32_t)(inside >> (3 * p)) & 7u) != 7u;
+    const int r = (int)byte_of(fr, 3 * p), g = (int)byte_of(fr, 3 * p + 1),
+              b = (int)byte_of(fr, 3 * p + 2);
+    bits |= (r1 & gray_and_skin(r, g, b, S, a1, a2)) << p;
+  }
+  return valid ? bits : 0u;
+}
+
+// ---------------------------------------------------------------- fast path
+__global__ void __launch_bounds__(256, 2) seg_fast_kernel(SegArgs a) {
+  extern __shared__ __align__(128) uint8_t sm[];          // kStages frame tiles
+  __shared__ __align__(8) uint64_t bar[kStages];
+  __shared__ uint32_t red_y[2][kWarpsPerCta], red_f[2][kWarpsPerCta];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t tile = blockIdx.x, grp = blockIdx.y;
+  const uint32_t f_begin = a.group_off[grp];
+  const uint32_t nf = a.group_off[grp + 1] - f_begin;
+  const uint32_t stream = a.frame_stream[a.group_frames[f_begin]];
+  const uint64_t tile_off = (uint64_t)tile * kTileBytes;
+  const uint64_t rem = a.frame_bytes - tile_off;
+  const uint32_t tile_bytes = rem < (uint64_t)kTileBytes ? (uint32_t)rem : (uint32_t)kTileBytes;
+  const uint32_t c = tile * kWarpsPerCta + warp;
+  const bool valid = (uint64_t)c * kChunkBytes + 48u * lane < a.frame_bytes;
+
+  EnvRegs e;
+  if (valid) {
+    const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + (uint64_t)c * kChunkBytes + 16 * lane;
+    load_env(e, elo, elo + a.env_plane);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 12; i++) e.loE[i] = e.loO[i] = e.hiE[i] = e.hiO[i] = 0;
+  }
+
+  uint64_t pol = 0;
+  if (tid == 0) {
+    pol = policy_evict_first();
+#pragma unroll
+    for (int s = 0; s < kStages; s++) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (uint32_t s = 0; s < nf && s < (uint32_t)kStages; s++) {
+      const uint32_t f = a.group_frames[f_begin + s];
+      mbar_arrive_expect_tx(&bar[s], tile_bytes);
+      bulk_g2s(sm + s * kTileBytes, a.frames + (uint64_t)f * a.frame_bytes + tile_off, tile_bytes,
+               &bar[s], pol);
+    }
+  }
+
+  for (uint32_t i = 0; i < nf; i++) {
+    const uint32_t s = i % kStages;
+    mbar_wait(&bar[s], (i / kStages) & 1u);
+    const uint32_t f = a.group_frames[f_begin + i];
+    uint32_t y = 0;
+    const uint32_t bits = seg16<false>(sm + s * kTileBytes + warp * kChunkBytes + 48 * lane, e,
+                                       valid, nullptr, (int)a.S, (int)a.a1, (int)a.a2, y);
+    const uint32_t hi16 = __shfl_down_sync(0xFFFFFFFFu, bits, 1);
+    const uint32_t word = bits | (hi16 << 16);
+    uint32_t pc = 0;
+    if (!(lane & 1) && valid) {
+      a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = word;
+      pc = __popc(word);
+    }
+    y = warp_sum_u32(y);
+    pc = warp_sum_u32(pc);
+    if (lane == 0) {
+      red_y[i & 1][warp] = y;
+      red_f[i & 1][warp] = pc;
+    }
+    __syncthreads();                          // stage s fully consumed, partials visible
+    if (tid == 0) {
+      unsigned long long sy = 0;
+      uint32_t sf = 0;
+#pragma unroll
+      for (int w = 0; w < kWarpsPerCta; w++) { sy += red_y[i & 1][w]; sf += red_f[i & 1][w]; }
+      atomicAdd(&a.luma[f], sy);
+      if (sf) atomicAdd(&a.fg[f], sf);
+      if (i + kStages < nf) {
+        const uint32_t fn = a.group_frames[f_begin + i + kStages];
+        mbar_arrive_expect_tx(&bar[s], tile_bytes);
+        bulk_g2s(sm + s * kTileBytes, a.frames + (uint64_t)fn * a.frame_bytes + tile_off,
+                 tile_bytes, &bar[s], pol);
+      }
+    }
+  }
+}
+
+// Frames whose mean luma is outside [luma_lo, luma_hi]: recompute their tiles
+// with the frame's gamma LUT (persistent grid over fix-list x tiles).
+__global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(16) uint8_t lut_s[256];
+  __shared__ uint32_t red_f[kWarpsPerCta];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t count = a.fix[0];
+  const uint64_t items = (uint64_t)count * a.tiles;
+  if (blockIdx.x >= items) return;
+  uint64_t pol = 0;
+  if (tid == 0) {
+    pol = policy_evict_first();
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (uint64_t it = blockIdx.x; it < items; it += gridDim.x, phase ^= 1u) {
+    const uint32_t f = a.fix[1 + it / a.tiles];
+    const uint32_t tile = (uint32_t)(it % a.tiles);
+    const uint64_t tile_off = (uint64_t)tile * kTileBytes;
+    const uint64_t rem = a.frame_bytes - tile_off;
+    const uint32_t tile_bytes = rem < (uint64_t)kTileBytes ? (uint32_t)rem : (uint32_t)kTileBytes;
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar, tile_bytes);
+      bulk_g2s(sm, a.frames + (uint64_t)f * a.frame_bytes + tile_off, tile_bytes, &bar, pol);
+    }
+    const uint64_t mean = (a.luma[f] + 500ull * a.N) / (1000ull * a.N);
+    if (tid < 64)
+      reinterpret_cast<uint32_t*>(lut_s)[tid] =
+          reinterpret_cast<const uint32_t*>(a.lut_table + mean * 256)[tid];
+    const uint32_t c = tile * kWarpsPerCta + warp;
+    const bool valid = (uint64_t)c * kChunkBytes + 48u * lane < a.frame_bytes;
+    const uint32_t stream = a.frame_stream[f];
+    EnvRegs e;
+    if (valid) {
+      const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + (uint64_t)c * kChunkBytes + 16 * lane;
+      load_env(e, elo, elo + a.env_plane);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 12; i++) e.loE[i] = e.loO[i] = e.hiE[i] = e.hiO[i] = 0;
+    }
+    __syncthreads();                          // LUT in shared memory
+    mbar_wait(&bar, phase);
+    uint32_t y = 0;
+    const uint32_t bits = seg16<true>(sm + warp * kChunkBytes + 48 * lane, e, valid, lut_s,
+                                      (int)a.S, (int)a.a1, (int)a.a2, y);
+    const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
+    uint32_t pc = 0;
+    if (!(lane & 1) && valid) {
+      a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = word;
+      pc = __popc(word);
+    }
+    pc = warp_sum_u32(pc);
+    if (lane == 0) red_f[warp] = pc;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t sf = 0;
+      for (int w = 0; w < kWarpsPerCta; w++) sf += red_f[w];
+      if (sf) atomicAdd(&a.fg[f], sf);
+    }
+    __syncthreads();                          // smem tile + LUT reused next item
+  }
+}
+
+// ------------------------------------------------------------- generic path
+// Any width: thread per pixel for the luma sum, warp per 32-pixel word of a
+// bit-mask row for the branch tests (ballot), after the means are known.
+__global__ void luma_generic_kernel(const uint8_t* __restrict__ frames, uint64_t N,
+                                    unsigned long long* __restrict__ luma) {
+  const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint32_t f = blockIdx.y;
+  uint32_t y = 0;
+  if (q < N) {
+    const uint8_t* p = frames + ((uint64_t)f * N + q) * 3;
+    y = 299u * p[0] + 587u * p[1] + 114u * p[2];
+  }
+  y = warp_sum_u32(y);
+  if ((threadIdx.x & 31) == 0 && y) atomicAdd(&luma[f], (unsigned long long)y);
+}
+
+__global__ void mask_generic_kernel(SegArgs a, uint32_t W, uint32_t H, uint32_t P, uint32_t n) {
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint64_t per_frame = (uint64_t)H * P;
+  if (gw >= per_frame * n) return;
+  const uint32_t f = (uint32_t)(gw / per_frame);
+  const uint32_t rw = (uint32_t)(gw % per_frame);
+  const uint32_t yrow = rw / P, k = rw % P;
+  const uint32_t x = 32 * k + lane;
+  const uint64_t mean = (a.luma[f] + 500ull * a.N) / (1000ull * a.N);
+  const uint8_t* L = a.lut_table + mean * 256;      // identity row when not corrected
+  uint32_t bit = 0;
+  if (x < W) {
+    const uint64_t q = (uint64_t)yrow * W + x;
+    const uint8_t* p = a.frames + ((uint64_t)f * a.N + q) * 3;
+    const uint32_t stream = a.frame_stream[f];
+    const uint8_t* lo = a.env + (uint64_t)stream * 2 * a.env_plane + q * 3;
+    const uint8_t* hi = lo + a.env_plane;
+    const int r = L[p[0]], g = L[p[1]], b = L[p[2]];
+    const bool inside = r >= lo[0] && r <= hi[0] && g >= lo[1] && g <= hi[1] && b >= lo[2] &&
+                        b <= hi[2];
+    bit = (uint32_t)!inside & gray_and_skin(r, g, b, (int)a.S, (int)a.a1, (int)a.a2);
+  }
+  const uint32_t word = __ballot_sync(0xFFFFFFFFu, bit);
+  if (lane == 0) {
+    a.bitA[(uint64_t)f * per_frame + rw] = word;
+    if (word) atomicAdd(&a.fg[f], (uint32_t)__popc(word));
+  }
+}
+
+// ------------------------------------------------------------ finalize (a2)
+__global__ void finalize_kernel(uint32_t n, uint64_t N, const unsigned long long* __restrict__ luma,
+                                uint32_t* __restrict__ fg, const double* __restrict__ gtab,
+                                const uint8_t* __restrict__ ctab,
+                                const uint32_t* __restrict__ frame_stream,
+                                const int64_t* __restrict__ frame_t, fizi_result* __restrict__ res,
+                                uint32_t* __restrict__ fix) {
+  const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n) return;
+  const uint32_t mean = (uint32_t)((luma[f] + 500ull * N) / (1000ull * N));
+  fizi_result r;
+  memset(&r, 0, sizeof(r));
+  r.t_ms = frame_t[f];
+  r.stream = frame_stream[f];
+  r.frame_idx = f;
+  r.mean_luma = (uint8_t)mean;
+  r.corrected = ctab[mean];
+  r.gamma = gtab[mean];
+  res[f] = r;
+  if (r.corrected) {
+    const uint32_t pos = atomicAdd(&fix[0], 1u);
+    fix[1 + pos] = f;
+    fg[f] = 0;
+  }
+}
+
+cudaError_t launch_segment(Ctx& c, const uint8_t* frames, uint32_t n, uint32_t n_groups,
+                           fizi_result* res, cudaStream_t st) {
+  SegArgs a;
+  a.frames = frames;
+  a.frame_bytes = c.N * 3;
+  a.N = c.N;
+  a.nchunks = c.nchunks;
+  a.tiles = (c.nchunks + kWarpsPerCta - 1) / kWarpsPerCta;
+  a.words_per_frame = c.H * c.P;
+  a.env = c.env;
+  a.env_plane = c.env_plane;
+  a.frame_stream = c.frame_stream;
+  a.group_frames = c.group_frames;
+  a.group_off = c.group_off;
+  a.bitA = c.bitA;
+  a.luma = c.luma;
+  a.fg = c.fg;
+  a.lut_table = c.lut;
+  a.fix = c.fix_count;
+  a.S = c.p.gray_tol_S;
+  a.a1 = c.p.hue_lo_deg;
+  a.a2 = c.p.hue_hi_deg;
+  cudaMemsetAsync(c.luma, 0, sizeof(unsigned long long) * n, st);
+  cudaMemsetAsync(c.fg, 0, sizeof(uint32_t) * n, st);
+  cudaMemsetAsync(c.fix_count, 0, sizeof(uint32_t), st);
+  const unsigned fin_blocks = (n + 255) / 256;
+  if (c.fast) {
+    seg_fast_kernel<<<dim3(a.tiles, n_groups), 256, kStages * kTileBytes, st>>>(a);
+    finalize_kernel<<<fin_blocks, 256, 0, st>>>(n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
+                                                 c.frame_stream, c.frame_t, res, c.fix_count);
+    fix_fast_kernel<<<2 * c.sms, 256, kTileBytes, st>>>(a);
+    c.launches += 3;
+  } else {
+    luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(frames, c.N,
+                                                                                c.luma);
+    finalize_kernel<<<fin_blocks, 256, 0, st>>>(n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
+                                                 c.frame_stream, c.frame_t, res, c.fix_count);
+    const uint64_t warps = (uint64_t)c.H * c.P * n;
+    mask_generic_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a, c.W, c.H, c.P, n);
+    c.launches += 3;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t init_segment(Ctx& c) {
+  (void)c;
+  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kStages * kTileBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fix_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes);
+  return e;
+}
+
+}  // namespace fizi

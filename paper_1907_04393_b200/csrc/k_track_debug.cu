@@ -1,0 +1,235 @@
+// k_track_debug.cu -- K7 (the Mouse fold, a8) and the parity/debug stage
+// kernels behind fizi_debug_stage.
+//
+// a8: §2, "This hand zone is converted into a pointer by the
+// Mouse module ... its movement, its state (click or not)"; reading L25-L27
+// (S:290-298): EMA with beta, snap on acquisition, visibility timeout (strict
+// >), dwell anchor / radius / time, one click per dwell episode.  Sequential
+// per stream (the only cross-frame dependency of the path); each product and
+// sum is a separate correctly-rounded IEEE operation (__dmul_rn/__dadd_rn):
+// no FMA contraction.
+#include "fizi_internal.cuh"
+
+namespace fizi {
+
+__device__ void track_one(const fizi_params& p, TrackState& s, fizi_result& r) {
+  const int64_t t = r.t_ms;
+  if (r.blob_area > 0) {
+    if (s.vis) {
+      const double b = p.beta, ob = __dadd_rn(1.0, -p.beta);
+      s.px = __dadd_rn(__dmul_rn(b, r.cx), __dmul_rn(ob, s.px));
+      s.py = __dadd_rn(__dmul_rn(b, r.cy), __dmul_rn(ob, s.py));
+      const double dx = __dadd_rn(s.px, -s.ax), dy = __dadd_rn(s.py, -s.ay);
+      const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+      const double R2 = __dmul_rn(p.dwell_radius_px, p.dwell_radius_px);
+      if (d2 > R2) {
+        s.ax = s.px; s.ay = s.py; s.anchor_t = t;
+        s.dwell = 0; s.fired = 0;
+      } else {
+        s.dwell = t - s.anchor_t;
+      }
+    } else {
+      s.px = r.cx; s.py = r.cy;
+      s.ax = r.cx; s.ay = r.cy; s.anchor_t = t;
+      s.dwell = 0; s.fired = 0;
+    }
+    s.vis = 1;
+    s.last_t = t;
+  } else {
+    if (s.vis && t - s.last_t > p.lost_timeout_ms) {
+      s.vis = 0; s.dwell = 0; s.fired = 0;
+    } else if (s.vis) {
+      s.dwell = t - s.anchor_t;
+    }
+  }
+  const int clicked = s.vis && !s.fired && s.dwell >= p.dwell_time_ms;
+  if (clicked) s.fired = 1;
+  r.visible = (uint8_t)s.vis;
+  r.clicked = (uint8_t)clicked;
+  r.px = s.px;
+  r.py = s.py;
+  r.dwell_ms = s.dwell;
+}
+
+// One thread per stream; frames of the batch in index order.
+__global__ void track_batch_kernel(fizi_params p, uint32_t n, uint32_t n_streams,
+                                   const uint32_t* __restrict__ frame_stream,
+                                   fizi_result* __restrict__ res, TrackState* __restrict__ ts) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_streams;
+       s += gridDim.x * blockDim.x) {
+    bool any = false;
+    TrackState st;
+    for (uint32_t f = 0; f < n; f++) {
+      if (frame_stream[f] != s) continue;
+      if (!any) { st = ts[s]; any = true; }
+      fizi_result r = res[f];
+      track_one(p, st, r);
+      res[f].visible = r.visible;
+      res[f].clicked = r.clicked;
+      res[f].px = r.px;
+      res[f].py = r.py;
+      res[f].dwell_ms = r.dwell_ms;
+    }
+    if (any) ts[s] = st;
+  }
+}
+
+__global__ void track_stream_kernel(fizi_params p, uint32_t n, fizi_result* __restrict__ res,
+                                    TrackState* __restrict__ ts) {
+  TrackState st = *ts;
+  for (uint32_t f = 0; f < n; f++) {
+    fizi_result r = res[f];
+    track_one(p, st, r);
+    res[f] = r;
+  }
+  *ts = st;
+}
+
+__global__ void tstate_reset_kernel(TrackState* ts, uint32_t count) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) {
+    TrackState z;
+    z.vis = 0; z.fired = 0;
+    z.px = z.py = z.ax = z.ay = 0.0;
+    z.last_t = z.anchor_t = z.dwell = 0;
+    ts[i] = z;
+  }
+}
+
+cudaError_t launch_track_batch(Ctx& c, uint32_t n, fizi_result* res, cudaStream_t st) {
+  const uint32_t threads = c.n_streams < 256 ? ((c.n_streams + 31) / 32) * 32 : 256;
+  const uint32_t blocks = (c.n_streams + threads - 1) / threads;
+  track_batch_kernel<<<blocks, threads, 0, st>>>(c.p, n, c.n_streams, c.frame_stream, res,
+                                                  reinterpret_cast<TrackState*>(c.tstate));
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,
+                                cudaStream_t st) {
+  track_stream_kernel<<<1, 1, 0, st>>>(c.p, n, res, reinterpret_cast<TrackState*>(c.tstate) + stream);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tstate_reset(Ctx& c, uint32_t first, uint32_t count, cudaStream_t st) {
+  tstate_reset_kernel<<<(count + 255) / 256, 256, 0, st>>>(
+      reinterpret_cast<TrackState*>(c.tstate) + first, count);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- debug stages
+// R1/R2/R3 recomputed per pixel from the last call's frames with the frame's
+// LUT; masks expanded from the bit planes; labels painted from the runs.
+__global__ void debug_branch_kernel(const uint8_t* __restrict__ frame, uint64_t N,
+                                    const uint8_t* __restrict__ env_lo,
+                                    const uint8_t* __restrict__ env_hi, bool fast,
+                                    const uint8_t* __restrict__ L, int stage, int S, int a1,
+                                    int a2, uint8_t* __restrict__ out) {
+  const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (q >= N) return;
+  const int v[3] = {L[frame[3 * q]], L[frame[3 * q + 1]], L[frame[3 * q + 2]]};
+  uint8_t o = 0;
+  if (stage == FIZI_STAGE_R1) {
+    bool inside = true;
+    for (int ch = 0; ch < 3; ch++) {
+      const uint64_t e = env_perm_index(3 * q + ch, fast);
+      inside = inside && v[ch] >= env_lo[e] && v[ch] <= env_hi[e];
+    }
+    o = !inside;
+  } else {
+    const int M = max(v[0], max(v[1], v[2])), m = min(v[0], min(v[1], v[2])), C = M - m;
+    if (stage == FIZI_STAGE_R2) {
+      o = C >= S;
+    } else {
+      int d, base;
+      if (M == v[0]) { d = v[1] - v[2]; base = v[1] < v[2] ? 360 : 0; }
+      else if (M == v[1]) { d = v[2] - v[0]; base = 120; }
+      else { d = v[0] - v[1]; base = 240; }
+      const int Hn = 60 * d + base * C, lo = a1 * C, hi = a2 * C;
+      const bool band = (a1 <= a2) ? (Hn >= lo && Hn <= hi) : (Hn >= lo || Hn <= hi);
+      o = (C > 0) && band;
+    }
+  }
+  out[q] = o;
+}
+
+__global__ void debug_labels_kernel(const Run* __restrict__ runs, const uint32_t* __restrict__ parent,
+                                    const uint32_t* __restrict__ row_off, uint32_t H, uint32_t W,
+                                    uint32_t* __restrict__ out) {
+  const uint32_t T = row_off[H];
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < T; g += gridDim.x * blockDim.x) {
+    const Run rg = runs[g];
+    const Run rr = runs[parent[g]];
+    const uint32_t label = 1u + (uint32_t)rr.y * W + rr.x0;
+    for (uint32_t x = rg.x0; x <= rg.x1; x++) out[(uint64_t)rg.y * W + x] = label;
+  }
+}
+
+__global__ void debug_contour_kernel(const uint32_t* __restrict__ F, uint32_t W, uint32_t H,
+                                     uint32_t P, uint8_t* __restrict__ out) {
+  const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (q >= (uint64_t)W * H) return;
+  const int x = (int)(q % W), y = (int)(q / W);
+  auto bit = [&](int xx, int yy) -> uint32_t {
+    if (xx < 0 || yy < 0 || xx >= (int)W || yy >= (int)H) return 0u;
+    return (F[(uint64_t)yy * P + (xx >> 5)] >> (xx & 31)) & 1u;
+  };
+  const uint32_t c = bit(x, y);
+  uint32_t all = 1;
+  for (int dy = -1; dy <= 1; dy++)
+    for (int dx = -1; dx <= 1; dx++) all &= bit(x + dx, y + dy);
+  out[q] = (uint8_t)(c & (all ^ 1u));
+}
+
+cudaError_t launch_expand_from(Ctx& c, const uint32_t* bits, uint32_t n, uint8_t* masks,
+                               cudaStream_t st);
+
+cudaError_t launch_debug_stage(Ctx& c, int stage, uint32_t f, void* out, cudaStream_t st) {
+  const uint64_t wpf = (uint64_t)c.H * c.P;
+  const unsigned blocks = (unsigned)((c.N + 255) / 256);
+  switch (stage) {
+    case FIZI_STAGE_R1:
+    case FIZI_STAGE_R2:
+    case FIZI_STAGE_R3: {
+      // the frame's LUT row: recompute the mean from the luma sum of the call
+      unsigned long long sum = 0;
+      cudaMemcpyAsync(&sum, c.luma + f, sizeof(sum), cudaMemcpyDeviceToHost, st);
+      uint32_t s = 0;
+      cudaMemcpyAsync(&s, c.frame_stream + f, sizeof(s), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const uint64_t mean = (sum + 500ull * c.N) / (1000ull * c.N);
+      const uint8_t* lo = c.env + (uint64_t)s * 2 * c.env_plane;
+      debug_branch_kernel<<<blocks, 256, 0, st>>>(c.last_frames + (uint64_t)f * c.N * 3, c.N, lo,
+                                                  lo + c.env_plane, c.fast, c.lut + mean * 256,
+                                                  stage, (int)c.p.gray_tol_S, (int)c.p.hue_lo_deg,
+                                                  (int)c.p.hue_hi_deg, (uint8_t*)out);
+      c.launches += 1;
+      return cudaGetLastError();
+    }
+    case FIZI_STAGE_MERGED:
+      return launch_expand_from(c, c.bitA + f * wpf, 1, (uint8_t*)out, st);
+    case FIZI_STAGE_OPENCLOSE:
+      return launch_expand_from(c, c.bitOC + f * wpf, 1, (uint8_t*)out, st);
+    case FIZI_STAGE_FINAL:
+      return launch_expand_from(c, c.bitO + f * wpf, 1, (uint8_t*)out, st);
+    case FIZI_STAGE_LABELS: {
+      cudaMemsetAsync(out, 0, c.N * sizeof(uint32_t), st);
+      debug_labels_kernel<<<256, 256, 0, st>>>(c.runs + (uint64_t)f * c.cap_runs,
+                                               c.parent + (uint64_t)f * c.cap_runs,
+                                               c.row_off + (uint64_t)f * (c.H + 1), c.H, c.W,
+                                               (uint32_t*)out);
+      c.launches += 1;
+      return cudaGetLastError();
+    }
+    case FIZI_STAGE_CONTOUR:
+      debug_contour_kernel<<<blocks, 256, 0, st>>>(c.bitO + f * wpf, c.W, c.H, c.P, (uint8_t*)out);
+      c.launches += 1;
+      return cudaGetLastError();
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace fizi

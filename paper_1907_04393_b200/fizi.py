@@ -1,0 +1,260 @@
+"""Thin ctypes binding of libfizi.so (include/fizi.h).
+
+Argument marshalling only: every step of the pixel path runs in the CUDA
+kernels behind the C ABI.  PyTorch provides device memory and the current CUDA
+stream.  There is no CPU fallback: if libfizi.so is missing or no CUDA device
+is present, constructing a ``Fizi`` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfizi.so")
+
+# fizi_status
+OK, E_ARG, E_EMPTY, E_DIMS, E_NOMODEL, E_TIME, E_CUDA, E_OOM, E_CAPACITY = 0, -1, -2, -3, -4, -5, -6, -7, -8
+
+STAGES = {"r1": 0, "r2": 1, "r3": 2, "merged": 3, "openclose": 4, "labels": 5, "final": 6,
+          "contour": 7}
+
+
+class FiziError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{msg} (status {status})")
+        self.status = status
+
+
+class Params(ctypes.Structure):
+    _fields_ = [
+        ("width", ctypes.c_uint32), ("height", ctypes.c_uint32),
+        ("gray_tol_S", ctypes.c_uint32), ("hue_lo_deg", ctypes.c_uint32),
+        ("hue_hi_deg", ctypes.c_uint32), ("se_radius", ctypes.c_uint32),
+        ("min_blob_ppm", ctypes.c_uint32), ("luma_target", ctypes.c_uint32),
+        ("luma_lo", ctypes.c_uint32), ("luma_hi", ctypes.c_uint32),
+        ("gamma_min", ctypes.c_double), ("gamma_max", ctypes.c_double),
+        ("beta", ctypes.c_double), ("dwell_radius_px", ctypes.c_double),
+        ("dwell_time_ms", ctypes.c_int64), ("lost_timeout_ms", ctypes.c_int64),
+        ("debug", ctypes.c_uint32), ("_reserved", ctypes.c_uint32),
+    ]
+
+
+# fizi_result as a numpy structured dtype (128 bytes, offsets of include/fizi.h)
+RESULT_DTYPE = np.dtype({
+    "names": ["t_ms", "stream", "frame_idx", "mean_luma", "corrected", "visible", "clicked",
+              "fg_merged", "fg_final", "n_comp_total", "n_comp_kept", "blob_area", "blob_label",
+              "bbox", "sum_x", "sum_y", "gamma", "cx", "cy", "px", "py", "dwell_ms"],
+    "formats": ["<i8", "<u4", "<u4", "u1", "u1", "u1", "u1", "<u4", "<u4", "<u4", "<u4", "<u4",
+                "<u4", ("<u4", (4,)), "<u8", "<u8", "<f8", "<f8", "<f8", "<f8", "<f8", "<i8"],
+    "offsets": [0, 8, 12, 16, 17, 18, 19, 20, 24, 28, 32, 36, 40, 44, 64, 72, 80, 88, 96, 104,
+                112, 120],
+    "itemsize": 128,
+})
+RESULT_BYTES = 128
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                               "(no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, u32, u8, i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint8, ctypes.c_int
+        L.fizi_params_default.argtypes = [ctypes.POINTER(Params), u32, u32]
+        L.fizi_create.argtypes = [ctypes.POINTER(Params), i32, u32, u32, ctypes.POINTER(vp)]
+        L.fizi_learn_background.argtypes = [vp, u32, vp, u32, u32, u32, u8, vp]
+        for fn in (L.fizi_process_frames, L.fizi_segment_frames, L.fizi_process_frames_host):
+            fn.argtypes = [vp, vp, vp, u32, u32, u32, vp, vp, vp, vp]
+        L.fizi_track.argtypes = [vp, u32, vp, u32, vp]
+        L.fizi_reset_tracker.argtypes = [vp, u32]
+        L.fizi_debug_stage.argtypes = [vp, i32, u32, vp, vp]
+        L.fizi_get_background.argtypes = [vp, u32, vp, vp, vp]
+        L.fizi_set_background.argtypes = [vp, u32, vp, vp, vp]
+        L.fizi_kernel_launches.argtypes = [vp]
+        L.fizi_kernel_launches.restype = ctypes.c_uint64
+        L.fizi_last_error.argtypes = [vp]
+        L.fizi_last_error.restype = ctypes.c_char_p
+        L.fizi_status_string.argtypes = [i32]
+        L.fizi_status_string.restype = ctypes.c_char_p
+        L.fizi_destroy.argtypes = [vp]
+        for name in ("fizi_params_default", "fizi_create", "fizi_learn_background",
+                     "fizi_process_frames", "fizi_segment_frames", "fizi_process_frames_host",
+                     "fizi_track", "fizi_reset_tracker", "fizi_debug_stage",
+                     "fizi_get_background", "fizi_set_background"):
+            getattr(L, name).restype = i32
+        _lib = L
+    return _lib
+
+
+def default_params(width: int, height: int, **kw) -> Params:
+    p = Params()
+    lib().fizi_params_default(ctypes.byref(p), width, height)
+    for k, v in kw.items():
+        if not hasattr(p, k):
+            raise TypeError(f"unknown parameter {k}")
+        setattr(p, k, v)
+    return p
+
+
+def _stream_handle(device) -> int:
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _u32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint32))
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+class Fizi:
+    """One libfizi context: n_streams camera streams of width x height frames."""
+
+    def __init__(self, width: int, height: int, n_streams: int = 1, max_batch: int = 64,
+                 device: int = 0, **params):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("libfizi needs a CUDA device (no CPU fallback)")
+        self.W, self.H = int(width), int(height)
+        self.n_streams, self.max_batch = int(n_streams), int(max_batch)
+        self.device = torch.device("cuda", device)
+        self.params = default_params(self.W, self.H, **params)
+        self._h = ctypes.c_void_p()
+        rc = lib().fizi_create(ctypes.byref(self.params), device, self.n_streams,
+                               self.max_batch, ctypes.byref(self._h))
+        if rc != OK:
+            raise FiziError(rc, f"fizi_create failed: {lib().fizi_status_string(rc).decode()}")
+
+    # ------------------------------------------------------------ helpers
+    def _check(self, rc: int, what: str):
+        if rc != OK:
+            raise FiziError(rc, f"{what}: {lib().fizi_status_string(rc).decode()}: "
+                                f"{lib().fizi_last_error(self._h).decode()}")
+
+    def _frames(self, frames):
+        import torch
+        if not (isinstance(frames, torch.Tensor) and frames.is_cuda and frames.dtype == torch.uint8):
+            raise TypeError("frames must be a CUDA uint8 tensor (n, H, W, 3)")
+        if not frames.is_contiguous():
+            raise ValueError("frames must be contiguous")
+        if frames.dim() == 3:
+            frames = frames.unsqueeze(0)
+        return frames
+
+    def close(self):
+        if self._h:
+            lib().fizi_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -------------------------------------------------------------- API
+    def learn_background(self, frames, stream: int = 0, margin: int = 10):
+        frames = self._frames(frames)
+        n = frames.shape[0]
+        self._check(lib().fizi_learn_background(self._h, stream, frames.data_ptr(), n,
+                                                self.W if n else self.W, self.H, margin,
+                                                _stream_handle(self.device)),
+                    "fizi_learn_background")
+
+    def _call(self, fn, name, frames, streams, t_ms, masks, results):
+        import torch
+        frames = self._frames(frames)
+        n = frames.shape[0]
+        if streams is None:
+            streams = np.zeros(n, np.uint32)
+        streams = _u32(np.broadcast_to(np.asarray(streams, np.uint32), (n,)))
+        t = _i64(np.zeros(n) if t_ms is None else t_ms)
+        if masks is True:
+            masks = torch.empty((n, self.H, self.W), dtype=torch.uint8, device=self.device)
+        if results is None:
+            results = torch.empty((n, RESULT_BYTES), dtype=torch.uint8, device=self.device)
+        self._check(fn(self._h, streams.ctypes.data, frames.data_ptr(), n, self.W, self.H,
+                       t.ctypes.data, masks.data_ptr() if masks is not None else None,
+                       results.data_ptr(), _stream_handle(self.device)), name)
+        return masks, results
+
+    def process_frames(self, frames, streams=None, t_ms=None, masks=True, results=None):
+        """Full path a2..a8; returns (masks uint8 (n,H,W) or None, results (n,128) uint8)."""
+        return self._call(lib().fizi_process_frames, "fizi_process_frames", frames, streams,
+                          t_ms, masks, results)
+
+    def segment_frames(self, frames, streams=None, t_ms=None, masks=True, results=None):
+        """Stateless a2..a7 (tracker untouched)."""
+        return self._call(lib().fizi_segment_frames, "fizi_segment_frames", frames, streams,
+                          t_ms, masks, results)
+
+    def track(self, results, stream: int = 0):
+        """Fold records (device (n,128) uint8 tensor) through stream's tracker in place."""
+        n = results.shape[0]
+        self._check(lib().fizi_track(self._h, stream, results.data_ptr(), n,
+                                     _stream_handle(self.device)), "fizi_track")
+        return results
+
+    def process_frames_host(self, frames: np.ndarray, streams=None, t_ms=None,
+                            masks: np.ndarray | None = None, results: np.ndarray | None = None):
+        """End-to-end on host buffers (H2D + path + D2H inside the call)."""
+        frames = np.ascontiguousarray(frames, np.uint8)
+        n = frames.shape[0]
+        streams = _u32(np.broadcast_to(np.asarray(0 if streams is None else streams, np.uint32), (n,)))
+        t = _i64(np.zeros(n) if t_ms is None else t_ms)
+        if results is None:
+            results = np.zeros(n, RESULT_DTYPE)
+        self._check(lib().fizi_process_frames_host(
+            self._h, streams.ctypes.data, frames.ctypes.data, n, self.W, self.H, t.ctypes.data,
+            masks.ctypes.data if masks is not None else None, results.ctypes.data,
+            _stream_handle(self.device)), "fizi_process_frames_host")
+        return masks, results
+
+    def reset_tracker(self, stream: int = 0):
+        self._check(lib().fizi_reset_tracker(self._h, stream), "fizi_reset_tracker")
+
+    def debug_stage(self, stage, frame: int = 0):
+        import torch
+        sid = STAGES[stage] if isinstance(stage, str) else int(stage)
+        dt = torch.int32 if sid == STAGES["labels"] else torch.uint8
+        out = torch.empty((self.H, self.W), dtype=dt, device=self.device)
+        self._check(lib().fizi_debug_stage(self._h, sid, frame, out.data_ptr(),
+                                           _stream_handle(self.device)), "fizi_debug_stage")
+        return out
+
+    def get_background(self, stream: int = 0):
+        import torch
+        lo = torch.empty((self.H, self.W, 3), dtype=torch.uint8, device=self.device)
+        hi = torch.empty_like(lo)
+        self._check(lib().fizi_get_background(self._h, stream, lo.data_ptr(), hi.data_ptr(),
+                                              _stream_handle(self.device)), "fizi_get_background")
+        return lo, hi
+
+    def set_background(self, lo, hi, stream: int = 0):
+        self._check(lib().fizi_set_background(self._h, stream, lo.data_ptr(), hi.data_ptr(),
+                                              _stream_handle(self.device)), "fizi_set_background")
+
+    def kernel_launches(self) -> int:
+        return int(lib().fizi_kernel_launches(self._h))
+
+
+def results_numpy(results) -> np.ndarray:
+    """(n,128) uint8 tensor/array of fizi_result -> numpy structured array."""
+    try:
+        import torch
+        if isinstance(results, torch.Tensor):
+            results = results.cpu().numpy()
+    except ImportError:
+        pass
+    a = np.ascontiguousarray(results)
+    if a.dtype == RESULT_DTYPE:
+        return a
+    return a.view(np.uint8).reshape(-1, RESULT_BYTES).view(RESULT_DTYPE).reshape(-1)
