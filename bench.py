@@ -1,0 +1,377 @@
+#!/usr/bin/env python3
+"""Benchmark of the FIZI + Mouse per-frame pixel path (arXiv 1907.04393) on B200.
+
+Default workload (N=1): BASELINE.json configs[2] -- one 1920x1080 camera stream,
+10,000 synthetic frames resident in HBM, batches of 64 frames per launch (the
+config the metric is quoted on at 1/2/4/8 GPUs).  A step = one batch through the
+whole hot path: fizi_segment_frames (a2..a7: luma + three branches, open-close,
+labelling, blob filter, hand blob, u8 mask write) then, after an NCCL
+all_gather of the tiny per-frame records when N > 1, fizi_track (a8, the
+Mouse fold) over the gathered records in frame order.  Rank r takes batch b
+when b % N == r (weak scaling: 64 frames per rank per step).
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle instead
+(the reference arm for this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/s and Mpixel/s per GPU and at 2/4/8 B200; % of HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=628)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="fizi", choices=["fizi", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=0, help="frames per launch (default: config's)")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps (capped)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-frames", type=int, default=0)
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML SM clock + throttle reasons, sampled in a thread during the timed region."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- reference arm
+def run_reference(args, cfg, rank, world):
+    """CPU oracle as it stands, frame-parallel over the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    cores = os.cpu_count() or 1
+    per_step = max(1, min(cores, 16))
+    learn = synth.learning_frames_host(cfg)
+    lo, hi = oracle.learn(learn, synth.MARGIN)
+    p = oracle.make_params(cfg.W, cfg.H)
+    pool = synth.frames_host(cfg, 0, range(per_step * 2))
+    t = np.array([synth.t_ms(k) for k in range(per_step * 2)], np.int64)
+    for i in range(args.warmup):
+        sl = slice((i % 2) * per_step, (i % 2 + 1) * per_step)
+        oracle.segment_batch(p, pool[sl], lo, hi, t_ms=t[sl], nthreads=cores)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        sl = slice((i % 2) * per_step, (i % 2 + 1) * per_step)
+        recs, _ = oracle.segment_batch(p, pool[sl], lo, hi, t_ms=t[sl], nthreads=cores)
+        tr = oracle.Tracker(p)
+        for r in recs:
+            tr.update(r)
+    dt = time.perf_counter() - t0
+    frames = per_step * args.steps
+    v = frames / dt
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s",
+        "mpix_per_s": v * cfg.npx / 1e6, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"C{cfg.cid} {cfg.W}x{cfg.H} stream, oracle sample of {per_step} "
+                               f"frames per step", "frames_per_step": per_step},
+        "cpu_baseline": {"value": v, "unit": "frames/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{per_step} frames x {args.steps} steps of C{cfg.cid}"},
+        "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(cfg, n_frames=0):
+    import oracle
+    import synth
+    cores = os.cpu_count() or 1
+    n = n_frames or max(8, min(64, 2 * cores))
+    learn = synth.learning_frames_host(cfg)
+    lo, hi = oracle.learn(learn, synth.MARGIN)
+    frames = synth.frames_host(cfg, 0, range(n))
+    p = oracle.make_params(cfg.W, cfg.H)
+    t0 = time.perf_counter()
+    recs, _ = oracle.segment_batch(p, frames, lo, hi, nthreads=cores)
+    tr = oracle.Tracker(p)
+    for r in recs:
+        tr.update(r)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "frames/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {n} frames of C{cfg.cid} ({cfg.W}x{cfg.H}), frame-parallel "
+                      f"oracle over {cores} host threads, {dt:.1f} s"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1907_04393_b200 import RESULT_BYTES, Fizi
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    B = args.batch or cfg.batch
+    n_batches = math.ceil(cfg.n_proc / B)
+    mine = [b for b in range(n_batches) if b % world == rank]
+    # resident frames: the rank's batches needed by warmup + steps (cycled)
+    need = min(len(mine), args.warmup + args.steps)
+    use = mine[:need]
+    frames_by_batch = []
+    for b in use:
+        ks = list(range(b * B, min(cfg.n_proc, (b + 1) * B)))
+        frames_by_batch.append((ks, synth.frames_dev(cfg, 0, ks, device=dev)))
+    learn = synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True, device=dev)
+
+    fz = Fizi(cfg.W, cfg.H, n_streams=1, max_batch=B, device=local)
+    fz.learn_background(learn, margin=synth.MARGIN)
+    masks = torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=dev)
+    res = torch.empty((B, RESULT_BYTES), dtype=torch.uint8, device=dev)
+    gathered = torch.empty((world * B, RESULT_BYTES), dtype=torch.uint8, device=dev)
+    del learn
+
+    def batch_len(r, i):
+        mine_r = [b for b in range(n_batches) if b % world == r]
+        use_r = mine_r[:min(len(mine_r), args.warmup + args.steps)]
+        if not use_r:
+            return 0
+        b = use_r[i % len(use_r)]
+        return min(B, cfg.n_proc - b * B)
+
+    def step(i):
+        ks, fr = frames_by_batch[i % len(frames_by_batch)]
+        n = len(ks)
+        t = np.asarray([synth.t_ms(k) for k in ks], np.int64)
+        # timestamps keep increasing across passes over the resident batches
+        t = t + (i // len(frames_by_batch)) * synth.t_ms(cfg.n_proc)
+        fz.segment_frames(fr[:n], t_ms=t, masks=masks[:n], results=res[:n])
+        if world > 1:
+            # records of this step's batches (consecutive in frame order) from every rank;
+            # each rank knows every rank's batch size for this step without communication
+            dist.all_gather_into_tensor(gathered, res)
+            for r in range(world):
+                nr = batch_len(r, i)
+                if nr:
+                    fz.track(gathered[r * B: r * B + nr])
+        else:
+            fz.track(res[:n])
+        return n
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    fz.profile_enable(True)
+    fz.profile_read(reset=True)
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = fz.kernel_launches()
+    frames_done = 0
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(st)
+        for i in range(args.steps):
+            frames_done += step(args.warmup + i)
+        e1.record(st)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = fz.kernel_launches() - launches0
+    ms = e0.elapsed_time(e1)
+    prof = fz.profile_read(reset=True)
+    fz.profile_enable(False)
+    tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
+    tot = torch.tensor([frames_done], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    ms_max = float(tmax.item())
+    total_frames = float(tot.item())
+    value = total_frames / (ms_max / 1e3)
+
+    # ---------------------------------------------------------- roofline
+    N = cfg.npx
+    hbm, peak_kind = peaks()
+    seg_ms, seg_n = prof["segment"]
+    # algorithmic bytes of one segment launch: B frames read (3N each), the
+    # stream's envelope once (6N), B bit masks written (N/8 each)
+    seg_bytes = B * (3 * N + N / 8) + 6 * N
+    seg_gbs = seg_bytes / (seg_ms / seg_n / 1e3) / 1e9 if seg_n else None
+    step_bytes = B * (3 * N + N) + 6 * N       # whole-path algorithmic bytes per step
+    step_ms = ms_max / args.steps
+    roofline = {
+        "bound": "hbm", "kernel": "seg_fast_kernel (fused luma + R1/R2/R3, a2+a3)",
+        "achieved": seg_gbs, "peak": hbm, "unit": "GB/s",
+        "frac": (seg_gbs / hbm) if seg_gbs else None, "traffic": None,
+        "peak_kind": peak_kind,
+        "algorithmic_bytes_per_launch": seg_bytes,
+        "kernel_ms_per_launch": seg_ms / seg_n if seg_n else None,
+        "step": {"achieved": step_bytes / (step_ms / 1e3) / 1e9,
+                 "frac": step_bytes / (step_ms / 1e3) / 1e9 / hbm,
+                 "algorithmic_bytes_per_step": step_bytes},
+        "stage_ms_per_step": {k: (v[0] / max(v[1], 1)) for k, v in prof.items()},
+        "stage_share": {k: v[0] / max(sum(x[0] for x in prof.values()), 1e-9)
+                        for k, v in prof.items()},
+    }
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "frames/s",
+        "mpix_per_s": value * N / 1e6, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"C{cfg.cid}: {cfg.W}x{cfg.H} stream, {cfg.n_proc} frames, "
+                               f"batches of {B} per launch (BASELINE.json configs[{cfg.cid - 1}])",
+                   "frames_per_step_per_gpu": B, "resident_batches_per_gpu": len(use),
+                   "l2": f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step",
+                   "parallelism": f"frames sharded by batch, dp{world}"},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "clocks": clk.summary(),
+    }
+
+    # --------------------------------------------------------------- e2e
+    if not args.no_e2e:
+        k2 = args.e2e_steps or min(args.steps, 40)
+        fe = Fizi(cfg.W, cfg.H, n_streams=1, max_batch=B, device=local)
+        learn = synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True, device=dev)
+        fe.learn_background(learn, margin=synth.MARGIN)
+        del learn
+        hosts = []
+        for j in range(min(2, len(frames_by_batch))):
+            ks, fr = frames_by_batch[j]
+            h = torch.empty((len(ks), cfg.H, cfg.W, 3), dtype=torch.uint8).pin_memory()
+            h.copy_(fr[: len(ks)])
+            hosts.append((ks, h.numpy()))
+        mask_h = torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8).pin_memory().numpy()
+        from paper_1907_04393_b200 import RESULT_DTYPE
+        res_h = np.zeros(B, RESULT_DTYPE)
+        t_base = 0
+
+        def estep(i):
+            ks, h = hosts[i % len(hosts)]
+            t = np.asarray([synth.t_ms(k) for k in ks], np.int64) + i * synth.t_ms(cfg.n_proc)
+            fe.process_frames_host(h, t_ms=t, masks=mask_h[: len(ks)], results=res_h[: len(ks)])
+            return len(ks)
+
+        for i in range(3):
+            estep(i)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        nfr = 0
+        for i in range(k2):
+            nfr += estep(3 + i)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        nn = torch.tensor([nfr], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dist.all_reduce(nn, op=dist.ReduceOp.SUM)
+        out["e2e"] = {"value": float(nn.item()) / float(tt.item()), "unit": "frames/s",
+                      "h2d_bytes_per_step": B * 3 * N, "d2h_bytes_per_step": B * (N + RESULT_BYTES),
+                      "steps": k2, "api": "fizi_process_frames_host (pinned host buffers)"}
+        fe.close()
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample_frames)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    fz.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -179,6 +179,22 @@ int fizi_get_background(fizi_ctx *ctx, uint32_t stream, uint8_t *lo_dev, uint8_t
 int fizi_set_background(fizi_ctx *ctx, uint32_t stream, const uint8_t *lo_dev,
                         const uint8_t *hi_dev, fizi_stream_t cuda_stream);
 
+/* Per-stage device timing.  When enabled, every subsequent call records CUDA
+ * events on its stream around each stage; fizi_profile_read synchronises
+ * those events and returns the accumulated milliseconds and the number of
+ * timed launches per slot (FIZI_PROF_*), optionally resetting them. */
+enum {
+    FIZI_PROF_SEGMENT = 0,    /* fused luma + three branches (a2+a3)          */
+    FIZI_PROF_FIXUP = 1,      /* mean -> gamma, LUT re-test of corrected frames */
+    FIZI_PROF_MORPH = 2,      /* open-close (a4)                              */
+    FIZI_PROF_CCL = 3,        /* labelling, filter, hand blob (a5-a7)         */
+    FIZI_PROF_EXPAND = 4,     /* final u8 mask write (a6 output)              */
+    FIZI_PROF_TRACK = 5,      /* Mouse fold (a8)                              */
+    FIZI_PROF_SLOTS = 6
+};
+int fizi_profile_enable(fizi_ctx *ctx, int enable);
+int fizi_profile_read(fizi_ctx *ctx, double *ms_out, uint64_t *count_out, int reset);
+
 /* Number of kernels this context has launched so far (evidence for the
  * bench's gpu_launches count). */
 uint64_t fizi_kernel_launches(const fizi_ctx *ctx);

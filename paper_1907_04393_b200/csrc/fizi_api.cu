@@ -24,6 +24,53 @@ struct fizi_ctx {
 
 using fizi::Ctx;
 
+namespace fizi {
+
+static cudaEvent_t prof_event(Ctx& c) {
+  if (!c.prof_free.empty()) {
+    cudaEvent_t e = c.prof_free.back();
+    c.prof_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+static void prof_resolve(Ctx& c) {
+  for (auto& r : c.prof_pending) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      c.prof_ms[r.slot] += ms;
+      c.prof_n[r.slot] += 1;
+    }
+    c.prof_free.push_back(r.a);
+    c.prof_free.push_back(r.b);
+  }
+  c.prof_pending.clear();
+}
+
+void prof_begin(Ctx& c, cudaStream_t st) {
+  if (!c.prof) return;
+  c.prof_open = prof_event(c);
+  cudaEventRecord(c.prof_open, st);
+}
+
+void prof_end(Ctx& c, int slot, cudaStream_t st) {
+  if (!c.prof || !c.prof_open) return;
+  cudaEvent_t b = prof_event(c);
+  cudaEventRecord(b, st);
+  c.prof_pending.push_back({slot, c.prof_open, b});
+  c.prof_open = nullptr;
+  if (c.prof_pending.size() > 4096) prof_resolve(c);
+}
+
+}  // namespace fizi
+
+using fizi::prof_begin;
+using fizi::prof_end;
+
 namespace {
 
 struct DeviceGuard {
@@ -86,6 +133,9 @@ void free_all(Ctx& c) {
     if (p) cudaFree(p);
   if (c.pinned) cudaFreeHost(c.pinned);
   if (c.pinned_ev) cudaEventDestroy(c.pinned_ev);
+  for (auto& r : c.prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : c.prof_free) cudaEventDestroy(e);
+  if (c.prof_open) cudaEventDestroy(c.prof_open);
 }
 
 // Upload the per-call frame table (timestamps, streams, same-stream groups).
@@ -152,20 +202,28 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   if (rc) return rc;
   cudaError_t e = fizi::launch_segment(c, frames, n, n_groups, res, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "segment");
+  prof_begin(c, st);
   e = fizi::launch_morph(c, n, st);
+  prof_end(c, FIZI_PROF_MORPH, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "morph");
   if (c.p.debug) {
     e = cudaMemcpyAsync(c.bitOC, c.bitO, (size_t)n * c.H * c.P * 4, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "debug copy");
   }
+  prof_begin(c, st);
   e = fizi::launch_ccl(c, n, res, st);
+  prof_end(c, FIZI_PROF_CCL, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "ccl");
   if (masks) {
+    prof_begin(c, st);
     e = fizi::launch_expand(c, n, masks, st);
+    prof_end(c, FIZI_PROF_EXPAND, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "expand");
   }
   if (track) {
+    prof_begin(c, st);
     e = fizi::launch_track_batch(c, n, res, st);
+    prof_end(c, FIZI_PROF_TRACK, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "track");
   }
   c.last_frames = frames;
@@ -369,8 +427,10 @@ int fizi_track(fizi_ctx* ctx, uint32_t stream, fizi_result* results_dev, uint32_
   if (n == 0) return FIZI_OK;
   if (!results_dev) return fail(c, FIZI_E_ARG, "results_dev is NULL");
   DeviceGuard guard(c.device);
-  cudaError_t e = fizi::launch_track_stream(c, stream, results_dev, n,
-                                            reinterpret_cast<cudaStream_t>(cuda_stream));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  prof_begin(c, st);
+  cudaError_t e = fizi::launch_track_stream(c, stream, results_dev, n, st);
+  prof_end(c, FIZI_PROF_TRACK, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "track");
   return FIZI_OK;
 }
@@ -468,6 +528,25 @@ int fizi_set_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* lo_dev,
   if (e != cudaSuccess) return cuda_fail(c, e, "set_background");
   c.env_valid[stream] = 1;
   c.has_t[stream] = 0;
+  return FIZI_OK;
+}
+
+int fizi_profile_enable(fizi_ctx* ctx, int enable) {
+  if (!ctx) return FIZI_E_ARG;
+  ctx->c.prof = enable != 0;
+  return FIZI_OK;
+}
+
+int fizi_profile_read(fizi_ctx* ctx, double* ms_out, uint64_t* count_out, int reset) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  DeviceGuard guard(c.device);
+  fizi::prof_resolve(c);
+  for (int i = 0; i < FIZI_PROF_SLOTS; i++) {
+    if (ms_out) ms_out[i] = c.prof_ms[i];
+    if (count_out) count_out[i] = c.prof_n[i];
+    if (reset) { c.prof_ms[i] = 0; c.prof_n[i] = 0; }
+  }
   return FIZI_OK;
 }
 

@@ -88,6 +88,14 @@ struct Ctx {
   uint8_t* pinned = nullptr;             // staging for the per-call upload
   size_t pinned_bytes = 0;
   cudaEvent_t pinned_ev = nullptr;
+  // per-stage timing (fizi_profile_*)
+  bool prof = false;
+  struct ProfRec { int slot; cudaEvent_t a, b; };
+  std::vector<ProfRec> prof_pending;
+  std::vector<cudaEvent_t> prof_free;
+  double prof_ms[FIZI_PROF_SLOTS] = {0};
+  uint64_t prof_n[FIZI_PROF_SLOTS] = {0};
+  cudaEvent_t prof_open = nullptr;
   // last call (debug)
   const uint8_t* last_frames = nullptr;
   uint32_t last_n = 0;
@@ -121,6 +129,9 @@ cudaError_t launch_env_export(Ctx& c, uint32_t stream, uint8_t* lo, uint8_t* hi,
                               const uint8_t* ilo, const uint8_t* ihi, cudaStream_t st);
 cudaError_t launch_segment(Ctx& c, const uint8_t* frames, uint32_t n, uint32_t n_groups,
                            fizi_result* res, cudaStream_t st);
+// the segment launcher marks the SEGMENT -> FIXUP boundary through this hook
+void prof_begin(Ctx& c, cudaStream_t st);
+void prof_end(Ctx& c, int slot, cudaStream_t st);
 cudaError_t launch_morph(Ctx& c, uint32_t n, cudaStream_t st);
 cudaError_t launch_ccl(Ctx& c, uint32_t n, fizi_result* res, cudaStream_t st);
 cudaError_t launch_expand(Ctx& c, uint32_t n, uint8_t* masks, cudaStream_t st);

@@ -405,18 +405,26 @@ cudaError_t launch_segment(Ctx& c, const uint8_t* frames, uint32_t n, uint32_t n
   cudaMemsetAsync(c.fix_count, 0, sizeof(uint32_t), st);
   const unsigned fin_blocks = (n + 255) / 256;
   if (c.fast) {
+    prof_begin(c, st);
     seg_fast_kernel<<<dim3(a.tiles, n_groups), 256, kStages * kTileBytes, st>>>(a);
+    prof_end(c, FIZI_PROF_SEGMENT, st);
+    prof_begin(c, st);
     finalize_kernel<<<fin_blocks, 256, 0, st>>>(n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
                                                  c.frame_stream, c.frame_t, res, c.fix_count);
     fix_fast_kernel<<<2 * c.sms, 256, kTileBytes, st>>>(a);
+    prof_end(c, FIZI_PROF_FIXUP, st);
     c.launches += 3;
   } else {
+    prof_begin(c, st);
     luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(frames, c.N,
                                                                                 c.luma);
+    prof_end(c, FIZI_PROF_SEGMENT, st);
+    prof_begin(c, st);
     finalize_kernel<<<fin_blocks, 256, 0, st>>>(n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
                                                  c.frame_stream, c.frame_t, res, c.fix_count);
     const uint64_t warps = (uint64_t)c.H * c.P * n;
     mask_generic_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a, c.W, c.H, c.P, n);
+    prof_end(c, FIZI_PROF_FIXUP, st);
     c.launches += 3;
   }
   return cudaGetLastError();

@@ -54,6 +54,8 @@ RESULT_DTYPE = np.dtype({
     "itemsize": 128,
 })
 RESULT_BYTES = 128
+PROF_NAMES = ("segment", "fixup", "morph", "ccl", "expand", "track")
+PROF_SLOTS = len(PROF_NAMES)
 
 _lib = None
 
@@ -76,6 +78,10 @@ def lib() -> ctypes.CDLL:
         L.fizi_debug_stage.argtypes = [vp, i32, u32, vp, vp]
         L.fizi_get_background.argtypes = [vp, u32, vp, vp, vp]
         L.fizi_set_background.argtypes = [vp, u32, vp, vp, vp]
+        L.fizi_profile_enable.argtypes = [vp, i32]
+        L.fizi_profile_enable.restype = i32
+        L.fizi_profile_read.argtypes = [vp, vp, vp, i32]
+        L.fizi_profile_read.restype = i32
         L.fizi_kernel_launches.argtypes = [vp]
         L.fizi_kernel_launches.restype = ctypes.c_uint64
         L.fizi_last_error.argtypes = [vp]
@@ -241,6 +247,16 @@ class Fizi:
     def set_background(self, lo, hi, stream: int = 0):
         self._check(lib().fizi_set_background(self._h, stream, lo.data_ptr(), hi.data_ptr(),
                                               _stream_handle(self.device)), "fizi_set_background")
+
+    def profile_enable(self, on: bool = True):
+        self._check(lib().fizi_profile_enable(self._h, int(on)), "fizi_profile_enable")
+
+    def profile_read(self, reset: bool = True) -> dict:
+        ms = np.zeros(PROF_SLOTS, np.float64)
+        cnt = np.zeros(PROF_SLOTS, np.uint64)
+        self._check(lib().fizi_profile_read(self._h, ms.ctypes.data, cnt.ctypes.data, int(reset)),
+                    "fizi_profile_read")
+        return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(PROF_NAMES)}
 
     def kernel_launches(self) -> int:
         return int(lib().fizi_kernel_launches(self._h))
