@@ -16,6 +16,7 @@ namespace fizi {
 uint32_t morph_tile_rows(const Ctx& c, size_t smem_budget);
 cudaError_t init_morph(Ctx& c);
 cudaError_t init_segment(Ctx& c);
+cudaError_t init_ccl(Ctx& c);
 }  // namespace fizi
 
 struct fizi_ctx {
@@ -127,7 +128,7 @@ cudaError_t dalloc(T** p, size_t bytes) {
 
 void free_all(Ctx& c) {
   void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.luma, c.fg, c.bitA, c.bitO, c.bitOC,
-                  c.row_cnt, c.row_off, c.runs, c.parent, c.stats, c.frame_t, c.fix_count,
+                  c.row_cnt, c.row_base, c.frame_runs, c.runs, c.parent, c.stats, c.frame_t, c.fix_count,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -221,8 +222,11 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
     if (e != cudaSuccess) return cuda_fail(c, e, "expand");
   }
   if (track) {
+    bool single = true;
+    for (uint32_t i = 1; i < n && single; i++) single = sof[i] == sof[0];
     prof_begin(c, st);
-    e = fizi::launch_track_batch(c, n, res, st);
+    e = single ? fizi::launch_track_stream(c, sof[0], res, n, st)
+               : fizi::launch_track_batch(c, n, res, st);
     prof_end(c, FIZI_PROF_TRACK, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "track");
   }
@@ -328,7 +332,8 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.bitO, mb * wpf * 4));
   if (c.p.debug) A(dalloc(&c.bitOC, mb * wpf * 4));
   A(dalloc(&c.row_cnt, mb * c.H * 4));
-  A(dalloc(&c.row_off, mb * (c.H + 1) * 4));
+  A(dalloc(&c.row_base, mb * c.H * 4));
+  A(dalloc(&c.frame_runs, mb * 4));
   A(dalloc(&c.runs, mb * c.cap_runs * sizeof(fizi::Run)));
   A(dalloc(&c.parent, mb * c.cap_runs * 4));
   A(dalloc(&c.stats, mb * c.cap_runs * sizeof(fizi::RootStats)));
@@ -353,6 +358,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   c.has_t.assign(n_streams, 0);
   e = fizi::init_segment(c);
   if (e == cudaSuccess) e = fizi::init_morph(c);
+  if (e == cudaSuccess) e = fizi::init_ccl(c);
   if (e == cudaSuccess) e = cudaMemset(c.env, 0, (uint64_t)n_streams * 2 * c.env_plane);
   if (e == cudaSuccess) e = fizi::launch_lut_table(c, 0);
   if (e == cudaSuccess) e = fizi::launch_tstate_reset(c, 0, n_streams, 0);
@@ -444,6 +450,7 @@ int fizi_process_frames_host(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* 
   if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
   if (n == 0) return FIZI_OK;
   if (!frames_host || !results_host) return fail(c, FIZI_E_ARG, "NULL pointer argument");
+  if (width != c.W || height != c.H) return fail(c, FIZI_E_DIMS, "frame dimensions differ from the context");
   if (n > c.max_batch) return fail(c, FIZI_E_CAPACITY, "n exceeds max_batch");
   DeviceGuard guard(c.device);
   cudaError_t e = cudaSuccess;

@@ -6,8 +6,9 @@
 //              coalesced 16-byte loads (see k_segment.cu: env_perm_index).
 //   bit masks  per frame: H rows x P = ceil(W/32) u32 words, bit i of word k
 //              = pixel x = 32k + i (LSB first); padding bits are always 0.
-//   runs       per frame: a region of cap_runs records (x0, x1, y) in raster
-//              order + union-find parent + per-root statistics.
+//   runs       per frame: up to cap_runs = H * ceil(W/2) compact runs; row y's
+//              runs are row_cnt[y] entries from row_base[y] (sorted by x),
+//              rows in arbitrary order; union-find parent + per-root stats.
 #pragma once
 
 #include <cstdint>
@@ -25,9 +26,10 @@ constexpr int kChunkBytes = 3 * kChunkPx;
 constexpr int kWarpsPerCta = 8;          // chunks per CTA tile
 constexpr int kTileBytes = kChunkBytes * kWarpsPerCta;   // 12 KiB frame bytes per tile
 constexpr int kFrameGroup = 16;          // frames sharing one envelope load
-constexpr int kStages = 4;               // bulk-copy pipeline depth (frames)
+constexpr int kWarpStages = 6;           // per-warp bulk-copy ring depth (frames)
 constexpr int kMaxRadius = 8;
 constexpr size_t kMorphSmem = 200 * 1024;  // dynamic smem budget of the morphology CTA
+constexpr uint32_t kCclSmemRuns = 16384;    // runs labelled in shared memory (else global)
 
 struct Run {                             // one horizontal run of foreground pixels
   uint16_t x0, x1, y, pad;
@@ -67,7 +69,8 @@ struct Ctx {
   uint32_t* bitO = nullptr;              // max_batch * H * P
   uint32_t* bitOC = nullptr;             // debug copy of O
   uint32_t* row_cnt = nullptr;           // max_batch * H   (runs per row)
-  uint32_t* row_off = nullptr;           // max_batch * (H+1)
+  uint32_t* row_base = nullptr;          // max_batch * H   (first run of the row)
+  uint32_t* frame_runs = nullptr;        // max_batch       (runs per frame)
   Run* runs = nullptr;                   // max_batch * cap_runs
   uint32_t* parent = nullptr;            // max_batch * cap_runs
   RootStats* stats = nullptr;            // max_batch * cap_runs

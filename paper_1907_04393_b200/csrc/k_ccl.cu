@@ -7,18 +7,22 @@
 // area * 1e6 >= ppm * W * H, hand = largest kept (ties -> smaller label),
 // centroid = (sum x / area, sum y / area).
 //
-// Run-based labelling, one CTA (1024 threads) per frame, working only on the
-// bit-packed mask (N/8 bytes) and on horizontal runs of 1-bits:
-//   1. runs per row (popcount of run starts, warp per row)
-//   2. exclusive block scan -> run index of each row's first run (raster order)
-//   3. emit runs (x0, x1, y): the k-th start and k-th end of a row pair up
-//   4. union-find over overlapping runs of adjacent rows (|dx| <= 1 overlap =
-//      8-connectivity), lock-free with atomicMin on parent (parent[g] <= g)
-//   5. path flattening: parent = root = the component's first run in raster
-//      order, whose first pixel is the component's min raster index
-//   6. per-root area, sum x, sum y, bbox (atomics)
-//   7. block reduction: #components, #kept, sum of kept areas, the largest
-//   8. dropped components' runs are cleared from the mask words in place
+// Run-based labelling on the compact runs the morphology kernel extracted
+// (row y's runs at row_base[y] .. + row_cnt[y], sorted by x; rows in any
+// order).  One CTA (1024 threads) per frame.  The frame's runs and the
+// union-find forest live in shared memory (up to kCclSmemRuns runs, else in
+// global memory), so every find / link is a shared-memory access:
+//   0. load runs, parent[i] = i, zero the per-root statistics
+//   1. union runs of adjacent rows whose x ranges overlap within one pixel
+//      (8-connectivity), one thread per row, two-pointer sweep over the two
+//      sorted rows; lock-free linking by CAS, the root with the larger raster
+//      key y*W+x0 goes under the smaller one, path halving in find
+//   2. flatten: parent = root = the run holding the component's first pixel
+//      in raster order, so label = 1 + key(root) = 1 + min raster index
+//   3. per-root area, sum x, sum y, bbox: warp-aggregated global atomics
+//   4. block reduction: #components, #kept, sum of kept areas, the largest
+//      (max area, ties -> smaller label)
+//   5. clear dropped components' runs from the mask words (final mask F)
 #include "dev_util.cuh"
 #include "fizi_internal.cuh"
 
@@ -28,9 +32,10 @@ struct CclArgs {
   uint32_t* O;
   uint32_t W, H, P;
   uint64_t N;
-  uint32_t* row_cnt;
-  uint32_t* row_off;
-  Run* runs;
+  const uint32_t* row_cnt;
+  const uint32_t* row_base;
+  const uint32_t* frame_runs;
+  const Run* runs;
   uint32_t* parent;
   RootStats* stats;
   uint64_t cap_runs;
@@ -39,193 +44,146 @@ struct CclArgs {
   uint32_t ppm;
 };
 
-__device__ __forceinline__ uint32_t find_root(const uint32_t* parent, uint32_t g) {
-  uint32_t p = __ldcg(parent + g);
-  while (p != g) {
-    g = p;
-    p = __ldcg(parent + g);
-  }
-  return g;
-}
-
-__device__ __forceinline__ void unite(uint32_t* parent, uint32_t a, uint32_t b) {
-  while (true) {
-    a = find_root(parent, a);
-    b = find_root(parent, b);
-    if (a == b) return;
-    if (a < b) { const uint32_t t = a; a = b; b = t; }   // link the larger root under the smaller
-    const uint32_t old = atomicMin(parent + a, b);
-    if (old == a) return;
-    a = old;                                             // a was re-linked concurrently: retry
-  }
-}
-
 __device__ __forceinline__ bool kept_area(uint32_t area, uint32_t ppm, uint64_t N) {
   return (uint64_t)area * 1000000ull >= (uint64_t)ppm * N;
 }
 
-__global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
-  __shared__ uint32_t s_tot;
-  __shared__ uint32_t s_wsum[32];
+template <bool kShared>
+__device__ __forceinline__ uint32_t ld_par(const uint32_t* p) {
+  if (kShared) return *reinterpret_cast<const volatile uint32_t*>(p);
+  return __ldcg(p);
+}
+
+template <bool kShared>
+__device__ __forceinline__ uint32_t find_root(uint32_t* par, uint32_t x) {
+  while (true) {
+    const uint32_t p = ld_par<kShared>(par + x);
+    if (p == x) return x;
+    const uint32_t gp = ld_par<kShared>(par + p);
+    if (gp != p) atomicCAS(par + x, p, gp);            // path halving
+    x = gp;
+  }
+}
+
+__device__ __forceinline__ uint32_t run_key(const Run* R, uint32_t i, uint32_t W) {
+  const Run r = R[i];
+  return (uint32_t)r.y * W + r.x0;
+}
+
+template <bool kShared>
+__device__ __forceinline__ void unite(uint32_t* par, const Run* R, uint32_t W, uint32_t a,
+                                      uint32_t b) {
+  while (true) {
+    a = find_root<kShared>(par, a);
+    b = find_root<kShared>(par, b);
+    if (a == b) return;
+    if (run_key(R, a, W) < run_key(R, b, W)) { const uint32_t t = a; a = b; b = t; }
+    const uint32_t old = atomicCAS(par + a, a, b);      // a: larger key, goes under b
+    if (old == a) return;
+    a = old;
+  }
+}
+
+template <bool kShared>
+__device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, uint32_t T) {
   __shared__ unsigned long long s_best[32];
   __shared__ uint32_t s_cnt[3][32];
-
-  const uint32_t f = blockIdx.x;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ unsigned long long s_key;
+  __shared__ uint32_t s_drop;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nthr = blockDim.x;
   const uint32_t W = a.W, H = a.H, P = a.P;
-  uint32_t* Of = a.O + (uint64_t)f * H * P;
-  uint32_t* rc = a.row_cnt + (uint64_t)f * H;
-  uint32_t* ro = a.row_off + (uint64_t)f * (H + 1);
-  Run* runs = a.runs + (uint64_t)f * a.cap_runs;
-  uint32_t* parent = a.parent + (uint64_t)f * a.cap_runs;
+  const uint32_t* cnt = a.row_cnt + (uint64_t)f * H;
+  const uint32_t* rb = a.row_base + (uint64_t)f * H;
+  const Run* gruns = a.runs + (uint64_t)f * a.cap_runs;
+  uint32_t* gpar = a.parent + (uint64_t)f * a.cap_runs;
   RootStats* stats = a.stats + (uint64_t)f * a.cap_runs;
 
-  // 1. runs per row
-  for (uint32_t y = warp; y < H; y += 32) {
-    const uint32_t* row = Of + (uint64_t)y * P;
-    uint32_t cnt = 0, carry = 0;
-    for (uint32_t k0 = 0; k0 < P; k0 += 32) {
-      const uint32_t k = k0 + lane;
-      const uint32_t w = k < P ? row[k] : 0u;
-      uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, w, 1);
-      if (lane == 0) prev = carry;
-      cnt += __popc(w & ~((w << 1) | (prev >> 31)));
-      carry = __shfl_sync(0xFFFFFFFFu, w, 31);
-    }
-    cnt = warp_sum_u32(cnt);
-    if (lane == 0) rc[y] = cnt;
+  // 0. load
+  for (uint32_t i = tid; i < T; i += nthr) {
+    if (kShared) R[i] = gruns[i];
+    par[i] = i;
+    RootStats z;
+    z.area = 0; z.xmin = 0xFFFFFFFFu; z.xmax = 0; z.ymin = 0xFFFFFFFFu; z.ymax = 0;
+    z.pad = 0; z.sx = 0; z.sy = 0;
+    stats[i] = z;
   }
   __syncthreads();
 
-  // 2. exclusive scan of H row counts (each thread a contiguous segment)
-  {
-    const uint32_t seg = (H + 1023) / 1024;
-    const uint32_t b0 = tid * seg, b1 = min(H, b0 + seg);
-    uint32_t local = 0;
-    for (uint32_t y = b0; y < b1; y++) local += rc[y];
-    uint32_t incl = local;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-      if (lane >= d) incl += v;
+  // 1. union with the previous row
+  for (uint32_t y = tid + 1; y < H; y += nthr) {
+    const uint32_t n = cnt[y], np = cnt[y - 1];
+    if (!n || !np) continue;
+    const uint32_t cb = rb[y], pb = rb[y - 1];
+    uint32_t h = 0;
+    for (uint32_t j = 0; j < n; j++) {
+      const Run rc = R[cb + j];
+      while (h < np && (uint32_t)R[pb + h].x1 + 1 < rc.x0) h++;
+      for (uint32_t h2 = h; h2 < np && R[pb + h2].x0 <= (uint32_t)rc.x1 + 1; h2++)
+        unite<kShared>(par, R, W, cb + j, pb + h2);
     }
-    if (lane == 31) s_wsum[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t v = s_wsum[lane], inc = v;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-        if (lane >= d) inc += u;
+  }
+  __syncthreads();
+
+  // 2. flatten
+  for (uint32_t i = tid; i < T; i += nthr) par[i] = find_root<kShared>(par, i);
+  __syncthreads();
+
+  // 3. statistics, aggregated over lanes of a warp that share a root
+  for (uint32_t i0 = 0; i0 < T; i0 += nthr) {
+    const uint32_t i = i0 + tid;
+    const bool act = i < T;
+    uint32_t root = 0xFFFFFFFFu, len = 0, x0 = 0xFFFFFFFFu, x1 = 0, y = 0;
+    unsigned long long sx = 0, sy = 0;
+    if (act) {
+      const Run r = R[i];
+      root = ld_par<kShared>(par + i);
+      len = (uint32_t)r.x1 - r.x0 + 1;
+      x0 = r.x0; x1 = r.x1; y = r.y;
+      sx = (unsigned long long)(r.x0 + r.x1) * len / 2;
+      sy = (unsigned long long)r.y * len;
+    }
+    if (__all_sync(0xFFFFFFFFu, !act)) continue;
+    const uint32_t m = __match_any_sync(0xFFFFFFFFu, root);
+    uint32_t g_area = 0, g_x0 = 0xFFFFFFFFu, g_x1 = 0, g_y0 = 0xFFFFFFFFu, g_y1 = 0;
+    unsigned long long g_sx = 0, g_sy = 0;
+#pragma unroll 4
+    for (int l = 0; l < 32; l++) {
+      const uint32_t o_len = __shfl_sync(0xFFFFFFFFu, len, l);
+      const uint32_t o_x0 = __shfl_sync(0xFFFFFFFFu, x0, l);
+      const uint32_t o_x1 = __shfl_sync(0xFFFFFFFFu, x1, l);
+      const uint32_t o_y = __shfl_sync(0xFFFFFFFFu, y, l);
+      const unsigned long long o_sx = __shfl_sync(0xFFFFFFFFu, sx, l);
+      const unsigned long long o_sy = __shfl_sync(0xFFFFFFFFu, sy, l);
+      if ((m >> l) & 1u) {
+        g_area += o_len; g_sx += o_sx; g_sy += o_sy;
+        g_x0 = min(g_x0, o_x0); g_x1 = max(g_x1, o_x1);
+        g_y0 = min(g_y0, o_y); g_y1 = max(g_y1, o_y);
       }
-      s_wsum[lane] = inc - v;                // exclusive warp offsets
-      if (lane == 31) s_tot = inc;
     }
-    __syncthreads();
-    uint32_t run = s_wsum[warp] + incl - local;
-    for (uint32_t y = b0; y < b1; y++) {
-      ro[y] = run;
-      run += rc[y];
-    }
-    if (tid == 0) ro[H] = s_tot;
-  }
-  __syncthreads();
-  const uint32_t T = s_tot;
-
-  // 3. emit runs in raster order
-  for (uint32_t y = warp; y < H; y += 32) {
-    const uint32_t* row = Of + (uint64_t)y * P;
-    const uint32_t base = ro[y];
-    uint32_t rank_s = 0, rank_e = 0, carry = 0;
-    for (uint32_t k0 = 0; k0 < P; k0 += 32) {
-      const uint32_t k = k0 + lane;
-      const uint32_t w = k < P ? row[k] : 0u;
-      uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, w, 1);
-      if (lane == 0) prev = carry;
-      uint32_t next = __shfl_down_sync(0xFFFFFFFFu, w, 1);
-      if (lane == 31) next = (k0 + 32 < P) ? row[k0 + 32] : 0u;
-      carry = __shfl_sync(0xFFFFFFFFu, w, 31);
-      uint32_t st = w & ~((w << 1) | (prev >> 31));
-      uint32_t en = w & ~((w >> 1) | (next << 31));
-      const uint32_t ns = __popc(st), ne = __popc(en);
-      uint32_t ps = ns, pe = ne;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, ps, d);
-        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pe, d);
-        if (lane >= d) { ps += u; pe += v; }
-      }
-      uint32_t is = base + rank_s + ps - ns, ie = base + rank_e + pe - ne;
-      while (st) {
-        const uint32_t bit = __ffs(st) - 1;
-        st &= st - 1;
-        runs[is].x0 = (uint16_t)(32 * k + bit);
-        runs[is].y = (uint16_t)y;
-        parent[is] = is;
-        RootStats z;
-        z.area = 0; z.xmin = 0xFFFFFFFFu; z.xmax = 0; z.ymin = 0xFFFFFFFFu; z.ymax = 0;
-        z.pad = 0; z.sx = 0; z.sy = 0;
-        stats[is] = z;
-        is++;
-      }
-      while (en) {
-        const uint32_t bit = __ffs(en) - 1;
-        en &= en - 1;
-        runs[ie].x1 = (uint16_t)(32 * k + bit);
-        ie++;
-      }
-      rank_s += __shfl_sync(0xFFFFFFFFu, ps, 31);
-      rank_e += __shfl_sync(0xFFFFFFFFu, pe, 31);
+    if (act && (uint32_t)lane == (uint32_t)(__ffs(m) - 1)) {
+      RootStats* st = stats + root;
+      atomicAdd(&st->area, g_area);
+      atomicAdd(&st->sx, g_sx);
+      atomicAdd(&st->sy, g_sy);
+      atomicMin(&st->xmin, g_x0);
+      atomicMax(&st->xmax, g_x1);
+      atomicMin(&st->ymin, g_y0);
+      atomicMax(&st->ymax, g_y1);
     }
   }
   __syncthreads();
 
-  // 4. union overlapping runs of row y-1 (8-connectivity: [x0-1, x1+1])
-  for (uint32_t g = tid; g < T; g += 1024) {
-    const Run rg = runs[g];
-    if (rg.y == 0) continue;
-    uint32_t lo = ro[rg.y - 1], hi = ro[rg.y];
-    const int x0 = (int)rg.x0 - 1, x1 = (int)rg.x1 + 1;
-    while (lo < hi) {                                  // first run with x1 >= x0-1
-      const uint32_t mid = (lo + hi) >> 1;
-      if ((int)runs[mid].x1 < x0) lo = mid + 1; else hi = mid;
-    }
-    for (uint32_t h = lo, e = ro[rg.y]; h < e && (int)runs[h].x0 <= x1; h++) unite(parent, g, h);
-  }
-  __syncthreads();
-
-  // 5. flatten
-  for (uint32_t g = tid; g < T; g += 1024) parent[g] = find_root(parent, g);
-  __syncthreads();
-
-  // 6. per-root statistics
-  for (uint32_t g = tid; g < T; g += 1024) {
-    const Run rg = runs[g];
-    const uint32_t root = __ldcg(parent + g);
-    const uint32_t len = (uint32_t)rg.x1 - rg.x0 + 1;
-    RootStats* s = stats + root;
-    atomicAdd(&s->area, len);
-    atomicAdd(&s->sx, (unsigned long long)((uint64_t)(rg.x0 + rg.x1) * len / 2));
-    atomicAdd(&s->sy, (unsigned long long)rg.y * len);
-    atomicMin(&s->xmin, (uint32_t)rg.x0);
-    atomicMax(&s->xmax, (uint32_t)rg.x1);
-    atomicMin(&s->ymin, (uint32_t)rg.y);
-    atomicMax(&s->ymax, (uint32_t)rg.y);
-  }
-  __syncthreads();
-
-  // 7. counts and the hand blob: key = area << 32 | ~label (max area, then min label)
+  // 4. counts and the hand blob: key = area << 32 | ~label
   uint32_t n_tot = 0, n_kept = 0, fg_final = 0;
   unsigned long long best = 0;
-  for (uint32_t g = tid; g < T; g += 1024) {
-    if (__ldcg(parent + g) != g) continue;
+  for (uint32_t i = tid; i < T; i += nthr) {
+    if (ld_par<kShared>(par + i) != i) continue;
     n_tot++;
-    const uint32_t area = __ldcg(&stats[g].area);
+    const uint32_t area = __ldcg(&stats[i].area);
     if (!kept_area(area, a.ppm, a.N)) continue;
     n_kept++;
     fg_final += area;
-    const Run rg = runs[g];
-    const uint32_t label = 1u + (uint32_t)rg.y * W + rg.x0;
+    const uint32_t label = 1u + run_key(R, i, W);
     const unsigned long long key = ((unsigned long long)area << 32) | (0xFFFFFFFFu - label);
     best = key > best ? key : best;
   }
@@ -245,10 +203,11 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   }
   __syncthreads();
   if (warp == 0) {
-    n_tot = warp_sum_u32(s_cnt[0][lane]);
-    n_kept = warp_sum_u32(s_cnt[1][lane]);
-    fg_final = warp_sum_u32(s_cnt[2][lane]);
-    best = s_best[lane];
+    const int nw = nthr >> 5;
+    n_tot = warp_sum_u32(lane < nw ? s_cnt[0][lane] : 0u);
+    n_kept = warp_sum_u32(lane < nw ? s_cnt[1][lane] : 0u);
+    fg_final = warp_sum_u32(lane < nw ? s_cnt[2][lane] : 0u);
+    best = lane < nw ? s_best[lane] : 0ull;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
       const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, best, d);
@@ -260,38 +219,40 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
       r->fg_final = fg_final;
       r->n_comp_total = n_tot;
       r->n_comp_kept = n_kept;
-      if (best) {
-        const uint32_t label = 0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFu);
-        const uint32_t ly = (label - 1) / W, lx = (label - 1) % W;
-        // root run = the run of row ly starting at lx: binary search
-        uint32_t lo = ro[ly], hi = ro[ly + 1];
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (runs[mid].x0 < lx) lo = mid + 1; else hi = mid;
-        }
-        const RootStats* s = stats + lo;
-        const uint32_t area = __ldcg(&s->area);
-        const unsigned long long sx = __ldcg(&s->sx), sy = __ldcg(&s->sy);
-        r->blob_area = area;
-        r->blob_label = label;
-        r->bbox[0] = __ldcg(&s->xmin); r->bbox[1] = __ldcg(&s->ymin);
-        r->bbox[2] = __ldcg(&s->xmax); r->bbox[3] = __ldcg(&s->ymax);
-        r->sum_x = sx;
-        r->sum_y = sy;
-        r->cx = __ddiv_rn(__ull2double_rn(sx), __uint2double_rn(area));
-        r->cy = __ddiv_rn(__ull2double_rn(sy), __uint2double_rn(area));
-      }
-      s_cnt[0][0] = n_tot - n_kept;          // dropped components
+      s_key = best;
+      s_drop = n_tot - n_kept;
     }
   }
   __syncthreads();
+  const unsigned long long bk = s_key;
+  if (bk) {                                   // the best root's thread writes the blob
+    const uint32_t blabel = 0xFFFFFFFFu - (uint32_t)(bk & 0xFFFFFFFFu);
+    for (uint32_t i = tid; i < T; i += nthr) {
+      if (ld_par<kShared>(par + i) != i || 1u + run_key(R, i, W) != blabel) continue;
+      fizi_result* r = a.res + f;
+      const RootStats* st = stats + i;
+      const uint32_t area = __ldcg(&st->area);
+      const unsigned long long sx = __ldcg(&st->sx), sy = __ldcg(&st->sy);
+      r->blob_area = area;
+      r->blob_label = blabel;
+      r->bbox[0] = __ldcg(&st->xmin); r->bbox[1] = __ldcg(&st->ymin);
+      r->bbox[2] = __ldcg(&st->xmax); r->bbox[3] = __ldcg(&st->ymax);
+      r->sum_x = sx;
+      r->sum_y = sy;
+      r->cx = __ddiv_rn(__ull2double_rn(sx), __uint2double_rn(area));
+      r->cy = __ddiv_rn(__ull2double_rn(sy), __uint2double_rn(area));
+    }
+  }
+  if (kShared)                                 // forest for fizi_debug_stage(LABELS)
+    for (uint32_t i = tid; i < T; i += nthr) gpar[i] = par[i];
 
-  // 8. clear the runs of dropped components from the mask (final mask F)
-  if (s_cnt[0][0] == 0) return;
-  for (uint32_t g = tid; g < T; g += 1024) {
-    const uint32_t root = __ldcg(parent + g);
+  // 5. clear the runs of dropped components from the mask (final mask F)
+  if (s_drop == 0) return;
+  uint32_t* Of = a.O + (uint64_t)f * H * P;
+  for (uint32_t i = tid; i < T; i += nthr) {
+    const uint32_t root = ld_par<kShared>(par + i);
     if (kept_area(__ldcg(&stats[root].area), a.ppm, a.N)) continue;
-    const Run rg = runs[g];
+    const Run rg = R[i];
     uint32_t* row = Of + (uint64_t)rg.y * P;
     for (uint32_t k = rg.x0 >> 5; k <= (uint32_t)(rg.x1 >> 5); k++) {
       const uint32_t b0 = k == (uint32_t)(rg.x0 >> 5) ? (rg.x0 & 31u) : 0u;
@@ -302,13 +263,36 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   }
 }
 
+__global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
+  extern __shared__ __align__(16) uint8_t smc[];
+  const uint32_t f = blockIdx.x;
+  const uint32_t T = a.frame_runs[f];
+  if (T <= kCclSmemRuns) {
+    Run* R = reinterpret_cast<Run*>(smc);
+    uint32_t* par = reinterpret_cast<uint32_t*>(smc + sizeof(Run) * kCclSmemRuns);
+    ccl_frame<true>(a, f, R, par, T);
+  } else {
+    ccl_frame<false>(a, f, const_cast<Run*>(a.runs + (uint64_t)f * a.cap_runs),
+                     a.parent + (uint64_t)f * a.cap_runs, T);
+  }
+}
+
+constexpr size_t kCclSmem = (sizeof(Run) + sizeof(uint32_t)) * kCclSmemRuns;
+
+cudaError_t init_ccl(Ctx& c) {
+  (void)c;
+  return cudaFuncSetAttribute(ccl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kCclSmem);
+}
+
 cudaError_t launch_ccl(Ctx& c, uint32_t n, fizi_result* res, cudaStream_t st) {
   CclArgs a;
   a.O = c.bitO;
   a.W = c.W; a.H = c.H; a.P = c.P;
   a.N = c.N;
   a.row_cnt = c.row_cnt;
-  a.row_off = c.row_off;
+  a.row_base = c.row_base;
+  a.frame_runs = c.frame_runs;
   a.runs = c.runs;
   a.parent = c.parent;
   a.stats = c.stats;
@@ -316,7 +300,7 @@ cudaError_t launch_ccl(Ctx& c, uint32_t n, fizi_result* res, cudaStream_t st) {
   a.res = res;
   a.fg = c.fg;
   a.ppm = c.p.min_blob_ppm;
-  ccl_kernel<<<n, 1024, 0, st>>>(a);
+  ccl_kernel<<<n, 1024, kCclSmem, st>>>(a);
   c.launches += 1;
   return cudaGetLastError();
 }

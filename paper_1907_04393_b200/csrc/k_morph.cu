@@ -1,79 +1,165 @@
-// k_morph.cu -- K4: open-close morphology on the bit-packed mask (a4).
+// k_morph.cu -- K4: open-close morphology on the bit-packed mask (a4), fused
+// with the run extraction that starts the labelling (a5, step 1).
 //
 // §3.1 P:138-139 "morphological operations, combining erosion and dilatation
 // operators ... remove the small noisy objects and ... connect neighborhood
 // zones"; reading L12: square SE of side 2r+1, O = E(D(D(E(A)))), positions
 // outside the frame count as 0 for both operators.
 //
-// One CTA = a band of TR output rows of one frame.  The band plus a 4r-row
-// halo is staged in shared memory once; the four passes run in shared memory
-// (ping-pong buffers), each shrinking the valid band by r rows.  A pixel word
-// (32 pixels) is processed by one thread with shifts across the neighbouring
-// words: horizontal op on rows y-r..y+r, then the vertical op, fused.
+// One CTA (32 x 8 threads) = a band of TR output rows of one frame.  The band
+// plus a 4r-row halo is staged in shared memory once; the four passes run in
+// shared memory (ping-pong), each shrinking the valid band by r rows.  A
+// 32-pixel word is one thread's work: shifts across the neighbouring words
+// give the horizontal op, rows y-r..y+r the vertical op (separable square SE).
+// The band's final rows are then written out and scanned for horizontal runs
+// of 1-bits; each non-empty row reserves a contiguous range of the frame's
+// compact run array with one atomicAdd (row_base[y], row_cnt[y]), its runs
+// sorted by x inside the range.  Rows land in arbitrary order: the labelling
+// identifies components by the raster key y*W+x0 of their runs, not by index.
+#include "dev_util.cuh"
 #include "fizi_internal.cuh"
 
 namespace fizi {
 
-__device__ __forceinline__ uint32_t hop(const uint32_t* row, uint32_t k, uint32_t P, uint32_t r,
-                                        bool ero) {
+struct MorphArgs {
+  const uint32_t* A;
+  uint32_t* O;
+  uint32_t W, H, P, TR;
+  uint64_t cap_runs;
+  uint32_t* row_cnt;
+  uint32_t* row_base;
+  uint32_t* frame_runs;
+  Run* runs;
+};
+
+template <int R, bool kErode>
+__device__ __forceinline__ uint32_t hop(const uint32_t* row, uint32_t k, uint32_t P) {
   const uint32_t w = row[k];
   const uint32_t L = k > 0 ? row[k - 1] : 0u;
-  const uint32_t R = k + 1 < P ? row[k + 1] : 0u;
+  const uint32_t Rw = k + 1 < P ? row[k + 1] : 0u;
   uint32_t h = w;
-  for (uint32_t d = 1; d <= r; d++) {
-    const uint32_t left = (w << d) | (L >> (32 - d));     // pixel x-d
-    const uint32_t right = (w >> d) | (R << (32 - d));    // pixel x+d
-    h = ero ? (h & left & right) : (h | left | right);
+#pragma unroll
+  for (int d = 1; d <= R; d++) {
+    const uint32_t left = (w << d) | (L >> (32 - d));      // pixel x-d
+    const uint32_t right = (w >> d) | (Rw << (32 - d));    // pixel x+d
+    h = kErode ? (h & left & right) : (h | left | right);
   }
   return h;
 }
 
-__global__ void __launch_bounds__(256) morph_kernel(const uint32_t* __restrict__ A,
-                                                    uint32_t* __restrict__ O, uint32_t W,
-                                                    uint32_t H, uint32_t P, uint32_t r,
-                                                    uint32_t TR) {
-  extern __shared__ uint32_t sm[];
-  const uint32_t rows = TR + 8 * r;
-  uint32_t* buf[2] = {sm, sm + rows * P};
-  const uint32_t f = blockIdx.y;
-  const int y0 = (int)(blockIdx.x * TR);
-  const int ybase = y0 - 4 * (int)r;
-  const uint32_t* Af = A + (uint64_t)f * H * P;
-  const uint32_t lastmask = (W & 31u) ? ((1u << (W & 31u)) - 1u) : 0xFFFFFFFFu;
-
-  for (uint32_t i = threadIdx.x; i < rows * P; i += blockDim.x) {
-    const int gy = ybase + (int)(i / P);
-    buf[0][i] = (gy >= 0 && gy < (int)H) ? Af[(uint64_t)gy * P + (i % P)] : 0u;
-  }
-  __syncthreads();
-#pragma unroll 1
-  for (uint32_t j = 0; j < 4; j++) {
-    const bool ero = (j == 0 || j == 3);
-    const uint32_t* src = buf[j & 1];
-    uint32_t* dst = buf[(j + 1) & 1];
-    const uint32_t lo = (j + 1) * r, hi = rows - (j + 1) * r;
-    for (uint32_t i = threadIdx.x; i < (hi - lo) * P; i += blockDim.x) {
-      const uint32_t rr = lo + i / P, k = i % P;
-      const int gy = ybase + (int)rr;
+template <int R, bool kErode>
+__device__ __forceinline__ void morph_pass(const uint32_t* src, uint32_t* dst, uint32_t rows,
+                                           uint32_t P, int ybase, uint32_t H, uint32_t lastmask,
+                                           uint32_t pass) {
+  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const uint32_t lo = (pass + 1) * R, hi = rows - (pass + 1) * R;
+  for (uint32_t rr = lo + ty; rr < hi; rr += 8) {
+    const int gy = ybase + (int)rr;
+    const bool in = gy >= 0 && gy < (int)H;
+    for (uint32_t k = tx; k < P; k += 32) {
       uint32_t out = 0;
-      if (gy >= 0 && gy < (int)H) {
-        uint32_t acc = ero ? 0xFFFFFFFFu : 0u;
-        for (uint32_t dy = rr - r; dy <= rr + r; dy++) {
-          const uint32_t h = hop(src + dy * P, k, P, r, ero);
-          acc = ero ? (acc & h) : (acc | h);
+      if (in) {
+        uint32_t acc = hop<R, kErode>(src + (rr - R) * P, k, P);
+#pragma unroll
+        for (int dy = 1 - R; dy <= R; dy++) {
+          const uint32_t h = hop<R, kErode>(src + (rr + dy) * P, k, P);
+          acc = kErode ? (acc & h) : (acc | h);
         }
         out = (k == P - 1) ? (acc & lastmask) : acc;
       }
       dst[rr * P + k] = out;
     }
-    __syncthreads();
   }
-  uint32_t* Of = O + (uint64_t)f * H * P;
-  const uint32_t* res = buf[0];                    // pass 4 wrote buf[0]
-  for (uint32_t i = threadIdx.x; i < TR * P; i += blockDim.x) {
-    const uint32_t rr = 4 * r + i / P;
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) morph_runs_kernel(MorphArgs a) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t P = a.P, H = a.H, TR = a.TR;
+  const uint32_t rows = TR + 8 * R;
+  uint32_t* b0 = sm;
+  uint32_t* b1 = sm + rows * P;
+  const uint32_t f = blockIdx.y;
+  const int y0 = (int)(blockIdx.x * TR);
+  const int ybase = y0 - 4 * R;
+  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const uint32_t lastmask = (a.W & 31u) ? ((1u << (a.W & 31u)) - 1u) : 0xFFFFFFFFu;
+  const uint32_t* Af = a.A + (uint64_t)f * H * P;
+
+  for (uint32_t rr = ty; rr < rows; rr += 8) {
     const int gy = ybase + (int)rr;
-    if (gy < (int)H) Of[(uint64_t)gy * P + (i % P)] = res[rr * P + (i % P)];
+    const bool in = gy >= 0 && gy < (int)H;
+    for (uint32_t k = tx; k < P; k += 32) b0[rr * P + k] = in ? __ldg(Af + (uint64_t)gy * P + k) : 0u;
+  }
+  __syncthreads();
+  morph_pass<R, true>(b0, b1, rows, P, ybase, H, lastmask, 0);
+  __syncthreads();
+  morph_pass<R, false>(b1, b0, rows, P, ybase, H, lastmask, 1);
+  __syncthreads();
+  morph_pass<R, false>(b0, b1, rows, P, ybase, H, lastmask, 2);
+  __syncthreads();
+  morph_pass<R, true>(b1, b0, rows, P, ybase, H, lastmask, 3);
+  __syncthreads();
+
+  // write O and extract the runs of each output row (one warp per row)
+  uint32_t* Of = a.O + (uint64_t)f * H * P;
+  Run* runs = a.runs + (uint64_t)f * a.cap_runs;
+  for (uint32_t i = ty; i < TR; i += 8) {
+    const uint32_t gy = (uint32_t)y0 + i;
+    if (gy >= H) break;
+    const uint32_t* row = b0 + (4 * R + i) * P;
+    // pass 1: count the row's runs
+    uint32_t cnt = 0;
+    for (uint32_t k0 = 0; k0 < P; k0 += 32) {
+      const uint32_t k = k0 + tx;
+      const uint32_t w = k < P ? row[k] : 0u;
+      if (k < P) Of[(uint64_t)gy * P + k] = w;
+      const uint32_t prev = (k > 0 && k <= P) ? row[k - 1] : 0u;
+      cnt += __popc(w & ~((w << 1) | (prev >> 31)));
+    }
+    cnt = warp_sum_u32(cnt);
+    uint32_t base = 0;
+    if (tx == 0) {
+      if (cnt) base = atomicAdd(a.frame_runs + f, cnt);
+      a.row_cnt[(uint64_t)f * H + gy] = cnt;
+      a.row_base[(uint64_t)f * H + gy] = base;
+    }
+    if (!cnt) continue;
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    // pass 2: emit (x0, x1, y); the k-th start and the k-th end pair up
+    uint32_t rank_s = 0, rank_e = 0;
+    for (uint32_t k0 = 0; k0 < P; k0 += 32) {
+      const uint32_t k = k0 + tx;
+      const uint32_t w = k < P ? row[k] : 0u;
+      const uint32_t prev = (k > 0 && k <= P) ? row[k - 1] : 0u;
+      const uint32_t next = k + 1 < P ? row[k + 1] : 0u;
+      uint32_t st = w & ~((w << 1) | (prev >> 31));
+      uint32_t en = w & ~((w >> 1) | (next << 31));
+      const uint32_t ns = __popc(st), ne = __popc(en);
+      uint32_t ps = ns, pe = ne;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, ps, d);
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pe, d);
+        if ((int)tx >= d) { ps += u; pe += v; }
+      }
+      uint32_t is = base + rank_s + ps - ns, ie = base + rank_e + pe - ne;
+      while (st) {
+        const uint32_t bit = __ffs(st) - 1;
+        st &= st - 1;
+        runs[is].x0 = (uint16_t)(32 * k + bit);
+        runs[is].y = (uint16_t)gy;
+        is++;
+      }
+      while (en) {
+        const uint32_t bit = __ffs(en) - 1;
+        en &= en - 1;
+        runs[ie].x1 = (uint16_t)(32 * k + bit);
+        ie++;
+      }
+      rank_s += __shfl_sync(0xFFFFFFFFu, ps, 31);
+      rank_e += __shfl_sync(0xFFFFFFFFu, pe, 31);
+    }
   }
 }
 
@@ -82,23 +168,63 @@ uint32_t morph_tile_rows(const Ctx& c, size_t smem_budget) {
   const size_t max_rows = smem_budget / per_row;
   if (max_rows <= 8ull * c.p.se_radius) return 0;
   uint32_t tr = (uint32_t)(max_rows - 8ull * c.p.se_radius);
+  // ~48 KB per CTA keeps 4 CTAs per SM; never fewer than 8 output rows
+  const size_t target = (48 * 1024) / per_row;
+  if (target > 8ull * c.p.se_radius + 8 && tr > target - 8ull * c.p.se_radius)
+    tr = (uint32_t)(target - 8ull * c.p.se_radius);
   if (tr > 64) tr = 64;
   if (tr > c.H) tr = c.H;
   return tr;
 }
 
+template <int R>
+static void launch_r(const MorphArgs& a, uint32_t n, size_t smem, cudaStream_t st) {
+  morph_runs_kernel<R><<<dim3((a.H + a.TR - 1) / a.TR, n), 256, smem, st>>>(a);
+}
+
 cudaError_t launch_morph(Ctx& c, uint32_t n, cudaStream_t st) {
+  MorphArgs a;
+  a.A = c.bitA;
+  a.O = c.bitO;
+  a.W = c.W; a.H = c.H; a.P = c.P; a.TR = c.morph_tr;
+  a.cap_runs = c.cap_runs;
+  a.row_cnt = c.row_cnt;
+  a.row_base = c.row_base;
+  a.frame_runs = c.frame_runs;
+  a.runs = c.runs;
+  cudaMemsetAsync(c.frame_runs, 0, n * sizeof(uint32_t), st);
   const uint32_t r = c.p.se_radius;
-  const uint32_t TR = c.morph_tr;
-  const size_t smem = 2ull * (TR + 8 * r) * c.P * sizeof(uint32_t);
-  morph_kernel<<<dim3((c.H + TR - 1) / TR, n), 256, smem, st>>>(c.bitA, c.bitO, c.W, c.H, c.P, r, TR);
+  const size_t smem = 2ull * (a.TR + 8 * r) * c.P * sizeof(uint32_t);
+  switch (r) {
+    case 1: launch_r<1>(a, n, smem, st); break;
+    case 2: launch_r<2>(a, n, smem, st); break;
+    case 3: launch_r<3>(a, n, smem, st); break;
+    case 4: launch_r<4>(a, n, smem, st); break;
+    case 5: launch_r<5>(a, n, smem, st); break;
+    case 6: launch_r<6>(a, n, smem, st); break;
+    case 7: launch_r<7>(a, n, smem, st); break;
+    default: launch_r<8>(a, n, smem, st); break;
+  }
   c.launches += 1;
   return cudaGetLastError();
 }
 
 cudaError_t init_morph(Ctx& c) {
-  return cudaFuncSetAttribute(morph_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kMorphSmem);
+  (void)c;
+  cudaError_t e = cudaSuccess;
+  auto set = [&](const void* fn) {
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMorphSmem);
+  };
+  set((const void*)morph_runs_kernel<1>);
+  set((const void*)morph_runs_kernel<2>);
+  set((const void*)morph_runs_kernel<3>);
+  set((const void*)morph_runs_kernel<4>);
+  set((const void*)morph_runs_kernel<5>);
+  set((const void*)morph_runs_kernel<6>);
+  set((const void*)morph_runs_kernel<7>);
+  set((const void*)morph_runs_kernel<8>);
+  return e;
 }
 
 }  // namespace fizi

@@ -6,9 +6,10 @@
 //
 // Fast path (W % 32 == 0): one CTA = 8 warps = 8 chunks of 512 pixels (a
 // 12 KiB tile of interleaved RGB bytes) x a group of up to 16 frames of one
-// stream.  The tile of each frame is fetched by the TMA engine
-// (cp.async.bulk, 4-stage mbarrier ring) into shared memory, so every frame
-// byte is read from HBM exactly once; the stream's envelope for the tile is
+// stream.  Each warp streams its chunk of every frame through its own TMA
+// ring (cp.async.bulk into shared memory, kWarpStages-deep mbarrier
+// pipeline), so every frame byte is read from HBM exactly once and warps
+// never synchronise with each other; the stream's envelope for the chunk is
 // loaded once into registers and reused for all frames of the group.
 // The luma sum is computed in the same pass (IDP.4A); the mask is computed
 // speculatively with the identity LUT, which is exact for every frame whose
@@ -159,25 +160,38 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
 }
 
 // ---------------------------------------------------------------- fast path
+// Each warp owns one 512-pixel chunk of the tile and runs its own TMA ring of
+// kWarpStages chunk buffers (1536 B) over the frames of the group: lane 0
+// issues cp.async.bulk for frame i + kWarpStages as soon as the warp has
+// consumed frame i, so warps never wait for each other.  Per-frame sums go
+// to shared-memory accumulators; the last warp to finish a frame flushes
+// them to global memory with one atomic each.
 __global__ void __launch_bounds__(256, 2) seg_fast_kernel(SegArgs a) {
-  extern __shared__ __align__(128) uint8_t sm[];          // kStages frame tiles
-  __shared__ __align__(8) uint64_t bar[kStages];
-  __shared__ uint32_t red_y[2][kWarpsPerCta], red_f[2][kWarpsPerCta];
+  extern __shared__ __align__(128) uint8_t sm[];          // 8 warps x kWarpStages chunks
+  __shared__ __align__(8) uint64_t bar[kWarpsPerCta][kWarpStages];
+  __shared__ unsigned long long acc_y[kFrameGroup];
+  __shared__ uint32_t acc_f[kFrameGroup], done[kFrameGroup];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t tile = blockIdx.x, grp = blockIdx.y;
   const uint32_t f_begin = a.group_off[grp];
   const uint32_t nf = a.group_off[grp + 1] - f_begin;
   const uint32_t stream = a.frame_stream[a.group_frames[f_begin]];
-  const uint64_t tile_off = (uint64_t)tile * kTileBytes;
-  const uint64_t rem = a.frame_bytes - tile_off;
-  const uint32_t tile_bytes = rem < (uint64_t)kTileBytes ? (uint32_t)rem : (uint32_t)kTileBytes;
   const uint32_t c = tile * kWarpsPerCta + warp;
-  const bool valid = (uint64_t)c * kChunkBytes + 48u * lane < a.frame_bytes;
+  const uint32_t n_active = min((uint32_t)kWarpsPerCta, a.nchunks - tile * kWarpsPerCta);
+  if (tid < kFrameGroup) { acc_y[tid] = 0; acc_f[tid] = 0; done[tid] = 0; }
+  __syncthreads();
+  if (c >= a.nchunks) return;                                // idle warps of the last tile
+  const uint64_t coff = (uint64_t)c * kChunkBytes;
+  const uint64_t rem = a.frame_bytes - coff;
+  const uint32_t cbytes = rem < (uint64_t)kChunkBytes ? (uint32_t)rem : (uint32_t)kChunkBytes;
+  const bool valid = 48u * lane < cbytes;
+  uint8_t* ring = sm + (uint32_t)warp * kWarpStages * kChunkBytes;
+  uint64_t* wbar = bar[warp];
 
   EnvRegs e;
   if (valid) {
-    const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + (uint64_t)c * kChunkBytes + 16 * lane;
+    const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * lane;
     load_env(e, elo, elo + a.env_plane);
   } else {
 #pragma unroll
@@ -185,31 +199,35 @@ __global__ void __launch_bounds__(256, 2) seg_fast_kernel(SegArgs a) {
   }
 
   uint64_t pol = 0;
-  if (tid == 0) {
+  if (lane == 0) {
     pol = policy_evict_first();
 #pragma unroll
-    for (int s = 0; s < kStages; s++) mbar_init(&bar[s], 1);
+    for (int s = 0; s < kWarpStages; s++) mbar_init(&wbar[s], 1);
     fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (uint32_t s = 0; s < nf && s < (uint32_t)kStages; s++) {
+    for (uint32_t s = 0; s < nf && s < (uint32_t)kWarpStages; s++) {
       const uint32_t f = a.group_frames[f_begin + s];
-      mbar_arrive_expect_tx(&bar[s], tile_bytes);
-      bulk_g2s(sm + s * kTileBytes, a.frames + (uint64_t)f * a.frame_bytes + tile_off, tile_bytes,
-               &bar[s], pol);
+      mbar_arrive_expect_tx(&wbar[s], cbytes);
+      bulk_g2s(ring + s * kChunkBytes, a.frames + (uint64_t)f * a.frame_bytes + coff, cbytes,
+               &wbar[s], pol);
     }
   }
+  __syncwarp();
 
   for (uint32_t i = 0; i < nf; i++) {
-    const uint32_t s = i % kStages;
-    mbar_wait(&bar[s], (i / kStages) & 1u);
+    const uint32_t s = i % kWarpStages;
+    mbar_wait(&wbar[s], (i / kWarpStages) & 1u);
     const uint32_t f = a.group_frames[f_begin + i];
     uint32_t y = 0;
-    const uint32_t bits = seg16<false>(sm + s * kTileBytes + warp * kChunkBytes + 48 * lane, e,
-                                       valid, nullptr, (int)a.S, (int)a.a1, (int)a.a2, y);
-    const uint32_t hi16 = __shfl_down_sync(0xFFFFFFFFu, bits, 1);
-    const uint32_t word = bits | (hi16 << 16);
+    const uint32_t bits = seg16<false>(ring + s * kChunkBytes + 48 * lane, e, valid, nullptr,
+                                       (int)a.S, (int)a.a1, (int)a.a2, y);
+    __syncwarp();                                           // chunk buffer s consumed
+    if (lane == 0 && i + kWarpStages < nf) {
+      const uint32_t fn = a.group_frames[f_begin + i + kWarpStages];
+      mbar_arrive_expect_tx(&wbar[s], cbytes);
+      bulk_g2s(ring + s * kChunkBytes, a.frames + (uint64_t)fn * a.frame_bytes + coff, cbytes,
+               &wbar[s], pol);
+    }
+    const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
     uint32_t pc = 0;
     if (!(lane & 1) && valid) {
       a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = word;
@@ -218,22 +236,15 @@ __global__ void __launch_bounds__(256, 2) seg_fast_kernel(SegArgs a) {
     y = warp_sum_u32(y);
     pc = warp_sum_u32(pc);
     if (lane == 0) {
-      red_y[i & 1][warp] = y;
-      red_f[i & 1][warp] = pc;
-    }
-    __syncthreads();                          // stage s fully consumed, partials visible
-    if (tid == 0) {
-      unsigned long long sy = 0;
-      uint32_t sf = 0;
-#pragma unroll
-      for (int w = 0; w < kWarpsPerCta; w++) { sy += red_y[i & 1][w]; sf += red_f[i & 1][w]; }
-      atomicAdd(&a.luma[f], sy);
-      if (sf) atomicAdd(&a.fg[f], sf);
-      if (i + kStages < nf) {
-        const uint32_t fn = a.group_frames[f_begin + i + kStages];
-        mbar_arrive_expect_tx(&bar[s], tile_bytes);
-        bulk_g2s(sm + s * kTileBytes, a.frames + (uint64_t)fn * a.frame_bytes + tile_off,
-                 tile_bytes, &bar[s], pol);
+      atomicAdd(&acc_y[i], (unsigned long long)y);
+      if (pc) atomicAdd(&acc_f[i], pc);
+      __threadfence_block();
+      if (atomicAdd(&done[i], 1u) == n_active - 1) {         // last warp of this frame
+        __threadfence_block();
+        const unsigned long long sy = atomicAdd(&acc_y[i], 0ull);
+        const uint32_t sf = atomicAdd(&acc_f[i], 0u);
+        atomicAdd(&a.luma[f], sy);
+        if (sf) atomicAdd(&a.fg[f], sf);
       }
     }
   }
@@ -406,7 +417,7 @@ cudaError_t launch_segment(Ctx& c, const uint8_t* frames, uint32_t n, uint32_t n
   const unsigned fin_blocks = (n + 255) / 256;
   if (c.fast) {
     prof_begin(c, st);
-    seg_fast_kernel<<<dim3(a.tiles, n_groups), 256, kStages * kTileBytes, st>>>(a);
+    seg_fast_kernel<<<dim3(a.tiles, n_groups), 256, kWarpsPerCta * kWarpStages * kChunkBytes, st>>>(a);
     prof_end(c, FIZI_PROF_SEGMENT, st);
     prof_begin(c, st);
     finalize_kernel<<<fin_blocks, 256, 0, st>>>(n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
@@ -433,7 +444,7 @@ cudaError_t launch_segment(Ctx& c, const uint8_t* frames, uint32_t n, uint32_t n
 cudaError_t init_segment(Ctx& c) {
   (void)c;
   cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kStages * kTileBytes);
+                                       kWarpsPerCta * kWarpStages * kChunkBytes);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(fix_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes);
   return e;

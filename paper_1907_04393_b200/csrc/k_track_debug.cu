@@ -74,15 +74,56 @@ __global__ void track_batch_kernel(fizi_params p, uint32_t n, uint32_t n_streams
   }
 }
 
-__global__ void track_stream_kernel(fizi_params p, uint32_t n, fizi_result* __restrict__ res,
-                                    TrackState* __restrict__ ts) {
-  TrackState st = *ts;
-  for (uint32_t f = 0; f < n; f++) {
-    fizi_result r = res[f];
-    track_one(p, st, r);
-    res[f] = r;
+// One stream: the inputs of up to kTrackChunk records are staged in shared
+// memory by the whole block, one thread folds them, the block writes back.
+constexpr int kTrackChunk = 512;
+
+__global__ void __launch_bounds__(256) track_stream_kernel(fizi_params p, uint32_t n,
+                                                           fizi_result* __restrict__ res,
+                                                           TrackState* __restrict__ ts) {
+  __shared__ int64_t t_s[kTrackChunk], dw_s[kTrackChunk];
+  __shared__ double cx_s[kTrackChunk], cy_s[kTrackChunk];
+  __shared__ uint32_t area_s[kTrackChunk];
+  __shared__ uint8_t vis_s[kTrackChunk], clk_s[kTrackChunk];
+  TrackState st;
+  if (threadIdx.x == 0) st = *ts;
+  for (uint32_t base = 0; base < n; base += kTrackChunk) {
+    const uint32_t m = min((uint32_t)kTrackChunk, n - base);
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const fizi_result& r = res[base + i];
+      t_s[i] = r.t_ms;
+      area_s[i] = r.blob_area;
+      cx_s[i] = r.cx;
+      cy_s[i] = r.cy;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (uint32_t i = 0; i < m; i++) {
+        fizi_result r;
+        r.t_ms = t_s[i];
+        r.blob_area = area_s[i];
+        r.cx = cx_s[i];
+        r.cy = cy_s[i];
+        track_one(p, st, r);
+        vis_s[i] = r.visible;
+        clk_s[i] = r.clicked;
+        cx_s[i] = r.px;                        // reuse the centroid slots for the pointer
+        cy_s[i] = r.py;
+        dw_s[i] = r.dwell_ms;
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      fizi_result& r = res[base + i];
+      r.visible = vis_s[i];
+      r.clicked = clk_s[i];
+      r.px = cx_s[i];
+      r.py = cy_s[i];
+      r.dwell_ms = dw_s[i];
+    }
+    __syncthreads();
   }
-  *ts = st;
+  if (threadIdx.x == 0) *ts = st;
 }
 
 __global__ void tstate_reset_kernel(TrackState* ts, uint32_t count) {
@@ -107,7 +148,7 @@ cudaError_t launch_track_batch(Ctx& c, uint32_t n, fizi_result* res, cudaStream_
 
 cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,
                                 cudaStream_t st) {
-  track_stream_kernel<<<1, 1, 0, st>>>(c.p, n, res, reinterpret_cast<TrackState*>(c.tstate) + stream);
+  track_stream_kernel<<<1, 256, 0, st>>>(c.p, n, res, reinterpret_cast<TrackState*>(c.tstate) + stream);
   c.launches += 1;
   return cudaGetLastError();
 }
@@ -156,12 +197,12 @@ __global__ void debug_branch_kernel(const uint8_t* __restrict__ frame, uint64_t 
 }
 
 __global__ void debug_labels_kernel(const Run* __restrict__ runs, const uint32_t* __restrict__ parent,
-                                    const uint32_t* __restrict__ row_off, uint32_t H, uint32_t W,
+                                    const uint32_t* __restrict__ frame_runs, uint32_t W,
                                     uint32_t* __restrict__ out) {
-  const uint32_t T = row_off[H];
-  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < T; g += gridDim.x * blockDim.x) {
-    const Run rg = runs[g];
-    const Run rr = runs[parent[g]];
+  const uint32_t T = *frame_runs;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < T; i += gridDim.x * blockDim.x) {
+    const Run rg = runs[i];
+    const Run rr = runs[parent[i]];
     const uint32_t label = 1u + (uint32_t)rr.y * W + rr.x0;
     for (uint32_t x = rg.x0; x <= rg.x1; x++) out[(uint64_t)rg.y * W + x] = label;
   }
@@ -218,8 +259,7 @@ cudaError_t launch_debug_stage(Ctx& c, int stage, uint32_t f, void* out, cudaStr
       cudaMemsetAsync(out, 0, c.N * sizeof(uint32_t), st);
       debug_labels_kernel<<<256, 256, 0, st>>>(c.runs + (uint64_t)f * c.cap_runs,
                                                c.parent + (uint64_t)f * c.cap_runs,
-                                               c.row_off + (uint64_t)f * (c.H + 1), c.H, c.W,
-                                               (uint32_t*)out);
+                                               c.frame_runs + f, c.W, (uint32_t*)out);
       c.launches += 1;
       return cudaGetLastError();
     }

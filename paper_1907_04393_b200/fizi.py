@@ -171,7 +171,7 @@ class Fizi:
         frames = self._frames(frames)
         n = frames.shape[0]
         self._check(lib().fizi_learn_background(self._h, stream, frames.data_ptr(), n,
-                                                self.W if n else self.W, self.H, margin,
+                                                frames.shape[2], frames.shape[1], margin,
                                                 _stream_handle(self.device)),
                     "fizi_learn_background")
 
@@ -187,8 +187,9 @@ class Fizi:
             masks = torch.empty((n, self.H, self.W), dtype=torch.uint8, device=self.device)
         if results is None:
             results = torch.empty((n, RESULT_BYTES), dtype=torch.uint8, device=self.device)
-        self._check(fn(self._h, streams.ctypes.data, frames.data_ptr(), n, self.W, self.H,
-                       t.ctypes.data, masks.data_ptr() if masks is not None else None,
+        self._last_frames = frames          # R1/R2/R3 debug stages re-read the last frames
+        self._check(fn(self._h, streams.ctypes.data, frames.data_ptr(), n, frames.shape[2],
+                       frames.shape[1], t.ctypes.data, masks.data_ptr() if masks is not None else None,
                        results.data_ptr(), _stream_handle(self.device)), name)
         return masks, results
 
@@ -219,7 +220,8 @@ class Fizi:
         if results is None:
             results = np.zeros(n, RESULT_DTYPE)
         self._check(lib().fizi_process_frames_host(
-            self._h, streams.ctypes.data, frames.ctypes.data, n, self.W, self.H, t.ctypes.data,
+            self._h, streams.ctypes.data, frames.ctypes.data, n, frames.shape[2], frames.shape[1],
+            t.ctypes.data,
             masks.ctypes.data if masks is not None else None, results.ctypes.data,
             _stream_handle(self.device)), "fizi_process_frames_host")
         return masks, results

@@ -319,7 +319,10 @@ def test_batch_size_invariance_and_sharded_track():
         parts.append(r)
     rb = torch.cat(parts)
     b.track(rb)
-    assert torch.equal(ra, rb)
+    na, nb = results_numpy(ra), results_numpy(rb)
+    for name in na.dtype.names:
+        if name != "frame_idx":                # index within its call, by definition
+            assert np.array_equal(na[name], nb[name]), name
     a.close()
     b.close()
 
