@@ -53,6 +53,7 @@ struct Ctx {
   uint64_t cap_runs = 0;                 // run capacity per frame
   bool fast = false;                     // W % 32 == 0: fused bulk-copy kernels
   int sms = 148;
+  int seg_variant = 2;                   // min CTAs/SM of the fused kernel
   uint32_t morph_tr = 0;                 // output rows per morphology CTA
   uint64_t launches = 0;
   std::string err;

@@ -163,6 +163,171 @@ __global__ void __launch_bounds__(256) morph_runs_kernel(MorphArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-pipelined variant (P <= 128 words, i.e. W <= 4096): one warp owns
+// a band of kBandRows output rows of one frame and the full row width (lane l
+// holds words l*WPL .. l*WPL+WPL-1).  Input rows stream through the four
+// passes as a software pipeline: each pass keeps the last 2R+1 horizontally
+// processed rows of its input in registers and emits row y as soon as row
+// y+R arrives, so pass 4 emits row y when input row y+4R is read.  Neighbour
+// words across lanes come from warp shuffles; no shared memory, no barriers.
+constexpr int kBandRows = 32;
+
+template <int WPL>
+struct RowW {
+  uint32_t w[WPL];
+};
+
+template <int R, bool kErode, int WPL>
+__device__ __forceinline__ RowW<WPL> hrow(const RowW<WPL>& in) {
+  const int lane = threadIdx.x & 31;
+  uint32_t left_nb = __shfl_up_sync(0xFFFFFFFFu, in.w[WPL - 1], 1);
+  uint32_t right_nb = __shfl_down_sync(0xFFFFFFFFu, in.w[0], 1);
+  if (lane == 0) left_nb = 0u;
+  if (lane == 31) right_nb = 0u;
+  RowW<WPL> o;
+#pragma unroll
+  for (int j = 0; j < WPL; j++) {
+    const uint32_t w = in.w[j];
+    const uint32_t L = j > 0 ? in.w[j - 1] : left_nb;
+    const uint32_t Rw = j + 1 < WPL ? in.w[j + 1] : right_nb;
+    uint32_t h = w;
+#pragma unroll
+    for (int d = 1; d <= R; d++) {
+      const uint32_t lft = __funnelshift_l(L, w, d);      // pixel x-d
+      const uint32_t rgt = __funnelshift_r(w, Rw, d);     // pixel x+d
+      h = kErode ? (h & lft & rgt) : (h | lft | rgt);
+    }
+    o.w[j] = h;
+  }
+  return o;
+}
+
+template <int R, bool kErode, int WPL>
+struct Pass {
+  RowW<WPL> win[2 * R + 1];     // horizontally processed input rows y-2R .. y
+  int filled = 0;
+
+  // push input row (already zero outside the frame); returns true when an
+  // output row (the centre of the window) is available in `out`.
+  __device__ __forceinline__ bool push(const RowW<WPL>& in, RowW<WPL>& out) {
+#pragma unroll
+    for (int i = 0; i < 2 * R; i++) win[i] = win[i + 1];
+    win[2 * R] = hrow<R, kErode, WPL>(in);
+    if (filled < 2 * R + 1) filled++;
+    if (filled < 2 * R + 1) return false;
+#pragma unroll
+    for (int j = 0; j < WPL; j++) {
+      uint32_t acc = win[0].w[j];
+#pragma unroll
+      for (int i = 1; i <= 2 * R; i++) acc = kErode ? (acc & win[i].w[j]) : (acc | win[i].w[j]);
+      out.w[j] = acc;
+    }
+    return true;
+  }
+};
+
+template <int R, int WPL>
+__global__ void __launch_bounds__(256) morph_rows_kernel(MorphArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t f = blockIdx.y;
+  const int y0 = (int)((blockIdx.x * 8 + warp) * kBandRows);
+  const uint32_t H = a.H, P = a.P;
+  if (y0 >= (int)H) return;
+  const int y_end = min((int)H, y0 + kBandRows);
+  const uint32_t lastmask = (a.W & 31u) ? ((1u << (a.W & 31u)) - 1u) : 0xFFFFFFFFu;
+  const uint32_t* Af = a.A + (uint64_t)f * H * P;
+  uint32_t* Of = a.O + (uint64_t)f * H * P;
+  Run* runs = a.runs + (uint64_t)f * a.cap_runs;
+
+  auto clean = [&](RowW<WPL>& r, int y) {          // zero padding outside the frame
+    const bool in = y >= 0 && y < (int)H;
+#pragma unroll
+    for (int j = 0; j < WPL; j++) {
+      const uint32_t k = (uint32_t)(lane * WPL + j);
+      r.w[j] = (in && k < P) ? (k == P - 1 ? (r.w[j] & lastmask) : r.w[j]) : 0u;
+    }
+  };
+
+  Pass<R, true, WPL> p1;
+  Pass<R, false, WPL> p2, p3;
+  Pass<R, true, WPL> p4;
+  const int first = y0 - 4 * R, last = y_end + 4 * R;       // input rows [first, last)
+  for (int yi = first; yi < last; yi++) {
+    RowW<WPL> in;
+    const bool rin = yi >= 0 && yi < (int)H;
+#pragma unroll
+    for (int j = 0; j < WPL; j++) {
+      const uint32_t k = (uint32_t)(lane * WPL + j);
+      in.w[j] = (rin && k < P) ? __ldg(Af + (uint64_t)yi * P + k) : 0u;
+    }
+    RowW<WPL> o1, o2, o3, o4;
+    if (!p1.push(in, o1)) continue;
+    clean(o1, yi - R);
+    if (!p2.push(o1, o2)) continue;
+    clean(o2, yi - 2 * R);
+    if (!p3.push(o2, o3)) continue;
+    clean(o3, yi - 3 * R);
+    if (!p4.push(o3, o4)) continue;
+    const int yo = yi - 4 * R;
+    if (yo < y0 || yo >= y_end) continue;
+    clean(o4, yo);
+    // write O and extract the row's runs
+    uint32_t prev_last = __shfl_up_sync(0xFFFFFFFFu, o4.w[WPL - 1], 1);
+    uint32_t next_first = __shfl_down_sync(0xFFFFFFFFu, o4.w[0], 1);
+    if (lane == 0) prev_last = 0u;
+    if (lane == 31) next_first = 0u;
+    uint32_t st[WPL], en[WPL], ns = 0, ne = 0;
+#pragma unroll
+    for (int j = 0; j < WPL; j++) {
+      const uint32_t k = (uint32_t)(lane * WPL + j);
+      const uint32_t w = o4.w[j];
+      if (k < P) Of[(uint64_t)yo * P + k] = w;
+      const uint32_t pv = j > 0 ? o4.w[j - 1] : prev_last;
+      const uint32_t nx = j + 1 < WPL ? o4.w[j + 1] : next_first;
+      st[j] = w & ~((w << 1) | (pv >> 31));
+      en[j] = w & ~((w >> 1) | (nx << 31));
+      ns += __popc(st[j]);
+      ne += __popc(en[j]);
+    }
+    const uint32_t cnt = warp_sum_u32(ns);
+    uint32_t base = 0;
+    if (lane == 0) {
+      if (cnt) base = atomicAdd(a.frame_runs + f, cnt);
+      a.row_cnt[(uint64_t)f * H + yo] = cnt;
+      a.row_base[(uint64_t)f * H + yo] = base;
+    }
+    if (!cnt) continue;
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    uint32_t ps = ns, pe = ne;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, ps, d);
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pe, d);
+      if (lane >= d) { ps += u; pe += v; }
+    }
+    uint32_t is = base + ps - ns, ie = base + pe - ne;
+#pragma unroll
+    for (int j = 0; j < WPL; j++) {
+      const uint32_t k = (uint32_t)(lane * WPL + j);
+      uint32_t s0 = st[j], e0 = en[j];
+      while (s0) {
+        const uint32_t bit = __ffs(s0) - 1;
+        s0 &= s0 - 1;
+        runs[is].x0 = (uint16_t)(32 * k + bit);
+        runs[is].y = (uint16_t)yo;
+        is++;
+      }
+      while (e0) {
+        const uint32_t bit = __ffs(e0) - 1;
+        e0 &= e0 - 1;
+        runs[ie].x1 = (uint16_t)(32 * k + bit);
+        ie++;
+      }
+    }
+  }
+}
+
 uint32_t morph_tile_rows(const Ctx& c, size_t smem_budget) {
   const size_t per_row = 2ull * c.P * sizeof(uint32_t);
   const size_t max_rows = smem_budget / per_row;
@@ -192,8 +357,26 @@ cudaError_t launch_morph(Ctx& c, uint32_t n, cudaStream_t st) {
   a.row_base = c.row_base;
   a.frame_runs = c.frame_runs;
   a.runs = c.runs;
-  cudaMemsetAsync(c.frame_runs, 0, n * sizeof(uint32_t), st);
   const uint32_t r = c.p.se_radius;
+  cudaMemsetAsync(c.frame_runs, 0, n * sizeof(uint32_t), st);
+  if (c.P <= 128 && r <= 4) {
+    const dim3 grid((c.H + 8 * kBandRows - 1) / (8 * kBandRows), n);
+#define FIZI_MORPH_ROWS(RR, WW) morph_rows_kernel<RR, WW><<<grid, 256, 0, st>>>(a)
+#define FIZI_MORPH_WPL(RR)                                    \
+    if (c.P <= 32) FIZI_MORPH_ROWS(RR, 1);                    \
+    else if (c.P <= 64) FIZI_MORPH_ROWS(RR, 2);               \
+    else FIZI_MORPH_ROWS(RR, 4);
+    switch (r) {
+      case 1: FIZI_MORPH_WPL(1) break;
+      case 2: FIZI_MORPH_WPL(2) break;
+      case 3: FIZI_MORPH_WPL(3) break;
+      default: FIZI_MORPH_WPL(4) break;
+    }
+#undef FIZI_MORPH_WPL
+#undef FIZI_MORPH_ROWS
+    c.launches += 1;
+    return cudaGetLastError();
+  }
   const size_t smem = 2ull * (a.TR + 8 * r) * c.P * sizeof(uint32_t);
   switch (r) {
     case 1: launch_r<1>(a, n, smem, st); break;

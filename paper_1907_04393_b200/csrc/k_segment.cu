@@ -23,6 +23,8 @@
 // IADD3 + LOP3) and the luma dot products.  Warps with any pixel outside the
 // envelope evaluate R1/R2/R3 per pixel in exact integer arithmetic (the hue is
 // compared by cross-multiplication, reading L8).
+#include <cstdlib>
+
 #include "dev_util.cuh"
 #include "fizi_internal.cuh"
 
@@ -72,9 +74,15 @@ __device__ __forceinline__ uint32_t gray_and_skin(int r, int g, int b, int S, in
   return (uint32_t)((C >= S) & (C > 0) & band);
 }
 
+// Envelope of the thread's 48 bytes, even / odd bytes in 16-bit lanes and
+// pre-biased: in each lane, v + KloX has bit 8 set iff v >= lo and KhiX - v
+// has bit 8 set iff v <= hi (KloX = 0x100 - lo, KhiX = hi + 0x100).
 struct EnvRegs {
-  uint32_t loE[12], loO[12], hiE[12], hiO[12];   // even / odd bytes in 16-bit lanes
+  uint32_t KloE[12], KloO[12], KhiE[12], KhiO[12];
 };
+
+__device__ __forceinline__ uint32_t even_bytes(uint32_t w) { return w & 0x00FF00FFu; }
+__device__ __forceinline__ uint32_t odd_bytes(uint32_t w) { return __byte_perm(w, 0u, 0x4341); }
 
 __device__ __forceinline__ void load_env(EnvRegs& e, const uint8_t* elo, const uint8_t* ehi) {
 #pragma unroll
@@ -84,16 +92,32 @@ __device__ __forceinline__ void load_env(EnvRegs& e, const uint8_t* elo, const u
     const uint32_t lw[4] = {l.x, l.y, l.z, l.w}, hw[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      e.loE[4 * k + j] = lw[j] & 0x00FF00FFu;
-      e.loO[4 * k + j] = (lw[j] >> 8) & 0x00FF00FFu;
-      e.hiE[4 * k + j] = hw[j] & 0x00FF00FFu;
-      e.hiO[4 * k + j] = (hw[j] >> 8) & 0x00FF00FFu;
+      e.KloE[4 * k + j] = 0x01000100u - even_bytes(lw[j]);
+      e.KloO[4 * k + j] = 0x01000100u - odd_bytes(lw[j]);
+      e.KhiE[4 * k + j] = 0x01000100u + even_bytes(hw[j]);
+      e.KhiO[4 * k + j] = 0x01000100u + odd_bytes(hw[j]);
     }
   }
 }
 
+__device__ __forceinline__ void zero_env(EnvRegs& e) {
+#pragma unroll
+  for (int i = 0; i < 12; i++) {
+    e.KloE[i] = e.KloO[i] = 0x01000100u;   // lo = 0, hi = 255: everything inside
+    e.KhiE[i] = e.KhiO[i] = 0x01FF01FFu;
+  }
+}
+
+// inside flags of the 4 bytes of word i: bits 8/24 of tE (bytes 0, 2) and tO (1, 3)
+__device__ __forceinline__ void r1_lanes(uint32_t w, const EnvRegs& e, int i, uint32_t& tE,
+                                         uint32_t& tO) {
+  const uint32_t vE = even_bytes(w), vO = odd_bytes(w);
+  tE = (vE + e.KloE[i]) & (e.KhiE[i] - vE);
+  tO = (vO + e.KloO[i]) & (e.KhiO[i] - vO);
+}
+
 // Process this thread's 16 pixels of one frame.  Returns the 16 merged bits
-// (bit p = pixel p); adds the pixels' luma to *luma_acc when !kLut.
+// (bit p = pixel p); adds the pixels' luma to luma_acc when !kLut.
 template <bool kLut>
 __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e, bool valid,
                                           const uint8_t* lut_s, int S, int a1, int a2,
@@ -126,35 +150,44 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
     }
     luma_acc += (ahi << 8) + alo;
   }
-  // R1 envelope test on all 48 bytes, two bytes per 32-bit op: in each 16-bit
-  // lane, v + 256 - lo has bit 8 set iff v >= lo; hi + 256 - v iff v <= hi.
+  // R1 envelope test on all 48 bytes, two bytes per 32-bit op
   uint32_t ok = 0xFFFFFFFFu;
 #pragma unroll
   for (int i = 0; i < 12; i++) {
-    const uint32_t vE = fr[i] & 0x00FF00FFu, vO = (fr[i] >> 8) & 0x00FF00FFu;
-    ok &= (vE + 0x01000100u - e.loE[i]) & (e.hiE[i] + 0x01000100u - vE);
-    ok &= (vO + 0x01000100u - e.loO[i]) & (e.hiO[i] + 0x01000100u - vO);
+    uint32_t tE, tO;
+    r1_lanes(fr[i], e, i, tE, tO);
+    ok &= tE & tO;
   }
-  const bool all_inside = !valid || (ok & 0x01000100u) == 0x01000100u;
+  const bool all_inside = (ok & 0x01000100u) == 0x01000100u;
   if (!__any_sync(0xFFFFFFFFu, !all_inside)) return 0u;   // whole warp is background
 
-  // Per-pixel path: per-byte inside flags, then R1 & R2 & R3 per pixel.
+  // Per-pixel path (rare: warps touching the hand): 48 per-byte inside flags,
+  // then R1 & R2 & R3 per pixel, 4 pixels (3 words) per rolled iteration.
   uint64_t inside = 0;
 #pragma unroll
   for (int i = 0; i < 12; i++) {
-    const uint32_t vE = fr[i] & 0x00FF00FFu, vO = (fr[i] >> 8) & 0x00FF00FFu;
-    const uint32_t tE = (vE + 0x01000100u - e.loE[i]) & (e.hiE[i] + 0x01000100u - vE);
-    const uint32_t tO = (vO + 0x01000100u - e.loO[i]) & (e.hiO[i] + 0x01000100u - vO);
+    uint32_t tE, tO;
+    r1_lanes(fr[i], e, i, tE, tO);
     const uint32_t f4 = ((tE >> 8) & 1u) | ((tO >> 7) & 2u) | ((tE >> 22) & 4u) | ((tO >> 21) & 8u);
     inside |= (uint64_t)f4 << (4 * i);
   }
   uint32_t bits = 0;
+#pragma unroll 1
+  for (int g = 0; g < 4; g++) {
+    const uint32_t w0 = fr[0], w1 = fr[1], w2 = fr[2];
+    const uint32_t in12 = (uint32_t)(inside >> (12 * g)) & 0xFFFu;
 #pragma unroll
-  for (int p = 0; p < 16; p++) {
-    const uint32_t r1 = ((uint32_t)(inside >> (3 * p)) & 7u) != 7u;
-    const int r = (int)byte_of(fr, 3 * p), g = (int)byte_of(fr, 3 * p + 1),
-              b = (int)byte_of(fr, 3 * p + 2);
-    bits |= (r1 & gray_and_skin(r, g, b, S, a1, a2)) << p;
+    for (int q = 0; q < 4; q++) {
+      const int b = 3 * q;                            // byte offset within the 3 words
+      auto byte = [&](int bb) -> int {
+        const uint32_t w = bb < 4 ? w0 : (bb < 8 ? w1 : w2);
+        return (int)((w >> (8 * (bb & 3))) & 0xFFu);
+      };
+      const uint32_t r1 = ((in12 >> b) & 7u) != 7u;
+      bits |= (r1 & gray_and_skin(byte(b), byte(b + 1), byte(b + 2), S, a1, a2)) << (4 * g + q);
+    }
+#pragma unroll
+    for (int i = 0; i < 9; i++) fr[i] = fr[i + 3];
   }
   return valid ? bits : 0u;
 }
@@ -166,7 +199,8 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
 // consumed frame i, so warps never wait for each other.  Per-frame sums go
 // to shared-memory accumulators; the last warp to finish a frame flushes
 // them to global memory with one atomic each.
-__global__ void __launch_bounds__(256, 2) seg_fast_kernel(SegArgs a) {
+template <int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   extern __shared__ __align__(128) uint8_t sm[];          // 8 warps x kWarpStages chunks
   __shared__ __align__(8) uint64_t bar[kWarpsPerCta][kWarpStages];
   __shared__ unsigned long long acc_y[kFrameGroup];
@@ -194,8 +228,7 @@ __global__ void __launch_bounds__(256, 2) seg_fast_kernel(SegArgs a) {
     const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * lane;
     load_env(e, elo, elo + a.env_plane);
   } else {
-#pragma unroll
-    for (int i = 0; i < 12; i++) e.loE[i] = e.loO[i] = e.hiE[i] = e.hiO[i] = 0;
+    zero_env(e);
   }
 
   uint64_t pol = 0;
@@ -291,8 +324,7 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
       const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + (uint64_t)c * kChunkBytes + 16 * lane;
       load_env(e, elo, elo + a.env_plane);
     } else {
-#pragma unroll
-      for (int i = 0; i < 12; i++) e.loE[i] = e.loO[i] = e.hiE[i] = e.hiO[i] = 0;
+      zero_env(e);
     }
     __syncthreads();                          // LUT in shared memory
     mbar_wait(&bar, phase);
@@ -417,7 +449,10 @@ cudaError_t launch_segment(Ctx& c, const uint8_t* frames, uint32_t n, uint32_t n
   const unsigned fin_blocks = (n + 255) / 256;
   if (c.fast) {
     prof_begin(c, st);
-    seg_fast_kernel<<<dim3(a.tiles, n_groups), 256, kWarpsPerCta * kWarpStages * kChunkBytes, st>>>(a);
+    if (c.seg_variant == 3)
+      seg_fast_kernel<3><<<dim3(a.tiles, n_groups), 256, kWarpsPerCta * kWarpStages * kChunkBytes, st>>>(a);
+    else
+      seg_fast_kernel<2><<<dim3(a.tiles, n_groups), 256, kWarpsPerCta * kWarpStages * kChunkBytes, st>>>(a);
     prof_end(c, FIZI_PROF_SEGMENT, st);
     prof_begin(c, st);
     finalize_kernel<<<fin_blocks, 256, 0, st>>>(n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
@@ -443,8 +478,13 @@ cudaError_t launch_segment(Ctx& c, const uint8_t* frames, uint32_t n, uint32_t n
 
 cudaError_t init_segment(Ctx& c) {
   (void)c;
-  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kWarpsPerCta * kWarpStages * kChunkBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(seg_fast_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kWarpsPerCta * kWarpStages * kChunkBytes);
+  const char* v = getenv("FIZI_SEG_VARIANT");           // experiment switch (default 2)
+  c.seg_variant = v ? atoi(v) : 2;
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(fix_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes);
   return e;
