@@ -171,7 +171,8 @@ __global__ void __launch_bounds__(256) morph_runs_kernel(MorphArgs a) {
 // processed rows of its input in registers and emits row y as soon as row
 // y+R arrives, so pass 4 emits row y when input row y+4R is read.  Neighbour
 // words across lanes come from warp shuffles; no shared memory, no barriers.
-constexpr int kBandRows = 32;
+constexpr int kBandRows = 16;
+constexpr int kPrefetch = 4;     // input rows loaded ahead of use
 
 template <int WPL>
 struct RowW {
@@ -253,14 +254,24 @@ __global__ void __launch_bounds__(256) morph_rows_kernel(MorphArgs a) {
   Pass<R, false, WPL> p2, p3;
   Pass<R, true, WPL> p4;
   const int first = y0 - 4 * R, last = y_end + 4 * R;       // input rows [first, last)
-  for (int yi = first; yi < last; yi++) {
-    RowW<WPL> in;
-    const bool rin = yi >= 0 && yi < (int)H;
+  auto load_row = [&](int yy) {
+    RowW<WPL> r;
+    const bool rin = yy >= 0 && yy < (int)H;
 #pragma unroll
     for (int j = 0; j < WPL; j++) {
       const uint32_t k = (uint32_t)(lane * WPL + j);
-      in.w[j] = (rin && k < P) ? __ldg(Af + (uint64_t)yi * P + k) : 0u;
+      r.w[j] = (rin && k < P) ? __ldg(Af + (uint64_t)yy * P + k) : 0u;
     }
+    return r;
+  };
+  RowW<WPL> pre[kPrefetch];                                  // rows yi .. yi+kPrefetch-1
+#pragma unroll
+  for (int q = 0; q < kPrefetch; q++) pre[q] = load_row(first + q);
+  for (int yi = first; yi < last; yi++) {
+    const RowW<WPL> in = pre[0];
+#pragma unroll
+    for (int q = 0; q < kPrefetch - 1; q++) pre[q] = pre[q + 1];
+    pre[kPrefetch - 1] = load_row(yi + kPrefetch);
     RowW<WPL> o1, o2, o3, o4;
     if (!p1.push(in, o1)) continue;
     clean(o1, yi - R);

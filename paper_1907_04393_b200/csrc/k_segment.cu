@@ -142,22 +142,26 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
               ((uint32_t)lut_s[(w >> 16) & 0xFF] << 16) | ((uint32_t)lut_s[w >> 24] << 24);
     }
   } else {
-    uint32_t alo = 0, ahi = 0;
+    // four independent accumulator chains per weight set (ILP)
+    uint32_t alo[4] = {0, 0, 0, 0}, ahi[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 12; i++) {
-      alo = __dp4a(fr[i], kWlo[i % 3], alo);
-      ahi = __dp4a(fr[i], kWhi[i % 3], ahi);
+      alo[i & 3] = __dp4a(fr[i], kWlo[i % 3], alo[i & 3]);
+      ahi[i & 3] = __dp4a(fr[i], kWhi[i % 3], ahi[i & 3]);
     }
-    luma_acc += (ahi << 8) + alo;
+    luma_acc += (((ahi[0] + ahi[1]) + (ahi[2] + ahi[3])) << 8) + ((alo[0] + alo[1]) + (alo[2] + alo[3]));
   }
   // R1 envelope test on all 48 bytes, two bytes per 32-bit op
-  uint32_t ok = 0xFFFFFFFFu;
+  uint32_t okw[12];
 #pragma unroll
   for (int i = 0; i < 12; i++) {
     uint32_t tE, tO;
     r1_lanes(fr[i], e, i, tE, tO);
-    ok &= tE & tO;
+    okw[i] = tE & tO;
   }
+  // balanced AND tree (no serial dependency chain)
+  const uint32_t ok = ((okw[0] & okw[1] & okw[2]) & (okw[3] & okw[4] & okw[5])) &
+                      ((okw[6] & okw[7] & okw[8]) & (okw[9] & okw[10] & okw[11]));
   const bool all_inside = (ok & 0x01000100u) == 0x01000100u;
   if (!__any_sync(0xFFFFFFFFu, !all_inside)) return 0u;   // whole warp is background
 
