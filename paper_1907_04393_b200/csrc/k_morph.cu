@@ -172,20 +172,17 @@ __global__ void __launch_bounds__(256) morph_runs_kernel(MorphArgs a) {
 // y+R arrives, so pass 4 emits row y when input row y+4R is read.  Neighbour
 // words across lanes come from warp shuffles; no shared memory, no barriers.
 constexpr int kBandRows = 16;
-constexpr int kPrefetch = 4;     // input rows loaded ahead of use
 
 template <int WPL>
 struct RowW {
   uint32_t w[WPL];
 };
 
+// lmask / rmask: all-ones except 0 on lane 0 / lane 31 (no neighbour there)
 template <int R, bool kErode, int WPL>
-__device__ __forceinline__ RowW<WPL> hrow(const RowW<WPL>& in) {
-  const int lane = threadIdx.x & 31;
-  uint32_t left_nb = __shfl_up_sync(0xFFFFFFFFu, in.w[WPL - 1], 1);
-  uint32_t right_nb = __shfl_down_sync(0xFFFFFFFFu, in.w[0], 1);
-  if (lane == 0) left_nb = 0u;
-  if (lane == 31) right_nb = 0u;
+__device__ __forceinline__ RowW<WPL> hrow(const RowW<WPL>& in, uint32_t lmask, uint32_t rmask) {
+  const uint32_t left_nb = __shfl_up_sync(0xFFFFFFFFu, in.w[WPL - 1], 1) & lmask;
+  const uint32_t right_nb = __shfl_down_sync(0xFFFFFFFFu, in.w[0], 1) & rmask;
   RowW<WPL> o;
 #pragma unroll
   for (int j = 0; j < WPL; j++) {
@@ -204,19 +201,24 @@ __device__ __forceinline__ RowW<WPL> hrow(const RowW<WPL>& in) {
   return o;
 }
 
+// One pass of the pipeline: the last 2R+1 horizontally processed input rows
+// are kept as a set (AND / OR are commutative), row yi in slot yi mod (2R+1),
+// so with the row loop unrolled by 2R+1 every slot index is static.
 template <int R, bool kErode, int WPL>
 struct Pass {
-  RowW<WPL> win[2 * R + 1];     // horizontally processed input rows y-2R .. y
-  int filled = 0;
+  RowW<WPL> win[2 * R + 1];
 
-  // push input row (already zero outside the frame); returns true when an
-  // output row (the centre of the window) is available in `out`.
-  __device__ __forceinline__ bool push(const RowW<WPL>& in, RowW<WPL>& out) {
+  __device__ __forceinline__ void init() {
 #pragma unroll
-    for (int i = 0; i < 2 * R; i++) win[i] = win[i + 1];
-    win[2 * R] = hrow<R, kErode, WPL>(in);
-    if (filled < 2 * R + 1) filled++;
-    if (filled < 2 * R + 1) return false;
+    for (int i = 0; i < 2 * R + 1; i++)
+#pragma unroll
+      for (int j = 0; j < WPL; j++) win[i].w[j] = 0u;
+  }
+
+  template <int SLOT>
+  __device__ __forceinline__ RowW<WPL> push(const RowW<WPL>& in, uint32_t lm, uint32_t rm) {
+    win[SLOT] = hrow<R, kErode, WPL>(in, lm, rm);
+    RowW<WPL> out;
 #pragma unroll
     for (int j = 0; j < WPL; j++) {
       uint32_t acc = win[0].w[j];
@@ -224,70 +226,80 @@ struct Pass {
       for (int i = 1; i <= 2 * R; i++) acc = kErode ? (acc & win[i].w[j]) : (acc | win[i].w[j]);
       out.w[j] = acc;
     }
-    return true;
+    return out;
   }
 };
 
 template <int R, int WPL>
-__global__ void __launch_bounds__(256) morph_rows_kernel(MorphArgs a) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t f = blockIdx.y;
-  const int y0 = (int)((blockIdx.x * 8 + warp) * kBandRows);
-  const uint32_t H = a.H, P = a.P;
-  if (y0 >= (int)H) return;
-  const int y_end = min((int)H, y0 + kBandRows);
-  const uint32_t lastmask = (a.W & 31u) ? ((1u << (a.W & 31u)) - 1u) : 0xFFFFFFFFu;
-  const uint32_t* Af = a.A + (uint64_t)f * H * P;
-  uint32_t* Of = a.O + (uint64_t)f * H * P;
-  Run* runs = a.runs + (uint64_t)f * a.cap_runs;
-
-  auto clean = [&](RowW<WPL>& r, int y) {          // zero padding outside the frame
-    const bool in = y >= 0 && y < (int)H;
-#pragma unroll
-    for (int j = 0; j < WPL; j++) {
-      const uint32_t k = (uint32_t)(lane * WPL + j);
-      r.w[j] = (in && k < P) ? (k == P - 1 ? (r.w[j] & lastmask) : r.w[j]) : 0u;
-    }
-  };
-
+struct MorphPipe {
+  const MorphArgs& a;
+  uint32_t f, H, P, lastmask;
+  int y0, y_end, lane;
+  uint32_t lmask, rmask, wmask[WPL];       // lane-edge masks, valid bits of each word
+  const uint32_t* Af;
+  uint32_t* Of;
+  Run* runs;
   Pass<R, true, WPL> p1;
   Pass<R, false, WPL> p2, p3;
   Pass<R, true, WPL> p4;
-  const int first = y0 - 4 * R, last = y_end + 4 * R;       // input rows [first, last)
-  auto load_row = [&](int yy) {
-    RowW<WPL> r;
-    const bool rin = yy >= 0 && yy < (int)H;
+  RowW<WPL> pre[2 * R + 1];                // prefetched input rows yi .. yi + 2R
+
+  __device__ __forceinline__ MorphPipe(const MorphArgs& args, uint32_t frame, int band0)
+      : a(args), f(frame), H(args.H), P(args.P), y0(band0) {
+    lane = threadIdx.x & 31;
+    y_end = min((int)H, y0 + kBandRows);
+    lastmask = (a.W & 31u) ? ((1u << (a.W & 31u)) - 1u) : 0xFFFFFFFFu;
+    lmask = lane == 0 ? 0u : 0xFFFFFFFFu;
+    rmask = lane == 31 ? 0u : 0xFFFFFFFFu;
 #pragma unroll
     for (int j = 0; j < WPL; j++) {
       const uint32_t k = (uint32_t)(lane * WPL + j);
-      r.w[j] = (rin && k < P) ? __ldg(Af + (uint64_t)yy * P + k) : 0u;
+      wmask[j] = k < P ? (k == P - 1 ? lastmask : 0xFFFFFFFFu) : 0u;
     }
+    Af = a.A + (uint64_t)f * H * P;
+    Of = a.O + (uint64_t)f * H * P;
+    runs = a.runs + (uint64_t)f * a.cap_runs;
+    p1.init(); p2.init(); p3.init(); p4.init();
+  }
+
+  __device__ __forceinline__ RowW<WPL> load_row(int yy) const {
+    RowW<WPL> r;
+    const bool rin = yy >= 0 && yy < (int)H;
+    const uint32_t* row = Af + (uint64_t)(rin ? yy : 0) * P + (uint32_t)lane * WPL;
+#pragma unroll
+    for (int j = 0; j < WPL; j++)
+      r.w[j] = (rin && wmask[j]) ? __ldg(row + j) : 0u;
     return r;
-  };
-  RowW<WPL> pre[kPrefetch];                                  // rows yi .. yi+kPrefetch-1
+  }
+
+  __device__ __forceinline__ void clean(RowW<WPL>& r, int y) const {   // zero padding
+    const uint32_t rowm = (y >= 0 && y < (int)H) ? 0xFFFFFFFFu : 0u;
 #pragma unroll
-  for (int q = 0; q < kPrefetch; q++) pre[q] = load_row(first + q);
-  for (int yi = first; yi < last; yi++) {
-    const RowW<WPL> in = pre[0];
-#pragma unroll
-    for (int q = 0; q < kPrefetch - 1; q++) pre[q] = pre[q + 1];
-    pre[kPrefetch - 1] = load_row(yi + kPrefetch);
-    RowW<WPL> o1, o2, o3, o4;
-    if (!p1.push(in, o1)) continue;
-    clean(o1, yi - R);
-    if (!p2.push(o1, o2)) continue;
-    clean(o2, yi - 2 * R);
-    if (!p3.push(o2, o3)) continue;
-    clean(o3, yi - 3 * R);
-    if (!p4.push(o3, o4)) continue;
+    for (int j = 0; j < WPL; j++) r.w[j] &= wmask[j] & rowm;
+  }
+
+  // input row yi (slot = yi - first mod 2R+1); emits output row yi - 4R
+  template <int SLOT>
+  __device__ __forceinline__ void step(int yi) {
+    const RowW<WPL> in = pre[SLOT];
+    pre[SLOT] = load_row(yi + 2 * R + 1);
+    RowW<WPL> o = p1.template push<SLOT>(in, lmask, rmask);
+    clean(o, yi - R);
+    o = p2.template push<SLOT>(o, lmask, rmask);
+    clean(o, yi - 2 * R);
+    o = p3.template push<SLOT>(o, lmask, rmask);
+    clean(o, yi - 3 * R);
+    o = p4.template push<SLOT>(o, lmask, rmask);
     const int yo = yi - 4 * R;
-    if (yo < y0 || yo >= y_end) continue;
-    clean(o4, yo);
-    // write O and extract the row's runs
-    uint32_t prev_last = __shfl_up_sync(0xFFFFFFFFu, o4.w[WPL - 1], 1);
-    uint32_t next_first = __shfl_down_sync(0xFFFFFFFFu, o4.w[0], 1);
-    if (lane == 0) prev_last = 0u;
-    if (lane == 31) next_first = 0u;
+    if (yo >= y0 && yo < y_end) {
+      clean(o, yo);
+      emit(o, yo);
+    }
+  }
+
+  __device__ __forceinline__ void emit(const RowW<WPL>& o4, int yo) {
+    const uint32_t prev_last = __shfl_up_sync(0xFFFFFFFFu, o4.w[WPL - 1], 1) & lmask;
+    const uint32_t next_first = __shfl_down_sync(0xFFFFFFFFu, o4.w[0], 1) & rmask;
     uint32_t st[WPL], en[WPL], ns = 0, ne = 0;
 #pragma unroll
     for (int j = 0; j < WPL; j++) {
@@ -308,7 +320,7 @@ __global__ void __launch_bounds__(256) morph_rows_kernel(MorphArgs a) {
       a.row_cnt[(uint64_t)f * H + yo] = cnt;
       a.row_base[(uint64_t)f * H + yo] = base;
     }
-    if (!cnt) continue;
+    if (cnt == 0) return;
     base = __shfl_sync(0xFFFFFFFFu, base, 0);
     uint32_t ps = ns, pe = ne;
 #pragma unroll
@@ -337,6 +349,27 @@ __global__ void __launch_bounds__(256) morph_rows_kernel(MorphArgs a) {
       }
     }
   }
+};
+
+template <int R, int WPL, int SLOT>
+__device__ __forceinline__ void unrolled_steps(MorphPipe<R, WPL>& mp, int yi, int last) {
+  if constexpr (SLOT < 2 * R + 1) {
+    if (yi + SLOT < last) mp.template step<SLOT>(yi + SLOT);
+    unrolled_steps<R, WPL, SLOT + 1>(mp, yi, last);
+  }
+}
+
+// One warp per CTA (the band depends on blockIdx only, so every branch is
+// warp-uniform and shuffles need no divergence handling).
+template <int R, int WPL>
+__global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
+  const int y0 = (int)(blockIdx.x * kBandRows);
+  if (y0 >= (int)a.H) return;
+  MorphPipe<R, WPL> mp(a, blockIdx.y, y0);
+  const int first = y0 - 4 * R, last = mp.y_end + 4 * R;     // input rows [first, last)
+#pragma unroll
+  for (int q = 0; q < 2 * R + 1; q++) mp.pre[q] = mp.load_row(first + q);
+  for (int yi = first; yi < last; yi += 2 * R + 1) unrolled_steps<R, WPL, 0>(mp, yi, last);
 }
 
 uint32_t morph_tile_rows(const Ctx& c, size_t smem_budget) {
@@ -371,8 +404,8 @@ cudaError_t launch_morph(Ctx& c, uint32_t n, cudaStream_t st) {
   const uint32_t r = c.p.se_radius;
   cudaMemsetAsync(c.frame_runs, 0, n * sizeof(uint32_t), st);
   if (c.P <= 128 && r <= 4) {
-    const dim3 grid((c.H + 8 * kBandRows - 1) / (8 * kBandRows), n);
-#define FIZI_MORPH_ROWS(RR, WW) morph_rows_kernel<RR, WW><<<grid, 256, 0, st>>>(a)
+    const dim3 grid((c.H + kBandRows - 1) / kBandRows, n);
+#define FIZI_MORPH_ROWS(RR, WW) morph_rows_kernel<RR, WW><<<grid, 32, 0, st>>>(a)
 #define FIZI_MORPH_WPL(RR)                                    \
     if (c.P <= 32) FIZI_MORPH_ROWS(RR, 1);                    \
     else if (c.P <= 64) FIZI_MORPH_ROWS(RR, 2);               \

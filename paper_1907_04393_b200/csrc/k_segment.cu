@@ -207,14 +207,16 @@ template <int kMinBlocks>
 __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   extern __shared__ __align__(128) uint8_t sm[];          // 8 warps x kWarpStages chunks
   __shared__ __align__(8) uint64_t bar[kWarpsPerCta][kWarpStages];
-  __shared__ unsigned long long acc_y[kFrameGroup];
-  __shared__ uint32_t acc_f[kFrameGroup], done[kFrameGroup];
+  // per-frame partial sums of the CTA: luma <= 8 warps * 512 px * 255000 < 2^32
+  __shared__ uint32_t acc_y[kFrameGroup], acc_f[kFrameGroup], done[kFrameGroup];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t tile = blockIdx.x, grp = blockIdx.y;
   const uint32_t f_begin = a.group_off[grp];
   const uint32_t nf = a.group_off[grp + 1] - f_begin;
-  const uint32_t stream = a.frame_stream[a.group_frames[f_begin]];
+  // frame ids of the group, lane i holds frame i (nf <= kFrameGroup <= 32)
+  const uint32_t fid_lane = (uint32_t)lane < nf ? a.group_frames[f_begin + lane] : 0u;
+  const uint32_t stream = a.frame_stream[__shfl_sync(0xFFFFFFFFu, fid_lane, 0)];
   const uint32_t c = tile * kWarpsPerCta + warp;
   const uint32_t n_active = min((uint32_t)kWarpsPerCta, a.nchunks - tile * kWarpsPerCta);
   if (tid < kFrameGroup) { acc_y[tid] = 0; acc_f[tid] = 0; done[tid] = 0; }
@@ -226,6 +228,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   const bool valid = 48u * lane < cbytes;
   uint8_t* ring = sm + (uint32_t)warp * kWarpStages * kChunkBytes;
   uint64_t* wbar = bar[warp];
+  const uint8_t* src0 = a.frames + coff;
+  uint32_t* dstw = a.bitA + (uint64_t)c * 16 + (lane >> 1);
 
   EnvRegs e;
   if (valid) {
@@ -241,46 +245,47 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
 #pragma unroll
     for (int s = 0; s < kWarpStages; s++) mbar_init(&wbar[s], 1);
     fence_mbar_init();
-    for (uint32_t s = 0; s < nf && s < (uint32_t)kWarpStages; s++) {
-      const uint32_t f = a.group_frames[f_begin + s];
-      mbar_arrive_expect_tx(&wbar[s], cbytes);
-      bulk_g2s(ring + s * kChunkBytes, a.frames + (uint64_t)f * a.frame_bytes + coff, cbytes,
-               &wbar[s], pol);
-    }
   }
   __syncwarp();
+#pragma unroll
+  for (int s = 0; s < kWarpStages; s++) {
+    const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, s);
+    if (lane == 0 && (uint32_t)s < nf) {
+      mbar_arrive_expect_tx(&wbar[s], cbytes);
+      bulk_g2s(ring + s * kChunkBytes, src0 + (uint64_t)f * a.frame_bytes, cbytes, &wbar[s], pol);
+    }
+  }
 
   for (uint32_t i = 0; i < nf; i++) {
     const uint32_t s = i % kWarpStages;
+    const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
+    const uint32_t fn = __shfl_sync(0xFFFFFFFFu, fid_lane, (i + kWarpStages) & 31);
     mbar_wait(&wbar[s], (i / kWarpStages) & 1u);
-    const uint32_t f = a.group_frames[f_begin + i];
     uint32_t y = 0;
     const uint32_t bits = seg16<false>(ring + s * kChunkBytes + 48 * lane, e, valid, nullptr,
                                        (int)a.S, (int)a.a1, (int)a.a2, y);
     __syncwarp();                                           // chunk buffer s consumed
     if (lane == 0 && i + kWarpStages < nf) {
-      const uint32_t fn = a.group_frames[f_begin + i + kWarpStages];
       mbar_arrive_expect_tx(&wbar[s], cbytes);
-      bulk_g2s(ring + s * kChunkBytes, a.frames + (uint64_t)fn * a.frame_bytes + coff, cbytes,
-               &wbar[s], pol);
+      bulk_g2s(ring + s * kChunkBytes, src0 + (uint64_t)fn * a.frame_bytes, cbytes, &wbar[s], pol);
     }
     const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
     uint32_t pc = 0;
     if (!(lane & 1) && valid) {
-      a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = word;
+      dstw[(uint64_t)f * a.words_per_frame] = word;
       pc = __popc(word);
     }
     y = warp_sum_u32(y);
     pc = warp_sum_u32(pc);
     if (lane == 0) {
-      atomicAdd(&acc_y[i], (unsigned long long)y);
+      atomicAdd(&acc_y[i], y);
       if (pc) atomicAdd(&acc_f[i], pc);
       __threadfence_block();
       if (atomicAdd(&done[i], 1u) == n_active - 1) {         // last warp of this frame
         __threadfence_block();
-        const unsigned long long sy = atomicAdd(&acc_y[i], 0ull);
+        const uint32_t sy = atomicAdd(&acc_y[i], 0u);
         const uint32_t sf = atomicAdd(&acc_f[i], 0u);
-        atomicAdd(&a.luma[f], sy);
+        atomicAdd(&a.luma[f], (unsigned long long)sy);
         if (sf) atomicAdd(&a.fg[f], sf);
       }
     }
