@@ -3,7 +3,9 @@
 //   segment (a2+a3) -> morphology (a4) -> labelling + filter + blob (a5-a7)
 //   -> final u8 mask (a6 output) -> Mouse fold (a8)
 // on the caller's CUDA stream.  No pixel is touched on the host.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -134,14 +136,25 @@ void free_all(Ctx& c) {
     if (p) cudaFree(p);
   if (c.pinned) cudaFreeHost(c.pinned);
   if (c.pinned_ev) cudaEventDestroy(c.pinned_ev);
+  for (auto ev : c.ev_seg)
+    if (ev) cudaEventDestroy(ev);
+  if (c.ev_join) cudaEventDestroy(c.ev_join);
+  if (c.side) cudaStreamDestroy(c.side);
   for (auto& r : c.prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c.prof_free) cudaEventDestroy(e);
   if (c.prof_open) cudaEventDestroy(c.prof_open);
 }
 
+struct SubBatch {
+  uint32_t f0, n, g0, ng;
+};
+
 // Upload the per-call frame table (timestamps, streams, same-stream groups).
-int upload_call(Ctx& c, const uint32_t* sof, const int64_t* t, uint32_t n, uint32_t* n_groups,
-                cudaStream_t st) {
+// Frames are cut into sub-batches of c.sub_frames (at most kMaxSub); inside a
+// sub-batch, groups are the frames of one stream in index order, split every
+// kFrameGroup frames.
+int upload_call(Ctx& c, const uint32_t* sof, const int64_t* t, uint32_t n,
+                std::vector<SubBatch>& subs, cudaStream_t st) {
   const uint32_t mb = c.max_batch;
   cudaError_t e = cudaEventSynchronize(c.pinned_ev);      // previous upload consumed
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventSynchronize");
@@ -153,24 +166,31 @@ int upload_call(Ctx& c, const uint32_t* sof, const int64_t* t, uint32_t n, uint3
     ht[i] = t ? t[i] : 0;
     hs[i] = sof[i];
   }
-  // groups: streams in order of first appearance, frames in index order,
-  // split every kFrameGroup frames
+  uint32_t sb = c.sub_frames;
+  if ((n + sb - 1) / sb > fizi::kMaxSub) sb = (n + fizi::kMaxSub - 1) / fizi::kMaxSub;
+  subs.clear();
   std::vector<uint8_t> seen(c.n_streams, 0);
   uint32_t pos = 0, g = 0;
-  for (uint32_t i = 0; i < n; i++) {
-    const uint32_t s = sof[i];
-    if (seen[s]) continue;
-    seen[s] = 1;
-    uint32_t in_group = 0;
-    for (uint32_t j = i; j < n; j++) {
-      if (sof[j] != s) continue;
-      if (in_group == 0) ho[g++] = pos;
-      hg[pos++] = j;
-      if (++in_group == (uint32_t)fizi::kFrameGroup) in_group = 0;
+  for (uint32_t f0 = 0; f0 < n; f0 += sb) {
+    const uint32_t f1 = std::min(n, f0 + sb);
+    SubBatch b{f0, f1 - f0, g, 0};
+    for (uint32_t i = f0; i < f1; i++) seen[sof[i]] = 0;
+    for (uint32_t i = f0; i < f1; i++) {
+      const uint32_t s = sof[i];
+      if (seen[s]) continue;
+      seen[s] = 1;
+      uint32_t in_group = 0;
+      for (uint32_t j = i; j < f1; j++) {
+        if (sof[j] != s) continue;
+        if (in_group == 0) ho[g++] = pos;
+        hg[pos++] = j;
+        if (++in_group == (uint32_t)fizi::kFrameGroup) in_group = 0;
+      }
     }
+    b.ng = g - b.g0;
+    subs.push_back(b);
   }
   ho[g] = pos;
-  *n_groups = g;
   const size_t bytes = (size_t)mb * 8 + (size_t)mb * 4 * 2 + (size_t)(mb + 1) * 4;
   e = cudaMemcpyAsync(c.frame_t, c.pinned, bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemcpyAsync(call table)");
@@ -196,40 +216,64 @@ int check_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, u
   return FIZI_OK;
 }
 
+// Launch sequence of one call.  Sub-batch k's fused segmentation runs on the
+// caller's stream; its tail (a2 finalisation + LUT re-test, a4 morphology,
+// a5-a7 labelling, the u8 mask, a8 fold) runs on the context's side stream,
+// overlapping segmentation of sub-batch k+1.  The caller's stream waits for
+// the side stream before the call returns, so outputs are ordered on it.
 int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, const int64_t* t,
              uint8_t* masks, fizi_result* res, bool track, cudaStream_t st) {
-  uint32_t n_groups = 0;
-  int rc = upload_call(c, sof, t, n, &n_groups, st);
+  std::vector<SubBatch> subs;
+  int rc = upload_call(c, sof, t, n, subs, st);
   if (rc) return rc;
-  cudaError_t e = fizi::launch_segment(c, frames, n, n_groups, res, st);
-  if (e != cudaSuccess) return cuda_fail(c, e, "segment");
-  prof_begin(c, st);
-  e = fizi::launch_morph(c, n, st);
-  prof_end(c, FIZI_PROF_MORPH, st);
-  if (e != cudaSuccess) return cuda_fail(c, e, "morph");
-  if (c.p.debug) {
-    e = cudaMemcpyAsync(c.bitOC, c.bitO, (size_t)n * c.H * c.P * 4, cudaMemcpyDeviceToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(c, e, "debug copy");
+  cudaError_t e = cudaMemsetAsync(c.luma, 0, sizeof(unsigned long long) * n, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c.fg, 0, sizeof(uint32_t) * n, st);
+  for (size_t k = 0; k < subs.size() && e == cudaSuccess; k++)
+    e = cudaMemsetAsync(c.fix_count + k * (c.max_batch + 1), 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "memset");
+  bool single = true;
+  for (uint32_t i = 1; i < n && single; i++) single = sof[i] == sof[0];
+  cudaStream_t sd = c.side;
+  for (size_t k = 0; k < subs.size(); k++) {
+    const SubBatch& b = subs[k];
+    e = fizi::launch_seg_main(c, frames, b.f0, b.n, b.g0, b.ng, (uint32_t)k, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "segment");
+    e = cudaEventRecord(c.ev_seg[k], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, c.ev_seg[k], 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "event");
+    e = fizi::launch_seg_fix(c, frames, b.f0, b.n, (uint32_t)k, res, sd);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
+    prof_begin(c, sd);
+    e = fizi::launch_morph(c, b.f0, b.n, sd);
+    prof_end(c, FIZI_PROF_MORPH, sd);
+    if (e != cudaSuccess) return cuda_fail(c, e, "morph");
+    if (c.p.debug) {
+      const size_t w = (size_t)c.H * c.P;
+      e = cudaMemcpyAsync(c.bitOC + b.f0 * w, c.bitO + b.f0 * w, (size_t)b.n * w * 4,
+                          cudaMemcpyDeviceToDevice, sd);
+      if (e != cudaSuccess) return cuda_fail(c, e, "debug copy");
+    }
+    prof_begin(c, sd);
+    e = fizi::launch_ccl(c, b.f0, b.n, res, sd);
+    prof_end(c, FIZI_PROF_CCL, sd);
+    if (e != cudaSuccess) return cuda_fail(c, e, "ccl");
+    if (masks) {
+      prof_begin(c, sd);
+      e = fizi::launch_expand(c, b.f0, b.n, masks, sd);
+      prof_end(c, FIZI_PROF_EXPAND, sd);
+      if (e != cudaSuccess) return cuda_fail(c, e, "expand");
+    }
+    if (track) {
+      prof_begin(c, sd);
+      e = single ? fizi::launch_track_stream(c, sof[0], res + b.f0, b.n, sd)
+                 : fizi::launch_track_batch(c, b.f0, b.n, res, sd);
+      prof_end(c, FIZI_PROF_TRACK, sd);
+      if (e != cudaSuccess) return cuda_fail(c, e, "track");
+    }
   }
-  prof_begin(c, st);
-  e = fizi::launch_ccl(c, n, res, st);
-  prof_end(c, FIZI_PROF_CCL, st);
-  if (e != cudaSuccess) return cuda_fail(c, e, "ccl");
-  if (masks) {
-    prof_begin(c, st);
-    e = fizi::launch_expand(c, n, masks, st);
-    prof_end(c, FIZI_PROF_EXPAND, st);
-    if (e != cudaSuccess) return cuda_fail(c, e, "expand");
-  }
-  if (track) {
-    bool single = true;
-    for (uint32_t i = 1; i < n && single; i++) single = sof[i] == sof[0];
-    prof_begin(c, st);
-    e = single ? fizi::launch_track_stream(c, sof[0], res, n, st)
-               : fizi::launch_track_batch(c, n, res, st);
-    prof_end(c, FIZI_PROF_TRACK, st);
-    if (e != cudaSuccess) return cuda_fail(c, e, "track");
-  }
+  e = cudaEventRecord(c.ev_join, sd);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c.ev_join, 0);
+  if (e != cudaSuccess) return cuda_fail(c, e, "join");
   c.last_frames = frames;
   c.last_n = n;
   return FIZI_OK;
@@ -339,10 +383,15 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.stats, mb * c.cap_runs * sizeof(fizi::RootStats)));
   const size_t table_bytes = mb * 8 + mb * 4 * 2 + (mb + 1) * 4;
   A(dalloc(&c.frame_t, table_bytes));
-  A(dalloc(&c.fix_count, (mb + 1) * 4));
+  A(dalloc(&c.fix_count, (uint64_t)fizi::kMaxSub * (mb + 1) * 4));
   A(dalloc(&c.tstate, (uint64_t)n_streams * sizeof(fizi::TrackState)));
   if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned), table_bytes);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.pinned_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking);
+  for (uint32_t k = 0; k < fizi::kMaxSub && e == cudaSuccess; k++)
+    e = cudaEventCreateWithFlags(&c.ev_seg[k], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming);
+  if (const char* sf = getenv("FIZI_SUB_FRAMES")) c.sub_frames = (uint32_t)atoi(sf) > 0 ? (uint32_t)atoi(sf) : 16;
   if (e != cudaSuccess) {
     cudaGetLastError();
     free_all(c);

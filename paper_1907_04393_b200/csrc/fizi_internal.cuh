@@ -25,11 +25,12 @@ constexpr int kChunkPx = 512;            // pixels per warp-chunk in the fused k
 constexpr int kChunkBytes = 3 * kChunkPx;
 constexpr int kWarpsPerCta = 8;          // chunks per CTA tile
 constexpr int kTileBytes = kChunkBytes * kWarpsPerCta;   // 12 KiB frame bytes per tile
-constexpr int kFrameGroup = 16;          // frames sharing one envelope load
-constexpr int kWarpStages = 6;           // per-warp bulk-copy ring depth (frames)
+constexpr int kFrameGroup = 32;          // frames sharing one envelope load (<= 32)
+constexpr int kWarpStages = 8;           // per-warp bulk-copy ring depth (frames, power of 2)
 constexpr int kMaxRadius = 8;
 constexpr size_t kMorphSmem = 200 * 1024;  // dynamic smem budget of the morphology CTA
-constexpr uint32_t kCclSmemRuns = 16384;    // runs labelled in shared memory (else global)
+constexpr uint32_t kCclSmemRuns = 4096;     // runs labelled in shared memory (else global)
+constexpr uint32_t kMaxSub = 8;             // sub-batches per call (stream pipeline)
 
 struct Run {                             // one horizontal run of foreground pixels
   uint16_t x0, x1, y, pad;
@@ -79,8 +80,12 @@ struct Ctx {
   int64_t* frame_t = nullptr;            // max_batch (start of the per-call table)
   uint32_t* group_frames = nullptr;      // max_batch (frame ids ordered by group)
   uint32_t* group_off = nullptr;         // max_batch + 1
-  uint32_t* fix_count = nullptr;         // 1 + max_batch (count, list of corrected frames)
+  uint32_t* fix_count = nullptr;         // kMaxSub x (1 + max_batch): per sub-batch count + list
   uint8_t* tstate = nullptr;             // n_streams tracker states
+  cudaStream_t side = nullptr;           // internal stream for the per-sub-batch tail
+  cudaEvent_t ev_seg[kMaxSub] = {};      // segment(k) done on the caller's stream
+  cudaEvent_t ev_join = nullptr;         // tail of the call done on the side stream
+  uint32_t sub_frames = 16;              // frames per sub-batch
   uint8_t* stage_frames = nullptr;       // device staging for fizi_process_frames_host
   uint8_t* stage_masks = nullptr;
   fizi_result* stage_results = nullptr;
@@ -131,15 +136,17 @@ cudaError_t launch_learn(Ctx& c, uint32_t stream, const uint8_t* frames, uint32_
                          uint32_t margin, cudaStream_t st);
 cudaError_t launch_env_export(Ctx& c, uint32_t stream, uint8_t* lo, uint8_t* hi, bool import,
                               const uint8_t* ilo, const uint8_t* ihi, cudaStream_t st);
-cudaError_t launch_segment(Ctx& c, const uint8_t* frames, uint32_t n, uint32_t n_groups,
+cudaError_t launch_seg_main(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t g0,
+                            uint32_t ng, uint32_t sub, cudaStream_t st);
+cudaError_t launch_seg_fix(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t sub,
                            fizi_result* res, cudaStream_t st);
 // the segment launcher marks the SEGMENT -> FIXUP boundary through this hook
 void prof_begin(Ctx& c, cudaStream_t st);
 void prof_end(Ctx& c, int slot, cudaStream_t st);
-cudaError_t launch_morph(Ctx& c, uint32_t n, cudaStream_t st);
-cudaError_t launch_ccl(Ctx& c, uint32_t n, fizi_result* res, cudaStream_t st);
-cudaError_t launch_expand(Ctx& c, uint32_t n, uint8_t* masks, cudaStream_t st);
-cudaError_t launch_track_batch(Ctx& c, uint32_t n, fizi_result* res, cudaStream_t st);
+cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, cudaStream_t st);
+cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st);
+cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st);
+cudaError_t launch_track_batch(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st);
 cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,
                                 cudaStream_t st);
 cudaError_t launch_tstate_reset(Ctx& c, uint32_t first, uint32_t count, cudaStream_t st);

@@ -29,6 +29,7 @@
 namespace fizi {
 
 struct CclArgs {
+  uint32_t f0;
   uint32_t* O;
   uint32_t W, H, P;
   uint64_t N;
@@ -265,7 +266,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
 
 __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   extern __shared__ __align__(16) uint8_t smc[];
-  const uint32_t f = blockIdx.x;
+  const uint32_t f = a.f0 + blockIdx.x;
   const uint32_t T = a.frame_runs[f];
   if (T <= kCclSmemRuns) {
     Run* R = reinterpret_cast<Run*>(smc);
@@ -285,8 +286,9 @@ cudaError_t init_ccl(Ctx& c) {
                               (int)kCclSmem);
 }
 
-cudaError_t launch_ccl(Ctx& c, uint32_t n, fizi_result* res, cudaStream_t st) {
+cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st) {
   CclArgs a;
+  a.f0 = f0;
   a.O = c.bitO;
   a.W = c.W; a.H = c.H; a.P = c.P;
   a.N = c.N;
@@ -348,8 +350,8 @@ cudaError_t launch_expand_from(Ctx& c, const uint32_t* bits, uint32_t n, uint8_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_expand(Ctx& c, uint32_t n, uint8_t* masks, cudaStream_t st) {
-  return launch_expand_from(c, c.bitO, n, masks, st);
+cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st) {
+  return launch_expand_from(c, c.bitO + (uint64_t)f0 * c.H * c.P, n, masks + (uint64_t)f0 * c.N, st);
 }
 
 }  // namespace fizi

@@ -22,6 +22,7 @@
 namespace fizi {
 
 struct MorphArgs {
+  uint32_t f0;                  // first frame of the launch (sub-batch)
   const uint32_t* A;
   uint32_t* O;
   uint32_t W, H, P, TR;
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(256) morph_runs_kernel(MorphArgs a) {
   const uint32_t rows = TR + 8 * R;
   uint32_t* b0 = sm;
   uint32_t* b1 = sm + rows * P;
-  const uint32_t f = blockIdx.y;
+  const uint32_t f = a.f0 + blockIdx.y;
   const int y0 = (int)(blockIdx.x * TR);
   const int ybase = y0 - 4 * R;
   const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -365,7 +366,7 @@ template <int R, int WPL>
 __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
   const int y0 = (int)(blockIdx.x * kBandRows);
   if (y0 >= (int)a.H) return;
-  MorphPipe<R, WPL> mp(a, blockIdx.y, y0);
+  MorphPipe<R, WPL> mp(a, a.f0 + blockIdx.y, y0);
   const int first = y0 - 4 * R, last = mp.y_end + 4 * R;     // input rows [first, last)
 #pragma unroll
   for (int q = 0; q < 2 * R + 1; q++) mp.pre[q] = mp.load_row(first + q);
@@ -391,8 +392,9 @@ static void launch_r(const MorphArgs& a, uint32_t n, size_t smem, cudaStream_t s
   morph_runs_kernel<R><<<dim3((a.H + a.TR - 1) / a.TR, n), 256, smem, st>>>(a);
 }
 
-cudaError_t launch_morph(Ctx& c, uint32_t n, cudaStream_t st) {
+cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, cudaStream_t st) {
   MorphArgs a;
+  a.f0 = f0;
   a.A = c.bitA;
   a.O = c.bitO;
   a.W = c.W; a.H = c.H; a.P = c.P; a.TR = c.morph_tr;
@@ -402,7 +404,7 @@ cudaError_t launch_morph(Ctx& c, uint32_t n, cudaStream_t st) {
   a.frame_runs = c.frame_runs;
   a.runs = c.runs;
   const uint32_t r = c.p.se_radius;
-  cudaMemsetAsync(c.frame_runs, 0, n * sizeof(uint32_t), st);
+  cudaMemsetAsync(c.frame_runs + f0, 0, n * sizeof(uint32_t), st);
   if (c.P <= 128 && r <= 4) {
     const dim3 grid((c.H + kBandRows - 1) / kBandRows, n);
 #define FIZI_MORPH_ROWS(RR, WW) morph_rows_kernel<RR, WW><<<grid, 32, 0, st>>>(a)

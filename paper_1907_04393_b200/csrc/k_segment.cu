@@ -46,6 +46,7 @@ struct SegArgs {
   const uint8_t* lut_table;
   const uint32_t* fix;          // [0] = count, [1..] = frame ids needing a LUT
   uint32_t S, a1, a2;
+  uint32_t f0, n;               // frame range of this launch (sub-batch)
 };
 
 // Rec.601 weights split so every dp4a weight fits a byte:
@@ -181,6 +182,9 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
     const uint32_t w0 = fr[0], w1 = fr[1], w2 = fr[2];
     const uint32_t in12 = (uint32_t)(inside >> (12 * g)) & 0xFFFu;
 #pragma unroll
+    for (int i = 0; i < 9; i++) fr[i] = fr[i + 3];
+    if (in12 == 0xFFFu) continue;                  // 4 background pixels: R1 = 0
+#pragma unroll
     for (int q = 0; q < 4; q++) {
       const int b = 3 * q;                            // byte offset within the 3 words
       auto byte = [&](int bb) -> int {
@@ -190,8 +194,6 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
       const uint32_t r1 = ((in12 >> b) & 7u) != 7u;
       bits |= (r1 & gray_and_skin(byte(b), byte(b + 1), byte(b + 2), S, a1, a2)) << (4 * g + q);
     }
-#pragma unroll
-    for (int i = 0; i < 9; i++) fr[i] = fr[i + 3];
   }
   return valid ? bits : 0u;
 }
@@ -203,12 +205,17 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
 // consumed frame i, so warps never wait for each other.  Per-frame sums go
 // to shared-memory accumulators; the last warp to finish a frame flushes
 // them to global memory with one atomic each.
+__device__ __forceinline__ void seg_warp(const SegArgs& a, uint32_t c, int lane, int warp,
+                                         uint32_t nf, uint32_t fid_lane, uint32_t stream,
+                                         uint8_t* sm, uint64_t* wbar, uint32_t* acc_y,
+                                         uint32_t* acc_f);
+
 template <int kMinBlocks>
 __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   extern __shared__ __align__(128) uint8_t sm[];          // 8 warps x kWarpStages chunks
   __shared__ __align__(8) uint64_t bar[kWarpsPerCta][kWarpStages];
   // per-frame partial sums of the CTA: luma <= 8 warps * 512 px * 255000 < 2^32
-  __shared__ uint32_t acc_y[kFrameGroup], acc_f[kFrameGroup], done[kFrameGroup];
+  __shared__ uint32_t acc_y[kFrameGroup], acc_f[kFrameGroup];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t tile = blockIdx.x, grp = blockIdx.y;
@@ -218,16 +225,27 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   const uint32_t fid_lane = (uint32_t)lane < nf ? a.group_frames[f_begin + lane] : 0u;
   const uint32_t stream = a.frame_stream[__shfl_sync(0xFFFFFFFFu, fid_lane, 0)];
   const uint32_t c = tile * kWarpsPerCta + warp;
-  const uint32_t n_active = min((uint32_t)kWarpsPerCta, a.nchunks - tile * kWarpsPerCta);
-  if (tid < kFrameGroup) { acc_y[tid] = 0; acc_f[tid] = 0; done[tid] = 0; }
+  if (tid < kFrameGroup) { acc_y[tid] = 0; acc_f[tid] = 0; }
   __syncthreads();
-  if (c >= a.nchunks) return;                                // idle warps of the last tile
+  if (c < a.nchunks) seg_warp(a, c, lane, warp, nf, fid_lane, stream, sm, bar[warp], acc_y, acc_f);
+  __syncthreads();                                           // flush the CTA's sums
+  if (tid < (int)nf) {
+    const uint32_t f = a.group_frames[f_begin + tid];
+    atomicAdd(&a.luma[f], (unsigned long long)acc_y[tid]);
+    if (acc_f[tid]) atomicAdd(&a.fg[f], acc_f[tid]);
+  }
+}
+
+// One warp: its chunk over the nf frames of the group.
+__device__ __forceinline__ void seg_warp(const SegArgs& a, uint32_t c, int lane, int warp,
+                                         uint32_t nf, uint32_t fid_lane, uint32_t stream,
+                                         uint8_t* sm, uint64_t* wbar, uint32_t* acc_y,
+                                         uint32_t* acc_f) {
   const uint64_t coff = (uint64_t)c * kChunkBytes;
   const uint64_t rem = a.frame_bytes - coff;
   const uint32_t cbytes = rem < (uint64_t)kChunkBytes ? (uint32_t)rem : (uint32_t)kChunkBytes;
   const bool valid = 48u * lane < cbytes;
   uint8_t* ring = sm + (uint32_t)warp * kWarpStages * kChunkBytes;
-  uint64_t* wbar = bar[warp];
   const uint8_t* src0 = a.frames + coff;
   uint32_t* dstw = a.bitA + (uint64_t)c * 16 + (lane >> 1);
 
@@ -257,7 +275,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   }
 
   for (uint32_t i = 0; i < nf; i++) {
-    const uint32_t s = i % kWarpStages;
+    const uint32_t s = i & (kWarpStages - 1);
     const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
     const uint32_t fn = __shfl_sync(0xFFFFFFFFu, fid_lane, (i + kWarpStages) & 31);
     mbar_wait(&wbar[s], (i / kWarpStages) & 1u);
@@ -280,14 +298,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     if (lane == 0) {
       atomicAdd(&acc_y[i], y);
       if (pc) atomicAdd(&acc_f[i], pc);
-      __threadfence_block();
-      if (atomicAdd(&done[i], 1u) == n_active - 1) {         // last warp of this frame
-        __threadfence_block();
-        const uint32_t sy = atomicAdd(&acc_y[i], 0u);
-        const uint32_t sf = atomicAdd(&acc_f[i], 0u);
-        atomicAdd(&a.luma[f], (unsigned long long)sy);
-        if (sf) atomicAdd(&a.fg[f], sf);
-      }
     }
   }
 }
@@ -361,10 +371,10 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
 // ------------------------------------------------------------- generic path
 // Any width: thread per pixel for the luma sum, warp per 32-pixel word of a
 // bit-mask row for the branch tests (ballot), after the means are known.
-__global__ void luma_generic_kernel(const uint8_t* __restrict__ frames, uint64_t N,
+__global__ void luma_generic_kernel(const uint8_t* __restrict__ frames, uint64_t N, uint32_t f0,
                                     unsigned long long* __restrict__ luma) {
   const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint32_t f = blockIdx.y;
+  const uint32_t f = f0 + blockIdx.y;
   uint32_t y = 0;
   if (q < N) {
     const uint8_t* p = frames + ((uint64_t)f * N + q) * 3;
@@ -379,7 +389,7 @@ __global__ void mask_generic_kernel(SegArgs a, uint32_t W, uint32_t H, uint32_t 
   const int lane = threadIdx.x & 31;
   const uint64_t per_frame = (uint64_t)H * P;
   if (gw >= per_frame * n) return;
-  const uint32_t f = (uint32_t)(gw / per_frame);
+  const uint32_t f = a.f0 + (uint32_t)(gw / per_frame);
   const uint32_t rw = (uint32_t)(gw % per_frame);
   const uint32_t yrow = rw / P, k = rw % P;
   const uint32_t x = 32 * k + lane;
@@ -405,14 +415,16 @@ __global__ void mask_generic_kernel(SegArgs a, uint32_t W, uint32_t H, uint32_t 
 }
 
 // ------------------------------------------------------------ finalize (a2)
-__global__ void finalize_kernel(uint32_t n, uint64_t N, const unsigned long long* __restrict__ luma,
+__global__ void finalize_kernel(uint32_t f0, uint32_t n, uint64_t N,
+                                const unsigned long long* __restrict__ luma,
                                 uint32_t* __restrict__ fg, const double* __restrict__ gtab,
                                 const uint8_t* __restrict__ ctab,
                                 const uint32_t* __restrict__ frame_stream,
                                 const int64_t* __restrict__ frame_t, fizi_result* __restrict__ res,
                                 uint32_t* __restrict__ fix) {
-  const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= n) return;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t f = f0 + i;
   const uint32_t mean = (uint32_t)((luma[f] + 500ull * N) / (1000ull * N));
   fizi_result r;
   memset(&r, 0, sizeof(r));
@@ -430,8 +442,8 @@ __global__ void finalize_kernel(uint32_t n, uint64_t N, const unsigned long long
   }
 }
 
-cudaError_t launch_segment(Ctx& c, const uint8_t* frames, uint32_t n, uint32_t n_groups,
-                           fizi_result* res, cudaStream_t st) {
+static SegArgs seg_args(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t g0,
+                        uint32_t sub) {
   SegArgs a;
   a.frames = frames;
   a.frame_bytes = c.N * 3;
@@ -443,45 +455,57 @@ cudaError_t launch_segment(Ctx& c, const uint8_t* frames, uint32_t n, uint32_t n
   a.env_plane = c.env_plane;
   a.frame_stream = c.frame_stream;
   a.group_frames = c.group_frames;
-  a.group_off = c.group_off;
+  a.group_off = c.group_off + g0;
   a.bitA = c.bitA;
   a.luma = c.luma;
   a.fg = c.fg;
   a.lut_table = c.lut;
-  a.fix = c.fix_count;
+  a.fix = c.fix_count + (uint64_t)sub * (c.max_batch + 1);
   a.S = c.p.gray_tol_S;
   a.a1 = c.p.hue_lo_deg;
   a.a2 = c.p.hue_hi_deg;
-  cudaMemsetAsync(c.luma, 0, sizeof(unsigned long long) * n, st);
-  cudaMemsetAsync(c.fg, 0, sizeof(uint32_t) * n, st);
-  cudaMemsetAsync(c.fix_count, 0, sizeof(uint32_t), st);
-  const unsigned fin_blocks = (n + 255) / 256;
+  a.f0 = f0;
+  a.n = n;
+  return a;
+}
+
+// a2 + a3 main pass over frames [f0, f0+n) (same-stream groups g0 .. g0+ng-1).
+cudaError_t launch_seg_main(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t g0,
+                            uint32_t ng, uint32_t sub, cudaStream_t st) {
+  SegArgs a = seg_args(c, frames, f0, n, g0, sub);
+  prof_begin(c, st);
   if (c.fast) {
-    prof_begin(c, st);
     if (c.seg_variant == 3)
-      seg_fast_kernel<3><<<dim3(a.tiles, n_groups), 256, kWarpsPerCta * kWarpStages * kChunkBytes, st>>>(a);
+      seg_fast_kernel<3><<<dim3(a.tiles, ng), 256, kWarpsPerCta * kWarpStages * kChunkBytes, st>>>(a);
     else
-      seg_fast_kernel<2><<<dim3(a.tiles, n_groups), 256, kWarpsPerCta * kWarpStages * kChunkBytes, st>>>(a);
-    prof_end(c, FIZI_PROF_SEGMENT, st);
-    prof_begin(c, st);
-    finalize_kernel<<<fin_blocks, 256, 0, st>>>(n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
-                                                 c.frame_stream, c.frame_t, res, c.fix_count);
-    fix_fast_kernel<<<2 * c.sms, 256, kTileBytes, st>>>(a);
-    prof_end(c, FIZI_PROF_FIXUP, st);
-    c.launches += 3;
+      seg_fast_kernel<2><<<dim3(a.tiles, ng), 256, kWarpsPerCta * kWarpStages * kChunkBytes, st>>>(a);
   } else {
-    prof_begin(c, st);
-    luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(frames, c.N,
+    luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(frames, c.N, f0,
                                                                                 c.luma);
-    prof_end(c, FIZI_PROF_SEGMENT, st);
-    prof_begin(c, st);
-    finalize_kernel<<<fin_blocks, 256, 0, st>>>(n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
-                                                 c.frame_stream, c.frame_t, res, c.fix_count);
+  }
+  prof_end(c, FIZI_PROF_SEGMENT, st);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+// a2 finalisation (mean -> gamma, record header) and the LUT re-test of the
+// sub-batch's corrected frames (fast path) / the branch tests (generic path).
+cudaError_t launch_seg_fix(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t sub,
+                           fizi_result* res, cudaStream_t st) {
+  SegArgs a = seg_args(c, frames, f0, n, 0, sub);
+  const unsigned fin_blocks = (n + 255) / 256;
+  prof_begin(c, st);
+  finalize_kernel<<<fin_blocks, 256, 0, st>>>(f0, n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
+                                               c.frame_stream, c.frame_t, res,
+                                               const_cast<uint32_t*>(a.fix));
+  if (c.fast) {
+    fix_fast_kernel<<<c.sms, 256, kTileBytes, st>>>(a);
+  } else {
     const uint64_t warps = (uint64_t)c.H * c.P * n;
     mask_generic_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a, c.W, c.H, c.P, n);
-    prof_end(c, FIZI_PROF_FIXUP, st);
-    c.launches += 3;
   }
+  prof_end(c, FIZI_PROF_FIXUP, st);
+  c.launches += 2;
   return cudaGetLastError();
 }
 

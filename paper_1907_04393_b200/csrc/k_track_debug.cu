@@ -52,14 +52,14 @@ __device__ void track_one(const fizi_params& p, TrackState& s, fizi_result& r) {
 }
 
 // One thread per stream; frames of the batch in index order.
-__global__ void track_batch_kernel(fizi_params p, uint32_t n, uint32_t n_streams,
+__global__ void track_batch_kernel(fizi_params p, uint32_t f0, uint32_t n, uint32_t n_streams,
                                    const uint32_t* __restrict__ frame_stream,
                                    fizi_result* __restrict__ res, TrackState* __restrict__ ts) {
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_streams;
        s += gridDim.x * blockDim.x) {
     bool any = false;
     TrackState st;
-    for (uint32_t f = 0; f < n; f++) {
+    for (uint32_t f = f0; f < f0 + n; f++) {
       if (frame_stream[f] != s) continue;
       if (!any) { st = ts[s]; any = true; }
       fizi_result r = res[f];
@@ -137,10 +137,10 @@ __global__ void tstate_reset_kernel(TrackState* ts, uint32_t count) {
   }
 }
 
-cudaError_t launch_track_batch(Ctx& c, uint32_t n, fizi_result* res, cudaStream_t st) {
+cudaError_t launch_track_batch(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st) {
   const uint32_t threads = c.n_streams < 256 ? ((c.n_streams + 31) / 32) * 32 : 256;
   const uint32_t blocks = (c.n_streams + threads - 1) / threads;
-  track_batch_kernel<<<blocks, threads, 0, st>>>(c.p, n, c.n_streams, c.frame_stream, res,
+  track_batch_kernel<<<blocks, threads, 0, st>>>(c.p, f0, n, c.n_streams, c.frame_stream, res,
                                                   reinterpret_cast<TrackState*>(c.tstate));
   c.launches += 1;
   return cudaGetLastError();
