@@ -283,10 +283,13 @@ def main():
     N = cfg.npx
     hbm, peak_kind = peaks()
     seg_ms, seg_n = prof["segment"]
-    # algorithmic bytes of one segment launch: B frames read (3N each), the
-    # stream's envelope once (6N), B bit masks written (N/8 each)
+    # algorithmic bytes the fused segmentation kernel moves per step: B frames
+    # read (3N each), the stream's envelope once (6N), B bit masks written
+    # (N/8 each); a step may issue several launches (sub-batches), so the
+    # achieved rate is total algorithmic bytes / total kernel time
     seg_bytes = B * (3 * N + N / 8) + 6 * N
-    seg_gbs = seg_bytes / (seg_ms / seg_n / 1e3) / 1e9 if seg_n else None
+    launches_per_step = seg_n / max(args.steps, 1)
+    seg_gbs = seg_bytes * args.steps / (seg_ms / 1e3) / 1e9 if seg_n else None
     step_bytes = B * (3 * N + N) + 6 * N       # whole-path algorithmic bytes per step
     step_ms = ms_max / args.steps
     roofline = {
@@ -294,12 +297,13 @@ def main():
         "achieved": seg_gbs, "peak": hbm, "unit": "GB/s",
         "frac": (seg_gbs / hbm) if seg_gbs else None, "traffic": None,
         "peak_kind": peak_kind,
-        "algorithmic_bytes_per_launch": seg_bytes,
-        "kernel_ms_per_launch": seg_ms / seg_n if seg_n else None,
+        "algorithmic_bytes_per_step": seg_bytes,
+        "launches_per_step": launches_per_step,
+        "kernel_ms_per_step": seg_ms / max(args.steps, 1),
         "step": {"achieved": step_bytes / (step_ms / 1e3) / 1e9,
                  "frac": step_bytes / (step_ms / 1e3) / 1e9 / hbm,
                  "algorithmic_bytes_per_step": step_bytes},
-        "stage_ms_per_step": {k: (v[0] / max(v[1], 1)) for k, v in prof.items()},
+        "stage_ms_per_step": {k: (v[0] / max(args.steps, 1)) for k, v in prof.items()},
         "stage_share": {k: v[0] / max(sum(x[0] for x in prof.values()), 1e-9)
                         for k, v in prof.items()},
     }

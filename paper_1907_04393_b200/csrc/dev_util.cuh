@@ -55,6 +55,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// 4 bits -> 4 bytes {0,1} (bit i -> byte i)
+__device__ __forceinline__ uint32_t expand4(uint32_t v) { return (v * 0x00204081u) & 0x01010101u; }
+
 __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
   return __reduce_add_sync(0xFFFFFFFFu, v);
 }

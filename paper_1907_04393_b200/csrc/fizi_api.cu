@@ -129,7 +129,7 @@ cudaError_t dalloc(T** p, size_t bytes) {
 }
 
 void free_all(Ctx& c) {
-  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.luma, c.fg, c.bitA, c.bitO, c.bitOC,
+  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.luma, c.fg, c.frame_done, c.sub_done, c.bitA, c.bitO, c.bitOC,
                   c.row_cnt, c.row_base, c.frame_runs, c.runs, c.parent, c.stats, c.frame_t, c.fix_count,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
@@ -228,15 +228,20 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   if (rc) return rc;
   cudaError_t e = cudaMemsetAsync(c.luma, 0, sizeof(unsigned long long) * n, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c.fg, 0, sizeof(uint32_t) * n, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c.frame_done, 0, sizeof(uint32_t) * n, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c.sub_done, 0, sizeof(uint32_t) * fizi::kMaxSub, st);
   for (size_t k = 0; k < subs.size() && e == cudaSuccess; k++)
     e = cudaMemsetAsync(c.fix_count + k * (c.max_batch + 1), 0, sizeof(uint32_t), st);
   if (e != cudaSuccess) return cuda_fail(c, e, "memset");
   bool single = true;
   for (uint32_t i = 1; i < n && single; i++) single = sof[i] == sof[0];
+  const int fold = !track ? -2 : (single ? (int)sof[0] : -1);
+  // the u8 mask is written by the register-pipelined morphology when it runs
+  const bool fused_mask = c.fast && c.P <= 128 && c.p.se_radius <= 4;
   cudaStream_t sd = c.side;
   for (size_t k = 0; k < subs.size(); k++) {
     const SubBatch& b = subs[k];
-    e = fizi::launch_seg_main(c, frames, b.f0, b.n, b.g0, b.ng, (uint32_t)k, st);
+    e = fizi::launch_seg_main(c, frames, b.f0, b.n, b.g0, b.ng, (uint32_t)k, res, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "segment");
     e = cudaEventRecord(c.ev_seg[k], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, c.ev_seg[k], 0);
@@ -244,7 +249,7 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
     e = fizi::launch_seg_fix(c, frames, b.f0, b.n, (uint32_t)k, res, sd);
     if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
     prof_begin(c, sd);
-    e = fizi::launch_morph(c, b.f0, b.n, sd);
+    e = fizi::launch_morph(c, b.f0, b.n, fused_mask ? masks : nullptr, sd);
     prof_end(c, FIZI_PROF_MORPH, sd);
     if (e != cudaSuccess) return cuda_fail(c, e, "morph");
     if (c.p.debug) {
@@ -254,21 +259,14 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
       if (e != cudaSuccess) return cuda_fail(c, e, "debug copy");
     }
     prof_begin(c, sd);
-    e = fizi::launch_ccl(c, b.f0, b.n, res, sd);
+    e = fizi::launch_ccl(c, b.f0, b.n, (uint32_t)k, res, fused_mask ? masks : nullptr, fold, sd);
     prof_end(c, FIZI_PROF_CCL, sd);
     if (e != cudaSuccess) return cuda_fail(c, e, "ccl");
-    if (masks) {
+    if (masks && !fused_mask) {
       prof_begin(c, sd);
       e = fizi::launch_expand(c, b.f0, b.n, masks, sd);
       prof_end(c, FIZI_PROF_EXPAND, sd);
       if (e != cudaSuccess) return cuda_fail(c, e, "expand");
-    }
-    if (track) {
-      prof_begin(c, sd);
-      e = single ? fizi::launch_track_stream(c, sof[0], res + b.f0, b.n, sd)
-                 : fizi::launch_track_batch(c, b.f0, b.n, res, sd);
-      prof_end(c, FIZI_PROF_TRACK, sd);
-      if (e != cudaSuccess) return cuda_fail(c, e, "track");
     }
   }
   e = cudaEventRecord(c.ev_join, sd);
@@ -372,6 +370,8 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.corr_tab, 256));
   A(dalloc(&c.luma, mb * 8));
   A(dalloc(&c.fg, mb * 4));
+  A(dalloc(&c.frame_done, mb * 4));
+  A(dalloc(&c.sub_done, fizi::kMaxSub * 4));
   A(dalloc(&c.bitA, mb * wpf * 4));
   A(dalloc(&c.bitO, mb * wpf * 4));
   if (c.p.debug) A(dalloc(&c.bitOC, mb * wpf * 4));

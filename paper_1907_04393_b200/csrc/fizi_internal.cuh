@@ -67,6 +67,8 @@ struct Ctx {
   uint8_t* corr_tab = nullptr;           // 256
   unsigned long long* luma = nullptr;    // max_batch
   uint32_t* fg = nullptr;                // max_batch (fg_merged)
+  uint32_t* frame_done = nullptr;        // max_batch (CTAs finished per frame)
+  uint32_t* sub_done = nullptr;          // kMaxSub (CCL CTAs finished per sub-batch)
   uint32_t* bitA = nullptr;              // max_batch * H * P
   uint32_t* bitO = nullptr;              // max_batch * H * P
   uint32_t* bitOC = nullptr;             // debug copy of O
@@ -137,14 +139,15 @@ cudaError_t launch_learn(Ctx& c, uint32_t stream, const uint8_t* frames, uint32_
 cudaError_t launch_env_export(Ctx& c, uint32_t stream, uint8_t* lo, uint8_t* hi, bool import,
                               const uint8_t* ilo, const uint8_t* ihi, cudaStream_t st);
 cudaError_t launch_seg_main(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t g0,
-                            uint32_t ng, uint32_t sub, cudaStream_t st);
+                            uint32_t ng, uint32_t sub, fizi_result* res, cudaStream_t st);
 cudaError_t launch_seg_fix(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t sub,
                            fizi_result* res, cudaStream_t st);
 // the segment launcher marks the SEGMENT -> FIXUP boundary through this hook
 void prof_begin(Ctx& c, cudaStream_t st);
 void prof_end(Ctx& c, int slot, cudaStream_t st);
-cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, cudaStream_t st);
-cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st);
+cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st);
+cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_result* res,
+                       uint8_t* masks, int track_stream, cudaStream_t st);
 cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st);
 cudaError_t launch_track_batch(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st);
 cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,

@@ -25,6 +25,7 @@
 //   5. clear dropped components' runs from the mask words (final mask F)
 #include "dev_util.cuh"
 #include "fizi_internal.cuh"
+#include "track.cuh"
 
 namespace fizi {
 
@@ -43,6 +44,15 @@ struct CclArgs {
   fizi_result* res;
   const uint32_t* fg;
   uint32_t ppm;
+  // fused a6 output / a8 fold
+  uint8_t* masks;               // u8 final mask written by morphology (cleared here) or nullptr
+  uint32_t n;                   // frames in the launch (sub-batch)
+  uint32_t* sub_done;           // CTAs finished in this launch
+  int track_stream;             // -2: no fold; -1: per-stream fold; >= 0: single stream
+  uint32_t n_streams;
+  const uint32_t* frame_stream;
+  TrackState* tstate;
+  fizi_params p;
 };
 
 __device__ __forceinline__ bool kept_area(uint32_t area, uint32_t ppm, uint64_t N) {
@@ -261,6 +271,66 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
       const uint32_t m = (b1 == 31u ? 0xFFFFFFFFu : ((1u << (b1 + 1)) - 1u)) & ~((1u << b0) - 1u);
       atomicAnd(row + k, ~m);
     }
+    if (a.masks) {
+      uint8_t* mrow = a.masks + ((uint64_t)f * H + rg.y) * W;
+      for (uint32_t x = rg.x0; x <= rg.x1; x++) mrow[x] = 0;
+    }
+  }
+}
+
+// a8 fold of the launch's records, run by the last CTA to finish: frames in
+// index order, one thread per stream (records staged through shared memory
+// for the single-stream case).
+__device__ void fold_records(const CclArgs& a, uint8_t* smem) {
+  const uint32_t f0 = a.f0, n = a.n;
+  if (a.track_stream >= 0) {
+    constexpr uint32_t kChunk = 1024;
+    int64_t* t_s = reinterpret_cast<int64_t*>(smem);
+    double* cx_s = reinterpret_cast<double*>(t_s + kChunk);
+    double* cy_s = cx_s + kChunk;
+    uint32_t* ar_s = reinterpret_cast<uint32_t*>(cy_s + kChunk);
+    TrackState st;
+    if (threadIdx.x == 0) st = a.tstate[a.track_stream];
+    for (uint32_t base = 0; base < n; base += kChunk) {
+      const uint32_t m = min(kChunk, n - base);
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const fizi_result& r = a.res[f0 + base + i];
+        t_s[i] = __ldcg(&r.t_ms);
+        ar_s[i] = __ldcg(&r.blob_area);
+        cx_s[i] = __ldcg(&r.cx);
+        cy_s[i] = __ldcg(&r.cy);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (uint32_t i = 0; i < m; i++) {
+          fizi_result r;
+          r.t_ms = t_s[i]; r.blob_area = ar_s[i]; r.cx = cx_s[i]; r.cy = cy_s[i];
+          track_one(a.p, st, r);
+          fizi_result& o = a.res[f0 + base + i];
+          o.visible = r.visible; o.clicked = r.clicked;
+          o.px = r.px; o.py = r.py; o.dwell_ms = r.dwell_ms;
+        }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) a.tstate[a.track_stream] = st;
+  } else {
+    for (uint32_t s = threadIdx.x; s < a.n_streams; s += blockDim.x) {
+      bool any = false;
+      TrackState st;
+      for (uint32_t f = f0; f < f0 + n; f++) {
+        if (a.frame_stream[f] != s) continue;
+        if (!any) { st = a.tstate[s]; any = true; }
+        fizi_result r;
+        r.t_ms = __ldcg(&a.res[f].t_ms); r.blob_area = __ldcg(&a.res[f].blob_area);
+        r.cx = __ldcg(&a.res[f].cx); r.cy = __ldcg(&a.res[f].cy);
+        track_one(a.p, st, r);
+        fizi_result& o = a.res[f];
+        o.visible = r.visible; o.clicked = r.clicked;
+        o.px = r.px; o.py = r.py; o.dwell_ms = r.dwell_ms;
+      }
+      if (any) a.tstate[s] = st;
+    }
   }
 }
 
@@ -276,9 +346,20 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
     ccl_frame<false>(a, f, const_cast<Run*>(a.runs + (uint64_t)f * a.cap_runs),
                      a.parent + (uint64_t)f * a.cap_runs, T);
   }
+  if (a.track_stream == -2) return;
+  __shared__ uint32_t s_last;
+  __syncthreads();                            // this frame's record is complete
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(a.sub_done, 1u) == a.n - 1;
+    __threadfence();
+  }
+  __syncthreads();
+  if (s_last) fold_records(a, smc);
 }
 
 constexpr size_t kCclSmem = (sizeof(Run) + sizeof(uint32_t)) * kCclSmemRuns;
+static_assert(kCclSmem >= 1024 * 28, "fold staging fits the labelling shared memory");
 
 cudaError_t init_ccl(Ctx& c) {
   (void)c;
@@ -286,9 +367,18 @@ cudaError_t init_ccl(Ctx& c) {
                               (int)kCclSmem);
 }
 
-cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st) {
+cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_result* res,
+                       uint8_t* masks, int track_stream, cudaStream_t st) {
   CclArgs a;
   a.f0 = f0;
+  a.masks = masks;
+  a.n = n;
+  a.sub_done = c.sub_done + sub;
+  a.track_stream = track_stream;
+  a.n_streams = c.n_streams;
+  a.frame_stream = c.frame_stream;
+  a.tstate = reinterpret_cast<TrackState*>(c.tstate);
+  a.p = c.p;
   a.O = c.bitO;
   a.W = c.W; a.H = c.H; a.P = c.P;
   a.N = c.N;
@@ -308,7 +398,6 @@ cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaSt
 }
 
 // ------------------------------------------------- final u8 mask (a6 output)
-__device__ __forceinline__ uint32_t expand4(uint32_t v) { return (v * 0x00204081u) & 0x01010101u; }
 
 __global__ void expand16_kernel(const uint32_t* __restrict__ F, uint8_t* __restrict__ out,
                                 uint64_t total16, uint32_t blocks_per_row, uint32_t P, uint32_t W) {

@@ -21,8 +21,10 @@
 
 namespace fizi {
 
+
 struct MorphArgs {
   uint32_t f0;                  // first frame of the launch (sub-batch)
+  uint8_t* masks;               // u8 final-mask output (fast path) or nullptr
   const uint32_t* A;
   uint32_t* O;
   uint32_t W, H, P, TR;
@@ -239,6 +241,7 @@ struct MorphPipe {
   uint32_t lmask, rmask, wmask[WPL];       // lane-edge masks, valid bits of each word
   const uint32_t* Af;
   uint32_t* Of;
+  uint8_t* Mf;                             // u8 mask of the frame (W % 32 == 0) or nullptr
   Run* runs;
   Pass<R, true, WPL> p1;
   Pass<R, false, WPL> p2, p3;
@@ -259,6 +262,7 @@ struct MorphPipe {
     }
     Af = a.A + (uint64_t)f * H * P;
     Of = a.O + (uint64_t)f * H * P;
+    Mf = a.masks ? a.masks + (uint64_t)f * H * a.W : nullptr;
     runs = a.runs + (uint64_t)f * a.cap_runs;
     p1.init(); p2.init(); p3.init(); p4.init();
   }
@@ -298,7 +302,47 @@ struct MorphPipe {
     }
   }
 
+  // the final u8 mask row (one byte per pixel, a6 output): speculatively O;
+  // the labelling kernel clears the pixels of components the area filter drops
+  __device__ __forceinline__ void write_mask_row(const RowW<WPL>& o, int yo) const {
+    if (!Mf) return;
+#pragma unroll
+    for (int j = 0; j < WPL; j++) {
+      const uint32_t k = (uint32_t)(lane * WPL + j);
+      if (k >= P) continue;
+      const uint32_t w = o.w[j];
+      uint4 lo, hi;
+      lo.x = expand4(w & 0xF); lo.y = expand4((w >> 4) & 0xF);
+      lo.z = expand4((w >> 8) & 0xF); lo.w = expand4((w >> 12) & 0xF);
+      hi.x = expand4((w >> 16) & 0xF); hi.y = expand4((w >> 20) & 0xF);
+      hi.z = expand4((w >> 24) & 0xF); hi.w = expand4(w >> 28);
+      uint4* dst = reinterpret_cast<uint4*>(Mf + (uint64_t)yo * a.W + 32ull * k);
+      __stcs(dst, lo);
+      __stcs(dst + 1, hi);
+    }
+  }
+
+  // band whose input rows are all zero: every output row is zero
+  __device__ __forceinline__ void zero_band() const {
+    RowW<WPL> z;
+#pragma unroll
+    for (int j = 0; j < WPL; j++) z.w[j] = 0u;
+    for (int yo = y0; yo < y_end; yo++) {
+#pragma unroll
+      for (int j = 0; j < WPL; j++) {
+        const uint32_t k = (uint32_t)(lane * WPL + j);
+        if (k < P) Of[(uint64_t)yo * P + k] = 0u;
+      }
+      write_mask_row(z, yo);
+      if (lane == 0) {
+        a.row_cnt[(uint64_t)f * H + yo] = 0u;
+        a.row_base[(uint64_t)f * H + yo] = 0u;
+      }
+    }
+  }
+
   __device__ __forceinline__ void emit(const RowW<WPL>& o4, int yo) {
+    write_mask_row(o4, yo);
     const uint32_t prev_last = __shfl_up_sync(0xFFFFFFFFu, o4.w[WPL - 1], 1) & lmask;
     const uint32_t next_first = __shfl_down_sync(0xFFFFFFFFu, o4.w[0], 1) & rmask;
     uint32_t st[WPL], en[WPL], ns = 0, ne = 0;
@@ -368,6 +412,18 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
   if (y0 >= (int)a.H) return;
   MorphPipe<R, WPL> mp(a, a.f0 + blockIdx.y, y0);
   const int first = y0 - 4 * R, last = mp.y_end + 4 * R;     // input rows [first, last)
+  {                                                          // all-zero band: skip the passes
+    uint32_t any = 0;
+    for (int yy = max(first, 0); yy < min(last, (int)a.H); yy++) {
+      const RowW<WPL> r = mp.load_row(yy);
+#pragma unroll
+      for (int j = 0; j < WPL; j++) any |= r.w[j];
+    }
+    if (!__any_sync(0xFFFFFFFFu, any != 0u)) {
+      mp.zero_band();
+      return;
+    }
+  }
 #pragma unroll
   for (int q = 0; q < 2 * R + 1; q++) mp.pre[q] = mp.load_row(first + q);
   for (int yi = first; yi < last; yi += 2 * R + 1) unrolled_steps<R, WPL, 0>(mp, yi, last);
@@ -392,9 +448,10 @@ static void launch_r(const MorphArgs& a, uint32_t n, size_t smem, cudaStream_t s
   morph_runs_kernel<R><<<dim3((a.H + a.TR - 1) / a.TR, n), 256, smem, st>>>(a);
 }
 
-cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, cudaStream_t st) {
+cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st) {
   MorphArgs a;
   a.f0 = f0;
+  a.masks = masks;
   a.A = c.bitA;
   a.O = c.bitO;
   a.W = c.W; a.H = c.H; a.P = c.P; a.TR = c.morph_tr;

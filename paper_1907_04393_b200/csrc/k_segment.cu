@@ -47,7 +47,35 @@ struct SegArgs {
   const uint32_t* fix;          // [0] = count, [1..] = frame ids needing a LUT
   uint32_t S, a1, a2;
   uint32_t f0, n;               // frame range of this launch (sub-batch)
+  // in-kernel finalisation (fast path): the last CTA of a frame writes its record
+  uint32_t* frame_done;         // per-frame count of finished CTAs
+  const double* gtab;
+  const uint8_t* ctab;
+  const int64_t* frame_t;
+  fizi_result* res;
 };
+
+// a2 finalisation of frame f from its exact luma sum: integer mean, gamma,
+// record header; corrected frames join the sub-batch's LUT re-test list.
+__device__ __forceinline__ void finalize_frame(const SegArgs& a, uint32_t f,
+                                               unsigned long long sum, uint32_t* fix,
+                                               uint32_t* fg) {
+  const uint32_t mean = (uint32_t)((sum + 500ull * a.N) / (1000ull * a.N));
+  fizi_result r;
+  memset(&r, 0, sizeof(r));
+  r.t_ms = a.frame_t[f];
+  r.stream = a.frame_stream[f];
+  r.frame_idx = f;
+  r.mean_luma = (uint8_t)mean;
+  r.corrected = a.ctab[mean];
+  r.gamma = a.gtab[mean];
+  a.res[f] = r;
+  if (r.corrected) {
+    const uint32_t pos = atomicAdd(&fix[0], 1u);
+    fix[1 + pos] = f;
+    fg[f] = 0;
+  }
+}
 
 // Rec.601 weights split so every dp4a weight fits a byte:
 // 299 r + 587 g + 114 b = 256 (r + 2 g) + (43 r + 75 g + 114 b).
@@ -231,8 +259,16 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   __syncthreads();                                           // flush the CTA's sums
   if (tid < (int)nf) {
     const uint32_t f = a.group_frames[f_begin + tid];
-    atomicAdd(&a.luma[f], (unsigned long long)acc_y[tid]);
+    const unsigned long long mine = acc_y[tid];
+    const unsigned long long before = atomicAdd(&a.luma[f], mine);
     if (acc_f[tid]) atomicAdd(&a.fg[f], acc_f[tid]);
+    __threadfence();
+    if (atomicAdd(&a.frame_done[f], 1u) == a.tiles - 1) {   // last CTA of frame f
+      __threadfence();
+      (void)before;
+      const unsigned long long sum = atomicAdd(&a.luma[f], 0ull);
+      finalize_frame(a, f, sum, const_cast<uint32_t*>(a.fix), a.fg);
+    }
   }
 }
 
@@ -466,13 +502,19 @@ static SegArgs seg_args(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, 
   a.a2 = c.p.hue_hi_deg;
   a.f0 = f0;
   a.n = n;
+  a.frame_done = c.frame_done;
+  a.gtab = c.gamma_tab;
+  a.ctab = c.corr_tab;
+  a.frame_t = c.frame_t;
+  a.res = nullptr;
   return a;
 }
 
 // a2 + a3 main pass over frames [f0, f0+n) (same-stream groups g0 .. g0+ng-1).
 cudaError_t launch_seg_main(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t g0,
-                            uint32_t ng, uint32_t sub, cudaStream_t st) {
+                            uint32_t ng, uint32_t sub, fizi_result* res, cudaStream_t st) {
   SegArgs a = seg_args(c, frames, f0, n, g0, sub);
+  a.res = res;
   prof_begin(c, st);
   if (c.fast) {
     if (c.seg_variant == 3)
@@ -493,19 +535,20 @@ cudaError_t launch_seg_main(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t
 cudaError_t launch_seg_fix(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t sub,
                            fizi_result* res, cudaStream_t st) {
   SegArgs a = seg_args(c, frames, f0, n, 0, sub);
-  const unsigned fin_blocks = (n + 255) / 256;
   prof_begin(c, st);
-  finalize_kernel<<<fin_blocks, 256, 0, st>>>(f0, n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
-                                               c.frame_stream, c.frame_t, res,
-                                               const_cast<uint32_t*>(a.fix));
-  if (c.fast) {
+  if (c.fast) {                      // finalisation already done by the fused kernel
     fix_fast_kernel<<<c.sms, 256, kTileBytes, st>>>(a);
+    c.launches += 1;
   } else {
+    const unsigned fin_blocks = (n + 255) / 256;
+    finalize_kernel<<<fin_blocks, 256, 0, st>>>(f0, n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
+                                                 c.frame_stream, c.frame_t, res,
+                                                 const_cast<uint32_t*>(a.fix));
     const uint64_t warps = (uint64_t)c.H * c.P * n;
     mask_generic_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a, c.W, c.H, c.P, n);
+    c.launches += 2;
   }
   prof_end(c, FIZI_PROF_FIXUP, st);
-  c.launches += 2;
   return cudaGetLastError();
 }
 

@@ -9,47 +9,9 @@
 // sum is a separate correctly-rounded IEEE operation (__dmul_rn/__dadd_rn):
 // no FMA contraction.
 #include "fizi_internal.cuh"
+#include "track.cuh"
 
 namespace fizi {
-
-__device__ void track_one(const fizi_params& p, TrackState& s, fizi_result& r) {
-  const int64_t t = r.t_ms;
-  if (r.blob_area > 0) {
-    if (s.vis) {
-      const double b = p.beta, ob = __dadd_rn(1.0, -p.beta);
-      s.px = __dadd_rn(__dmul_rn(b, r.cx), __dmul_rn(ob, s.px));
-      s.py = __dadd_rn(__dmul_rn(b, r.cy), __dmul_rn(ob, s.py));
-      const double dx = __dadd_rn(s.px, -s.ax), dy = __dadd_rn(s.py, -s.ay);
-      const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-      const double R2 = __dmul_rn(p.dwell_radius_px, p.dwell_radius_px);
-      if (d2 > R2) {
-        s.ax = s.px; s.ay = s.py; s.anchor_t = t;
-        s.dwell = 0; s.fired = 0;
-      } else {
-        s.dwell = t - s.anchor_t;
-      }
-    } else {
-      s.px = r.cx; s.py = r.cy;
-      s.ax = r.cx; s.ay = r.cy; s.anchor_t = t;
-      s.dwell = 0; s.fired = 0;
-    }
-    s.vis = 1;
-    s.last_t = t;
-  } else {
-    if (s.vis && t - s.last_t > p.lost_timeout_ms) {
-      s.vis = 0; s.dwell = 0; s.fired = 0;
-    } else if (s.vis) {
-      s.dwell = t - s.anchor_t;
-    }
-  }
-  const int clicked = s.vis && !s.fired && s.dwell >= p.dwell_time_ms;
-  if (clicked) s.fired = 1;
-  r.visible = (uint8_t)s.vis;
-  r.clicked = (uint8_t)clicked;
-  r.px = s.px;
-  r.py = s.py;
-  r.dwell_ms = s.dwell;
-}
 
 // One thread per stream; frames of the batch in index order.
 __global__ void track_batch_kernel(fizi_params p, uint32_t f0, uint32_t n, uint32_t n_streams,
