@@ -26,7 +26,7 @@ constexpr int kChunkBytes = 3 * kChunkPx;
 constexpr int kWarpsPerCta = 8;          // chunks per CTA tile
 constexpr int kTileBytes = kChunkBytes * kWarpsPerCta;   // 12 KiB frame bytes per tile
 constexpr int kFrameGroup = 32;          // frames sharing one envelope load (<= 32)
-constexpr int kWarpStages = 8;           // per-warp bulk-copy ring depth (frames, power of 2)
+constexpr int kStages = 8;               // bulk-copy ring depth in frames (power of 2)
 constexpr int kMaxRadius = 8;
 constexpr size_t kMorphSmem = 200 * 1024;  // dynamic smem budget of the morphology CTA
 constexpr uint32_t kCclSmemRuns = 4096;     // runs labelled in shared memory (else global)

@@ -5,12 +5,13 @@
 //     R3 hue-band test, AND-merged into a bit-packed mask (bit = pixel).
 //
 // Fast path (W % 32 == 0): one CTA = 8 warps = 8 chunks of 512 pixels (a
-// 12 KiB tile of interleaved RGB bytes) x a group of up to 16 frames of one
-// stream.  Each warp streams its chunk of every frame through its own TMA
-// ring (cp.async.bulk into shared memory, kWarpStages-deep mbarrier
-// pipeline), so every frame byte is read from HBM exactly once and warps
-// never synchronise with each other; the stream's envelope for the chunk is
-// loaded once into registers and reused for all frames of the group.
+// 12 KiB tile of interleaved RGB bytes) x a group of up to 32 frames of one
+// stream.  The tile of every frame streams through a kStages-deep ring of
+// shared-memory buffers filled by the TMA engine (cp.async.bulk, mbarrier
+// completion), so every frame byte is read from HBM exactly once; warps
+// release stages through a shared counter instead of a block barrier; the
+// stream's envelope for the chunk is loaded once into registers and reused
+// for all frames of the group.
 // The luma sum is computed in the same pass (IDP.4A); the mask is computed
 // speculatively with the identity LUT, which is exact for every frame whose
 // mean lands in [luma_lo, luma_hi] (the common case).  The few frames outside
@@ -150,7 +151,7 @@ __device__ __forceinline__ void r1_lanes(uint32_t w, const EnvRegs& e, int i, ui
 template <bool kLut>
 __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e, bool valid,
                                           const uint8_t* lut_s, int S, int a1, int a2,
-                                          uint32_t& luma_acc) {
+                                          uint32_t& luma_acc, bool& slow) {
   uint32_t fr[12];
   {
     const uint4* q = reinterpret_cast<const uint4*>(px48);
@@ -193,6 +194,7 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
                       ((okw[6] & okw[7] & okw[8]) & (okw[9] & okw[10] & okw[11]));
   const bool all_inside = (ok & 0x01000100u) == 0x01000100u;
   if (!__any_sync(0xFFFFFFFFu, !all_inside)) return 0u;   // whole warp is background
+  slow = true;
 
   // Per-pixel path (rare: warps touching the hand): 48 per-byte inside flags,
   // then R1 & R2 & R3 per pixel, 4 pixels (3 words) per rolled iteration.
@@ -227,21 +229,17 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
 }
 
 // ---------------------------------------------------------------- fast path
-// Each warp owns one 512-pixel chunk of the tile and runs its own TMA ring of
-// kWarpStages chunk buffers (1536 B) over the frames of the group: lane 0
-// issues cp.async.bulk for frame i + kWarpStages as soon as the warp has
-// consumed frame i, so warps never wait for each other.  Per-frame sums go
-// to shared-memory accumulators; the last warp to finish a frame flushes
-// them to global memory with one atomic each.
-__device__ __forceinline__ void seg_warp(const SegArgs& a, uint32_t c, int lane, int warp,
-                                         uint32_t nf, uint32_t fid_lane, uint32_t stream,
-                                         uint8_t* sm, uint64_t* wbar, uint32_t* acc_y,
-                                         uint32_t* acc_f);
-
+// Fast path.  CTA = 8 warps = one 12 KiB tile (8 chunks of 512 pixels) of
+// every frame of a same-stream group.  Tiles stream through a kStages-deep
+// ring of shared-memory buffers filled by the TMA engine (cp.async.bulk,
+// mbarrier completion).  Warps consume independently: each warp counts
+// itself out of stage s when done (shared atomic); the last one re-issues
+// the stage for frame i + kStages.  No block barrier inside the frame loop.
 template <int kMinBlocks>
 __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
-  extern __shared__ __align__(128) uint8_t sm[];          // 8 warps x kWarpStages chunks
-  __shared__ __align__(8) uint64_t bar[kWarpsPerCta][kWarpStages];
+  extern __shared__ __align__(128) uint8_t sm[];          // kStages x 12 KiB tiles
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ uint32_t empty_cnt[kStages];
   // per-frame partial sums of the CTA: luma <= 8 warps * 512 px * 255000 < 2^32
   __shared__ uint32_t acc_y[kFrameGroup], acc_f[kFrameGroup];
 
@@ -252,88 +250,90 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   // frame ids of the group, lane i holds frame i (nf <= kFrameGroup <= 32)
   const uint32_t fid_lane = (uint32_t)lane < nf ? a.group_frames[f_begin + lane] : 0u;
   const uint32_t stream = a.frame_stream[__shfl_sync(0xFFFFFFFFu, fid_lane, 0)];
-  const uint32_t c = tile * kWarpsPerCta + warp;
+  const uint64_t toff = (uint64_t)tile * kTileBytes;
+  const uint64_t trem = a.frame_bytes - toff;
+  const uint32_t tbytes = trem < (uint64_t)kTileBytes ? (uint32_t)trem : (uint32_t)kTileBytes;
+  const uint32_t n_active = min((uint32_t)kWarpsPerCta, a.nchunks - tile * kWarpsPerCta);
+  const uint8_t* src0 = a.frames + toff;
+
+  uint64_t pol = 0;
   if (tid < kFrameGroup) { acc_y[tid] = 0; acc_f[tid] = 0; }
+  if (tid < kStages) empty_cnt[tid] = 0;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
   __syncthreads();
-  if (c < a.nchunks) seg_warp(a, c, lane, warp, nf, fid_lane, stream, sm, bar[warp], acc_y, acc_f);
+  if (warp == 0) {                                           // prologue: fill the ring
+    pol = policy_evict_first();
+#pragma unroll
+    for (int s = 0; s < kStages; s++) {
+      const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, s);
+      if (lane == 0 && (uint32_t)s < nf) {
+        mbar_arrive_expect_tx(&full[s], tbytes);
+        bulk_g2s(sm + s * kTileBytes, src0 + (uint64_t)f * a.frame_bytes, tbytes, &full[s], pol);
+      }
+    }
+  }
+  const uint32_t c = tile * kWarpsPerCta + warp;
+  if (c < a.nchunks) {
+    const uint64_t coff = (uint64_t)c * kChunkBytes;
+    const bool valid = coff + 48u * lane < a.frame_bytes;
+    EnvRegs e;
+    if (valid) {
+      const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * lane;
+      load_env(e, elo, elo + a.env_plane);
+    } else {
+      zero_env(e);
+    }
+    if (warp != 0) pol = policy_evict_first();
+    const uint8_t* my = sm + warp * kChunkBytes + 48 * lane;
+    uint32_t* dstw = a.bitA + (uint64_t)c * 16 + (lane >> 1);
+    for (uint32_t i = 0; i < nf; i++) {
+      const uint32_t s = i & (kStages - 1);
+      const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
+      mbar_wait(&full[s], (i / kStages) & 1u);
+      uint32_t y = 0;
+      bool slow = false;
+      const uint32_t bits = seg16<false>(my + s * kTileBytes, e, valid, nullptr, (int)a.S,
+                                         (int)a.a1, (int)a.a2, y, slow);
+      const uint32_t fnext = __shfl_sync(0xFFFFFFFFu, fid_lane, (i + kStages) & 31);
+      __syncwarp();                                          // this warp is done with stage s
+      if (lane == 0 && atomicAdd(&empty_cnt[s], 1u) == n_active - 1) {
+        empty_cnt[s] = 0;                                    // last warp out: refill stage s
+        if (i + kStages < nf) {
+          mbar_arrive_expect_tx(&full[s], tbytes);
+          bulk_g2s(sm + s * kTileBytes, src0 + (uint64_t)fnext * a.frame_bytes, tbytes, &full[s],
+                   pol);
+        }
+      }
+      y = warp_sum_u32(y);
+      if (!slow) {
+        if (!(lane & 1) && valid) dstw[(uint64_t)f * a.words_per_frame] = 0u;
+      } else {
+        const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
+        uint32_t pc = 0;
+        if (!(lane & 1) && valid) {
+          dstw[(uint64_t)f * a.words_per_frame] = word;
+          pc = __popc(word);
+        }
+        pc = warp_sum_u32(pc);
+        if (lane == 0 && pc) atomicAdd(&acc_f[i], pc);
+      }
+      if (lane == 0) atomicAdd(&acc_y[i], y);
+    }
+  }
   __syncthreads();                                           // flush the CTA's sums
   if (tid < (int)nf) {
     const uint32_t f = a.group_frames[f_begin + tid];
-    const unsigned long long mine = acc_y[tid];
-    const unsigned long long before = atomicAdd(&a.luma[f], mine);
+    atomicAdd(&a.luma[f], (unsigned long long)acc_y[tid]);
     if (acc_f[tid]) atomicAdd(&a.fg[f], acc_f[tid]);
     __threadfence();
     if (atomicAdd(&a.frame_done[f], 1u) == a.tiles - 1) {   // last CTA of frame f
       __threadfence();
-      (void)before;
       const unsigned long long sum = atomicAdd(&a.luma[f], 0ull);
       finalize_frame(a, f, sum, const_cast<uint32_t*>(a.fix), a.fg);
-    }
-  }
-}
-
-// One warp: its chunk over the nf frames of the group.
-__device__ __forceinline__ void seg_warp(const SegArgs& a, uint32_t c, int lane, int warp,
-                                         uint32_t nf, uint32_t fid_lane, uint32_t stream,
-                                         uint8_t* sm, uint64_t* wbar, uint32_t* acc_y,
-                                         uint32_t* acc_f) {
-  const uint64_t coff = (uint64_t)c * kChunkBytes;
-  const uint64_t rem = a.frame_bytes - coff;
-  const uint32_t cbytes = rem < (uint64_t)kChunkBytes ? (uint32_t)rem : (uint32_t)kChunkBytes;
-  const bool valid = 48u * lane < cbytes;
-  uint8_t* ring = sm + (uint32_t)warp * kWarpStages * kChunkBytes;
-  const uint8_t* src0 = a.frames + coff;
-  uint32_t* dstw = a.bitA + (uint64_t)c * 16 + (lane >> 1);
-
-  EnvRegs e;
-  if (valid) {
-    const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * lane;
-    load_env(e, elo, elo + a.env_plane);
-  } else {
-    zero_env(e);
-  }
-
-  uint64_t pol = 0;
-  if (lane == 0) {
-    pol = policy_evict_first();
-#pragma unroll
-    for (int s = 0; s < kWarpStages; s++) mbar_init(&wbar[s], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-#pragma unroll
-  for (int s = 0; s < kWarpStages; s++) {
-    const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, s);
-    if (lane == 0 && (uint32_t)s < nf) {
-      mbar_arrive_expect_tx(&wbar[s], cbytes);
-      bulk_g2s(ring + s * kChunkBytes, src0 + (uint64_t)f * a.frame_bytes, cbytes, &wbar[s], pol);
-    }
-  }
-
-  for (uint32_t i = 0; i < nf; i++) {
-    const uint32_t s = i & (kWarpStages - 1);
-    const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
-    const uint32_t fn = __shfl_sync(0xFFFFFFFFu, fid_lane, (i + kWarpStages) & 31);
-    mbar_wait(&wbar[s], (i / kWarpStages) & 1u);
-    uint32_t y = 0;
-    const uint32_t bits = seg16<false>(ring + s * kChunkBytes + 48 * lane, e, valid, nullptr,
-                                       (int)a.S, (int)a.a1, (int)a.a2, y);
-    __syncwarp();                                           // chunk buffer s consumed
-    if (lane == 0 && i + kWarpStages < nf) {
-      mbar_arrive_expect_tx(&wbar[s], cbytes);
-      bulk_g2s(ring + s * kChunkBytes, src0 + (uint64_t)fn * a.frame_bytes, cbytes, &wbar[s], pol);
-    }
-    const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
-    uint32_t pc = 0;
-    if (!(lane & 1) && valid) {
-      dstw[(uint64_t)f * a.words_per_frame] = word;
-      pc = __popc(word);
-    }
-    y = warp_sum_u32(y);
-    pc = warp_sum_u32(pc);
-    if (lane == 0) {
-      atomicAdd(&acc_y[i], y);
-      if (pc) atomicAdd(&acc_f[i], pc);
     }
   }
 }
@@ -384,8 +384,9 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
     __syncthreads();                          // LUT in shared memory
     mbar_wait(&bar, phase);
     uint32_t y = 0;
+    bool slow = false;
     const uint32_t bits = seg16<true>(sm + warp * kChunkBytes + 48 * lane, e, valid, lut_s,
-                                      (int)a.S, (int)a.a1, (int)a.a2, y);
+                                      (int)a.S, (int)a.a1, (int)a.a2, y, slow);
     const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
     uint32_t pc = 0;
     if (!(lane & 1) && valid) {
@@ -518,9 +519,9 @@ cudaError_t launch_seg_main(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t
   prof_begin(c, st);
   if (c.fast) {
     if (c.seg_variant == 3)
-      seg_fast_kernel<3><<<dim3(a.tiles, ng), 256, kWarpsPerCta * kWarpStages * kChunkBytes, st>>>(a);
+      seg_fast_kernel<3><<<dim3(a.tiles, ng), 256, kStages * kTileBytes, st>>>(a);
     else
-      seg_fast_kernel<2><<<dim3(a.tiles, ng), 256, kWarpsPerCta * kWarpStages * kChunkBytes, st>>>(a);
+      seg_fast_kernel<2><<<dim3(a.tiles, ng), 256, kStages * kTileBytes, st>>>(a);
   } else {
     luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(frames, c.N, f0,
                                                                                 c.luma);
@@ -555,10 +556,10 @@ cudaError_t launch_seg_fix(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t 
 cudaError_t init_segment(Ctx& c) {
   (void)c;
   cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kWarpsPerCta * kWarpStages * kChunkBytes);
+                                       kStages * kTileBytes);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(seg_fast_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kWarpsPerCta * kWarpStages * kChunkBytes);
+                             kStages * kTileBytes);
   const char* v = getenv("FIZI_SEG_VARIANT");           // experiment switch (default 2)
   c.seg_variant = v ? atoi(v) : 2;
   if (e == cudaSuccess)
