@@ -391,7 +391,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   for (uint32_t k = 0; k < fizi::kMaxSub && e == cudaSuccess; k++)
     e = cudaEventCreateWithFlags(&c.ev_seg[k], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming);
-  if (const char* sf = getenv("FIZI_SUB_FRAMES")) c.sub_frames = (uint32_t)atoi(sf) > 0 ? (uint32_t)atoi(sf) : 16;
+  if (const char* sf = getenv("FIZI_SUB_FRAMES")) c.sub_frames = (uint32_t)atoi(sf) > 0 ? (uint32_t)atoi(sf) : 65535;
   if (e != cudaSuccess) {
     cudaGetLastError();
     free_all(c);

@@ -87,7 +87,7 @@ struct Ctx {
   cudaStream_t side = nullptr;           // internal stream for the per-sub-batch tail
   cudaEvent_t ev_seg[kMaxSub] = {};      // segment(k) done on the caller's stream
   cudaEvent_t ev_join = nullptr;         // tail of the call done on the side stream
-  uint32_t sub_frames = 16;              // frames per sub-batch
+  uint32_t sub_frames = 65535;           // frames per sub-batch (default: whole call)
   uint8_t* stage_frames = nullptr;       // device staging for fizi_process_frames_host
   uint8_t* stage_masks = nullptr;
   fizi_result* stage_results = nullptr;
