@@ -4,10 +4,11 @@
 Default workload (N=1): BASELINE.json configs[2] -- one 1920x1080 camera stream,
 10,000 synthetic frames resident in HBM, batches of 64 frames per launch (the
 config the metric is quoted on at 1/2/4/8 GPUs).  A step = one batch through the
-whole hot path: fizi_segment_frames (a2..a7: luma + three branches, open-close,
-labelling, blob filter, hand blob, u8 mask write) then, after an NCCL
-all_gather of the tiny per-frame records when N > 1, fizi_track (a8, the
-Mouse fold) over the gathered records in frame order.  Rank r takes batch b
+whole hot path.  N = 1: fizi_process_frames (a2..a8: luma + three branches,
+open-close, labelling, blob filter, hand blob, u8 mask write, Mouse fold).
+N > 1: fizi_segment_frames (a2..a7) on the rank's batch, an NCCL all_gather
+of the tiny per-frame records, then fizi_track (a8) over the gathered
+records in frame order.  Rank r takes batch b
 when b % N == r (weak scaling: 64 frames per rank per step).
 
 Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle instead
@@ -231,6 +232,9 @@ def main():
         t = np.asarray([synth.t_ms(k) for k in ks], np.int64)
         # timestamps keep increasing across passes over the resident batches
         t = t + (i // len(frames_by_batch)) * synth.t_ms(cfg.n_proc)
+        if world == 1:                 # the whole path in one call (fold fused into labelling)
+            fz.process_frames(fr[:n], t_ms=t, masks=masks[:n], results=res[:n])
+            return n
         fz.segment_frames(fr[:n], t_ms=t, masks=masks[:n], results=res[:n])
         if world > 1:
             # records of this step's batches (consecutive in frame order) from every rank;

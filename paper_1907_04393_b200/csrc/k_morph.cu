@@ -240,6 +240,8 @@ struct MorphPipe {
   int y0, y_end, lane;
   uint32_t lmask, rmask, wmask[WPL];       // lane-edge masks, valid bits of each word
   const uint32_t* Af;
+  const uint32_t* band;                    // shared-memory copy of input rows [first, last)
+  int first;
   uint32_t* Of;
   uint8_t* Mf;                             // u8 mask of the frame (W % 32 == 0) or nullptr
   Run* runs;
@@ -267,13 +269,15 @@ struct MorphPipe {
     p1.init(); p2.init(); p3.init(); p4.init();
   }
 
+  // input row yy of the band from shared memory (rows outside the band and
+  // the frame are zero there)
   __device__ __forceinline__ RowW<WPL> load_row(int yy) const {
     RowW<WPL> r;
-    const bool rin = yy >= 0 && yy < (int)H;
-    const uint32_t* row = Af + (uint64_t)(rin ? yy : 0) * P + (uint32_t)lane * WPL;
+    const int i = yy - first;
+    const bool rin = i >= 0 && i < (int)(kBandRows + 8 * R);
+    const uint32_t* row = band + (rin ? i : 0) * (int)P + lane * WPL;
 #pragma unroll
-    for (int j = 0; j < WPL; j++)
-      r.w[j] = (rin && wmask[j]) ? __ldg(row + j) : 0u;
+    for (int j = 0; j < WPL; j++) r.w[j] = (rin && wmask[j]) ? row[j] : 0u;
     return r;
   }
 
@@ -408,21 +412,30 @@ __device__ __forceinline__ void unrolled_steps(MorphPipe<R, WPL>& mp, int yi, in
 // warp-uniform and shuffles need no divergence handling).
 template <int R, int WPL>
 __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
+  extern __shared__ uint32_t band[];                          // (kBandRows + 8R) x P words
   const int y0 = (int)(blockIdx.x * kBandRows);
   if (y0 >= (int)a.H) return;
   MorphPipe<R, WPL> mp(a, a.f0 + blockIdx.y, y0);
   const int first = y0 - 4 * R, last = mp.y_end + 4 * R;     // input rows [first, last)
-  {                                                          // all-zero band: skip the passes
+  mp.band = band;
+  mp.first = first;
+  {                                     // stage the band (all loads in flight), detect zero bands
+    const int rows = kBandRows + 8 * R;
+    const uint32_t P = a.P;
+    const uint32_t total = (uint32_t)rows * P;
     uint32_t any = 0;
-    for (int yy = max(first, 0); yy < min(last, (int)a.H); yy++) {
-      const RowW<WPL> r = mp.load_row(yy);
-#pragma unroll
-      for (int j = 0; j < WPL; j++) any |= r.w[j];
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < total; i += 32) {
+      const int yy = first + (int)(i / P);
+      const uint32_t v = (yy >= 0 && yy < (int)a.H) ? __ldg(mp.Af + (uint64_t)yy * P + (i % P)) : 0u;
+      band[i] = v;
+      any |= v;
     }
     if (!__any_sync(0xFFFFFFFFu, any != 0u)) {
       mp.zero_band();
       return;
     }
+    __syncwarp();
   }
 #pragma unroll
   for (int q = 0; q < 2 * R + 1; q++) mp.pre[q] = mp.load_row(first + q);
@@ -464,7 +477,8 @@ cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaSt
   cudaMemsetAsync(c.frame_runs + f0, 0, n * sizeof(uint32_t), st);
   if (c.P <= 128 && r <= 4) {
     const dim3 grid((c.H + kBandRows - 1) / kBandRows, n);
-#define FIZI_MORPH_ROWS(RR, WW) morph_rows_kernel<RR, WW><<<grid, 32, 0, st>>>(a)
+    const size_t band_smem = (size_t)(kBandRows + 8 * r) * c.P * sizeof(uint32_t);
+#define FIZI_MORPH_ROWS(RR, WW) morph_rows_kernel<RR, WW><<<grid, 32, band_smem, st>>>(a)
 #define FIZI_MORPH_WPL(RR)                                    \
     if (c.P <= 32) FIZI_MORPH_ROWS(RR, 1);                    \
     else if (c.P <= 64) FIZI_MORPH_ROWS(RR, 2);               \

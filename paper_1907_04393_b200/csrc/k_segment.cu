@@ -104,15 +104,20 @@ __device__ __forceinline__ uint32_t gray_and_skin(int r, int g, int b, int S, in
   return (uint32_t)((C >= S) & (C > 0) & band);
 }
 
-// Envelope of the thread's 48 bytes, even / odd bytes in 16-bit lanes and
-// pre-biased: in each lane, v + KloX has bit 8 set iff v >= lo and KhiX - v
-// has bit 8 set iff v <= hi (KloX = 0x100 - lo, KhiX = hi + 0x100).
+// Envelope of the thread's 48 bytes, even / odd bytes in signed 16-bit
+// lanes: NlX = -lo, NhX = -(hi + 1).  Per lane v + NlX >= 0 iff v >= lo and
+// v + NhX < 0 iff v <= hi; the fused add + min / add + max DPX instruction
+// (VIADDMNMX.S16x2) accumulates both tests over all 48 bytes.
 struct EnvRegs {
-  uint32_t KloE[12], KloO[12], KhiE[12], KhiO[12];
+  uint32_t NlE[12], NlO[12], NhE[12], NhO[12];
 };
 
 __device__ __forceinline__ uint32_t even_bytes(uint32_t w) { return w & 0x00FF00FFu; }
 __device__ __forceinline__ uint32_t odd_bytes(uint32_t w) { return __byte_perm(w, 0u, 0x4341); }
+
+// per 16-bit lane: -x (x in [0, 255]), -(x + 1)
+__device__ __forceinline__ uint32_t neg_lanes(uint32_t x) { return __vsub2(0u, x); }
+__device__ __forceinline__ uint32_t neg1_lanes(uint32_t x) { return __vsub2(0xFFFFFFFFu, x); }
 
 __device__ __forceinline__ void load_env(EnvRegs& e, const uint8_t* elo, const uint8_t* ehi) {
 #pragma unroll
@@ -122,10 +127,10 @@ __device__ __forceinline__ void load_env(EnvRegs& e, const uint8_t* elo, const u
     const uint32_t lw[4] = {l.x, l.y, l.z, l.w}, hw[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      e.KloE[4 * k + j] = 0x01000100u - even_bytes(lw[j]);
-      e.KloO[4 * k + j] = 0x01000100u - odd_bytes(lw[j]);
-      e.KhiE[4 * k + j] = 0x01000100u + even_bytes(hw[j]);
-      e.KhiO[4 * k + j] = 0x01000100u + odd_bytes(hw[j]);
+      e.NlE[4 * k + j] = neg_lanes(even_bytes(lw[j]));
+      e.NlO[4 * k + j] = neg_lanes(odd_bytes(lw[j]));
+      e.NhE[4 * k + j] = neg1_lanes(even_bytes(hw[j]));
+      e.NhO[4 * k + j] = neg1_lanes(odd_bytes(hw[j]));
     }
   }
 }
@@ -133,17 +138,21 @@ __device__ __forceinline__ void load_env(EnvRegs& e, const uint8_t* elo, const u
 __device__ __forceinline__ void zero_env(EnvRegs& e) {
 #pragma unroll
   for (int i = 0; i < 12; i++) {
-    e.KloE[i] = e.KloO[i] = 0x01000100u;   // lo = 0, hi = 255: everything inside
-    e.KhiE[i] = e.KhiO[i] = 0x01FF01FFu;
+    e.NlE[i] = e.NlO[i] = 0u;                 // lo = 0
+    e.NhE[i] = e.NhO[i] = 0xFF00FF00u;        // hi = 255: -(256) per lane
   }
 }
 
-// inside flags of the 4 bytes of word i: bits 8/24 of tE (bytes 0, 2) and tO (1, 3)
+// per-byte inside flags of word i: bit 15 / bit 31 of the returned E / O words
 __device__ __forceinline__ void r1_lanes(uint32_t w, const EnvRegs& e, int i, uint32_t& tE,
                                          uint32_t& tO) {
   const uint32_t vE = even_bytes(w), vO = odd_bytes(w);
-  tE = (vE + e.KloE[i]) & (e.KhiE[i] - vE);
-  tO = (vO + e.KloO[i]) & (e.KhiO[i] - vO);
+  const uint32_t aE = __viaddmax_s16x2(vE, e.NlE[i], 0x80008000u);   // v - lo (no carry)
+  const uint32_t bE = __viaddmax_s16x2(vE, e.NhE[i], 0x80008000u);   // v - hi - 1
+  const uint32_t aO = __viaddmax_s16x2(vO, e.NlO[i], 0x80008000u);
+  const uint32_t bO = __viaddmax_s16x2(vO, e.NhO[i], 0x80008000u);
+  tE = ~aE & bE;                              // sign(v-lo) = 0 and sign(v-hi-1) = 1
+  tO = ~aO & bO;
 }
 
 // Process this thread's 16 pixels of one frame.  Returns the 16 merged bits
@@ -181,18 +190,20 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
     }
     luma_acc += (((ahi[0] + ahi[1]) + (ahi[2] + ahi[3])) << 8) + ((alo[0] + alo[1]) + (alo[2] + alo[3]));
   }
-  // R1 envelope test on all 48 bytes, two bytes per 32-bit op
-  uint32_t okw[12];
+  // R1 envelope test on all 48 bytes: running min of (v - lo) and max of
+  // (v - hi - 1) per 16-bit lane, four independent accumulator chains
+  uint32_t amin[2] = {0x7FFF7FFFu, 0x7FFF7FFFu}, bmax[2] = {0x80008000u, 0x80008000u};
 #pragma unroll
   for (int i = 0; i < 12; i++) {
-    uint32_t tE, tO;
-    r1_lanes(fr[i], e, i, tE, tO);
-    okw[i] = tE & tO;
+    const uint32_t vE = even_bytes(fr[i]), vO = odd_bytes(fr[i]);
+    amin[i & 1] = __viaddmin_s16x2(vE, e.NlE[i], amin[i & 1]);
+    bmax[i & 1] = __viaddmax_s16x2(vE, e.NhE[i], bmax[i & 1]);
+    amin[i & 1] = __viaddmin_s16x2(vO, e.NlO[i], amin[i & 1]);
+    bmax[i & 1] = __viaddmax_s16x2(vO, e.NhO[i], bmax[i & 1]);
   }
-  // balanced AND tree (no serial dependency chain)
-  const uint32_t ok = ((okw[0] & okw[1] & okw[2]) & (okw[3] & okw[4] & okw[5])) &
-                      ((okw[6] & okw[7] & okw[8]) & (okw[9] & okw[10] & okw[11]));
-  const bool all_inside = (ok & 0x01000100u) == 0x01000100u;
+  const uint32_t am = __vimin3_s16x2(amin[0], amin[1], amin[1]);
+  const uint32_t bm = __vimax3_s16x2(bmax[0], bmax[1], bmax[1]);
+  const bool all_inside = ((am | ~bm) & 0x80008000u) == 0u;
   if (!__any_sync(0xFFFFFFFFu, !all_inside)) return 0u;   // whole warp is background
   slow = true;
 
@@ -203,7 +214,7 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
   for (int i = 0; i < 12; i++) {
     uint32_t tE, tO;
     r1_lanes(fr[i], e, i, tE, tO);
-    const uint32_t f4 = ((tE >> 8) & 1u) | ((tO >> 7) & 2u) | ((tE >> 22) & 4u) | ((tO >> 21) & 8u);
+    const uint32_t f4 = ((tE >> 15) & 1u) | ((tO >> 14) & 2u) | ((tE >> 29) & 4u) | ((tO >> 28) & 8u);
     inside |= (uint64_t)f4 << (4 * i);
   }
   uint32_t bits = 0;
