@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-frames", type=int, default=0)
+    ap.add_argument("--diag-no-hand", action="store_true",
+                    help="diagnostic only: frames without the hand (pure background path)")
     return ap.parse_args()
 
 
@@ -208,7 +210,13 @@ def main():
     frames_by_batch = []
     for b in use:
         ks = list(range(b * B, min(cfg.n_proc, (b + 1) * B)))
-        frames_by_batch.append((ks, synth.frames_dev(cfg, 0, ks, device=dev)))
+        if args.diag_no_hand:
+            pf = synth.frame_params(cfg, 0, ks)
+            pf[:, 4] = 0
+            frames_by_batch.append((ks, synth.gen_dev(cfg.W, cfg.H, cfg.seed, 0, pf,
+                                                      synth.clutter(cfg, 0), device=dev)))
+        else:
+            frames_by_batch.append((ks, synth.frames_dev(cfg, 0, ks, device=dev)))
     learn = synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True, device=dev)
 
     fz = Fizi(cfg.W, cfg.H, n_streams=1, max_batch=B, device=local)

@@ -155,43 +155,39 @@ __device__ __forceinline__ void r1_lanes(uint32_t w, const EnvRegs& e, int i, ui
   tO = ~aO & bO;
 }
 
-// Process this thread's 16 pixels of one frame.  Returns the 16 merged bits
-// (bit p = pixel p); adds the pixels' luma to luma_acc when !kLut.
-template <bool kLut>
-__device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e, bool valid,
-                                          const uint8_t* lut_s, int S, int a1, int a2,
-                                          uint32_t& luma_acc, bool& slow) {
-  uint32_t fr[12];
-  {
-    const uint4* q = reinterpret_cast<const uint4*>(px48);
-    const uint4 q0 = q[0], q1 = q[1], q2 = q[2];
-    fr[0] = q0.x; fr[1] = q0.y; fr[2] = q0.z; fr[3] = q0.w;
-    fr[4] = q1.x; fr[5] = q1.y; fr[6] = q1.z; fr[7] = q1.w;
-    fr[8] = q2.x; fr[9] = q2.y; fr[10] = q2.z; fr[11] = q2.w;
-  }
-  if (!valid) {
+__device__ __forceinline__ void load48(const uint8_t* px48, bool valid, uint32_t (&fr)[12]) {
+  const uint4* q = reinterpret_cast<const uint4*>(px48);
+  uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0, q2 = q0;
+  if (valid) { q0 = q[0]; q1 = q[1]; q2 = q[2]; }
+  fr[0] = q0.x; fr[1] = q0.y; fr[2] = q0.z; fr[3] = q0.w;
+  fr[4] = q1.x; fr[5] = q1.y; fr[6] = q1.z; fr[7] = q1.w;
+  fr[8] = q2.x; fr[9] = q2.y; fr[10] = q2.z; fr[11] = q2.w;
+}
+
+__device__ __forceinline__ void apply_lut(uint32_t (&fr)[12], const uint8_t* lut_s) {
 #pragma unroll
-    for (int i = 0; i < 12; i++) fr[i] = 0;
+  for (int i = 0; i < 12; i++) {
+    const uint32_t w = fr[i];
+    fr[i] = (uint32_t)lut_s[w & 0xFF] | ((uint32_t)lut_s[(w >> 8) & 0xFF] << 8) |
+            ((uint32_t)lut_s[(w >> 16) & 0xFF] << 16) | ((uint32_t)lut_s[w >> 24] << 24);
   }
-  if (kLut) {
+}
+
+// Exact sum of 299 r + 587 g + 114 b over the thread's 16 pixels.
+__device__ __forceinline__ uint32_t luma16(const uint32_t (&fr)[12]) {
+  uint32_t alo[4] = {0, 0, 0, 0}, ahi[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int i = 0; i < 12; i++) {
-      const uint32_t w = fr[i];
-      fr[i] = (uint32_t)lut_s[w & 0xFF] | ((uint32_t)lut_s[(w >> 8) & 0xFF] << 8) |
-              ((uint32_t)lut_s[(w >> 16) & 0xFF] << 16) | ((uint32_t)lut_s[w >> 24] << 24);
-    }
-  } else {
-    // four independent accumulator chains per weight set (ILP)
-    uint32_t alo[4] = {0, 0, 0, 0}, ahi[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int i = 0; i < 12; i++) {
-      alo[i & 3] = __dp4a(fr[i], kWlo[i % 3], alo[i & 3]);
-      ahi[i & 3] = __dp4a(fr[i], kWhi[i % 3], ahi[i & 3]);
-    }
-    luma_acc += (((ahi[0] + ahi[1]) + (ahi[2] + ahi[3])) << 8) + ((alo[0] + alo[1]) + (alo[2] + alo[3]));
+  for (int i = 0; i < 12; i++) {
+    alo[i & 3] = __dp4a(fr[i], kWlo[i % 3], alo[i & 3]);
+    ahi[i & 3] = __dp4a(fr[i], kWhi[i % 3], ahi[i & 3]);
   }
-  // R1 envelope test on all 48 bytes: running min of (v - lo) and max of
-  // (v - hi - 1) per 16-bit lane, four independent accumulator chains
+  return (((ahi[0] + ahi[1]) + (ahi[2] + ahi[3])) << 8) + ((alo[0] + alo[1]) + (alo[2] + alo[3]));
+}
+
+// R1 on all 48 bytes: true iff every byte lies inside its envelope (then the
+// 16 pixels are background and their merged bits are 0).  Running min of
+// (v - lo) and max of (v - hi - 1) per 16-bit lane, four accumulator chains.
+__device__ __forceinline__ bool all_inside16(const uint32_t (&fr)[12], const EnvRegs& e) {
   uint32_t amin[2] = {0x7FFF7FFFu, 0x7FFF7FFFu}, bmax[2] = {0x80008000u, 0x80008000u};
 #pragma unroll
   for (int i = 0; i < 12; i++) {
@@ -203,12 +199,12 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
   }
   const uint32_t am = __vimin3_s16x2(amin[0], amin[1], amin[1]);
   const uint32_t bm = __vimax3_s16x2(bmax[0], bmax[1], bmax[1]);
-  const bool all_inside = ((am | ~bm) & 0x80008000u) == 0u;
-  if (!__any_sync(0xFFFFFFFFu, !all_inside)) return 0u;   // whole warp is background
-  slow = true;
+  return ((am | ~bm) & 0x80008000u) == 0u;
+}
 
-  // Per-pixel path (rare: warps touching the hand): 48 per-byte inside flags,
-  // then R1 & R2 & R3 per pixel, 4 pixels (3 words) per rolled iteration.
+// Per-pixel R1 & R2 & R3 of the thread's 16 pixels (bit p = pixel p).
+__device__ __forceinline__ uint32_t slow_bits16(uint32_t (&fr)[12], const EnvRegs& e, int S,
+                                                int a1, int a2) {
   uint64_t inside = 0;
 #pragma unroll
   for (int i = 0; i < 12; i++) {
@@ -236,6 +232,22 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
       bits |= (r1 & gray_and_skin(byte(b), byte(b + 1), byte(b + 2), S, a1, a2)) << (4 * g + q);
     }
   }
+  return bits;
+}
+
+// Process this thread's 16 pixels of one frame in one go (LUT re-test path).
+template <bool kLut>
+__device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e, bool valid,
+                                          const uint8_t* lut_s, int S, int a1, int a2,
+                                          uint32_t& luma_acc, bool& slow) {
+  uint32_t fr[12];
+  load48(px48, valid, fr);
+  if (kLut) apply_lut(fr, lut_s);
+  else luma_acc += luma16(fr);
+  const bool all_inside = all_inside16(fr, e) || !valid;
+  if (!__any_sync(0xFFFFFFFFu, !all_inside)) return 0u;   // whole warp is background
+  slow = true;
+  const uint32_t bits = slow_bits16(fr, e, S, a1, a2);
   return valid ? bits : 0u;
 }
 
@@ -301,14 +313,17 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     if (warp != 0) pol = policy_evict_first();
     const uint8_t* my = sm + warp * kChunkBytes + 48 * lane;
     uint32_t* dstw = a.bitA + (uint64_t)c * 16 + (lane >> 1);
+    uint32_t deferred = 0;                                   // frames with non-background pixels
+    uint32_t luma_lane = 0;                                  // lane i: this warp's luma of frame i
     for (uint32_t i = 0; i < nf; i++) {
       const uint32_t s = i & (kStages - 1);
       const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
       mbar_wait(&full[s], (i / kStages) & 1u);
-      uint32_t y = 0;
-      bool slow = false;
-      const uint32_t bits = seg16<false>(my + s * kTileBytes, e, valid, nullptr, (int)a.S,
-                                         (int)a.a1, (int)a.a2, y, slow);
+      uint32_t fr[12];
+      load48(my + s * kTileBytes, valid, fr);
+      uint32_t y = luma16(fr);
+      const bool inside = all_inside16(fr, e) || !valid;
+      const bool slow = __any_sync(0xFFFFFFFFu, !inside);
       const uint32_t fnext = __shfl_sync(0xFFFFFFFFu, fid_lane, (i + kStages) & 31);
       __syncwarp();                                          // this warp is done with stage s
       if (lane == 0 && atomicAdd(&empty_cnt[s], 1u) == n_active - 1) {
@@ -320,19 +335,28 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
         }
       }
       y = warp_sum_u32(y);
-      if (!slow) {
-        if (!(lane & 1) && valid) dstw[(uint64_t)f * a.words_per_frame] = 0u;
-      } else {
-        const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
-        uint32_t pc = 0;
-        if (!(lane & 1) && valid) {
-          dstw[(uint64_t)f * a.words_per_frame] = word;
-          pc = __popc(word);
-        }
-        pc = warp_sum_u32(pc);
-        if (lane == 0 && pc) atomicAdd(&acc_f[i], pc);
+      if ((uint32_t)lane == i) luma_lane = y;
+      if (slow) deferred |= 1u << i;
+      else if (!(lane & 1) && valid) dstw[(uint64_t)f * a.words_per_frame] = 0u;
+    }
+    if ((uint32_t)lane < nf) atomicAdd(&acc_y[lane], luma_lane);
+    // deferred per-pixel work (chunks touching the hand): re-read the chunk
+    while (deferred) {
+      const uint32_t i = __ffs(deferred) - 1;
+      deferred &= deferred - 1;
+      const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
+      uint32_t fr[12];
+      load48(a.frames + (uint64_t)f * a.frame_bytes + coff + 48 * lane, valid, fr);
+      uint32_t bits = slow_bits16(fr, e, (int)a.S, (int)a.a1, (int)a.a2);
+      bits = valid ? bits : 0u;
+      const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
+      uint32_t pc = 0;
+      if (!(lane & 1) && valid) {
+        dstw[(uint64_t)f * a.words_per_frame] = word;
+        pc = __popc(word);
       }
-      if (lane == 0) atomicAdd(&acc_y[i], y);
+      pc = warp_sum_u32(pc);
+      if (lane == 0 && pc) atomicAdd(&acc_f[i], pc);
     }
   }
   __syncthreads();                                           // flush the CTA's sums
