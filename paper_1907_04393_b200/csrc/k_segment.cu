@@ -265,6 +265,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   __shared__ uint32_t empty_cnt[kStages];
   // per-frame partial sums of the CTA: luma <= 8 warps * 512 px * 255000 < 2^32
   __shared__ uint32_t acc_y[kFrameGroup], acc_f[kFrameGroup];
+  // deferred (frame, warp) items whose chunk has non-background pixels
+  __shared__ uint16_t q_item[kFrameGroup * kWarpsPerCta];
+  __shared__ uint32_t q_tail, q_head;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t tile = blockIdx.x, grp = blockIdx.y;
@@ -283,6 +286,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   if (tid < kFrameGroup) { acc_y[tid] = 0; acc_f[tid] = 0; }
   if (tid < kStages) empty_cnt[tid] = 0;
   if (tid == 0) {
+    q_tail = 0;
+    q_head = 0;
 #pragma unroll
     for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
     fence_mbar_init();
@@ -313,7 +318,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     if (warp != 0) pol = policy_evict_first();
     const uint8_t* my = sm + warp * kChunkBytes + 48 * lane;
     uint32_t* dstw = a.bitA + (uint64_t)c * 16 + (lane >> 1);
-    uint32_t deferred = 0;                                   // frames with non-background pixels
     uint32_t luma_lane = 0;                                  // lane i: this warp's luma of frame i
     for (uint32_t i = 0; i < nf; i++) {
       const uint32_t s = i & (kStages - 1);
@@ -336,28 +340,45 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
       }
       y = warp_sum_u32(y);
       if ((uint32_t)lane == i) luma_lane = y;
-      if (slow) deferred |= 1u << i;
-      else if (!(lane & 1) && valid) dstw[(uint64_t)f * a.words_per_frame] = 0u;
+      if (slow) {
+        if (lane == 0) q_item[atomicAdd(&q_tail, 1u)] = (uint16_t)((i << 3) | warp);
+      } else if (!(lane & 1) && valid) {
+        dstw[(uint64_t)f * a.words_per_frame] = 0u;
+      }
     }
     if ((uint32_t)lane < nf) atomicAdd(&acc_y[lane], luma_lane);
-    // deferred per-pixel work (chunks touching the hand): re-read the chunk
-    while (deferred) {
-      const uint32_t i = __ffs(deferred) - 1;
-      deferred &= deferred - 1;
-      const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
-      uint32_t fr[12];
-      load48(a.frames + (uint64_t)f * a.frame_bytes + coff + 48 * lane, valid, fr);
-      uint32_t bits = slow_bits16(fr, e, (int)a.S, (int)a.a1, (int)a.a2);
-      bits = valid ? bits : 0u;
-      const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
-      uint32_t pc = 0;
-      if (!(lane & 1) && valid) {
-        dstw[(uint64_t)f * a.words_per_frame] = word;
-        pc = __popc(word);
-      }
-      pc = warp_sum_u32(pc);
-      if (lane == 0 && pc) atomicAdd(&acc_f[i], pc);
+  }
+  __syncthreads();
+  // deferred per-pixel work (chunks touching the hand), shared by all warps
+  // of the CTA: re-read the chunk and its envelope (L2) and test per pixel
+  const uint32_t nq = q_tail;
+  while (true) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(&q_head, 1u);
+    item = __shfl_sync(0xFFFFFFFFu, item, 0);
+    if (item >= nq) break;
+    const uint32_t it = q_item[item];
+    const uint32_t i = it >> 3, w = it & 7u;
+    const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
+    const uint32_t cq = tile * kWarpsPerCta + w;
+    const uint64_t coff = (uint64_t)cq * kChunkBytes;
+    const bool valid = coff + 48u * lane < a.frame_bytes;
+    EnvRegs e;
+    const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * lane;
+    if (valid) load_env(e, elo, elo + a.env_plane);
+    else zero_env(e);
+    uint32_t fr[12];
+    load48(a.frames + (uint64_t)f * a.frame_bytes + coff + 48 * lane, valid, fr);
+    uint32_t bits = slow_bits16(fr, e, (int)a.S, (int)a.a1, (int)a.a2);
+    bits = valid ? bits : 0u;
+    const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
+    uint32_t pc = 0;
+    if (!(lane & 1) && valid) {
+      a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)cq * 16 + (lane >> 1)] = word;
+      pc = __popc(word);
     }
+    pc = warp_sum_u32(pc);
+    if (lane == 0 && pc) atomicAdd(&acc_f[i], pc);
   }
   __syncthreads();                                           // flush the CTA's sums
   if (tid < (int)nf) {
