@@ -420,16 +420,31 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
   mp.band = band;
   mp.first = first;
   {                                     // stage the band (all loads in flight), detect zero bands
-    const int rows = kBandRows + 8 * R;
-    const uint32_t P = a.P;
-    const uint32_t total = (uint32_t)rows * P;
+    constexpr int kRows = kBandRows + 8 * R;
     uint32_t any = 0;
-#pragma unroll 4
-    for (uint32_t i = threadIdx.x; i < total; i += 32) {
-      const int yy = first + (int)(i / P);
-      const uint32_t v = (yy >= 0 && yy < (int)a.H) ? __ldg(mp.Af + (uint64_t)yy * P + (i % P)) : 0u;
-      band[i] = v;
-      any |= v;
+    const uint32_t P = a.P;
+    const int lane = mp.lane;
+    uint32_t* dst = band + lane * WPL;
+#pragma unroll
+    for (int rr = 0; rr < kRows; rr++) {
+      const int yy = first + rr;
+      const bool rin = yy >= 0 && yy < (int)a.H;
+      const uint32_t* src = mp.Af + (uint64_t)(rin ? yy : 0) * P + lane * WPL;
+      RowW<WPL> v;
+      if (WPL == 2 && (P & 1u) == 0) {                       // 8-byte aligned word pairs
+        uint2 t = make_uint2(0u, 0u);
+        if (rin && mp.wmask[0]) t = __ldg(reinterpret_cast<const uint2*>(src));
+        v.w[0] = t.x;
+        v.w[WPL - 1] = t.y;
+      } else {
+#pragma unroll
+        for (int j = 0; j < WPL; j++) v.w[j] = (rin && mp.wmask[j]) ? __ldg(src + j) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < WPL; j++) {
+        if (lane * WPL + j < (int)P) dst[rr * P + j] = v.w[j];
+        any |= v.w[j];
+      }
     }
     if (!__any_sync(0xFFFFFFFFu, any != 0u)) {
       mp.zero_band();
@@ -437,8 +452,6 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
     }
     __syncwarp();
   }
-#pragma unroll
-  for (int q = 0; q < 2 * R + 1; q++) mp.pre[q] = mp.load_row(first + q);
   for (int yi = first; yi < last; yi += 2 * R + 1) unrolled_steps<R, WPL, 0>(mp, yi, last);
 }
 
