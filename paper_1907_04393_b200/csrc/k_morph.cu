@@ -452,6 +452,8 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
     }
     __syncwarp();
   }
+#pragma unroll
+  for (int q = 0; q < 2 * R + 1; q++) mp.pre[q] = mp.load_row(first + q);
   for (int yi = first; yi < last; yi += 2 * R + 1) unrolled_steps<R, WPL, 0>(mp, yi, last);
 }
 
