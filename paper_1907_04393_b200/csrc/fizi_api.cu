@@ -235,7 +235,9 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   if (e != cudaSuccess) return cuda_fail(c, e, "memset");
   bool single = true;
   for (uint32_t i = 1; i < n && single; i++) single = sof[i] == sof[0];
-  const int fold = !track ? -2 : (single ? (int)sof[0] : -1);
+  int fold = !track ? -2 : (single ? (int)sof[0] : -1);
+  static const bool kNoFoldDiag = getenv("FIZI_DIAG_NO_FOLD") != nullptr;   // timing experiments only
+  if (kNoFoldDiag) fold = -2;
   // the u8 mask is written by the register-pipelined morphology when it runs
   const bool fused_mask = c.fast && c.P <= 128 && c.p.se_radius <= 4;
   cudaStream_t sd = c.side;

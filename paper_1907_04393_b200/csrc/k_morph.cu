@@ -241,6 +241,7 @@ struct MorphPipe {
   uint32_t lmask, rmask, wmask[WPL];       // lane-edge masks, valid bits of each word
   const uint32_t* Af;
   const uint32_t* band;                    // shared-memory copy of input rows [first, last)
+                                           // (output rows overwrite consumed input rows)
   int first;
   uint32_t* Of;
   uint8_t* Mf;                             // u8 mask of the frame (W % 32 == 0) or nullptr
@@ -345,56 +346,96 @@ struct MorphPipe {
     }
   }
 
+  // output row yo: u8 mask + O row to global memory, words kept in the band
+  // buffer (the slot of input row yo was consumed long before) and the row's
+  // run count in lane (yo - y0); runs are emitted after the band is done
+  uint32_t my_cnt = 0;
+
   __device__ __forceinline__ void emit(const RowW<WPL>& o4, int yo) {
     write_mask_row(o4, yo);
     const uint32_t prev_last = __shfl_up_sync(0xFFFFFFFFu, o4.w[WPL - 1], 1) & lmask;
-    const uint32_t next_first = __shfl_down_sync(0xFFFFFFFFu, o4.w[0], 1) & rmask;
-    uint32_t st[WPL], en[WPL], ns = 0, ne = 0;
+    uint32_t ns = 0;
+    uint32_t* slot = const_cast<uint32_t*>(band) + (yo - first) * (int)P + lane * WPL;
 #pragma unroll
     for (int j = 0; j < WPL; j++) {
       const uint32_t k = (uint32_t)(lane * WPL + j);
       const uint32_t w = o4.w[j];
-      if (k < P) Of[(uint64_t)yo * P + k] = w;
+      if (k < P) {
+        Of[(uint64_t)yo * P + k] = w;
+        slot[j] = w;
+      }
       const uint32_t pv = j > 0 ? o4.w[j - 1] : prev_last;
-      const uint32_t nx = j + 1 < WPL ? o4.w[j + 1] : next_first;
-      st[j] = w & ~((w << 1) | (pv >> 31));
-      en[j] = w & ~((w >> 1) | (nx << 31));
-      ns += __popc(st[j]);
-      ne += __popc(en[j]);
+      ns += __popc(w & ~((w << 1) | (pv >> 31)));
     }
     const uint32_t cnt = warp_sum_u32(ns);
-    uint32_t base = 0;
-    if (lane == 0) {
-      if (cnt) base = atomicAdd(a.frame_runs + f, cnt);
-      a.row_cnt[(uint64_t)f * H + yo] = cnt;
-      a.row_base[(uint64_t)f * H + yo] = base;
-    }
-    if (cnt == 0) return;
-    base = __shfl_sync(0xFFFFFFFFu, base, 0);
-    uint32_t ps = ns, pe = ne;
+    if (lane == yo - y0) my_cnt = cnt;
+  }
+
+  // one atomic reservation for the band's runs, then (x0, x1, y) per run
+  __device__ __forceinline__ void emit_runs() {
+    uint32_t incl = my_cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, ps, d);
-      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pe, d);
-      if (lane >= d) { ps += u; pe += v; }
+      const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= d) incl += u;
     }
-    uint32_t is = base + ps - ns, ie = base + pe - ne;
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    uint32_t base = 0;
+    if (lane == 0 && total) base = atomicAdd(a.frame_runs + f, total);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    const uint32_t row_base = base + incl - my_cnt;
+    if (lane < y_end - y0) {
+      a.row_cnt[(uint64_t)f * H + y0 + lane] = my_cnt;
+      a.row_base[(uint64_t)f * H + y0 + lane] = my_cnt ? row_base : 0u;
+    }
+    if (!total) return;
+    __syncwarp();
+    for (int r = 0; r < y_end - y0; r++) {
+      const uint32_t rc = __shfl_sync(0xFFFFFFFFu, my_cnt, r);
+      const uint32_t rbase = __shfl_sync(0xFFFFFFFFu, row_base, r);
+      if (!rc) continue;
+      const int yo = y0 + r;
+      const uint32_t* row = band + (yo - first) * (int)P + lane * WPL;
+      uint32_t w[WPL];
 #pragma unroll
-    for (int j = 0; j < WPL; j++) {
-      const uint32_t k = (uint32_t)(lane * WPL + j);
-      uint32_t s0 = st[j], e0 = en[j];
-      while (s0) {
-        const uint32_t bit = __ffs(s0) - 1;
-        s0 &= s0 - 1;
-        runs[is].x0 = (uint16_t)(32 * k + bit);
-        runs[is].y = (uint16_t)yo;
-        is++;
+      for (int j = 0; j < WPL; j++) w[j] = (lane * WPL + j < (int)P) ? row[j] : 0u;
+      const uint32_t prev_last = __shfl_up_sync(0xFFFFFFFFu, w[WPL - 1], 1) & lmask;
+      const uint32_t next_first = __shfl_down_sync(0xFFFFFFFFu, w[0], 1) & rmask;
+      uint32_t st[WPL], en[WPL], ns = 0, ne = 0;
+#pragma unroll
+      for (int j = 0; j < WPL; j++) {
+        const uint32_t pv = j > 0 ? w[j - 1] : prev_last;
+        const uint32_t nx = j + 1 < WPL ? w[j + 1] : next_first;
+        st[j] = w[j] & ~((w[j] << 1) | (pv >> 31));
+        en[j] = w[j] & ~((w[j] >> 1) | (nx << 31));
+        ns += __popc(st[j]);
+        ne += __popc(en[j]);
       }
-      while (e0) {
-        const uint32_t bit = __ffs(e0) - 1;
-        e0 &= e0 - 1;
-        runs[ie].x1 = (uint16_t)(32 * k + bit);
-        ie++;
+      uint32_t ps = ns, pe = ne;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, ps, d);
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pe, d);
+        if (lane >= d) { ps += u; pe += v; }
+      }
+      uint32_t is = rbase + ps - ns, ie = rbase + pe - ne;
+#pragma unroll
+      for (int j = 0; j < WPL; j++) {
+        const uint32_t k = (uint32_t)(lane * WPL + j);
+        uint32_t s0 = st[j], e0 = en[j];
+        while (s0) {
+          const uint32_t bit = __ffs(s0) - 1;
+          s0 &= s0 - 1;
+          runs[is].x0 = (uint16_t)(32 * k + bit);
+          runs[is].y = (uint16_t)yo;
+          is++;
+        }
+        while (e0) {
+          const uint32_t bit = __ffs(e0) - 1;
+          e0 &= e0 - 1;
+          runs[ie].x1 = (uint16_t)(32 * k + bit);
+          ie++;
+        }
       }
     }
   }
@@ -455,6 +496,8 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
 #pragma unroll
   for (int q = 0; q < 2 * R + 1; q++) mp.pre[q] = mp.load_row(first + q);
   for (int yi = first; yi < last; yi += 2 * R + 1) unrolled_steps<R, WPL, 0>(mp, yi, last);
+  __syncwarp();
+  mp.emit_runs();
 }
 
 uint32_t morph_tile_rows(const Ctx& c, size_t smem_budget) {
