@@ -308,37 +308,41 @@ struct MorphPipe {
   }
 
   // the final u8 mask row (one byte per pixel, a6 output): speculatively O;
-  // the labelling kernel clears the pixels of components the area filter drops
+  // the labelling kernel clears the pixels of components the area filter
+  // drops.  Warp-coalesced: lane l writes bytes 16l + 512m of the row (16
+  // pixels = half a word), fetched from the owning lane by shuffles.
   __device__ __forceinline__ void write_mask_row(const RowW<WPL>& o, int yo) const {
     if (!Mf) return;
+    uint8_t* row = Mf + (uint64_t)yo * a.W;
 #pragma unroll
-    for (int j = 0; j < WPL; j++) {
-      const uint32_t k = (uint32_t)(lane * WPL + j);
-      if (k >= P) continue;
-      const uint32_t w = o.w[j];
-      uint4 lo, hi;
-      lo.x = expand4(w & 0xF); lo.y = expand4((w >> 4) & 0xF);
-      lo.z = expand4((w >> 8) & 0xF); lo.w = expand4((w >> 12) & 0xF);
-      hi.x = expand4((w >> 16) & 0xF); hi.y = expand4((w >> 20) & 0xF);
-      hi.z = expand4((w >> 24) & 0xF); hi.w = expand4(w >> 28);
-      uint4* dst = reinterpret_cast<uint4*>(Mf + (uint64_t)yo * a.W + 32ull * k);
-      __stcs(dst, lo);
-      __stcs(dst + 1, hi);
+    for (int m = 0; m < 2 * WPL; m++) {                       // 16 words (512 px) per m
+      const uint32_t hw = (uint32_t)lane / 2 + 16u * m;         // word index of my 16 pixels
+      const int src = (int)(hw / WPL);
+      uint32_t w = 0;
+#pragma unroll
+      for (int j = 0; j < WPL; j++) {
+        const uint32_t v = __shfl_sync(0xFFFFFFFFu, o.w[j], src);
+        if ((int)(hw % WPL) == j) w = v;
+      }
+      if (hw < P) {
+        const uint32_t b = (w >> (16 * (lane & 1))) & 0xFFFFu;
+        uint4 q;
+        q.x = expand4(b & 0xF); q.y = expand4((b >> 4) & 0xF);
+        q.z = expand4((b >> 8) & 0xF); q.w = expand4(b >> 12);
+        __stcs(reinterpret_cast<uint4*>(row + 16ull * (hw * 2 + (lane & 1))), q);
+      }
     }
   }
 
   // band whose input rows are all zero: every output row is zero
   __device__ __forceinline__ void zero_band() const {
-    RowW<WPL> z;
-#pragma unroll
-    for (int j = 0; j < WPL; j++) z.w[j] = 0u;
     for (int yo = y0; yo < y_end; yo++) {
-#pragma unroll
-      for (int j = 0; j < WPL; j++) {
-        const uint32_t k = (uint32_t)(lane * WPL + j);
-        if (k < P) Of[(uint64_t)yo * P + k] = 0u;
+      for (uint32_t k = lane; k < P; k += 32) Of[(uint64_t)yo * P + k] = 0u;
+      if (Mf) {
+        uint8_t* row = Mf + (uint64_t)yo * a.W;
+        for (uint32_t b = 16u * lane; b < a.W; b += 512u)
+          __stcs(reinterpret_cast<uint4*>(row + b), make_uint4(0u, 0u, 0u, 0u));
       }
-      write_mask_row(z, yo);
       if (lane == 0) {
         a.row_cnt[(uint64_t)f * H + yo] = 0u;
         a.row_base[(uint64_t)f * H + yo] = 0u;
