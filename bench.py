@@ -51,6 +51,21 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(seg_bytes):
+    """DRAM bytes per launch of the fused kernel from the latest committed
+    ncu --set full capture (profiles/r*_seg_fast_traffic.json), if it was
+    taken on the same per-launch workload."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_seg_fast_traffic.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    if abs(d.get("algorithmic_bytes_per_launch", 0) - seg_bytes) > 1:
+        return None, None
+    return d["dram_bytes_per_launch"], os.path.relpath(files[-1], ROOT)
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -202,21 +217,24 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     B = args.batch or cfg.batch
-    n_batches = math.ceil(cfg.n_proc / B)
-    mine = [b for b in range(n_batches) if b % world == rank]
-    # resident frames: the rank's batches needed by warmup + steps (cycled)
-    need = min(len(mine), args.warmup + args.steps)
-    use = mine[:need]
-    frames_by_batch = []
-    for b in use:
-        ks = list(range(b * B, min(cfg.n_proc, (b + 1) * B)))
+    from paper_1907_04393_b200 import shard
+    # round r: rank takes batch r*world + rank (weak scaling, B frames per rank
+    # per step); the resident rounds are cycled if warmup + steps exceeds them
+    need = min(shard.n_rounds(cfg.n_proc, B, world), args.warmup + args.steps)
+    frames_by_round = []
+    for rnd in range(need):
+        b = shard.round_batch(cfg.n_proc, B, world, rank, rnd)
+        if b is None:
+            frames_by_round.append(None)
+            continue
+        ks = list(range(b.k0, b.k1))
         if args.diag_no_hand:
             pf = synth.frame_params(cfg, 0, ks)
             pf[:, 4] = 0
-            frames_by_batch.append((ks, synth.gen_dev(cfg.W, cfg.H, cfg.seed, 0, pf,
-                                                      synth.clutter(cfg, 0), device=dev)))
+            fr = synth.gen_dev(cfg.W, cfg.H, cfg.seed, 0, pf, synth.clutter(cfg, 0), device=dev)
         else:
-            frames_by_batch.append((ks, synth.frames_dev(cfg, 0, ks, device=dev)))
+            fr = synth.frames_dev(cfg, 0, ks, device=dev)
+        frames_by_round.append((ks, fr))
     learn = synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True, device=dev)
 
     fz = Fizi(cfg.W, cfg.H, n_streams=1, max_batch=B, device=local)
@@ -226,34 +244,25 @@ def main():
     gathered = torch.empty((world * B, RESULT_BYTES), dtype=torch.uint8, device=dev)
     del learn
 
-    def batch_len(r, i):
-        mine_r = [b for b in range(n_batches) if b % world == r]
-        use_r = mine_r[:min(len(mine_r), args.warmup + args.steps)]
-        if not use_r:
-            return 0
-        b = use_r[i % len(use_r)]
-        return min(B, cfg.n_proc - b * B)
-
     def step(i):
-        ks, fr = frames_by_batch[i % len(frames_by_batch)]
-        n = len(ks)
-        t = np.asarray([synth.t_ms(k) for k in ks], np.int64)
-        # timestamps keep increasing across passes over the resident batches
-        t = t + (i // len(frames_by_batch)) * synth.t_ms(cfg.n_proc)
-        if world == 1:                 # the whole path in one call (fold fused into labelling)
-            fz.process_frames(fr[:n], t_ms=t, masks=masks[:n], results=res[:n])
-            return n
-        fz.segment_frames(fr[:n], t_ms=t, masks=masks[:n], results=res[:n])
-        if world > 1:
-            # records of this step's batches (consecutive in frame order) from every rank;
-            # each rank knows every rank's batch size for this step without communication
-            dist.all_gather_into_tensor(gathered, res)
-            for r in range(world):
-                nr = batch_len(r, i)
-                if nr:
-                    fz.track(gathered[r * B: r * B + nr])
-        else:
-            fz.track(res[:n])
+        rnd = i % need
+        item = frames_by_round[rnd]
+        n = 0
+        if item is not None:
+            ks, fr = item
+            n = len(ks)
+            # timestamps keep increasing across passes over the resident rounds
+            t = np.asarray([synth.t_ms(k) for k in ks], np.int64)
+            t = t + (i // need) * synth.t_ms(cfg.n_proc)
+            if world == 1:             # the whole path in one call (fold fused into labelling)
+                fz.process_frames(fr[:n], t_ms=t, masks=masks[:n], results=res[:n])
+                return n
+            fz.segment_frames(fr[:n], t_ms=t, masks=masks[:n], results=res[:n])
+        # a8 across ranks: gather the step's records (frame order = rank order)
+        # and fold them on every rank
+        dist.all_gather_into_tensor(gathered, res)
+        for off, cnt in shard.gathered_slices(cfg.n_proc, B, world, rnd):
+            fz.track(gathered[off: off + cnt])
         return n
 
     for i in range(args.warmup):
@@ -304,10 +313,12 @@ def main():
     seg_gbs = seg_bytes * args.steps / (seg_ms / 1e3) / 1e9 if seg_n else None
     step_bytes = B * (3 * N + N) + 6 * N       # whole-path algorithmic bytes per step
     step_ms = ms_max / args.steps
+    traffic, traffic_src = ncu_traffic(seg_bytes) if launches_per_step == 1 else (None, None)
     roofline = {
         "bound": "hbm", "kernel": "seg_fast_kernel (fused luma + R1/R2/R3, a2+a3)",
         "achieved": seg_gbs, "peak": hbm, "unit": "GB/s",
-        "frac": (seg_gbs / hbm) if seg_gbs else None, "traffic": None,
+        "frac": (seg_gbs / hbm) if seg_gbs else None, "traffic": traffic,
+        "traffic_source": traffic_src,
         "peak_kind": peak_kind,
         "algorithmic_bytes_per_step": seg_bytes,
         "launches_per_step": launches_per_step,
@@ -327,7 +338,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": f"C{cfg.cid}: {cfg.W}x{cfg.H} stream, {cfg.n_proc} frames, "
                                f"batches of {B} per launch (BASELINE.json configs[{cfg.cid - 1}])",
-                   "frames_per_step_per_gpu": B, "resident_batches_per_gpu": len(use),
+                   "frames_per_step_per_gpu": B, "resident_batches_per_gpu": need,
                    "l2": f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step",
                    "parallelism": f"frames sharded by batch, dp{world}"},
         "gpu_launches": launches,
@@ -343,8 +354,8 @@ def main():
         fe.learn_background(learn, margin=synth.MARGIN)
         del learn
         hosts = []
-        for j in range(min(2, len(frames_by_batch))):
-            ks, fr = frames_by_batch[j]
+        for item in [x for x in frames_by_round if x is not None][:2]:
+            ks, fr = item
             h = torch.empty((len(ks), cfg.H, cfg.W, 3), dtype=torch.uint8).pin_memory()
             h.copy_(fr[: len(ks)])
             hosts.append((ks, h.numpy()))

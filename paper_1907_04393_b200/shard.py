@@ -1,0 +1,59 @@
+"""Frame sharding across ranks.
+
+Per-frame work is independent given the stream's envelope, so a stream
+of frames is cut into batches and round r gives batch r*world + rank to each
+rank (no data-path collective).  The per-frame records (128 bytes each) are
+all-gathered once per round; concatenated in rank order they are in frame
+order, so every rank can run the sequential Mouse fold (a8) over them.
+
+Pure host logic with injected callables, shared by bench.py (NCCL, libfizi)
+and tests/test_multirank.py (gloo, CPU).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class Batch:
+    index: int      # batch number in the stream
+    k0: int         # first frame (inclusive)
+    k1: int         # last frame (exclusive)
+
+    @property
+    def n(self) -> int:
+        return self.k1 - self.k0
+
+
+def n_batches(n_frames: int, batch: int) -> int:
+    return math.ceil(n_frames / batch)
+
+
+def n_rounds(n_frames: int, batch: int, world: int) -> int:
+    return math.ceil(n_batches(n_frames, batch) / world)
+
+
+def round_batch(n_frames: int, batch: int, world: int, rank: int, rnd: int) -> Batch | None:
+    """Batch rank `rank` processes in round `rnd` (rounds wrap), or None."""
+    rnd %= n_rounds(n_frames, batch, world)
+    b = rnd * world + rank
+    if b >= n_batches(n_frames, batch):
+        return None
+    k0 = b * batch
+    return Batch(b, k0, min(n_frames, k0 + batch))
+
+
+def round_sizes(n_frames: int, batch: int, world: int, rnd: int) -> list[int]:
+    """Frames each rank contributes in round `rnd` (0 for an idle rank)."""
+    out = []
+    for r in range(world):
+        b = round_batch(n_frames, batch, world, r, rnd)
+        out.append(b.n if b else 0)
+    return out
+
+
+def gathered_slices(n_frames: int, batch: int, world: int, rnd: int):
+    """(offset, n) of each rank's records inside the gathered buffer of
+    world * batch records, in frame order."""
+    return [(r * batch, n) for r, n in enumerate(round_sizes(n_frames, batch, world, rnd)) if n]

@@ -1,0 +1,125 @@
+"""World-size-2 gloo test of the sharded path's host logic.
+
+Each rank segments its batches of a config-1/2-shaped stream with the oracle
+(the per-frame, stateless part), the ranks all_gather the 128-byte records per
+round, and every rank folds the gathered records in frame order.  The result
+must equal a single-process run over all frames, on every rank.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_1907_04393_b200 import shard
+from paper_1907_04393_b200.fizi import RESULT_BYTES, RESULT_DTYPE
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _to_result_bytes(recs, ks):
+    out = np.zeros(len(recs), RESULT_DTYPE)
+    for i, (r, k) in enumerate(zip(recs, ks)):
+        out[i]["t_ms"] = r.t_ms
+        out[i]["frame_idx"] = k
+        out[i]["blob_area"] = r.blob_area
+        out[i]["cx"] = r.cx
+        out[i]["cy"] = r.cy
+    return out.view(np.uint8).reshape(len(recs), RESULT_BYTES)
+
+
+def _fold(params, rows):
+    tr = oracle.Tracker(params)
+    out = []
+    for row in rows:
+        rec = oracle.record_from_blob(int(row["t_ms"]), int(row["blob_area"]), float(row["cx"]),
+                                      float(row["cy"]))
+        tr.update(rec)
+        out.append((int(row["frame_idx"]), rec.visible, rec.clicked, rec.px, rec.py, rec.dwell_ms))
+    return out
+
+
+def _stream(cid, n_frames):
+    cfg = synth.CONFIGS[cid]
+    learn = synth.learning_frames_host(cfg)
+    lo, hi = oracle.learn(learn, synth.MARGIN)
+    frames = synth.frames_host(cfg, 0, range(n_frames))
+    return cfg, lo, hi, frames
+
+
+def _worker(rank, world, port, cid, n_frames, batch, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg, lo, hi, frames = _stream(cid, n_frames)
+    p = oracle.make_params(cfg.W, cfg.H)
+    folded = []
+    gathered = torch.zeros(world * batch, RESULT_BYTES, dtype=torch.uint8)
+    tr = oracle.Tracker(p)
+    for rnd in range(shard.n_rounds(n_frames, batch, world)):
+        b = shard.round_batch(n_frames, batch, world, rank, rnd)
+        mine = torch.zeros(batch, RESULT_BYTES, dtype=torch.uint8)
+        if b is not None:
+            ks = list(range(b.k0, b.k1))
+            recs = [oracle.segment(p, frames[k], lo, hi, t_ms=synth.t_ms(k), stages=False)[0]
+                    for k in ks]
+            mine[: b.n] = torch.from_numpy(_to_result_bytes(recs, ks))
+        parts = list(gathered.chunk(world))
+        dist.all_gather(parts, mine)
+        gathered = torch.cat(parts)
+        rows = gathered.numpy().view(RESULT_DTYPE).reshape(-1)
+        for off, n in shard.gathered_slices(n_frames, batch, world, rnd):
+            for row in rows[off: off + n]:
+                rec = oracle.record_from_blob(int(row["t_ms"]), int(row["blob_area"]),
+                                              float(row["cx"]), float(row["cy"]))
+                tr.update(rec)
+                folded.append((int(row["frame_idx"]), rec.visible, rec.clicked, rec.px, rec.py,
+                               rec.dwell_ms))
+    q.put((rank, folded))
+    dist.destroy_process_group()
+
+
+def test_shard_assignment_covers_every_frame_once():
+    for n_frames, batch, world in [(10000, 64, 1), (10000, 64, 2), (10000, 64, 8), (30, 4, 3),
+                                   (7, 8, 2)]:
+        seen = []
+        for rnd in range(shard.n_rounds(n_frames, batch, world)):
+            for r in range(world):
+                b = shard.round_batch(n_frames, batch, world, r, rnd)
+                if b:
+                    seen.extend(range(b.k0, b.k1))
+        assert seen == list(range(n_frames))
+
+
+@pytest.mark.parametrize("cid,n_frames,batch", [(1, 20, 3), (2, 12, 4)])
+def test_two_ranks_match_single_process(cid, n_frames, batch):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cid, n_frames, batch, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = dict(q.get(timeout=600) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    # reference: one process, all frames in order
+    cfg, lo, hi, frames = _stream(cid, n_frames)
+    p = oracle.make_params(cfg.W, cfg.H)
+    recs = [oracle.segment(p, frames[k], lo, hi, t_ms=synth.t_ms(k), stages=False)[0]
+            for k in range(n_frames)]
+    ref = _fold(p, _to_result_bytes(recs, range(n_frames)).view(RESULT_DTYPE).reshape(-1))
+    for r in range(world):
+        assert results[r] == ref
