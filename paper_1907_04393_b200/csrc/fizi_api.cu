@@ -129,7 +129,7 @@ cudaError_t dalloc(T** p, size_t bytes) {
 }
 
 void free_all(Ctx& c) {
-  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.luma, c.fg, c.frame_done, c.sub_done, c.bitA, c.bitO, c.bitOC,
+  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.luma, c.fg, c.frame_done, c.sub_done, c.bitA, c.bitO, c.bitOC,
                   c.row_cnt, c.row_base, c.frame_runs, c.runs, c.parent, c.stats, c.frame_t, c.fix_count,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
@@ -370,6 +370,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.lut, 256 * 256));
   A(dalloc(&c.gamma_tab, 256 * sizeof(double)));
   A(dalloc(&c.corr_tab, 256));
+  A(dalloc(&c.skin_tab, (1u << 19) * 4));
   A(dalloc(&c.luma, mb * 8));
   A(dalloc(&c.fg, mb * 4));
   A(dalloc(&c.frame_done, mb * 4));
@@ -412,6 +413,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   if (e == cudaSuccess) e = fizi::init_ccl(c);
   if (e == cudaSuccess) e = cudaMemset(c.env, 0, (uint64_t)n_streams * 2 * c.env_plane);
   if (e == cudaSuccess) e = fizi::launch_lut_table(c, 0);
+  if (e == cudaSuccess) e = fizi::launch_skin_table(c, 0);
   if (e == cudaSuccess) e = fizi::launch_tstate_reset(c, 0, n_streams, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {

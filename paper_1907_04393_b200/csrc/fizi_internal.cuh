@@ -65,6 +65,7 @@ struct Ctx {
   uint8_t* lut = nullptr;                // 256 means x 256 entries
   double* gamma_tab = nullptr;           // 256
   uint8_t* corr_tab = nullptr;           // 256
+  uint32_t* skin_tab = nullptr;          // 2^24 bits: R2 & R3 of every corrected colour
   unsigned long long* luma = nullptr;    // max_batch
   uint32_t* fg = nullptr;                // max_batch (fg_merged)
   uint32_t* frame_done = nullptr;        // max_batch (CTAs finished per frame)
@@ -134,6 +135,7 @@ __host__ __device__ __forceinline__ uint64_t env_perm_index(uint64_t b, bool fas
 // All return cudaGetLastError() of their launches; each increments
 // ctx.launches by the number of kernels launched.
 cudaError_t launch_lut_table(Ctx& c, cudaStream_t st);
+cudaError_t launch_skin_table(Ctx& c, cudaStream_t st);
 cudaError_t launch_learn(Ctx& c, uint32_t stream, const uint8_t* frames, uint32_t n,
                          uint32_t margin, cudaStream_t st);
 cudaError_t launch_env_export(Ctx& c, uint32_t stream, uint8_t* lo, uint8_t* hi, bool import,

@@ -47,6 +47,7 @@ struct SegArgs {
   const uint8_t* lut_table;
   const uint32_t* fix;          // [0] = count, [1..] = frame ids needing a LUT
   uint32_t S, a1, a2;
+  const uint32_t* skin;         // 2^24-bit R2 & R3 colour table
   uint32_t f0, n;               // frame range of this launch (sub-batch)
   // in-kernel finalisation (fast path): the last CTA of a frame writes its record
   uint32_t* frame_done;         // per-frame count of finished CTAs
@@ -108,6 +109,27 @@ __device__ __forceinline__ uint32_t gray_and_skin(int r, int g, int b, int S, in
 // lanes: NlX = -lo, NhX = -(hi + 1).  Per lane v + NlX >= 0 iff v >= lo and
 // v + NhX < 0 iff v <= hi; the fused add + min / add + max DPX instruction
 // (VIADDMNMX.S16x2) accumulates both tests over all 48 bytes.
+// R2 & R3 as a function of the corrected colour only: bit (r<<16 | g<<8 | b)
+// of a 2^24-bit table built once per context from the same exact integer
+// test (gray_and_skin), so a per-pixel test is one load + a bit extract.
+__global__ void skin_table_kernel(uint32_t* __restrict__ tab, int S, int a1, int a2) {
+  const uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x;    // word index, 2^19 words
+  if (wi >= (1u << 19)) return;
+  uint32_t w = 0;
+  for (int j = 0; j < 32; j++) {
+    const uint32_t c = wi * 32 + j;
+    w |= gray_and_skin((int)(c >> 16), (int)((c >> 8) & 0xFF), (int)(c & 0xFF), S, a1, a2) << j;
+  }
+  tab[wi] = w;
+}
+
+cudaError_t launch_skin_table(Ctx& c, cudaStream_t st) {
+  skin_table_kernel<<<(1u << 19) / 256, 256, 0, st>>>(c.skin_tab, (int)c.p.gray_tol_S,
+                                                      (int)c.p.hue_lo_deg, (int)c.p.hue_hi_deg);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
 struct EnvRegs {
   uint32_t NlE[12], NlO[12], NhE[12], NhO[12];
 };
@@ -202,9 +224,10 @@ __device__ __forceinline__ bool all_inside16(const uint32_t (&fr)[12], const Env
   return ((am | ~bm) & 0x80008000u) == 0u;
 }
 
-// Per-pixel R1 & R2 & R3 of the thread's 16 pixels (bit p = pixel p).
-__device__ __forceinline__ uint32_t slow_bits16(uint32_t (&fr)[12], const EnvRegs& e, int S,
-                                                int a1, int a2) {
+// Per-pixel R1 & R2 & R3 of the thread's 16 pixels (bit p = pixel p):
+// R1 per byte from the envelope lanes, R2 & R3 from the colour table.
+__device__ __forceinline__ uint32_t slow_bits16(const uint32_t (&fr)[12], const EnvRegs& e,
+                                                const uint32_t* __restrict__ skin) {
   uint64_t inside = 0;
 #pragma unroll
   for (int i = 0; i < 12; i++) {
@@ -213,32 +236,28 @@ __device__ __forceinline__ uint32_t slow_bits16(uint32_t (&fr)[12], const EnvReg
     const uint32_t f4 = ((tE >> 15) & 1u) | ((tO >> 14) & 2u) | ((tE >> 29) & 4u) | ((tO >> 28) & 8u);
     inside |= (uint64_t)f4 << (4 * i);
   }
-  uint32_t bits = 0;
-#pragma unroll 1
-  for (int g = 0; g < 4; g++) {
-    const uint32_t w0 = fr[0], w1 = fr[1], w2 = fr[2];
-    const uint32_t in12 = (uint32_t)(inside >> (12 * g)) & 0xFFFu;
+  // colour index r<<16 | g<<8 | b of pixel p from the interleaved words
+  uint32_t tw[16];
 #pragma unroll
-    for (int i = 0; i < 9; i++) fr[i] = fr[i + 3];
-    if (in12 == 0xFFFu) continue;                  // 4 background pixels: R1 = 0
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const int b = 3 * q;                            // byte offset within the 3 words
-      auto byte = [&](int bb) -> int {
-        const uint32_t w = bb < 4 ? w0 : (bb < 8 ? w1 : w2);
-        return (int)((w >> (8 * (bb & 3))) & 0xFFu);
-      };
-      const uint32_t r1 = ((in12 >> b) & 7u) != 7u;
-      bits |= (r1 & gray_and_skin(byte(b), byte(b + 1), byte(b + 2), S, a1, a2)) << (4 * g + q);
-    }
+  for (int p = 0; p < 16; p++) {
+    const int b0 = 3 * p;                              // byte of r
+    const uint32_t lo = fr[b0 >> 2], hi = fr[(b0 >> 2) + ((b0 & 3) > 1 ? 1 : 0)];
+    // bytes r, g, b sit at b0, b0+1, b0+2 of the pair (lo, hi); PRMT them into b | g<<8 | r<<16
+    const uint32_t o = b0 & 3;
+    const uint32_t sel = ((o + 2) & 0x7) | (((o + 1) & 0x7) << 4) | ((o & 0x7) << 8) | 0x4000u;
+    const uint32_t idx = __byte_perm(lo, hi, sel) & 0x00FFFFFFu;
+    tw[p] = ((inside >> b0) & 7u) == 7u ? 0u : (__ldg(skin + (idx >> 5)) >> (idx & 31)) & 1u;
   }
+  uint32_t bits = 0;
+#pragma unroll
+  for (int p = 0; p < 16; p++) bits |= tw[p] << p;
   return bits;
 }
 
 // Process this thread's 16 pixels of one frame in one go (LUT re-test path).
 template <bool kLut>
 __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e, bool valid,
-                                          const uint8_t* lut_s, int S, int a1, int a2,
+                                          const uint8_t* lut_s, const uint32_t* skin,
                                           uint32_t& luma_acc, bool& slow) {
   uint32_t fr[12];
   load48(px48, valid, fr);
@@ -247,7 +266,7 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
   const bool all_inside = all_inside16(fr, e) || !valid;
   if (!__any_sync(0xFFFFFFFFu, !all_inside)) return 0u;   // whole warp is background
   slow = true;
-  const uint32_t bits = slow_bits16(fr, e, S, a1, a2);
+  const uint32_t bits = slow_bits16(fr, e, skin);
   return valid ? bits : 0u;
 }
 
@@ -369,7 +388,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     else zero_env(e);
     uint32_t fr[12];
     load48(a.frames + (uint64_t)f * a.frame_bytes + coff + 48 * lane, valid, fr);
-    uint32_t bits = slow_bits16(fr, e, (int)a.S, (int)a.a1, (int)a.a2);
+    uint32_t bits = slow_bits16(fr, e, a.skin);
     bits = valid ? bits : 0u;
     const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
     uint32_t pc = 0;
@@ -442,7 +461,7 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
     uint32_t y = 0;
     bool slow = false;
     const uint32_t bits = seg16<true>(sm + warp * kChunkBytes + 48 * lane, e, valid, lut_s,
-                                      (int)a.S, (int)a.a1, (int)a.a2, y, slow);
+                                      a.skin, y, slow);
     const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
     uint32_t pc = 0;
     if (!(lane & 1) && valid) {
@@ -557,6 +576,7 @@ static SegArgs seg_args(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, 
   a.S = c.p.gray_tol_S;
   a.a1 = c.p.hue_lo_deg;
   a.a2 = c.p.hue_hi_deg;
+  a.skin = c.skin_tab;
   a.f0 = f0;
   a.n = n;
   a.frame_done = c.frame_done;
