@@ -23,6 +23,8 @@
 //   4. block reduction: #components, #kept, sum of kept areas, the largest
 //      (max area, ties -> smaller label)
 //   5. clear dropped components' runs from the mask words (final mask F)
+#include <cstdlib>
+
 #include "dev_util.cuh"
 #include "fizi_internal.cuh"
 #include "track.cuh"
@@ -284,11 +286,11 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
 __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
   const uint32_t f0 = a.f0, n = a.n;
   if (a.track_stream >= 0) {
-    constexpr uint32_t kChunk = 1024;
-    int64_t* t_s = reinterpret_cast<int64_t*>(smem);
-    double* cx_s = reinterpret_cast<double*>(t_s + kChunk);
-    double* cy_s = cx_s + kChunk;
-    uint32_t* ar_s = reinterpret_cast<uint32_t*>(cy_s + kChunk);
+    constexpr uint32_t kChunk = 512;
+    int64_t* t_s = reinterpret_cast<int64_t*>(smem);              // in: t, out: dwell
+    double* cx_s = reinterpret_cast<double*>(t_s + kChunk);       // in: cx, out: px
+    double* cy_s = cx_s + kChunk;                                 // in: cy, out: py
+    uint32_t* ar_s = reinterpret_cast<uint32_t*>(cy_s + kChunk);  // in: area, out: vis | clk<<1
     TrackState st;
     if (threadIdx.x == 0) st = a.tstate[a.track_stream];
     for (uint32_t base = 0; base < n; base += kChunk) {
@@ -306,10 +308,15 @@ __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
           fizi_result r;
           r.t_ms = t_s[i]; r.blob_area = ar_s[i]; r.cx = cx_s[i]; r.cy = cy_s[i];
           track_one(a.p, st, r);
-          fizi_result& o = a.res[f0 + base + i];
-          o.visible = r.visible; o.clicked = r.clicked;
-          o.px = r.px; o.py = r.py; o.dwell_ms = r.dwell_ms;
+          t_s[i] = r.dwell_ms; cx_s[i] = r.px; cy_s[i] = r.py;
+          ar_s[i] = (uint32_t)r.visible | ((uint32_t)r.clicked << 1);
         }
+      }
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        fizi_result& o = a.res[f0 + base + i];
+        o.visible = (uint8_t)(ar_s[i] & 1u); o.clicked = (uint8_t)(ar_s[i] >> 1);
+        o.px = cx_s[i]; o.py = cy_s[i]; o.dwell_ms = t_s[i];
       }
       __syncthreads();
     }
@@ -359,7 +366,7 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
 }
 
 constexpr size_t kCclSmem = (sizeof(Run) + sizeof(uint32_t)) * kCclSmemRuns;
-static_assert(kCclSmem >= 1024 * 28, "fold staging fits the labelling shared memory");
+static_assert(kCclSmem >= 512 * 28, "fold staging fits the labelling shared memory");
 
 cudaError_t init_ccl(Ctx& c) {
   (void)c;
@@ -392,7 +399,8 @@ cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_resul
   a.res = res;
   a.fg = c.fg;
   a.ppm = c.p.min_blob_ppm;
-  ccl_kernel<<<n, 1024, kCclSmem, st>>>(a);
+  static const int threads = getenv("FIZI_CCL_THREADS") ? atoi(getenv("FIZI_CCL_THREADS")) : 1024;
+  ccl_kernel<<<n, threads, kCclSmem, st>>>(a);
   c.launches += 1;
   return cudaGetLastError();
 }
