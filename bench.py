@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-frames", type=int, default=0)
+    ap.add_argument("--diag-no-masks", action="store_true",
+                    help="diagnostic only: do not request the u8 masks (masks_dev = NULL)")
     ap.add_argument("--diag-no-hand", action="store_true",
                     help="diagnostic only: frames without the hand (pure background path)")
     return ap.parse_args()
@@ -254,10 +256,11 @@ def main():
             # timestamps keep increasing across passes over the resident rounds
             t = np.asarray([synth.t_ms(k) for k in ks], np.int64)
             t = t + (i // need) * synth.t_ms(cfg.n_proc)
+            mk = None if args.diag_no_masks else masks[:n]
             if world == 1:             # the whole path in one call (fold fused into labelling)
-                fz.process_frames(fr[:n], t_ms=t, masks=masks[:n], results=res[:n])
+                fz.process_frames(fr[:n], t_ms=t, masks=mk, results=res[:n])
                 return n
-            fz.segment_frames(fr[:n], t_ms=t, masks=masks[:n], results=res[:n])
+            fz.segment_frames(fr[:n], t_ms=t, masks=mk, results=res[:n])
         # a8 across ranks: gather the step's records (frame order = rank order)
         # and fold them on every rank
         dist.all_gather_into_tensor(gathered, res)
