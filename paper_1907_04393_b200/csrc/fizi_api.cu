@@ -129,7 +129,7 @@ cudaError_t dalloc(T** p, size_t bytes) {
 }
 
 void free_all(Ctx& c) {
-  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.luma, c.fg, c.frame_done, c.sub_done, c.bitA, c.bitO, c.bitOC,
+  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.luma, c.fg, c.frame_done, c.dirty, c.sub_done, c.bitA, c.bitO, c.bitOC,
                   c.row_cnt, c.row_base, c.frame_runs, c.runs, c.parent, c.stats, c.frame_t, c.fix_count,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
@@ -139,6 +139,7 @@ void free_all(Ctx& c) {
   for (auto ev : c.ev_seg)
     if (ev) cudaEventDestroy(ev);
   if (c.ev_join) cudaEventDestroy(c.ev_join);
+  if (c.ev_start) cudaEventDestroy(c.ev_start);
   if (c.side) cudaStreamDestroy(c.side);
   for (auto& r : c.prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c.prof_free) cudaEventDestroy(e);
@@ -229,6 +230,8 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   cudaError_t e = cudaMemsetAsync(c.luma, 0, sizeof(unsigned long long) * n, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c.fg, 0, sizeof(uint32_t) * n, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c.frame_done, 0, sizeof(uint32_t) * n, st);
+  if (e == cudaSuccess && c.use_dirty)
+    e = cudaMemsetAsync(c.dirty, 0, sizeof(uint32_t) * c.dirty_words * n, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c.sub_done, 0, sizeof(uint32_t) * fizi::kMaxSub, st);
   for (size_t k = 0; k < subs.size() && e == cudaSuccess; k++)
     e = cudaMemsetAsync(c.fix_count + k * (c.max_batch + 1), 0, sizeof(uint32_t), st);
@@ -241,6 +244,16 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   // the u8 mask is written by the register-pipelined morphology when it runs
   const bool fused_mask = c.fast && c.P <= 128 && c.p.se_radius <= 4;
   cudaStream_t sd = c.side;
+  // with the dirty-chunk bitmap, all-zero mask rows are not written by the
+  // morphology: the u8 mask buffer is zeroed by a memset on the side stream
+  // that overlaps the fused segmentation kernel
+  const bool premask = masks && fused_mask && c.use_dirty;
+  if (premask) {
+    e = cudaEventRecord(c.ev_start, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, c.ev_start, 0);
+    if (e == cudaSuccess) e = cudaMemsetAsync(masks, 0, (size_t)n * c.N, sd);
+    if (e != cudaSuccess) return cuda_fail(c, e, "mask memset");
+  }
   for (size_t k = 0; k < subs.size(); k++) {
     const SubBatch& b = subs[k];
     e = fizi::launch_seg_main(c, frames, b.f0, b.n, b.g0, b.ng, (uint32_t)k, res, st);
@@ -251,7 +264,7 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
     e = fizi::launch_seg_fix(c, frames, b.f0, b.n, (uint32_t)k, res, sd);
     if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
     prof_begin(c, sd);
-    e = fizi::launch_morph(c, b.f0, b.n, fused_mask ? masks : nullptr, sd);
+    e = fizi::launch_morph(c, b.f0, b.n, fused_mask ? masks : nullptr, premask, sd);
     prof_end(c, FIZI_PROF_MORPH, sd);
     if (e != cudaSuccess) return cuda_fail(c, e, "morph");
     if (c.p.debug) {
@@ -358,6 +371,10 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   c.cap_runs = (uint64_t)c.H * ((c.W + 1) / 2);
   cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, cuda_device);
   c.morph_tr = fizi::morph_tile_rows(c, fizi::kMorphSmem);
+  // clean chunks of the merged mask are left unwritten when the register-
+  // pipelined morphology (which reads the dirty bitmap) runs and no debug
+  // stage needs the full mask
+  c.use_dirty = c.fast && c.P <= 128 && params->se_radius <= 4 && !params->debug;
   if (c.morph_tr == 0) {
     delete x;
     return FIZI_E_ARG;
@@ -374,6 +391,8 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.luma, mb * 8));
   A(dalloc(&c.fg, mb * 4));
   A(dalloc(&c.frame_done, mb * 4));
+  c.dirty_words = (c.nchunks + 31) / 32;
+  A(dalloc(&c.dirty, mb * c.dirty_words * 4));
   A(dalloc(&c.sub_done, fizi::kMaxSub * 4));
   A(dalloc(&c.bitA, mb * wpf * 4));
   A(dalloc(&c.bitO, mb * wpf * 4));
@@ -394,6 +413,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   for (uint32_t k = 0; k < fizi::kMaxSub && e == cudaSuccess; k++)
     e = cudaEventCreateWithFlags(&c.ev_seg[k], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_start, cudaEventDisableTiming);
   if (const char* sf = getenv("FIZI_SUB_FRAMES")) c.sub_frames = (uint32_t)atoi(sf) > 0 ? (uint32_t)atoi(sf) : 65535;
   if (e != cudaSuccess) {
     cudaGetLastError();

@@ -55,6 +55,7 @@ struct Ctx {
   bool fast = false;                     // W % 32 == 0: fused bulk-copy kernels
   int sms = 148;
   int seg_variant = 2;                   // min CTAs/SM of the fused kernel
+  bool use_dirty = false;                // clean chunks of A are not written (dirty bitmap)
   uint32_t morph_tr = 0;                 // output rows per morphology CTA
   uint64_t launches = 0;
   std::string err;
@@ -69,6 +70,8 @@ struct Ctx {
   unsigned long long* luma = nullptr;    // max_batch
   uint32_t* fg = nullptr;                // max_batch (fg_merged)
   uint32_t* frame_done = nullptr;        // max_batch (CTAs finished per frame)
+  uint32_t* dirty = nullptr;             // max_batch x dirty_words: chunks with non-zero A words
+  uint32_t dirty_words = 0;              // ceil(nchunks / 32)
   uint32_t* sub_done = nullptr;          // kMaxSub (CCL CTAs finished per sub-batch)
   uint32_t* bitA = nullptr;              // max_batch * H * P
   uint32_t* bitO = nullptr;              // max_batch * H * P
@@ -88,6 +91,7 @@ struct Ctx {
   cudaStream_t side = nullptr;           // internal stream for the per-sub-batch tail
   cudaEvent_t ev_seg[kMaxSub] = {};      // segment(k) done on the caller's stream
   cudaEvent_t ev_join = nullptr;         // tail of the call done on the side stream
+  cudaEvent_t ev_start = nullptr;        // call start on the caller's stream
   uint32_t sub_frames = 65535;           // frames per sub-batch (default: whole call)
   uint8_t* stage_frames = nullptr;       // device staging for fizi_process_frames_host
   uint8_t* stage_masks = nullptr;
@@ -147,7 +151,8 @@ cudaError_t launch_seg_fix(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t 
 // the segment launcher marks the SEGMENT -> FIXUP boundary through this hook
 void prof_begin(Ctx& c, cudaStream_t st);
 void prof_end(Ctx& c, int slot, cudaStream_t st);
-cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st);
+cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, bool masks_zeroed,
+                         cudaStream_t st);
 cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_result* res,
                        uint8_t* masks, int track_stream, cudaStream_t st);
 cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st);

@@ -25,6 +25,10 @@ namespace fizi {
 struct MorphArgs {
   uint32_t f0;                  // first frame of the launch (sub-batch)
   uint8_t* masks;               // u8 final-mask output (fast path) or nullptr
+  bool masks_zeroed;            // masks pre-zeroed: all-zero bands skip their rows
+  const uint32_t* dirty;        // per-frame chunk bitmap (fast path) or nullptr
+  uint32_t dirty_words;
+  bool write_zero_o;            // zero bands still write their O rows (debug / expand)
   const uint32_t* A;
   uint32_t* O;
   uint32_t W, H, P, TR;
@@ -337,8 +341,9 @@ struct MorphPipe {
   // band whose input rows are all zero: every output row is zero
   __device__ __forceinline__ void zero_band() const {
     for (int yo = y0; yo < y_end; yo++) {
-      for (uint32_t k = lane; k < P; k += 32) Of[(uint64_t)yo * P + k] = 0u;
-      if (Mf) {
+      if (a.write_zero_o)
+        for (uint32_t k = lane; k < P; k += 32) Of[(uint64_t)yo * P + k] = 0u;
+      if (Mf && !a.masks_zeroed) {
         uint8_t* row = Mf + (uint64_t)yo * a.W;
         for (uint32_t b = 16u * lane; b < a.W; b += 512u)
           __stcs(reinterpret_cast<uint4*>(row + b), make_uint4(0u, 0u, 0u, 0u));
@@ -464,6 +469,23 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
   const int first = y0 - 4 * R, last = mp.y_end + 4 * R;     // input rows [first, last)
   mp.band = band;
   mp.first = first;
+  const uint32_t* dmap = a.dirty ? a.dirty + (uint64_t)mp.f * a.dirty_words : nullptr;
+  if (dmap) {                           // zero band from the dirty-chunk bitmap, no loads
+    const int r0 = max(first, 0), r1 = min(last, (int)a.H);
+    const uint32_t c0 = (uint32_t)((uint64_t)r0 * a.P / 16);
+    const uint32_t c1 = (uint32_t)(((uint64_t)r1 * a.P - 1) / 16);
+    bool any = false;
+    for (uint32_t wi = (c0 >> 5) + threadIdx.x; wi <= (c1 >> 5); wi += 32) {
+      uint32_t m = __ldg(dmap + wi);
+      if (wi == (c0 >> 5)) m &= 0xFFFFFFFFu << (c0 & 31);
+      if (wi == (c1 >> 5) && (c1 & 31) != 31) m &= (2u << (c1 & 31)) - 1u;
+      any |= m != 0u;
+    }
+    if (!__any_sync(0xFFFFFFFFu, any)) {
+      mp.zero_band();
+      return;
+    }
+  }
   {                                     // stage the band (all loads in flight), detect zero bands
     constexpr int kRows = kBandRows + 8 * R;
     uint32_t any = 0;
@@ -476,14 +498,14 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
       const bool rin = yy >= 0 && yy < (int)a.H;
       const uint32_t* src = mp.Af + (uint64_t)(rin ? yy : 0) * P + lane * WPL;
       RowW<WPL> v;
-      if (WPL == 2 && (P & 1u) == 0) {                       // 8-byte aligned word pairs
-        uint2 t = make_uint2(0u, 0u);
-        if (rin && mp.wmask[0]) t = __ldg(reinterpret_cast<const uint2*>(src));
-        v.w[0] = t.x;
-        v.w[WPL - 1] = t.y;
-      } else {
 #pragma unroll
-        for (int j = 0; j < WPL; j++) v.w[j] = (rin && mp.wmask[j]) ? __ldg(src + j) : 0u;
+      for (int j = 0; j < WPL; j++) {
+        bool ld = rin && mp.wmask[j];
+        if (dmap && ld) {                // words of clean chunks are zero and unwritten
+          const uint32_t c = (uint32_t)(((uint64_t)yy * P + lane * WPL + j) >> 4);
+          ld = (__ldg(dmap + (c >> 5)) >> (c & 31)) & 1u;
+        }
+        v.w[j] = ld ? __ldg(src + j) : 0u;
       }
 #pragma unroll
       for (int j = 0; j < WPL; j++) {
@@ -523,10 +545,15 @@ static void launch_r(const MorphArgs& a, uint32_t n, size_t smem, cudaStream_t s
   morph_runs_kernel<R><<<dim3((a.H + a.TR - 1) / a.TR, n), 256, smem, st>>>(a);
 }
 
-cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st) {
+cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, bool masks_zeroed,
+                         cudaStream_t st) {
   MorphArgs a;
   a.f0 = f0;
   a.masks = masks;
+  a.masks_zeroed = masks_zeroed;
+  a.dirty = c.fast ? c.dirty : nullptr;
+  a.dirty_words = c.dirty_words;
+  a.write_zero_o = c.p.debug != 0;
   a.A = c.bitA;
   a.O = c.bitO;
   a.W = c.W; a.H = c.H; a.P = c.P; a.TR = c.morph_tr;

@@ -48,6 +48,9 @@ struct SegArgs {
   const uint32_t* fix;          // [0] = count, [1..] = frame ids needing a LUT
   uint32_t S, a1, a2;
   const uint32_t* skin;         // 2^24-bit R2 & R3 colour table
+  uint32_t* dirty;              // per frame: bit c = chunk c has a non-zero mask word
+  uint32_t dirty_words;         // words per frame of the dirty bitmap
+  bool write_zero;              // background chunks still write their zero words
   uint32_t f0, n;               // frame range of this launch (sub-batch)
   // in-kernel finalisation (fast path): the last CTA of a frame writes its record
   uint32_t* frame_done;         // per-frame count of finished CTAs
@@ -56,6 +59,8 @@ struct SegArgs {
   const int64_t* frame_t;
   fizi_result* res;
 };
+
+__device__ __forceinline__ bool valid_chunk(const SegArgs& a, uint32_t c) { return c < a.nchunks; }
 
 // a2 finalisation of frame f from its exact luma sum: integer mean, gamma,
 // record header; corrected frames join the sub-batch's LUT re-test list.
@@ -76,6 +81,8 @@ __device__ __forceinline__ void finalize_frame(const SegArgs& a, uint32_t f,
     const uint32_t pos = atomicAdd(&fix[0], 1u);
     fix[1 + pos] = f;
     fg[f] = 0;
+    // the identity-LUT mask is void: the LUT re-test rewrites every word
+    for (uint32_t w = 0; w < a.dirty_words; w++) a.dirty[(uint64_t)f * a.dirty_words + w] = 0u;
   }
 }
 
@@ -85,6 +92,9 @@ __device__ __forceinline__ void finalize_frame(const SegArgs& a, uint32_t f,
 // (i%3 = 0: r g b r), (1: g b r g), (2: b r g b).
 __constant__ uint32_t kWlo[3] = {0x2B724B2Bu, 0x4B2B724Bu, 0x724B2B72u};
 __constant__ uint32_t kWhi[3] = {0x01000201u, 0x02010002u, 0x00020100u};
+
+struct SegArgs;
+__device__ __forceinline__ bool valid_chunk(const SegArgs& a, uint32_t c);
 
 __device__ __forceinline__ uint32_t byte_of(const uint32_t (&w)[12], int b) {
   return (w[b >> 2] >> (8 * (b & 3))) & 0xFFu;
@@ -336,7 +346,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     }
     if (warp != 0) pol = policy_evict_first();
     const uint8_t* my = sm + warp * kChunkBytes + 48 * lane;
-    uint32_t* dstw = a.bitA + (uint64_t)c * 16 + (lane >> 1);
     uint32_t luma_lane = 0;                                  // lane i: this warp's luma of frame i
     for (uint32_t i = 0; i < nf; i++) {
       const uint32_t s = i & (kStages - 1);
@@ -359,11 +368,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
       }
       y = warp_sum_u32(y);
       if ((uint32_t)lane == i) luma_lane = y;
-      if (slow) {
-        if (lane == 0) q_item[atomicAdd(&q_tail, 1u)] = (uint16_t)((i << 3) | warp);
-      } else if (!(lane & 1) && valid) {
-        dstw[(uint64_t)f * a.words_per_frame] = 0u;
-      }
+      // background chunks write nothing: their words are implied zero by the
+      // frame's dirty bitmap (only chunks with non-zero words are marked)
+      if (slow && lane == 0) q_item[atomicAdd(&q_tail, 1u)] = (uint16_t)((i << 3) | warp);
+      if (!slow && a.write_zero && !(lane & 1) && valid)
+        a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
     }
     if ((uint32_t)lane < nf) atomicAdd(&acc_y[lane], luma_lane);
   }
@@ -397,7 +406,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
       pc = __popc(word);
     }
     pc = warp_sum_u32(pc);
-    if (lane == 0 && pc) atomicAdd(&acc_f[i], pc);
+    if (lane == 0 && pc) {
+      atomicAdd(&acc_f[i], pc);
+      atomicOr(a.dirty + (uint64_t)f * a.dirty_words + (cq >> 5), 1u << (cq & 31));
+    }
   }
   __syncthreads();                                           // flush the CTA's sums
   if (tid < (int)nf) {
@@ -469,7 +481,10 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
       pc = __popc(word);
     }
     pc = warp_sum_u32(pc);
-    if (lane == 0) red_f[warp] = pc;
+    if (lane == 0) {
+      red_f[warp] = pc;
+      if (pc && valid_chunk(a, c)) atomicOr(a.dirty + (uint64_t)f * a.dirty_words + (c >> 5), 1u << (c & 31));
+    }
     __syncthreads();
     if (tid == 0) {
       uint32_t sf = 0;
@@ -577,6 +592,9 @@ static SegArgs seg_args(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, 
   a.a1 = c.p.hue_lo_deg;
   a.a2 = c.p.hue_hi_deg;
   a.skin = c.skin_tab;
+  a.dirty = c.dirty;
+  a.dirty_words = c.dirty_words;
+  a.write_zero = !c.use_dirty;
   a.f0 = f0;
   a.n = n;
   a.frame_done = c.frame_done;
