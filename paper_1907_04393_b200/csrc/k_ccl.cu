@@ -23,6 +23,7 @@
 //   4. block reduction: #components, #kept, sum of kept areas, the largest
 //      (max area, ties -> smaller label)
 //   5. clear dropped components' runs from the mask words (final mask F)
+#include <cstdio>
 #include <cstdlib>
 
 #include "dev_util.cuh"
@@ -51,6 +52,7 @@ struct CclArgs {
   uint32_t n;                   // frames in the launch (sub-batch)
   uint32_t* sub_done;           // CTAs finished in this launch
   int track_stream;             // -2: no fold; -1: per-stream fold; >= 0: single stream
+  int trace;                    // diagnostics: block 0 prints phase clocks
   uint32_t n_streams;
   const uint32_t* frame_stream;
   TrackState* tstate;
@@ -97,8 +99,11 @@ __device__ __forceinline__ void unite(uint32_t* par, const Run* R, uint32_t W, u
   }
 }
 
+#define CCL_MARK(k) if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) t_mark[k] = clock64();
+
 template <bool kShared>
-__device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, uint32_t T) {
+__device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, uint32_t T,
+                          long long* t_mark) {
   __shared__ unsigned long long s_best[32];
   __shared__ uint32_t s_cnt[3][32];
   __shared__ unsigned long long s_key;
@@ -111,6 +116,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   uint32_t* gpar = a.parent + (uint64_t)f * a.cap_runs;
   RootStats* stats = a.stats + (uint64_t)f * a.cap_runs;
 
+  CCL_MARK(0)
   // 0. load
   for (uint32_t i = tid; i < T; i += nthr) {
     if (kShared) R[i] = gruns[i];
@@ -122,6 +128,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   }
   __syncthreads();
 
+  CCL_MARK(1)
   // 1. union with the previous row
   for (uint32_t y = tid + 1; y < H; y += nthr) {
     const uint32_t n = cnt[y], np = cnt[y - 1];
@@ -137,9 +144,11 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   }
   __syncthreads();
 
+  CCL_MARK(2)
   // 2. flatten
   for (uint32_t i = tid; i < T; i += nthr) par[i] = find_root<kShared>(par, i);
   __syncthreads();
+  CCL_MARK(3)
 
   // 3. statistics, aggregated over lanes of a warp that share a root
   for (uint32_t i0 = 0; i0 < T; i0 += nthr) {
@@ -186,6 +195,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   }
   __syncthreads();
 
+  CCL_MARK(4)
   // 4. counts and the hand blob: key = area << 32 | ~label
   uint32_t n_tot = 0, n_kept = 0, fg_final = 0;
   unsigned long long best = 0;
@@ -237,6 +247,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     }
   }
   __syncthreads();
+  CCL_MARK(5)
   const unsigned long long bk = s_key;
   if (bk) {                                   // the best root's thread writes the blob
     const uint32_t blabel = 0xFFFFFFFFu - (uint32_t)(bk & 0xFFFFFFFFu);
@@ -259,6 +270,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   if (kShared)                                 // forest for fizi_debug_stage(LABELS)
     for (uint32_t i = tid; i < T; i += nthr) gpar[i] = par[i];
 
+  CCL_MARK(6)
   // 5. clear the runs of dropped components from the mask (final mask F)
   if (s_drop == 0) return;
   uint32_t* Of = a.O + (uint64_t)f * H * P;
@@ -345,13 +357,21 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   extern __shared__ __align__(16) uint8_t smc[];
   const uint32_t f = a.f0 + blockIdx.x;
   const uint32_t T = a.frame_runs[f];
+  __shared__ long long t_mark[10];
+  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) t_mark[9] = clock64();
   if (T <= kCclSmemRuns) {
     Run* R = reinterpret_cast<Run*>(smc);
     uint32_t* par = reinterpret_cast<uint32_t*>(smc + sizeof(Run) * kCclSmemRuns);
-    ccl_frame<true>(a, f, R, par, T);
+    ccl_frame<true>(a, f, R, par, T, t_mark);
   } else {
     ccl_frame<false>(a, f, const_cast<Run*>(a.runs + (uint64_t)f * a.cap_runs),
-                     a.parent + (uint64_t)f * a.cap_runs, T);
+                     a.parent + (uint64_t)f * a.cap_runs, T, t_mark);
+  }
+  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) {
+    t_mark[7] = clock64();
+    printf("CCL_TRACE T=%u start->load %lld load %lld union %lld flatten %lld stats %lld select %lld blob %lld tail %lld\n", T,
+           t_mark[0] - t_mark[9], t_mark[1] - t_mark[0], t_mark[2] - t_mark[1], t_mark[3] - t_mark[2],
+           t_mark[4] - t_mark[3], t_mark[5] - t_mark[4], t_mark[6] - t_mark[5], t_mark[7] - t_mark[6]);
   }
   if (a.track_stream == -2) return;
   __shared__ uint32_t s_last;
@@ -362,7 +382,11 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
     __threadfence();
   }
   __syncthreads();
-  if (s_last) fold_records(a, smc);
+  if (s_last) {
+    long long t0 = clock64();
+    fold_records(a, smc);
+    if (a.trace && threadIdx.x == 0) printf("CCL_TRACE fold %lld cycles (n=%u)\n", clock64() - t0, a.n);
+  }
 }
 
 constexpr size_t kCclSmem = (sizeof(Run) + sizeof(uint32_t)) * kCclSmemRuns;
@@ -386,6 +410,8 @@ cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_resul
   a.frame_stream = c.frame_stream;
   a.tstate = reinterpret_cast<TrackState*>(c.tstate);
   a.p = c.p;
+  static const int trace = getenv("FIZI_CCL_TRACE") ? 1 : 0;
+  a.trace = trace;
   a.O = c.bitO;
   a.W = c.W; a.H = c.H; a.P = c.P;
   a.N = c.N;
