@@ -145,9 +145,20 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   __syncthreads();
 
   CCL_MARK(2)
-  // 2. flatten
-  for (uint32_t i = tid; i < T; i += nthr) par[i] = find_root<kShared>(par, i);
-  __syncthreads();
+  // 2. flatten by lockstep pointer jumping (the forest depth halves every
+  //    round; concurrent unions can leave long chains along tall components)
+  while (true) {
+    int changed = 0;
+    for (uint32_t i = tid; i < T; i += nthr) {
+      const uint32_t p = ld_par<kShared>(par + i);
+      const uint32_t gp = ld_par<kShared>(par + p);
+      if (gp != p) {
+        par[i] = gp;
+        changed = 1;
+      }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
   CCL_MARK(3)
 
   // 3. statistics, aggregated over lanes of a warp that share a root
@@ -168,6 +179,20 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     const uint32_t m = __match_any_sync(0xFFFFFFFFu, root);
     uint32_t g_area = 0, g_x0 = 0xFFFFFFFFu, g_x1 = 0, g_y0 = 0xFFFFFFFFu, g_y1 = 0;
     unsigned long long g_sx = 0, g_sy = 0;
+    if (__all_sync(0xFFFFFFFFu, m == 0xFFFFFFFFu)) {        // one root for the whole warp
+      g_area = __reduce_add_sync(0xFFFFFFFFu, len);
+      g_x0 = __reduce_min_sync(0xFFFFFFFFu, x0);
+      g_x1 = __reduce_max_sync(0xFFFFFFFFu, x1);
+      g_y0 = __reduce_min_sync(0xFFFFFFFFu, y);
+      g_y1 = __reduce_max_sync(0xFFFFFFFFu, y);
+      g_sx = sx;
+      g_sy = sy;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        g_sx += __shfl_xor_sync(0xFFFFFFFFu, g_sx, d);
+        g_sy += __shfl_xor_sync(0xFFFFFFFFu, g_sy, d);
+      }
+    } else
 #pragma unroll 4
     for (int l = 0; l < 32; l++) {
       const uint32_t o_len = __shfl_sync(0xFFFFFFFFu, len, l);
