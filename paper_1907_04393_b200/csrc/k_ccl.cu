@@ -147,7 +147,9 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   CCL_MARK(2)
   // 2. flatten by lockstep pointer jumping (the forest depth halves every
   //    round; concurrent unions can leave long chains along tall components)
+  int rounds = 0;
   while (true) {
+    rounds++;
     int changed = 0;
     for (uint32_t i = tid; i < T; i += nthr) {
       const uint32_t p = ld_par<kShared>(par + i);
@@ -159,6 +161,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     }
     if (!__syncthreads_or(changed)) break;
   }
+  (void)rounds;
   CCL_MARK(3)
 
   // 3. statistics, aggregated over lanes of a warp that share a root

@@ -178,7 +178,10 @@ __global__ void __launch_bounds__(256) morph_runs_kernel(MorphArgs a) {
 // processed rows of its input in registers and emits row y as soon as row
 // y+R arrives, so pass 4 emits row y when input row y+4R is read.  Neighbour
 // words across lanes come from warp shuffles; no shared memory, no barriers.
-constexpr int kBandRows = 16;
+#ifndef FIZI_BAND_ROWS
+#define FIZI_BAND_ROWS 16
+#endif
+constexpr int kBandRows = FIZI_BAND_ROWS;
 
 template <int WPL>
 struct RowW {
