@@ -16,6 +16,8 @@
 // compact run array with one atomicAdd (row_base[y], row_cnt[y]), its runs
 // sorted by x inside the range.  Rows land in arbitrary order: the labelling
 // identifies components by the raster key y*W+x0 of their runs, not by index.
+#include <cstdlib>
+
 #include "dev_util.cuh"
 #include "fizi_internal.cuh"
 
@@ -29,6 +31,7 @@ struct MorphArgs {
   const uint32_t* dirty;        // per-frame chunk bitmap (fast path) or nullptr
   uint32_t dirty_words;
   bool write_zero_o;            // zero bands still write their O rows (debug / expand)
+  int trace;
   const uint32_t* A;
   uint32_t* O;
   uint32_t W, H, P, TR;
@@ -402,52 +405,31 @@ struct MorphPipe {
     }
     if (!total) return;
     __syncwarp();
-    for (int r = 0; r < y_end - y0; r++) {
-      const uint32_t rc = __shfl_sync(0xFFFFFFFFu, my_cnt, r);
-      const uint32_t rbase = __shfl_sync(0xFFFFFFFFu, row_base, r);
-      if (!rc) continue;
-      const int yo = y0 + r;
-      const uint32_t* row = band + (yo - first) * (int)P + lane * WPL;
-      uint32_t w[WPL];
-#pragma unroll
-      for (int j = 0; j < WPL; j++) w[j] = (lane * WPL + j < (int)P) ? row[j] : 0u;
-      const uint32_t prev_last = __shfl_up_sync(0xFFFFFFFFu, w[WPL - 1], 1) & lmask;
-      const uint32_t next_first = __shfl_down_sync(0xFFFFFFFFu, w[0], 1) & rmask;
-      uint32_t st[WPL], en[WPL], ns = 0, ne = 0;
-#pragma unroll
-      for (int j = 0; j < WPL; j++) {
-        const uint32_t pv = j > 0 ? w[j - 1] : prev_last;
-        const uint32_t nx = j + 1 < WPL ? w[j + 1] : next_first;
-        st[j] = w[j] & ~((w[j] << 1) | (pv >> 31));
-        en[j] = w[j] & ~((w[j] >> 1) | (nx << 31));
-        ns += __popc(st[j]);
-        ne += __popc(en[j]);
-      }
-      uint32_t ps = ns, pe = ne;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, ps, d);
-        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pe, d);
-        if (lane >= d) { ps += u; pe += v; }
-      }
-      uint32_t is = rbase + ps - ns, ie = rbase + pe - ne;
-#pragma unroll
-      for (int j = 0; j < WPL; j++) {
-        const uint32_t k = (uint32_t)(lane * WPL + j);
-        uint32_t s0 = st[j], e0 = en[j];
-        while (s0) {
-          const uint32_t bit = __ffs(s0) - 1;
-          s0 &= s0 - 1;
-          runs[is].x0 = (uint16_t)(32 * k + bit);
-          runs[is].y = (uint16_t)yo;
-          is++;
+    // one lane per output row: scan the row's words (shared memory) and write
+    // its runs in order; the k-th start and the k-th end of a row pair up
+    if (lane < y_end - y0 && my_cnt) {
+      const int yo = y0 + lane;
+      const uint32_t* row = band + (yo - first) * (int)P;
+      uint32_t slot = row_base, prev = 0u, x0 = 0u;
+      for (uint32_t k = 0; k < P; k++) {
+        const uint32_t w = row[k];
+        if (w == 0u && !(prev >> 31)) { prev = w; continue; }
+        const uint32_t nx = k + 1 < P ? row[k + 1] : 0u;
+        uint32_t st = w & ~((w << 1) | (prev >> 31));
+        uint32_t en = w & ~((w >> 1) | (nx << 31));
+        while (st | en) {
+          const uint32_t bs = st ? __ffs(st) - 1 : 32u, be = en ? __ffs(en) - 1 : 32u;
+          if (bs <= be) {                        // a run starts (it may also end here)
+            x0 = 32 * k + bs;
+            st &= st - 1;
+          } else {
+            Run r;
+            r.x0 = (uint16_t)x0; r.x1 = (uint16_t)(32 * k + be); r.y = (uint16_t)yo; r.pad = 0;
+            runs[slot++] = r;
+            en &= en - 1;
+          }
         }
-        while (e0) {
-          const uint32_t bit = __ffs(e0) - 1;
-          e0 &= e0 - 1;
-          runs[ie].x1 = (uint16_t)(32 * k + bit);
-          ie++;
-        }
+        prev = w;
       }
     }
   }
@@ -463,11 +445,32 @@ __device__ __forceinline__ void unrolled_steps(MorphPipe<R, WPL>& mp, int yi, in
 
 // One warp per CTA (the band depends on blockIdx only, so every branch is
 // warp-uniform and shuffles need no divergence handling).
+__device__ unsigned long long g_morph_trace[16384][5];      // diagnostics (FIZI_MORPH_TRACE)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <int R, int WPL>
 __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
   extern __shared__ uint32_t band[];                          // (kBandRows + 8R) x P words
   const int y0 = (int)(blockIdx.x * kBandRows);
   if (y0 >= (int)a.H) return;
+  const unsigned long long t_start = a.trace ? gtimer() : 0ull;
+  struct TraceEnd {
+    const MorphArgs& a; unsigned long long t0; int nz = 0;
+    unsigned long long t_staged = 0, t_piped = 0;
+    __device__ ~TraceEnd() {
+      if (a.trace && threadIdx.x == 0) {
+        const uint32_t id = blockIdx.y * gridDim.x + blockIdx.x;
+        if (id < 16384) {
+          g_morph_trace[id][0] = t0; g_morph_trace[id][1] = gtimer(); g_morph_trace[id][2] = nz;
+          g_morph_trace[id][3] = t_staged; g_morph_trace[id][4] = t_piped;
+        }
+      }
+    }
+  } trace_end{a, t_start};
   MorphPipe<R, WPL> mp(a, a.f0 + blockIdx.y, y0);
   const int first = y0 - 4 * R, last = mp.y_end + 4 * R;     // input rows [first, last)
   mp.band = band;
@@ -489,7 +492,34 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
       return;
     }
   }
-  {                                     // stage the band (all loads in flight), detect zero bands
+  if (dmap && (a.P & 3u) == 0) {        // TMA: the band's rows are one contiguous range
+    __shared__ __align__(8) uint64_t sbar;
+    const uint32_t P = a.P;
+    const int r0 = max(first, 0), r1 = min(first + kBandRows + 8 * R, (int)a.H);
+    const uint32_t bytes = (uint32_t)(r1 - r0) * P * 4u;
+    uint32_t* dst = band + (r0 - first) * (int)P;
+    if (mp.lane == 0) {
+      mbar_init(&sbar, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(&sbar, bytes);
+      bulk_g2s(dst, mp.Af + (uint64_t)r0 * P, bytes, &sbar, policy_evict_first());
+    }
+    // rows of the band outside the frame are zero
+    for (uint32_t i = mp.lane; i < (uint32_t)(r0 - first) * P; i += 32) band[i] = 0u;
+    const uint32_t tail0 = (uint32_t)(r1 - first) * P, tend = (uint32_t)(kBandRows + 8 * R) * P;
+    for (uint32_t i = tail0 + mp.lane; i < tend; i += 32) band[i] = 0u;
+    __syncwarp();
+    mbar_wait(&sbar, 0);
+    // words of clean chunks were not written this call: zero them
+    const uint64_t w0 = (uint64_t)r0 * P, w1 = (uint64_t)r1 * P;     // frame word range
+    const uint32_t c0 = (uint32_t)(w0 >> 4), c1 = (uint32_t)((w1 - 1) >> 4);
+    for (uint32_t cc = c0 + mp.lane; cc <= c1; cc += 32) {
+      if ((__ldg(dmap + (cc >> 5)) >> (cc & 31)) & 1u) continue;
+      const uint64_t a0 = max((uint64_t)cc * 16, w0), a1 = min((uint64_t)cc * 16 + 16, w1);
+      for (uint64_t wi = a0; wi < a1; wi++) dst[wi - w0] = 0u;
+    }
+    __syncwarp();
+  } else {                              // stage the band (all loads in flight), detect zero bands
     constexpr int kRows = kBandRows + 8 * R;
     uint32_t any = 0;
     const uint32_t P = a.P;
@@ -522,10 +552,13 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
     }
     __syncwarp();
   }
+  trace_end.nz = 1;
+  if (a.trace) trace_end.t_staged = gtimer();
 #pragma unroll
   for (int q = 0; q < 2 * R + 1; q++) mp.pre[q] = mp.load_row(first + q);
   for (int yi = first; yi < last; yi += 2 * R + 1) unrolled_steps<R, WPL, 0>(mp, yi, last);
   __syncwarp();
+  if (a.trace) trace_end.t_piped = gtimer();
   mp.emit_runs();
 }
 
@@ -557,6 +590,8 @@ cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, bool m
   a.dirty = c.fast ? c.dirty : nullptr;
   a.dirty_words = c.dirty_words;
   a.write_zero_o = c.p.debug != 0;
+  static const int trace = getenv("FIZI_MORPH_TRACE") ? 1 : 0;
+  a.trace = trace;
   a.A = c.bitA;
   a.O = c.bitO;
   a.W = c.W; a.H = c.H; a.P = c.P; a.TR = c.morph_tr;
@@ -620,3 +655,8 @@ cudaError_t init_morph(Ctx& c) {
 }
 
 }  // namespace fizi
+
+// diagnostics only (not part of include/fizi.h)
+extern "C" int fizi_diag_morph_trace(unsigned long long* host, unsigned int n) {
+  return (int)cudaMemcpyFromSymbol(host, fizi::g_morph_trace, sizeof(unsigned long long) * 5 * n);
+}
