@@ -244,10 +244,10 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   // the u8 mask is written by the register-pipelined morphology when it runs
   const bool fused_mask = c.fast && c.P <= 128 && c.p.se_radius <= 4;
   cudaStream_t sd = c.side;
-  // with the dirty-chunk bitmap, all-zero mask rows are not written by the
-  // morphology: the u8 mask buffer is zeroed by a memset on the side stream
-  // that overlaps the fused segmentation kernel
-  const bool premask = masks && fused_mask && c.use_dirty;
+  // the u8 mask buffer is zeroed by a memset on the side stream that overlaps
+  // the fused segmentation kernel; the labelling kernel then writes the bytes
+  // of the kept components only
+  const bool premask = masks && fused_mask;
   if (premask) {
     e = cudaEventRecord(c.ev_start, st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, c.ev_start, 0);
@@ -274,7 +274,8 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
       if (e != cudaSuccess) return cuda_fail(c, e, "debug copy");
     }
     prof_begin(c, sd);
-    e = fizi::launch_ccl(c, b.f0, b.n, (uint32_t)k, res, fused_mask ? masks : nullptr, fold, sd);
+    e = fizi::launch_ccl(c, b.f0, b.n, (uint32_t)k, res, fused_mask ? masks : nullptr, premask, fold,
+                         sd);
     prof_end(c, FIZI_PROF_CCL, sd);
     if (e != cudaSuccess) return cuda_fail(c, e, "ccl");
     if (masks && !fused_mask) {

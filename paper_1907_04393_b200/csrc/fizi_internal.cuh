@@ -154,7 +154,7 @@ void prof_end(Ctx& c, int slot, cudaStream_t st);
 cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, bool masks_zeroed,
                          cudaStream_t st);
 cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_result* res,
-                       uint8_t* masks, int track_stream, cudaStream_t st);
+                       uint8_t* masks, bool masks_zeroed, int track_stream, cudaStream_t st);
 cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st);
 cudaError_t launch_track_batch(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st);
 cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,

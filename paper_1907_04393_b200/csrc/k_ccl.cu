@@ -48,7 +48,9 @@ struct CclArgs {
   const uint32_t* fg;
   uint32_t ppm;
   // fused a6 output / a8 fold
-  uint8_t* masks;               // u8 final mask written by morphology (cleared here) or nullptr
+  uint8_t* masks;               // u8 final mask: written by morphology (dropped blobs cleared
+                                // here) or, when pre-zeroed, written here from the kept runs
+  bool masks_zeroed;
   uint32_t n;                   // frames in the launch (sub-batch)
   uint32_t* sub_done;           // CTAs finished in this launch
   int track_stream;             // -2: no fold; -1: per-stream fold; >= 0: single stream
@@ -299,7 +301,23 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     for (uint32_t i = tid; i < T; i += nthr) gpar[i] = par[i];
 
   CCL_MARK(6)
-  // 5. clear the runs of dropped components from the mask (final mask F)
+  // 5a. pre-zeroed u8 mask: write the bytes of every run of a kept component
+  if (a.masks && a.masks_zeroed) {
+    for (uint32_t i = tid; i < T; i += nthr) {
+      const uint32_t root = ld_par<kShared>(par + i);
+      if (!kept_area(__ldcg(&stats[root].area), a.ppm, a.N)) continue;
+      const Run rg = R[i];
+      uint8_t* p = a.masks + ((uint64_t)f * H + rg.y) * W;
+      uint32_t x = rg.x0;
+      const uint32_t xe = (uint32_t)rg.x1 + 1;
+      for (; x < xe && (x & 15u); x++) p[x] = 1;
+      for (; x + 16 <= xe; x += 16)
+        *reinterpret_cast<uint4*>(p + x) = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+      for (; x < xe; x++) p[x] = 1;
+    }
+  }
+
+  // 5. clear the runs of dropped components from the bit mask (final mask F)
   if (s_drop == 0) return;
   uint32_t* Of = a.O + (uint64_t)f * H * P;
   for (uint32_t i = tid; i < T; i += nthr) {
@@ -313,7 +331,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
       const uint32_t m = (b1 == 31u ? 0xFFFFFFFFu : ((1u << (b1 + 1)) - 1u)) & ~((1u << b0) - 1u);
       atomicAnd(row + k, ~m);
     }
-    if (a.masks) {
+    if (a.masks && !a.masks_zeroed) {
       uint8_t* mrow = a.masks + ((uint64_t)f * H + rg.y) * W;
       for (uint32_t x = rg.x0; x <= rg.x1; x++) mrow[x] = 0;
     }
@@ -427,10 +445,11 @@ cudaError_t init_ccl(Ctx& c) {
 }
 
 cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_result* res,
-                       uint8_t* masks, int track_stream, cudaStream_t st) {
+                       uint8_t* masks, bool masks_zeroed, int track_stream, cudaStream_t st) {
   CclArgs a;
   a.f0 = f0;
   a.masks = masks;
+  a.masks_zeroed = masks_zeroed;
   a.n = n;
   a.sub_done = c.sub_done + sub;
   a.track_stream = track_stream;

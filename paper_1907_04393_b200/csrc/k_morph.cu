@@ -317,33 +317,6 @@ struct MorphPipe {
     }
   }
 
-  // the final u8 mask row (one byte per pixel, a6 output): speculatively O;
-  // the labelling kernel clears the pixels of components the area filter
-  // drops.  Warp-coalesced: lane l writes bytes 16l + 512m of the row (16
-  // pixels = half a word), fetched from the owning lane by shuffles.
-  __device__ __forceinline__ void write_mask_row(const RowW<WPL>& o, int yo) const {
-    if (!Mf) return;
-    uint8_t* row = Mf + (uint64_t)yo * a.W;
-#pragma unroll
-    for (int m = 0; m < 2 * WPL; m++) {                       // 16 words (512 px) per m
-      const uint32_t hw = (uint32_t)lane / 2 + 16u * m;         // word index of my 16 pixels
-      const int src = (int)(hw / WPL);
-      uint32_t w = 0;
-#pragma unroll
-      for (int j = 0; j < WPL; j++) {
-        const uint32_t v = __shfl_sync(0xFFFFFFFFu, o.w[j], src);
-        if ((int)(hw % WPL) == j) w = v;
-      }
-      if (hw < P) {
-        const uint32_t b = (w >> (16 * (lane & 1))) & 0xFFFFu;
-        uint4 q;
-        q.x = expand4(b & 0xF); q.y = expand4((b >> 4) & 0xF);
-        q.z = expand4((b >> 8) & 0xF); q.w = expand4(b >> 12);
-        __stcs(reinterpret_cast<uint4*>(row + 16ull * (hw * 2 + (lane & 1))), q);
-      }
-    }
-  }
-
   // band whose input rows are all zero: every output row is zero
   __device__ __forceinline__ void zero_band() const {
     for (int yo = y0; yo < y_end; yo++) {
@@ -367,23 +340,46 @@ struct MorphPipe {
   uint32_t my_cnt = 0;
 
   __device__ __forceinline__ void emit(const RowW<WPL>& o4, int yo) {
-    write_mask_row(o4, yo);
     const uint32_t prev_last = __shfl_up_sync(0xFFFFFFFFu, o4.w[WPL - 1], 1) & lmask;
     uint32_t ns = 0;
     uint32_t* slot = const_cast<uint32_t*>(band) + (yo - first) * (int)P + lane * WPL;
 #pragma unroll
     for (int j = 0; j < WPL; j++) {
-      const uint32_t k = (uint32_t)(lane * WPL + j);
       const uint32_t w = o4.w[j];
-      if (k < P) {
-        Of[(uint64_t)yo * P + k] = w;
-        slot[j] = w;
-      }
+      if (lane * WPL + j < (int)P) slot[j] = w;
       const uint32_t pv = j > 0 ? o4.w[j - 1] : prev_last;
       ns += __popc(w & ~((w << 1) | (pv >> 31)));
     }
     const uint32_t cnt = warp_sum_u32(ns);
     if (lane == yo - y0) my_cnt = cnt;
+  }
+
+  // after the pipeline: the band's O rows (one bulk store) and u8 mask rows
+  __device__ __forceinline__ void write_rows() {
+    const uint32_t* out0 = band + (y0 - first) * (int)P;
+    const uint32_t nrows = (uint32_t)(y_end - y0);
+    __syncwarp();
+    if ((P & 3u) == 0u) {
+      if (lane == 0) bulk_s2g(Of + (uint64_t)y0 * P, out0, nrows * P * 4u);
+    } else {
+      for (uint32_t i = lane; i < nrows * P; i += 32) Of[(uint64_t)y0 * P + i] = out0[i];
+    }
+    if (Mf && !a.masks_zeroed) {                        // (else the labelling kernel writes them)
+      const uint32_t groups = a.W / 16;                 // 16-pixel groups per row
+      for (uint32_t r = 0; r < nrows; r++) {
+        const uint32_t rc = __shfl_sync(0xFFFFFFFFu, my_cnt, r);
+        if (a.masks_zeroed && rc == 0u) continue;       // zero row already zeroed
+        const uint32_t* row = out0 + r * P;
+        uint8_t* mrow = Mf + (uint64_t)(y0 + r) * a.W;
+        for (uint32_t g = lane; g < groups; g += 32) {
+          const uint32_t b = (row[g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
+          uint4 q;
+          q.x = expand4(b & 0xF); q.y = expand4((b >> 4) & 0xF);
+          q.z = expand4((b >> 8) & 0xF); q.w = expand4(b >> 12);
+          __stcs(reinterpret_cast<uint4*>(mrow + 16ull * g), q);
+        }
+      }
+    }
   }
 
   // one atomic reservation for the band's runs, then (x0, x1, y) per run
@@ -559,7 +555,9 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
   for (int yi = first; yi < last; yi += 2 * R + 1) unrolled_steps<R, WPL, 0>(mp, yi, last);
   __syncwarp();
   if (a.trace) trace_end.t_piped = gtimer();
+  mp.write_rows();
   mp.emit_runs();
+  if (mp.lane == 0 && (a.P & 3u) == 0u) bulk_s2g_wait();
 }
 
 uint32_t morph_tile_rows(const Ctx& c, size_t smem_budget) {
