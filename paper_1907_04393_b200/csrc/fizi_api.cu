@@ -410,7 +410,13 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.tstate, (uint64_t)n_streams * sizeof(fizi::TrackState)));
   if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned), table_bytes);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.pinned_ev, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) {
+    // the tail (labelling etc.) is latency-bound: its CTAs go before pending
+    // CTAs of the throughput-bound segmentation kernel
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    e = cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking, hi_prio);
+  }
   for (uint32_t k = 0; k < fizi::kMaxSub && e == cudaSuccess; k++)
     e = cudaEventCreateWithFlags(&c.ev_seg[k], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming);
