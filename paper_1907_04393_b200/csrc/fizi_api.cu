@@ -129,7 +129,7 @@ cudaError_t dalloc(T** p, size_t bytes) {
 }
 
 void free_all(Ctx& c) {
-  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.luma, c.fg, c.frame_done, c.dirty, c.sub_done, c.bitA, c.bitO, c.bitOC,
+  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.luma, c.fg, c.frame_done, c.dirty, c.sub_done, c.fold_sync, c.bitA, c.bitO, c.bitOC,
                   c.row_cnt, c.row_base, c.frame_runs, c.runs, c.parent, c.stats, c.frame_t, c.fix_count,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
@@ -273,6 +273,10 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
                           cudaMemcpyDeviceToDevice, sd);
       if (e != cudaSuccess) return cuda_fail(c, e, "debug copy");
     }
+    if (fold >= 0) {
+      e = cudaMemsetAsync(c.fold_sync, 0, sizeof(uint32_t) * (b.n + 2), sd);
+      if (e != cudaSuccess) return cuda_fail(c, e, "fold memset");
+    }
     prof_begin(c, sd);
     e = fizi::launch_ccl(c, b.f0, b.n, (uint32_t)k, res, fused_mask ? masks : nullptr, premask, fold,
                          sd);
@@ -395,6 +399,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   c.dirty_words = (c.nchunks + 31) / 32;
   A(dalloc(&c.dirty, mb * c.dirty_words * 4));
   A(dalloc(&c.sub_done, fizi::kMaxSub * 4));
+  A(dalloc(&c.fold_sync, (mb + 2) * 4));
   A(dalloc(&c.bitA, mb * wpf * 4));
   A(dalloc(&c.bitO, mb * wpf * 4));
   if (c.p.debug) A(dalloc(&c.bitOC, mb * wpf * 4));
@@ -410,13 +415,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.tstate, (uint64_t)n_streams * sizeof(fizi::TrackState)));
   if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned), table_bytes);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.pinned_ev, cudaEventDisableTiming);
-  if (e == cudaSuccess) {
-    // the tail (labelling etc.) is latency-bound: its CTAs go before pending
-    // CTAs of the throughput-bound segmentation kernel
-    int lo_prio = 0, hi_prio = 0;
-    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
-    e = cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking, hi_prio);
-  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking);
   for (uint32_t k = 0; k < fizi::kMaxSub && e == cudaSuccess; k++)
     e = cudaEventCreateWithFlags(&c.ev_seg[k], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming);

@@ -73,6 +73,7 @@ struct Ctx {
   uint32_t* dirty = nullptr;             // max_batch x dirty_words: chunks with non-zero A words
   uint32_t dirty_words = 0;              // ceil(nchunks / 32)
   uint32_t* sub_done = nullptr;          // kMaxSub (CCL CTAs finished per sub-batch)
+  uint32_t* fold_sync = nullptr;         // 2 + max_batch: incremental fold lock / cursor / ready
   uint32_t* bitA = nullptr;              // max_batch * H * P
   uint32_t* bitO = nullptr;              // max_batch * H * P
   uint32_t* bitOC = nullptr;             // debug copy of O

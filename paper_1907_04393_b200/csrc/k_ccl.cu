@@ -53,6 +53,7 @@ struct CclArgs {
   bool masks_zeroed;
   uint32_t n;                   // frames in the launch (sub-batch)
   uint32_t* sub_done;           // CTAs finished in this launch
+  uint32_t* fold_sync;          // [0] lock, [1] cursor, [2 + i] frame f0+i ready (zeroed per call)
   int track_stream;             // -2: no fold; -1: per-stream fold; >= 0: single stream
   int trace;                    // diagnostics: block 0 prints phase clocks
   uint32_t n_streams;
@@ -399,7 +400,15 @@ __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
   }
 }
 
+__device__ unsigned long long g_ccl_trace[4096][4];          // diagnostics (FIZI_CCL_TRACE)
+__device__ __forceinline__ unsigned long long gtimer_ccl() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
+  const unsigned long long g_t0 = a.trace ? gtimer_ccl() : 0ull;
   extern __shared__ __align__(16) uint8_t smc[];
   const uint32_t f = a.f0 + blockIdx.x;
   const uint32_t T = a.frame_runs[f];
@@ -415,11 +424,53 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   }
   if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) {
     t_mark[7] = clock64();
-    printf("CCL_TRACE T=%u start->load %lld load %lld union %lld flatten %lld stats %lld select %lld blob %lld tail %lld\n", T,
+    if (false) printf("CCL_TRACE T=%u start->load %lld load %lld union %lld flatten %lld stats %lld select %lld blob %lld tail %lld\n", T,
            t_mark[0] - t_mark[9], t_mark[1] - t_mark[0], t_mark[2] - t_mark[1], t_mark[3] - t_mark[2],
            t_mark[4] - t_mark[3], t_mark[5] - t_mark[4], t_mark[6] - t_mark[5], t_mark[7] - t_mark[6]);
   }
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < 4096) {
+    g_ccl_trace[blockIdx.x][0] = g_t0;
+    g_ccl_trace[blockIdx.x][1] = gtimer_ccl();
+    g_ccl_trace[blockIdx.x][2] = T;
+  }
   if (a.track_stream == -2) return;
+  if (a.track_stream >= 0) {
+    // single stream: the fold advances while other frames are still being
+    // labelled.  Frame f is marked ready; whoever holds the fold lock folds
+    // consecutive ready frames from the cursor; after releasing the lock the
+    // holder re-checks the cursor, so a frame that became ready while the
+    // lock was held is never left behind.  Nobody waits for another CTA.
+    __syncthreads();                          // this frame's record is complete
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicExch(a.fold_sync + 2 + (f - a.f0), 1u);
+      volatile uint32_t* cursor = a.fold_sync + 1;
+      while (true) {
+        if (atomicCAS(a.fold_sync, 0u, 1u) != 0u) break;    // someone else folds
+        __threadfence();
+        TrackState st = a.tstate[a.track_stream];
+        uint32_t i = *cursor;
+        while (i < a.n && atomicAdd(a.fold_sync + 2 + i, 0u) != 0u) {
+          __threadfence();                                    // acquire frame i's record
+          fizi_result& r = a.res[a.f0 + i];
+          fizi_result q;
+          q.t_ms = __ldcg(&r.t_ms); q.blob_area = __ldcg(&r.blob_area);
+          q.cx = __ldcg(&r.cx); q.cy = __ldcg(&r.cy);
+          track_one(a.p, st, q);
+          r.visible = q.visible; r.clicked = q.clicked;
+          r.px = q.px; r.py = q.py; r.dwell_ms = q.dwell_ms;
+          i++;
+        }
+        a.tstate[a.track_stream] = st;
+        *cursor = i;
+        __threadfence();
+        atomicExch(a.fold_sync, 0u);                          // release
+        __threadfence();
+        if (i >= a.n || atomicAdd(a.fold_sync + 2 + i, 0u) == 0u) break;   // nothing left for now
+      }
+    }
+    return;
+  }
   __shared__ uint32_t s_last;
   __syncthreads();                            // this frame's record is complete
   if (threadIdx.x == 0) {
@@ -429,9 +480,8 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   }
   __syncthreads();
   if (s_last) {
-    long long t0 = clock64();
     fold_records(a, smc);
-    if (a.trace && threadIdx.x == 0) printf("CCL_TRACE fold %lld cycles (n=%u)\n", clock64() - t0, a.n);
+    if (a.trace && threadIdx.x == 0 && blockIdx.x < 4096) g_ccl_trace[blockIdx.x][3] = gtimer_ccl();
   }
 }
 
@@ -452,6 +502,7 @@ cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_resul
   a.masks_zeroed = masks_zeroed;
   a.n = n;
   a.sub_done = c.sub_done + sub;
+  a.fold_sync = c.fold_sync;
   a.track_stream = track_stream;
   a.n_streams = c.n_streams;
   a.frame_stream = c.frame_stream;
@@ -525,3 +576,7 @@ cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaS
 }
 
 }  // namespace fizi
+
+extern "C" int fizi_diag_ccl_trace(unsigned long long* host, unsigned int n) {
+  return (int)cudaMemcpyFromSymbol(host, fizi::g_ccl_trace, sizeof(unsigned long long) * 4 * n);
+}
