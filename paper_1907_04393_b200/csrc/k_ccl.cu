@@ -436,38 +436,77 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   if (a.track_stream == -2) return;
   if (a.track_stream >= 0) {
     // single stream: the fold advances while other frames are still being
-    // labelled.  Frame f is marked ready; whoever holds the fold lock folds
-    // consecutive ready frames from the cursor; after releasing the lock the
-    // holder re-checks the cursor, so a frame that became ready while the
-    // lock was held is never left behind.  Nobody waits for another CTA.
+    // labelled.  Frame f is marked ready; the CTA that holds the fold lock
+    // loads the ready records from the cursor on (all threads, in parallel)
+    // and thread 0 folds them from shared memory.  After releasing the lock
+    // the holder re-checks the cursor, so a frame that became ready while
+    // the lock was held is never left behind.  Nobody waits for another CTA.
+    __shared__ uint32_t s_own, s_i0, s_cnt;
     __syncthreads();                          // this frame's record is complete
     if (threadIdx.x == 0) {
       __threadfence();
       atomicExch(a.fold_sync + 2 + (f - a.f0), 1u);
-      volatile uint32_t* cursor = a.fold_sync + 1;
-      while (true) {
-        if (atomicCAS(a.fold_sync, 0u, 1u) != 0u) break;    // someone else folds
+    }
+    int64_t* t_s = reinterpret_cast<int64_t*>(smc);
+    double* cx_s = reinterpret_cast<double*>(t_s + 1024);
+    double* cy_s = cx_s + 1024;
+    uint32_t* ar_s = reinterpret_cast<uint32_t*>(cy_s + 1024);
+    while (true) {
+      if (threadIdx.x == 0) {
+        s_own = atomicCAS(a.fold_sync, 0u, 1u) == 0u;
+        if (s_own) {
+          __threadfence();
+          s_i0 = *reinterpret_cast<volatile uint32_t*>(a.fold_sync + 1);
+          s_cnt = 0xFFFFFFFFu;
+        }
+      }
+      __syncthreads();
+      if (!s_own) break;                                   // someone else folds
+      const uint32_t i0 = s_i0;
+      // length of the ready prefix from the cursor (at most blockDim frames)
+      const uint32_t i = i0 + threadIdx.x;
+      const bool rdy = i < a.n && atomicAdd(a.fold_sync + 2 + i, 0u) != 0u;
+      if (!rdy && i <= a.n) atomicMin(&s_cnt, threadIdx.x);
+      __syncthreads();
+      const uint32_t cnt = min(s_cnt, blockDim.x);
+      if (threadIdx.x < cnt) {
         __threadfence();
+        const fizi_result& r = a.res[a.f0 + i];
+        t_s[threadIdx.x] = __ldcg(&r.t_ms);
+        ar_s[threadIdx.x] = __ldcg(&r.blob_area);
+        cx_s[threadIdx.x] = __ldcg(&r.cx);
+        cy_s[threadIdx.x] = __ldcg(&r.cy);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
         TrackState st = a.tstate[a.track_stream];
-        uint32_t i = *cursor;
-        while (i < a.n && atomicAdd(a.fold_sync + 2 + i, 0u) != 0u) {
-          __threadfence();                                    // acquire frame i's record
-          fizi_result& r = a.res[a.f0 + i];
+        for (uint32_t k = 0; k < cnt; k++) {
           fizi_result q;
-          q.t_ms = __ldcg(&r.t_ms); q.blob_area = __ldcg(&r.blob_area);
-          q.cx = __ldcg(&r.cx); q.cy = __ldcg(&r.cy);
+          q.t_ms = t_s[k]; q.blob_area = ar_s[k]; q.cx = cx_s[k]; q.cy = cy_s[k];
           track_one(a.p, st, q);
-          r.visible = q.visible; r.clicked = q.clicked;
-          r.px = q.px; r.py = q.py; r.dwell_ms = q.dwell_ms;
-          i++;
+          t_s[k] = q.dwell_ms; cx_s[k] = q.px; cy_s[k] = q.py;
+          ar_s[k] = (uint32_t)q.visible | ((uint32_t)q.clicked << 1);
         }
         a.tstate[a.track_stream] = st;
-        *cursor = i;
-        __threadfence();
-        atomicExch(a.fold_sync, 0u);                          // release
-        __threadfence();
-        if (i >= a.n || atomicAdd(a.fold_sync + 2 + i, 0u) == 0u) break;   // nothing left for now
       }
+      __syncthreads();
+      if (threadIdx.x < cnt) {
+        fizi_result& o = a.res[a.f0 + i];
+        o.visible = (uint8_t)(ar_s[threadIdx.x] & 1u); o.clicked = (uint8_t)(ar_s[threadIdx.x] >> 1);
+        o.px = cx_s[threadIdx.x]; o.py = cy_s[threadIdx.x]; o.dwell_ms = t_s[threadIdx.x];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const uint32_t nxt = i0 + cnt;
+        *reinterpret_cast<volatile uint32_t*>(a.fold_sync + 1) = nxt;
+        __threadfence();
+        atomicExch(a.fold_sync, 0u);                        // release
+        __threadfence();
+        // retry iff a frame at the cursor became ready meanwhile
+        s_own = nxt < a.n && atomicAdd(a.fold_sync + 2 + nxt, 0u) != 0u;
+      }
+      __syncthreads();
+      if (!s_own) break;
     }
     return;
   }
