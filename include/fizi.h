@@ -179,10 +179,12 @@ int fizi_get_background(fizi_ctx *ctx, uint32_t stream, uint8_t *lo_dev, uint8_t
 int fizi_set_background(fizi_ctx *ctx, uint32_t stream, const uint8_t *lo_dev,
                         const uint8_t *hi_dev, fizi_stream_t cuda_stream);
 
-/* Per-stage device timing.  When enabled, every subsequent call records CUDA
- * events on its stream around each stage; fizi_profile_read synchronises
- * those events and returns the accumulated milliseconds and the number of
- * timed launches per slot (FIZI_PROF_*), optionally resetting them. */
+/* Per-stage device timing.  mode 1: every subsequent call records CUDA
+ * events on its streams around each stage; mode 2: around the fused
+ * segmentation kernel only (two events per call); 0: off.
+ * fizi_profile_read synchronises those events and returns the accumulated
+ * milliseconds and the number of timed launches per slot (FIZI_PROF_*),
+ * optionally resetting them. */
 enum {
     FIZI_PROF_SEGMENT = 0,    /* fused luma + three branches (a2+a3)          */
     FIZI_PROF_FIXUP = 1,      /* mean -> gamma, LUT re-test of corrected frames */
@@ -192,7 +194,7 @@ enum {
     FIZI_PROF_TRACK = 5,      /* Mouse fold (a8)                              */
     FIZI_PROF_SLOTS = 6
 };
-int fizi_profile_enable(fizi_ctx *ctx, int enable);
+int fizi_profile_enable(fizi_ctx *ctx, int mode);
 int fizi_profile_read(fizi_ctx *ctx, double *ms_out, uint64_t *count_out, int reset);
 
 /* Number of kernels this context has launched so far (evidence for the

@@ -56,12 +56,18 @@ static void prof_resolve(Ctx& c) {
 
 void prof_begin(Ctx& c, cudaStream_t st) {
   if (!c.prof) return;
+  c.prof_skip = false;
   c.prof_open = prof_event(c);
   cudaEventRecord(c.prof_open, st);
 }
 
 void prof_end(Ctx& c, int slot, cudaStream_t st) {
   if (!c.prof || !c.prof_open) return;
+  if (c.prof_mode == 2 && slot != FIZI_PROF_SEGMENT) {   // mode 2: fused kernel only
+    c.prof_free.push_back(c.prof_open);
+    c.prof_open = nullptr;
+    return;
+  }
   cudaEvent_t b = prof_event(c);
   cudaEventRecord(b, st);
   c.prof_pending.push_back({slot, c.prof_open, b});
@@ -129,8 +135,8 @@ cudaError_t dalloc(T** p, size_t bytes) {
 }
 
 void free_all(Ctx& c) {
-  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.luma, c.fg, c.frame_done, c.dirty, c.sub_done, c.fold_sync, c.bitA, c.bitO, c.bitOC,
-                  c.row_cnt, c.row_base, c.frame_runs, c.runs, c.parent, c.stats, c.frame_t, c.fix_count,
+  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.zero_block, c.bitA, c.bitO, c.bitOC,
+                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.frame_t,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -227,14 +233,7 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   std::vector<SubBatch> subs;
   int rc = upload_call(c, sof, t, n, subs, st);
   if (rc) return rc;
-  cudaError_t e = cudaMemsetAsync(c.luma, 0, sizeof(unsigned long long) * n, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(c.fg, 0, sizeof(uint32_t) * n, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(c.frame_done, 0, sizeof(uint32_t) * n, st);
-  if (e == cudaSuccess && c.use_dirty)
-    e = cudaMemsetAsync(c.dirty, 0, sizeof(uint32_t) * c.dirty_words * n, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(c.sub_done, 0, sizeof(uint32_t) * fizi::kMaxSub, st);
-  for (size_t k = 0; k < subs.size() && e == cudaSuccess; k++)
-    e = cudaMemsetAsync(c.fix_count + k * (c.max_batch + 1), 0, sizeof(uint32_t), st);
+  cudaError_t e = cudaMemsetAsync(c.zero_block, 0, c.zero_bytes, st);   // every per-call counter
   if (e != cudaSuccess) return cuda_fail(c, e, "memset");
   bool single = true;
   for (uint32_t i = 1; i < n && single; i++) single = sof[i] == sof[0];
@@ -272,10 +271,6 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
       e = cudaMemcpyAsync(c.bitOC + b.f0 * w, c.bitO + b.f0 * w, (size_t)b.n * w * 4,
                           cudaMemcpyDeviceToDevice, sd);
       if (e != cudaSuccess) return cuda_fail(c, e, "debug copy");
-    }
-    if (fold >= 0) {
-      e = cudaMemsetAsync(c.fold_sync, 0, sizeof(uint32_t) * (b.n + 2), sd);
-      if (e != cudaSuccess) return cuda_fail(c, e, "fold memset");
     }
     prof_begin(c, sd);
     e = fizi::launch_ccl(c, b.f0, b.n, (uint32_t)k, res, fused_mask ? masks : nullptr, premask, fold,
@@ -393,25 +388,34 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.gamma_tab, 256 * sizeof(double)));
   A(dalloc(&c.corr_tab, 256));
   A(dalloc(&c.skin_tab, (1u << 19) * 4));
-  A(dalloc(&c.luma, mb * 8));
-  A(dalloc(&c.fg, mb * 4));
-  A(dalloc(&c.frame_done, mb * 4));
+  // per-call counters and flags: one block, cleared by one memset per call
   c.dirty_words = (c.nchunks + 31) / 32;
-  A(dalloc(&c.dirty, mb * c.dirty_words * 4));
-  A(dalloc(&c.sub_done, fizi::kMaxSub * 4));
-  A(dalloc(&c.fold_sync, (mb + 2) * 4));
+  {
+    const uint64_t zb = mb * 8 + mb * 4 * 3 + fizi::kMaxSub * 4 + fizi::kMaxSub * (mb + 2) * 4 +
+                        fizi::kMaxSub * (mb + 1) * 4 + mb * c.dirty_words * 4;
+    c.zero_bytes = zb;
+    A(dalloc(&c.zero_block, zb));
+    uint8_t* z = c.zero_block;
+    c.luma = reinterpret_cast<unsigned long long*>(z); z += mb * 8;
+    c.fg = reinterpret_cast<uint32_t*>(z); z += mb * 4;
+    c.frame_done = reinterpret_cast<uint32_t*>(z); z += mb * 4;
+    c.frame_runs = reinterpret_cast<uint32_t*>(z); z += mb * 4;
+    c.sub_done = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * 4;
+    c.fold_sync = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * (mb + 2) * 4;
+    c.fix_count = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * (mb + 1) * 4;
+    c.dirty = reinterpret_cast<uint32_t*>(z);
+  }
+
   A(dalloc(&c.bitA, mb * wpf * 4));
   A(dalloc(&c.bitO, mb * wpf * 4));
   if (c.p.debug) A(dalloc(&c.bitOC, mb * wpf * 4));
   A(dalloc(&c.row_cnt, mb * c.H * 4));
   A(dalloc(&c.row_base, mb * c.H * 4));
-  A(dalloc(&c.frame_runs, mb * 4));
   A(dalloc(&c.runs, mb * c.cap_runs * sizeof(fizi::Run)));
   A(dalloc(&c.parent, mb * c.cap_runs * 4));
   A(dalloc(&c.stats, mb * c.cap_runs * sizeof(fizi::RootStats)));
   const size_t table_bytes = mb * 8 + mb * 4 * 2 + (mb + 1) * 4;
   A(dalloc(&c.frame_t, table_bytes));
-  A(dalloc(&c.fix_count, (uint64_t)fizi::kMaxSub * (mb + 1) * 4));
   A(dalloc(&c.tstate, (uint64_t)n_streams * sizeof(fizi::TrackState)));
   if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned), table_bytes);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.pinned_ev, cudaEventDisableTiming);
@@ -617,9 +621,10 @@ int fizi_set_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* lo_dev,
   return FIZI_OK;
 }
 
-int fizi_profile_enable(fizi_ctx* ctx, int enable) {
-  if (!ctx) return FIZI_E_ARG;
-  ctx->c.prof = enable != 0;
+int fizi_profile_enable(fizi_ctx* ctx, int mode) {
+  if (!ctx || mode < 0 || mode > 2) return FIZI_E_ARG;
+  ctx->c.prof = mode != 0;
+  ctx->c.prof_mode = mode;
   return FIZI_OK;
 }
 

@@ -67,13 +67,15 @@ struct Ctx {
   double* gamma_tab = nullptr;           // 256
   uint8_t* corr_tab = nullptr;           // 256
   uint32_t* skin_tab = nullptr;          // 2^24 bits: R2 & R3 of every corrected colour
+  uint8_t* zero_block = nullptr;         // per-call counters (cleared each call), views below
+  uint64_t zero_bytes = 0;
   unsigned long long* luma = nullptr;    // max_batch
   uint32_t* fg = nullptr;                // max_batch (fg_merged)
   uint32_t* frame_done = nullptr;        // max_batch (CTAs finished per frame)
   uint32_t* dirty = nullptr;             // max_batch x dirty_words: chunks with non-zero A words
   uint32_t dirty_words = 0;              // ceil(nchunks / 32)
   uint32_t* sub_done = nullptr;          // kMaxSub (CCL CTAs finished per sub-batch)
-  uint32_t* fold_sync = nullptr;         // 2 + max_batch: incremental fold lock / cursor / ready
+  uint32_t* fold_sync = nullptr;         // kMaxSub x (2 + max_batch): fold lock / cursor / ready
   uint32_t* bitA = nullptr;              // max_batch * H * P
   uint32_t* bitO = nullptr;              // max_batch * H * P
   uint32_t* bitOC = nullptr;             // debug copy of O
@@ -107,6 +109,8 @@ struct Ctx {
   cudaEvent_t pinned_ev = nullptr;
   // per-stage timing (fizi_profile_*)
   bool prof = false;
+  int prof_mode = 0;                     // 1: all stages, 2: fused kernel only
+  bool prof_skip = false;
   struct ProfRec { int slot; cudaEvent_t a, b; };
   std::vector<ProfRec> prof_pending;
   std::vector<cudaEvent_t> prof_free;

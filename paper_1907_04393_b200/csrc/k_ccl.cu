@@ -541,7 +541,7 @@ cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_resul
   a.masks_zeroed = masks_zeroed;
   a.n = n;
   a.sub_done = c.sub_done + sub;
-  a.fold_sync = c.fold_sync;
+  a.fold_sync = c.fold_sync + (uint64_t)sub * (c.max_batch + 2);
   a.track_stream = track_stream;
   a.n_streams = c.n_streams;
   a.frame_stream = c.frame_stream;

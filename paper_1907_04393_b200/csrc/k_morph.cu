@@ -599,7 +599,6 @@ cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, bool m
   a.frame_runs = c.frame_runs;
   a.runs = c.runs;
   const uint32_t r = c.p.se_radius;
-  cudaMemsetAsync(c.frame_runs + f0, 0, n * sizeof(uint32_t), st);
   if (c.P <= 128 && r <= 4) {
     const dim3 grid((c.H + kBandRows - 1) / kBandRows, n);
     const size_t band_smem = (size_t)(kBandRows + 8 * r) * c.P * sizeof(uint32_t);

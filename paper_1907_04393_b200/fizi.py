@@ -250,8 +250,9 @@ class Fizi:
         self._check(lib().fizi_set_background(self._h, stream, lo.data_ptr(), hi.data_ptr(),
                                               _stream_handle(self.device)), "fizi_set_background")
 
-    def profile_enable(self, on: bool = True):
-        self._check(lib().fizi_profile_enable(self._h, int(on)), "fizi_profile_enable")
+    def profile_enable(self, mode=True):
+        """mode True/1: every stage; 2: the fused segmentation kernel only; False/0: off."""
+        self._check(lib().fizi_profile_enable(self._h, int(mode)), "fizi_profile_enable")
 
     def profile_read(self, reset: bool = True) -> dict:
         ms = np.zeros(PROF_SLOTS, np.float64)
