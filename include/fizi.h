@@ -179,6 +179,23 @@ int fizi_get_background(fizi_ctx *ctx, uint32_t stream, uint8_t *lo_dev, uint8_t
 int fizi_set_background(fizi_ctx *ctx, uint32_t stream, const uint8_t *lo_dev,
                         const uint8_t *hi_dev, fizi_stream_t cuda_stream);
 
+/* Pipelined mode (enable = 1; default 0).  By default every output of a
+ * fizi_process_frames / fizi_segment_frames call is complete in cuda_stream
+ * order when the call returns.  In pipelined mode a call's tail (LUT
+ * re-test, a4-a7, the u8 mask, the a8 fold) runs on the context's internal
+ * stream and is NOT joined into cuda_stream, so that it overlaps the next
+ * call's segmentation; per-call state is double-buffered inside the context.
+ * Outputs of pipelined calls are complete on a stream after fizi_flush on
+ * that stream; until then the caller must not read or reuse their masks /
+ * results buffers, nor overwrite their frames.  Every other entry point
+ * that touches the tail's state (learn / set_background / track / debug /
+ * host entry) joins the outstanding tails into its stream itself. */
+int fizi_set_pipeline(fizi_ctx *ctx, int enable);
+
+/* Make cuda_stream wait for the tails of all previous calls (no-op when
+ * nothing is outstanding).  Enqueues only; does not block the host. */
+int fizi_flush(fizi_ctx *ctx, fizi_stream_t cuda_stream);
+
 /* Per-stage device timing.  mode 1: every subsequent call records CUDA
  * events on its streams around each stage; mode 2: around the fused
  * segmentation kernel only (two events per call); 0: off.

@@ -134,38 +134,75 @@ cudaError_t dalloc(T** p, size_t bytes) {
   return cudaMalloc(reinterpret_cast<void**>(p), bytes ? bytes : 16);
 }
 
+void destroy_graphs(Ctx& c);
+
 void free_all(Ctx& c) {
-  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.zero_block, c.bitA, c.bitO, c.bitOC,
-                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.frame_t,
+  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.zero_blocks[0], c.zero_blocks[1],
+                  c.bitAs[0], c.bitAs[1], c.bitO, c.bitOC, c.calls[0], c.calls[1],
+                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  if (c.pinned) cudaFreeHost(c.pinned);
-  if (c.pinned_ev) cudaEventDestroy(c.pinned_ev);
+  destroy_graphs(c);
+  for (int i = 0; i < 2; i++) {
+    if (c.pinned[i]) cudaFreeHost(c.pinned[i]);
+    if (c.pinned_ev[i]) cudaEventDestroy(c.pinned_ev[i]);
+  }
+  if (c.cap) cudaStreamDestroy(c.cap);
   for (auto ev : c.ev_seg)
     if (ev) cudaEventDestroy(ev);
   if (c.ev_join) cudaEventDestroy(c.ev_join);
   if (c.ev_start) cudaEventDestroy(c.ev_start);
+  for (int i = 0; i < 2; i++) {
+    if (c.ev_head[i]) cudaEventDestroy(c.ev_head[i]);
+    if (c.ev_tail[i]) cudaEventDestroy(c.ev_tail[i]);
+  }
   if (c.side) cudaStreamDestroy(c.side);
   for (auto& r : c.prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c.prof_free) cudaEventDestroy(e);
   if (c.prof_open) cudaEventDestroy(c.prof_open);
 }
 
+// Point the context's per-call views at slot s.
+void select_slot(Ctx& c, uint32_t s) {
+  const uint64_t mb = c.max_batch;
+  uint8_t* z = c.zero_blocks[s];
+  c.zero_block = z;
+  c.luma = reinterpret_cast<unsigned long long*>(z); z += mb * 8;
+  c.fg = reinterpret_cast<uint32_t*>(z); z += mb * 4;
+  c.frame_done = reinterpret_cast<uint32_t*>(z); z += mb * 4;
+  c.frame_runs = reinterpret_cast<uint32_t*>(z); z += mb * 4;
+  c.sub_done = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * 4;
+  c.fold_sync = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * (mb + 2) * 4;
+  c.fix_count = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * (mb + 1) * 4;
+  c.dirty = reinterpret_cast<uint32_t*>(z);
+  c.bitA = c.bitAs[s];
+  c.call = c.calls[s];
+  c.frame_t = reinterpret_cast<int64_t*>(c.call + 1);
+  c.frame_stream = reinterpret_cast<uint32_t*>(c.frame_t + mb);
+  c.group_frames = c.frame_stream + mb;
+  c.group_off = c.group_frames + mb;
+}
+
+// Make st wait for every outstanding pipelined tail (side stream is in order).
+cudaError_t join_tail(Ctx& c, cudaStream_t st) {
+  if (!c.tail_pending) return cudaSuccess;
+  return cudaStreamWaitEvent(st, c.ev_tail[c.last_slot], 0);
+}
+
 struct SubBatch {
   uint32_t f0, n, g0, ng;
 };
 
-// Upload the per-call frame table (timestamps, streams, same-stream groups).
-// Frames are cut into sub-batches of c.sub_frames (at most kMaxSub); inside a
-// sub-batch, groups are the frames of one stream in index order, split every
-// kFrameGroup frames.
-int upload_call(Ctx& c, const uint32_t* sof, const int64_t* t, uint32_t n,
-                std::vector<SubBatch>& subs, cudaStream_t st) {
+// Host side of the per-call table: CallPtrs, timestamps, streams and the
+// same-stream groups, written into pinned slot `slot`.  Frames are cut into
+// sub-batches of c.sub_frames (at most kMaxSub); inside a sub-batch, groups
+// are the frames of one stream in index order, split every kFrameGroup frames.
+void fill_call(Ctx& c, uint32_t slot, const fizi::CallPtrs& cp, const uint32_t* sof,
+               const int64_t* t, uint32_t n, std::vector<SubBatch>& subs) {
   const uint32_t mb = c.max_batch;
-  cudaError_t e = cudaEventSynchronize(c.pinned_ev);      // previous upload consumed
-  if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventSynchronize");
-  int64_t* ht = reinterpret_cast<int64_t*>(c.pinned);
+  *reinterpret_cast<fizi::CallPtrs*>(c.pinned[slot]) = cp;
+  int64_t* ht = reinterpret_cast<int64_t*>(c.pinned[slot] + sizeof(fizi::CallPtrs));
   uint32_t* hs = reinterpret_cast<uint32_t*>(ht + mb);
   uint32_t* hg = hs + mb;
   uint32_t* ho = hg + mb;
@@ -198,11 +235,165 @@ int upload_call(Ctx& c, const uint32_t* sof, const int64_t* t, uint32_t n,
     subs.push_back(b);
   }
   ho[g] = pos;
-  const size_t bytes = (size_t)mb * 8 + (size_t)mb * 4 * 2 + (size_t)(mb + 1) * 4;
-  e = cudaMemcpyAsync(c.frame_t, c.pinned, bytes, cudaMemcpyHostToDevice, st);
+}
+
+struct CallPlan {
+  uint32_t n = 0, slot = 0;
+  std::vector<SubBatch> subs;
+  int fold = -2;               // -2 no fold, -1 per-stream end fold, >= 0 single-stream fold
+  bool fused_mask = false;     // the labelling kernel writes the u8 mask (pre-zeroed)
+  bool premask = false;
+  uint8_t* masks = nullptr;    // caller's u8 masks (expand path only)
+};
+
+// Parts of a call's launch sequence.  kWhole: everything on the caller's
+// stream st (sub-batch k's tail forked to the side stream, overlapping the
+// segmentation of sub-batch k+1, joined back).  Pipelined mode splits the
+// call into kHead (upload + counters + fused segmentation, on st) and kTail
+// (u8 mask zeroing, LUT re-test, a4 morphology, a5-a7 labelling + u8 mask,
+// a8 fold, on the side stream) so that call k's tail overlaps call k+1's head.
+enum Part { kWhole = 0, kHead = 1, kTail = 2 };
+
+int enqueue_head(Ctx& c, const CallPlan& pl, cudaStream_t st) {
+  cudaError_t e = cudaMemcpyAsync(c.call, c.pinned[pl.slot], c.pinned_bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemcpyAsync(call table)");
-  e = cudaEventRecord(c.pinned_ev, st);
-  if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
+  e = cudaMemsetAsync(c.zero_block, 0, c.zero_bytes, st);   // every per-call counter
+  if (e != cudaSuccess) return cuda_fail(c, e, "memset");
+  return FIZI_OK;
+}
+
+int enqueue_tail(Ctx& c, const CallPlan& pl, const SubBatch& b, uint32_t k, cudaStream_t sd) {
+  cudaError_t e = fizi::launch_seg_fix(c, b.f0, b.n, k, sd);
+  if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
+  prof_begin(c, sd);
+  e = fizi::launch_morph(c, b.f0, b.n, nullptr, pl.premask, sd);
+  prof_end(c, FIZI_PROF_MORPH, sd);
+  if (e != cudaSuccess) return cuda_fail(c, e, "morph");
+  if (c.p.debug) {
+    const size_t w = (size_t)c.H * c.P;
+    e = cudaMemcpyAsync(c.bitOC + b.f0 * w, c.bitO + b.f0 * w, (size_t)b.n * w * 4,
+                        cudaMemcpyDeviceToDevice, sd);
+    if (e != cudaSuccess) return cuda_fail(c, e, "debug copy");
+  }
+  prof_begin(c, sd);
+  e = fizi::launch_ccl(c, b.f0, b.n, k, pl.premask, pl.fold, sd);
+  prof_end(c, FIZI_PROF_CCL, sd);
+  if (e != cudaSuccess) return cuda_fail(c, e, "ccl");
+  if (pl.masks && !pl.fused_mask) {
+    prof_begin(c, sd);
+    e = fizi::launch_expand(c, b.f0, b.n, pl.masks, sd);
+    prof_end(c, FIZI_PROF_EXPAND, sd);
+    if (e != cudaSuccess) return cuda_fail(c, e, "expand");
+  }
+  return FIZI_OK;
+}
+
+// The launch sequence of one part on stream st.  It is identical for every
+// call of the same plan (all per-call pointers travel in the uploaded
+// CallPtrs), so it is captured once into a CUDA graph and replayed.
+int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+  int rc = FIZI_OK;
+  if (part == kHead) {
+    rc = enqueue_head(c, pl, st);
+    if (rc) return rc;
+    e = fizi::launch_seg_main(c, 0, pl.n, 0, pl.subs[0].ng, 0, st);
+    return e == cudaSuccess ? FIZI_OK : cuda_fail(c, e, "segment");
+  }
+  if (part == kTail) {
+    if (pl.premask) {
+      e = fizi::launch_zero_masks(c, pl.n, st);
+      if (e != cudaSuccess) return cuda_fail(c, e, "mask zero");
+    }
+    return enqueue_tail(c, pl, pl.subs[0], 0, st);
+  }
+  rc = enqueue_head(c, pl, st);
+  if (rc) return rc;
+  cudaStream_t sd = c.side;
+  e = cudaEventRecord(c.ev_start, st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, c.ev_start, 0);
+  if (e != cudaSuccess) return cuda_fail(c, e, "fork");
+  // the u8 mask target is zeroed on the side stream while the fused
+  // segmentation kernel runs; the labelling kernel then writes the bytes of
+  // the kept components only
+  if (pl.premask) {
+    e = fizi::launch_zero_masks(c, pl.n, sd);
+    if (e != cudaSuccess) return cuda_fail(c, e, "mask zero");
+  }
+  for (size_t k = 0; k < pl.subs.size(); k++) {
+    const SubBatch& b = pl.subs[k];
+    e = fizi::launch_seg_main(c, b.f0, b.n, b.g0, b.ng, (uint32_t)k, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "segment");
+    e = cudaEventRecord(c.ev_seg[k], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, c.ev_seg[k], 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "event");
+    rc = enqueue_tail(c, pl, b, (uint32_t)k, sd);
+    if (rc) return rc;
+  }
+  e = cudaEventRecord(c.ev_join, sd);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c.ev_join, 0);
+  if (e != cudaSuccess) return cuda_fail(c, e, "join");
+  return FIZI_OK;
+}
+
+void destroy_graphs(Ctx& c) {
+  for (auto& g : c.graphs)
+    for (auto x : g.exec)
+      if (x) cudaGraphExecDestroy(x);
+  c.graphs.clear();
+}
+
+// Run one part: replay (capturing on first use) the graph of this plan's
+// shape, or launch directly (profiling, or graphs disabled).
+int run_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
+  const bool graph = c.use_graphs && !c.prof && !(pl.masks && !pl.fused_mask);
+  if (!graph) return enqueue_part(c, pl, part, st);
+  std::vector<uint32_t> key = {(uint32_t)part, pl.n, (uint32_t)(pl.fold + 2), (uint32_t)pl.premask,
+                               (uint32_t)pl.fused_mask};
+  for (const SubBatch& b : pl.subs) {
+    key.push_back(b.n);
+    key.push_back(b.g0);
+    key.push_back(b.ng);
+  }
+  Ctx::GraphEntry* ent = nullptr;
+  for (auto& g : c.graphs)
+    if (g.key == key) { ent = &g; break; }
+  if (!ent) {
+    constexpr size_t kMaxGraphs = 16;
+    if (c.graphs.size() >= kMaxGraphs) {               // evict the least recently used
+      size_t lru = 0;
+      for (size_t i = 1; i < c.graphs.size(); i++)
+        if (c.graphs[i].used < c.graphs[lru].used) lru = i;
+      for (auto x : c.graphs[lru].exec)
+        if (x) cudaGraphExecDestroy(x);
+      c.graphs.erase(c.graphs.begin() + (long)lru);
+    }
+    c.graphs.emplace_back();
+    ent = &c.graphs.back();
+    ent->key = key;
+  }
+  ent->used = ++c.graph_clock;
+  if (!ent->exec[pl.slot]) {
+    const uint64_t l0 = c.launches;
+    cudaError_t e = cudaStreamBeginCapture(c.cap, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamBeginCapture");
+    const int rc = enqueue_part(c, pl, part, c.cap);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(c.cap, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&ent->exec[pl.slot], g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
+    ent->kernels = c.launches - l0;
+    c.launches = l0;
+  }
+  cudaError_t e = cudaGraphLaunch(ent->exec[pl.slot], st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphLaunch");
+  c.launches += ent->kernels;
   return FIZI_OK;
 }
 
@@ -223,70 +414,55 @@ int check_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, u
   return FIZI_OK;
 }
 
-// Launch sequence of one call.  Sub-batch k's fused segmentation runs on the
-// caller's stream; its tail (a2 finalisation + LUT re-test, a4 morphology,
-// a5-a7 labelling, the u8 mask, a8 fold) runs on the context's side stream,
-// overlapping segmentation of sub-batch k+1.  The caller's stream waits for
-// the side stream before the call returns, so outputs are ordered on it.
 int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, const int64_t* t,
              uint8_t* masks, fizi_result* res, bool track, cudaStream_t st) {
-  std::vector<SubBatch> subs;
-  int rc = upload_call(c, sof, t, n, subs, st);
-  if (rc) return rc;
-  cudaError_t e = cudaMemsetAsync(c.zero_block, 0, c.zero_bytes, st);   // every per-call counter
-  if (e != cudaSuccess) return cuda_fail(c, e, "memset");
+  CallPlan pl;
+  pl.n = n;
   bool single = true;
   for (uint32_t i = 1; i < n && single; i++) single = sof[i] == sof[0];
-  int fold = !track ? -2 : (single ? (int)sof[0] : -1);
+  pl.fold = !track ? -2 : (single ? (int)sof[0] : -1);
   static const bool kNoFoldDiag = getenv("FIZI_DIAG_NO_FOLD") != nullptr;   // timing experiments only
-  if (kNoFoldDiag) fold = -2;
-  // the u8 mask is written by the register-pipelined morphology when it runs
-  const bool fused_mask = c.fast && c.P <= 128 && c.p.se_radius <= 4;
-  cudaStream_t sd = c.side;
-  // the u8 mask buffer is zeroed by a memset on the side stream that overlaps
-  // the fused segmentation kernel; the labelling kernel then writes the bytes
-  // of the kept components only
-  const bool premask = masks && fused_mask;
-  if (premask) {
-    e = cudaEventRecord(c.ev_start, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, c.ev_start, 0);
-    if (e == cudaSuccess) e = cudaMemsetAsync(masks, 0, (size_t)n * c.N, sd);
-    if (e != cudaSuccess) return cuda_fail(c, e, "mask memset");
+  if (kNoFoldDiag) pl.fold = -2;
+  // the u8 mask is written by the labelling kernel when the register-pipelined
+  // morphology runs; otherwise it is expanded from the final bit mask
+  pl.fused_mask = c.fast && c.P <= 128 && c.p.se_radius <= 4;
+  pl.premask = masks && pl.fused_mask;
+  pl.masks = masks;
+  const bool pipelined = c.pipeline && !c.p.debug;
+  pl.slot = c.pinned_next;
+  c.pinned_next ^= 1u;
+  cudaError_t e = cudaEventSynchronize(c.pinned_ev[pl.slot]);   // slot's last upload consumed
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventSynchronize");
+  fizi::CallPtrs cp{frames, pl.fused_mask ? masks : nullptr, res, n};
+  const uint32_t sub_frames = c.sub_frames;
+  if (pipelined) c.sub_frames = 65535;                 // one sub-batch: the tail is the overlap
+  fill_call(c, pl.slot, cp, sof, t, n, pl.subs);
+  c.sub_frames = sub_frames;
+  select_slot(c, pl.slot);
+  // the slot's previous call (two calls back) must be complete
+  e = cudaStreamWaitEvent(st, c.ev_tail[pl.slot], 0);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamWaitEvent");
+  int rc;
+  if (!pipelined) {
+    rc = run_part(c, pl, kWhole, st);
+    if (rc) return rc;
+    e = cudaEventRecord(c.pinned_ev[pl.slot], st);
+    if (e == cudaSuccess) e = cudaEventRecord(c.ev_tail[pl.slot], st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
+  } else {
+    rc = run_part(c, pl, kHead, st);
+    if (rc) return rc;
+    e = cudaEventRecord(c.pinned_ev[pl.slot], st);
+    if (e == cudaSuccess) e = cudaEventRecord(c.ev_head[pl.slot], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side, c.ev_head[pl.slot], 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fork");
+    rc = run_part(c, pl, kTail, c.side);
+    if (rc) return rc;
+    e = cudaEventRecord(c.ev_tail[pl.slot], c.side);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
   }
-  for (size_t k = 0; k < subs.size(); k++) {
-    const SubBatch& b = subs[k];
-    e = fizi::launch_seg_main(c, frames, b.f0, b.n, b.g0, b.ng, (uint32_t)k, res, st);
-    if (e != cudaSuccess) return cuda_fail(c, e, "segment");
-    e = cudaEventRecord(c.ev_seg[k], st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, c.ev_seg[k], 0);
-    if (e != cudaSuccess) return cuda_fail(c, e, "event");
-    e = fizi::launch_seg_fix(c, frames, b.f0, b.n, (uint32_t)k, res, sd);
-    if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
-    prof_begin(c, sd);
-    e = fizi::launch_morph(c, b.f0, b.n, fused_mask ? masks : nullptr, premask, sd);
-    prof_end(c, FIZI_PROF_MORPH, sd);
-    if (e != cudaSuccess) return cuda_fail(c, e, "morph");
-    if (c.p.debug) {
-      const size_t w = (size_t)c.H * c.P;
-      e = cudaMemcpyAsync(c.bitOC + b.f0 * w, c.bitO + b.f0 * w, (size_t)b.n * w * 4,
-                          cudaMemcpyDeviceToDevice, sd);
-      if (e != cudaSuccess) return cuda_fail(c, e, "debug copy");
-    }
-    prof_begin(c, sd);
-    e = fizi::launch_ccl(c, b.f0, b.n, (uint32_t)k, res, fused_mask ? masks : nullptr, premask, fold,
-                         sd);
-    prof_end(c, FIZI_PROF_CCL, sd);
-    if (e != cudaSuccess) return cuda_fail(c, e, "ccl");
-    if (masks && !fused_mask) {
-      prof_begin(c, sd);
-      e = fizi::launch_expand(c, b.f0, b.n, masks, sd);
-      prof_end(c, FIZI_PROF_EXPAND, sd);
-      if (e != cudaSuccess) return cuda_fail(c, e, "expand");
-    }
-  }
-  e = cudaEventRecord(c.ev_join, sd);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c.ev_join, 0);
-  if (e != cudaSuccess) return cuda_fail(c, e, "join");
+  c.tail_pending = true;
+  c.last_slot = pl.slot;
   c.last_frames = frames;
   c.last_n = n;
   return FIZI_OK;
@@ -394,19 +570,12 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
     const uint64_t zb = mb * 8 + mb * 4 * 3 + fizi::kMaxSub * 4 + fizi::kMaxSub * (mb + 2) * 4 +
                         fizi::kMaxSub * (mb + 1) * 4 + mb * c.dirty_words * 4;
     c.zero_bytes = zb;
-    A(dalloc(&c.zero_block, zb));
-    uint8_t* z = c.zero_block;
-    c.luma = reinterpret_cast<unsigned long long*>(z); z += mb * 8;
-    c.fg = reinterpret_cast<uint32_t*>(z); z += mb * 4;
-    c.frame_done = reinterpret_cast<uint32_t*>(z); z += mb * 4;
-    c.frame_runs = reinterpret_cast<uint32_t*>(z); z += mb * 4;
-    c.sub_done = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * 4;
-    c.fold_sync = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * (mb + 2) * 4;
-    c.fix_count = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * (mb + 1) * 4;
-    c.dirty = reinterpret_cast<uint32_t*>(z);
+    A(dalloc(&c.zero_blocks[0], zb));
+    A(dalloc(&c.zero_blocks[1], zb));
   }
 
-  A(dalloc(&c.bitA, mb * wpf * 4));
+  A(dalloc(&c.bitAs[0], mb * wpf * 4));
+  A(dalloc(&c.bitAs[1], mb * wpf * 4));
   A(dalloc(&c.bitO, mb * wpf * 4));
   if (c.p.debug) A(dalloc(&c.bitOC, mb * wpf * 4));
   A(dalloc(&c.row_cnt, mb * c.H * 4));
@@ -414,16 +583,33 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.runs, mb * c.cap_runs * sizeof(fizi::Run)));
   A(dalloc(&c.parent, mb * c.cap_runs * 4));
   A(dalloc(&c.stats, mb * c.cap_runs * sizeof(fizi::RootStats)));
-  const size_t table_bytes = mb * 8 + mb * 4 * 2 + (mb + 1) * 4;
-  A(dalloc(&c.frame_t, table_bytes));
+  const size_t table_bytes = sizeof(fizi::CallPtrs) + mb * 8 + mb * 4 * 2 + (mb + 1) * 4;
+  A(dalloc(&c.calls[0], table_bytes));
+  A(dalloc(&c.calls[1], table_bytes));
   A(dalloc(&c.tstate, (uint64_t)n_streams * sizeof(fizi::TrackState)));
-  if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned), table_bytes);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.pinned_ev, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; i++) {
+    e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned[i]), table_bytes);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.pinned_ev[i], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) {
+    // the tail runs at the highest priority: its CTAs take SM slots as the
+    // next call's segmentation CTAs retire
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    const char* sp = getenv("FIZI_SIDE_PRIO");
+    e = cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking,
+                                     (sp && atoi(sp) == 0) ? lo_prio : hi_prio);
+  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.cap, cudaStreamNonBlocking);
   for (uint32_t k = 0; k < fizi::kMaxSub && e == cudaSuccess; k++)
     e = cudaEventCreateWithFlags(&c.ev_seg[k], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_start, cudaEventDisableTiming);
+  for (int i = 0; i < 2 && e == cudaSuccess; i++) {
+    e = cudaEventCreateWithFlags(&c.ev_head[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_tail[i], cudaEventDisableTiming);
+  }
+  c.use_graphs = getenv("FIZI_NO_GRAPH") == nullptr;
   if (const char* sf = getenv("FIZI_SUB_FRAMES")) c.sub_frames = (uint32_t)atoi(sf) > 0 ? (uint32_t)atoi(sf) : 65535;
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -431,10 +617,8 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
     delete x;
     return FIZI_E_OOM;
   }
-  c.frame_stream = reinterpret_cast<uint32_t*>(c.frame_t + mb);
-  c.group_frames = c.frame_stream + mb;
-  c.group_off = c.group_frames + mb;
   c.pinned_bytes = table_bytes;
+  select_slot(c, 0);
   c.env_valid.assign(n_streams, 0);
   c.last_t.assign(n_streams, 0);
   c.has_t.assign(n_streams, 0);
@@ -470,7 +654,9 @@ int fizi_learn_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* frames_
     return fail(c, FIZI_E_ARG, "frames_dev must be 16-byte aligned");
   DeviceGuard guard(c.device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
-  cudaError_t e = fizi::launch_learn(c, stream, frames_dev, n_frames, margin, st);
+  cudaError_t e = join_tail(c, st);                   // pipelined tails read the envelope
+  if (e != cudaSuccess) return cuda_fail(c, e, "join");
+  e = fizi::launch_learn(c, stream, frames_dev, n_frames, margin, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "learn");
   e = fizi::launch_tstate_reset(c, stream, 1, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "tracker reset");
@@ -517,8 +703,10 @@ int fizi_track(fizi_ctx* ctx, uint32_t stream, fizi_result* results_dev, uint32_
   if (!results_dev) return fail(c, FIZI_E_ARG, "results_dev is NULL");
   DeviceGuard guard(c.device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  cudaError_t e = join_tail(c, st);                   // fold order after pipelined tails
+  if (e != cudaSuccess) return cuda_fail(c, e, "join");
   prof_begin(c, st);
-  cudaError_t e = fizi::launch_track_stream(c, stream, results_dev, n, st);
+  e = fizi::launch_track_stream(c, stream, results_dev, n, st);
   prof_end(c, FIZI_PROF_TRACK, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "track");
   return FIZI_OK;
@@ -552,6 +740,8 @@ int fizi_process_frames_host(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* 
   int rc = fizi_process_frames(ctx, sof, c.stage_frames, n, width, height, t_ms,
                                masks_host ? c.stage_masks : nullptr, c.stage_results, cuda_stream);
   if (rc) return rc;
+  e = join_tail(c, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "join");
   if (masks_host) {
     e = cudaMemcpyAsync(masks_host, c.stage_masks, (size_t)n * c.N, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "D2H masks");
@@ -585,8 +775,9 @@ int fizi_debug_stage(fizi_ctx* ctx, int stage, uint32_t frame, void* out_dev,
   if (frame >= c.last_n) return fail(c, FIZI_E_ARG, "frame index beyond the last call");
   if (stage < FIZI_STAGE_R1 || stage > FIZI_STAGE_CONTOUR) return fail(c, FIZI_E_ARG, "bad stage");
   DeviceGuard guard(c.device);
-  cudaError_t e = fizi::launch_debug_stage(c, stage, frame, out_dev,
-                                           reinterpret_cast<cudaStream_t>(cuda_stream));
+  cudaError_t e = join_tail(c, reinterpret_cast<cudaStream_t>(cuda_stream));
+  if (e == cudaSuccess)
+    e = fizi::launch_debug_stage(c, stage, frame, out_dev, reinterpret_cast<cudaStream_t>(cuda_stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "debug stage");
   return FIZI_OK;
 }
@@ -613,11 +804,27 @@ int fizi_set_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* lo_dev,
   if (!lo_dev || !hi_dev) return fail(c, FIZI_E_ARG, "NULL pointer argument");
   DeviceGuard guard(c.device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
-  cudaError_t e = fizi::launch_env_export(c, stream, nullptr, nullptr, true, lo_dev, hi_dev, st);
+  cudaError_t e = join_tail(c, st);
+  if (e == cudaSuccess) e = fizi::launch_env_export(c, stream, nullptr, nullptr, true, lo_dev, hi_dev, st);
   if (e == cudaSuccess) e = fizi::launch_tstate_reset(c, stream, 1, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "set_background");
   c.env_valid[stream] = 1;
   c.has_t[stream] = 0;
+  return FIZI_OK;
+}
+
+int fizi_set_pipeline(fizi_ctx* ctx, int enable) {
+  if (!ctx || enable < 0 || enable > 1) return FIZI_E_ARG;
+  ctx->c.pipeline = enable != 0;
+  return FIZI_OK;
+}
+
+int fizi_flush(fizi_ctx* ctx, fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  DeviceGuard guard(c.device);
+  cudaError_t e = join_tail(c, reinterpret_cast<cudaStream_t>(cuda_stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "join");
   return FIZI_OK;
 }
 

@@ -36,6 +36,15 @@ struct Run {                             // one horizontal run of foreground pix
   uint16_t x0, x1, y, pad;
 };
 
+// Per-call pointers, uploaded with the per-call table so that the kernels of
+// one call shape are launch-invariant (a captured CUDA graph replays them).
+struct CallPtrs {
+  const uint8_t* frames;                 // n x 3N interleaved RGB (device)
+  uint8_t* masks;                        // u8 mask target of the fused path, or nullptr
+  fizi_result* res;                      // n records (device)
+  uint64_t n;
+};
+
 struct RootStats {                       // per component (indexed by its root run)
   uint32_t area;
   uint32_t xmin, xmax, ymin, ymax;
@@ -67,7 +76,13 @@ struct Ctx {
   double* gamma_tab = nullptr;           // 256
   uint8_t* corr_tab = nullptr;           // 256
   uint32_t* skin_tab = nullptr;          // 2^24 bits: R2 & R3 of every corrected colour
-  uint8_t* zero_block = nullptr;         // per-call counters (cleared each call), views below
+  // Per-call state lives in two slots (calls alternate between them) so that
+  // a call's tail can still run while the next call segments (pipelined
+  // mode).  The pointers below are views of the current slot (select_slot).
+  uint8_t* zero_blocks[2] = {};          // per-call counters (cleared each call)
+  uint32_t* bitAs[2] = {};               // merged masks A
+  CallPtrs* calls[2] = {};               // per-call tables
+  uint8_t* zero_block = nullptr;         // views of the current slot's block below
   uint64_t zero_bytes = 0;
   unsigned long long* luma = nullptr;    // max_batch
   uint32_t* fg = nullptr;                // max_batch (fg_merged)
@@ -86,7 +101,8 @@ struct Ctx {
   uint32_t* parent = nullptr;            // max_batch * cap_runs
   RootStats* stats = nullptr;            // max_batch * cap_runs
   uint32_t* frame_stream = nullptr;      // max_batch
-  int64_t* frame_t = nullptr;            // max_batch (start of the per-call table)
+  CallPtrs* call = nullptr;              // start of the per-call table (device)
+  int64_t* frame_t = nullptr;            // max_batch
   uint32_t* group_frames = nullptr;      // max_batch (frame ids ordered by group)
   uint32_t* group_off = nullptr;         // max_batch + 1
   uint32_t* fix_count = nullptr;         // kMaxSub x (1 + max_batch): per sub-batch count + list
@@ -95,6 +111,11 @@ struct Ctx {
   cudaEvent_t ev_seg[kMaxSub] = {};      // segment(k) done on the caller's stream
   cudaEvent_t ev_join = nullptr;         // tail of the call done on the side stream
   cudaEvent_t ev_start = nullptr;        // call start on the caller's stream
+  cudaEvent_t ev_head[2] = {};           // pipelined: slot's segmentation done
+  cudaEvent_t ev_tail[2] = {};           // slot's last call fully done (slot reusable)
+  bool pipeline = false;                 // fizi_set_pipeline: tails not joined per call
+  bool tail_pending = false;             // some pipelined tail may be outstanding
+  uint32_t last_slot = 0;
   uint32_t sub_frames = 65535;           // frames per sub-batch (default: whole call)
   uint8_t* stage_frames = nullptr;       // device staging for fizi_process_frames_host
   uint8_t* stage_masks = nullptr;
@@ -104,9 +125,21 @@ struct Ctx {
   std::vector<uint8_t> env_valid;
   std::vector<int64_t> last_t;
   std::vector<uint8_t> has_t;
-  uint8_t* pinned = nullptr;             // staging for the per-call upload
+  uint8_t* pinned[2] = {};               // staging for the per-call upload (ring of 2)
   size_t pinned_bytes = 0;
-  cudaEvent_t pinned_ev = nullptr;
+  cudaEvent_t pinned_ev[2] = {};
+  uint32_t pinned_next = 0;
+  // captured launch sequences, one per call shape and pinned slot
+  struct GraphEntry {
+    std::vector<uint32_t> key;
+    cudaGraphExec_t exec[2] = {};
+    uint64_t kernels = 0;                // kernel nodes per replay
+    uint64_t used = 0;
+  };
+  std::vector<GraphEntry> graphs;
+  uint64_t graph_clock = 0;
+  bool use_graphs = true;                // FIZI_NO_GRAPH=1 disables (A/B timing)
+  cudaStream_t cap = nullptr;            // capture origin stream
   // per-stage timing (fizi_profile_*)
   bool prof = false;
   int prof_mode = 0;                     // 1: all stages, 2: fused kernel only
@@ -149,17 +182,19 @@ cudaError_t launch_learn(Ctx& c, uint32_t stream, const uint8_t* frames, uint32_
                          uint32_t margin, cudaStream_t st);
 cudaError_t launch_env_export(Ctx& c, uint32_t stream, uint8_t* lo, uint8_t* hi, bool import,
                               const uint8_t* ilo, const uint8_t* ihi, cudaStream_t st);
-cudaError_t launch_seg_main(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t g0,
-                            uint32_t ng, uint32_t sub, fizi_result* res, cudaStream_t st);
-cudaError_t launch_seg_fix(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t sub,
-                           fizi_result* res, cudaStream_t st);
+// frames / records / u8 masks of a call come from c.call (the uploaded CallPtrs)
+cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32_t ng, uint32_t sub,
+                            cudaStream_t st);
+cudaError_t launch_seg_fix(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st);
 // the segment launcher marks the SEGMENT -> FIXUP boundary through this hook
 void prof_begin(Ctx& c, cudaStream_t st);
 void prof_end(Ctx& c, int slot, cudaStream_t st);
 cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, bool masks_zeroed,
                          cudaStream_t st);
-cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_result* res,
-                       uint8_t* masks, bool masks_zeroed, int track_stream, cudaStream_t st);
+// masks_zeroed: c.call->masks (if any) was zeroed by launch_zero_masks
+cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, bool masks_zeroed,
+                       int track_stream, cudaStream_t st);
+cudaError_t launch_zero_masks(Ctx& c, uint32_t n, cudaStream_t st);
 cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st);
 cudaError_t launch_track_batch(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st);
 cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,

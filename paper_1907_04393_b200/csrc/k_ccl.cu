@@ -44,12 +44,12 @@ struct CclArgs {
   uint32_t* parent;
   RootStats* stats;
   uint64_t cap_runs;
-  fizi_result* res;
+  const CallPtrs* call;         // records + u8 mask target of the call (device)
   const uint32_t* fg;
   uint32_t ppm;
   // fused a6 output / a8 fold
-  uint8_t* masks;               // u8 final mask: written by morphology (dropped blobs cleared
-                                // here) or, when pre-zeroed, written here from the kept runs
+  // call->masks, the u8 final mask: written by morphology (dropped blobs
+  // cleared here) or, when pre-zeroed, written here from the kept runs
   bool masks_zeroed;
   uint32_t n;                   // frames in the launch (sub-batch)
   uint32_t* sub_done;           // CTAs finished in this launch
@@ -102,7 +102,7 @@ __device__ __forceinline__ void unite(uint32_t* par, const Run* R, uint32_t W, u
   }
 }
 
-#define CCL_MARK(k) if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) t_mark[k] = clock64();
+#define CCL_MARK(k) if (a.trace && threadIdx.x == 0) t_mark[k] = clock64();
 
 template <bool kShared>
 __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, uint32_t T,
@@ -164,7 +164,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     }
     if (!__syncthreads_or(changed)) break;
   }
-  (void)rounds;
+  if (a.trace && tid == 0) t_mark[8] = rounds;
   CCL_MARK(3)
 
   // 3. statistics, aggregated over lanes of a warp that share a root
@@ -268,7 +268,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
       best = o > best ? o : best;
     }
     if (lane == 0) {
-      fizi_result* r = a.res + f;
+      fizi_result* r = a.call->res + f;
       r->fg_merged = a.fg[f];
       r->fg_final = fg_final;
       r->n_comp_total = n_tot;
@@ -284,7 +284,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     const uint32_t blabel = 0xFFFFFFFFu - (uint32_t)(bk & 0xFFFFFFFFu);
     for (uint32_t i = tid; i < T; i += nthr) {
       if (ld_par<kShared>(par + i) != i || 1u + run_key(R, i, W) != blabel) continue;
-      fizi_result* r = a.res + f;
+      fizi_result* r = a.call->res + f;
       const RootStats* st = stats + i;
       const uint32_t area = __ldcg(&st->area);
       const unsigned long long sx = __ldcg(&st->sx), sy = __ldcg(&st->sy);
@@ -303,12 +303,12 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
 
   CCL_MARK(6)
   // 5a. pre-zeroed u8 mask: write the bytes of every run of a kept component
-  if (a.masks && a.masks_zeroed) {
+  if (a.call->masks && a.masks_zeroed) {
     for (uint32_t i = tid; i < T; i += nthr) {
       const uint32_t root = ld_par<kShared>(par + i);
       if (!kept_area(__ldcg(&stats[root].area), a.ppm, a.N)) continue;
       const Run rg = R[i];
-      uint8_t* p = a.masks + ((uint64_t)f * H + rg.y) * W;
+      uint8_t* p = a.call->masks + ((uint64_t)f * H + rg.y) * W;
       uint32_t x = rg.x0;
       const uint32_t xe = (uint32_t)rg.x1 + 1;
       for (; x < xe && (x & 15u); x++) p[x] = 1;
@@ -332,8 +332,8 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
       const uint32_t m = (b1 == 31u ? 0xFFFFFFFFu : ((1u << (b1 + 1)) - 1u)) & ~((1u << b0) - 1u);
       atomicAnd(row + k, ~m);
     }
-    if (a.masks && !a.masks_zeroed) {
-      uint8_t* mrow = a.masks + ((uint64_t)f * H + rg.y) * W;
+    if (a.call->masks && !a.masks_zeroed) {
+      uint8_t* mrow = a.call->masks + ((uint64_t)f * H + rg.y) * W;
       for (uint32_t x = rg.x0; x <= rg.x1; x++) mrow[x] = 0;
     }
   }
@@ -355,7 +355,7 @@ __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
     for (uint32_t base = 0; base < n; base += kChunk) {
       const uint32_t m = min(kChunk, n - base);
       for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-        const fizi_result& r = a.res[f0 + base + i];
+        const fizi_result& r = a.call->res[f0 + base + i];
         t_s[i] = __ldcg(&r.t_ms);
         ar_s[i] = __ldcg(&r.blob_area);
         cx_s[i] = __ldcg(&r.cx);
@@ -373,7 +373,7 @@ __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
       }
       __syncthreads();
       for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-        fizi_result& o = a.res[f0 + base + i];
+        fizi_result& o = a.call->res[f0 + base + i];
         o.visible = (uint8_t)(ar_s[i] & 1u); o.clicked = (uint8_t)(ar_s[i] >> 1);
         o.px = cx_s[i]; o.py = cy_s[i]; o.dwell_ms = t_s[i];
       }
@@ -388,10 +388,10 @@ __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
         if (a.frame_stream[f] != s) continue;
         if (!any) { st = a.tstate[s]; any = true; }
         fizi_result r;
-        r.t_ms = __ldcg(&a.res[f].t_ms); r.blob_area = __ldcg(&a.res[f].blob_area);
-        r.cx = __ldcg(&a.res[f].cx); r.cy = __ldcg(&a.res[f].cy);
+        r.t_ms = __ldcg(&a.call->res[f].t_ms); r.blob_area = __ldcg(&a.call->res[f].blob_area);
+        r.cx = __ldcg(&a.call->res[f].cx); r.cy = __ldcg(&a.call->res[f].cy);
         track_one(a.p, st, r);
-        fizi_result& o = a.res[f];
+        fizi_result& o = a.call->res[f];
         o.visible = r.visible; o.clicked = r.clicked;
         o.px = r.px; o.py = r.py; o.dwell_ms = r.dwell_ms;
       }
@@ -400,7 +400,7 @@ __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
   }
 }
 
-__device__ unsigned long long g_ccl_trace[4096][4];          // diagnostics (FIZI_CCL_TRACE)
+__device__ unsigned long long g_ccl_trace[4096][12];   // start, end, T, fold end, phase clocks          // diagnostics (FIZI_CCL_TRACE)
 __device__ __forceinline__ unsigned long long gtimer_ccl() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   const uint32_t f = a.f0 + blockIdx.x;
   const uint32_t T = a.frame_runs[f];
   __shared__ long long t_mark[10];
-  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) t_mark[9] = clock64();
+  if (a.trace && threadIdx.x == 0) t_mark[9] = clock64();
   if (T <= kCclSmemRuns) {
     Run* R = reinterpret_cast<Run*>(smc);
     uint32_t* par = reinterpret_cast<uint32_t*>(smc + sizeof(Run) * kCclSmemRuns);
@@ -422,16 +422,12 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
     ccl_frame<false>(a, f, const_cast<Run*>(a.runs + (uint64_t)f * a.cap_runs),
                      a.parent + (uint64_t)f * a.cap_runs, T, t_mark);
   }
-  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) {
-    t_mark[7] = clock64();
-    if (false) printf("CCL_TRACE T=%u start->load %lld load %lld union %lld flatten %lld stats %lld select %lld blob %lld tail %lld\n", T,
-           t_mark[0] - t_mark[9], t_mark[1] - t_mark[0], t_mark[2] - t_mark[1], t_mark[3] - t_mark[2],
-           t_mark[4] - t_mark[3], t_mark[5] - t_mark[4], t_mark[6] - t_mark[5], t_mark[7] - t_mark[6]);
-  }
   if (a.trace && threadIdx.x == 0 && blockIdx.x < 4096) {
+    t_mark[7] = clock64();
     g_ccl_trace[blockIdx.x][0] = g_t0;
     g_ccl_trace[blockIdx.x][1] = gtimer_ccl();
-    g_ccl_trace[blockIdx.x][2] = T;
+    g_ccl_trace[blockIdx.x][2] = T | ((unsigned long long)t_mark[8] << 32);
+    for (int k = 0; k < 8; k++) g_ccl_trace[blockIdx.x][4 + k] = (unsigned long long)(t_mark[k] - t_mark[9]);
   }
   if (a.track_stream == -2) return;
   if (a.track_stream >= 0) {
@@ -471,7 +467,7 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
       const uint32_t cnt = min(s_cnt, blockDim.x);
       if (threadIdx.x < cnt) {
         __threadfence();
-        const fizi_result& r = a.res[a.f0 + i];
+        const fizi_result& r = a.call->res[a.f0 + i];
         t_s[threadIdx.x] = __ldcg(&r.t_ms);
         ar_s[threadIdx.x] = __ldcg(&r.blob_area);
         cx_s[threadIdx.x] = __ldcg(&r.cx);
@@ -491,7 +487,7 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
       }
       __syncthreads();
       if (threadIdx.x < cnt) {
-        fizi_result& o = a.res[a.f0 + i];
+        fizi_result& o = a.call->res[a.f0 + i];
         o.visible = (uint8_t)(ar_s[threadIdx.x] & 1u); o.clicked = (uint8_t)(ar_s[threadIdx.x] >> 1);
         o.px = cx_s[threadIdx.x]; o.py = cy_s[threadIdx.x]; o.dwell_ms = t_s[threadIdx.x];
       }
@@ -533,11 +529,11 @@ cudaError_t init_ccl(Ctx& c) {
                               (int)kCclSmem);
 }
 
-cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_result* res,
-                       uint8_t* masks, bool masks_zeroed, int track_stream, cudaStream_t st) {
+cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, bool masks_zeroed,
+                       int track_stream, cudaStream_t st) {
   CclArgs a;
   a.f0 = f0;
-  a.masks = masks;
+  a.call = c.call;
   a.masks_zeroed = masks_zeroed;
   a.n = n;
   a.sub_done = c.sub_done + sub;
@@ -559,7 +555,6 @@ cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, fizi_resul
   a.parent = c.parent;
   a.stats = c.stats;
   a.cap_runs = c.cap_runs;
-  a.res = res;
   a.fg = c.fg;
   a.ppm = c.p.min_blob_ppm;
   static const int threads = getenv("FIZI_CCL_THREADS") ? atoi(getenv("FIZI_CCL_THREADS")) : 1024;
@@ -610,6 +605,31 @@ cudaError_t launch_expand_from(Ctx& c, const uint32_t* bits, uint32_t n, uint8_t
   return cudaGetLastError();
 }
 
+// zero the call's u8 mask target (call->masks, call->n frames); runs on the
+// side stream while the fused segmentation kernel streams the frames
+__global__ void __launch_bounds__(512) zero_masks_kernel(const CallPtrs* call, uint64_t N) {
+  uint8_t* m = call->masks;
+  if (!m) return;
+  const uint64_t total = call->n * N;
+  const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t head = min(total, (uint64_t)((16u - (reinterpret_cast<uintptr_t>(m) & 15u)) & 15u));
+  if (gt < head) m[gt] = 0;
+  uint4* body = reinterpret_cast<uint4*>(m + head);
+  const uint64_t nb = (total - head) / 16;
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  for (uint64_t i = gt; i < nb; i += stride) body[i] = z;
+  const uint64_t tail = head + nb * 16;
+  if (gt < total - tail) m[tail + gt] = 0;
+}
+
+cudaError_t launch_zero_masks(Ctx& c, uint32_t n, cudaStream_t st) {
+  (void)n;
+  zero_masks_kernel<<<c.sms * 2, 512, 0, st>>>(c.call, c.N);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st) {
   return launch_expand_from(c, c.bitO + (uint64_t)f0 * c.H * c.P, n, masks + (uint64_t)f0 * c.N, st);
 }
@@ -617,5 +637,5 @@ cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaS
 }  // namespace fizi
 
 extern "C" int fizi_diag_ccl_trace(unsigned long long* host, unsigned int n) {
-  return (int)cudaMemcpyFromSymbol(host, fizi::g_ccl_trace, sizeof(unsigned long long) * 4 * n);
+  return (int)cudaMemcpyFromSymbol(host, fizi::g_ccl_trace, sizeof(unsigned long long) * 12 * n);
 }

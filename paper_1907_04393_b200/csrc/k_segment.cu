@@ -32,7 +32,7 @@
 namespace fizi {
 
 struct SegArgs {
-  const uint8_t* frames;
+  const CallPtrs* call;         // frames / records of the call (device)
   uint64_t frame_bytes;         // 3N
   uint64_t N;
   uint32_t nchunks, tiles, words_per_frame;
@@ -57,7 +57,6 @@ struct SegArgs {
   const double* gtab;
   const uint8_t* ctab;
   const int64_t* frame_t;
-  fizi_result* res;
 };
 
 __device__ __forceinline__ bool valid_chunk(const SegArgs& a, uint32_t c) { return c < a.nchunks; }
@@ -76,7 +75,7 @@ __device__ __forceinline__ void finalize_frame(const SegArgs& a, uint32_t f,
   r.mean_luma = (uint8_t)mean;
   r.corrected = a.ctab[mean];
   r.gamma = a.gtab[mean];
-  a.res[f] = r;
+  a.call->res[f] = r;
   if (r.corrected) {
     const uint32_t pos = atomicAdd(&fix[0], 1u);
     fix[1 + pos] = f;
@@ -309,7 +308,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   const uint64_t trem = a.frame_bytes - toff;
   const uint32_t tbytes = trem < (uint64_t)kTileBytes ? (uint32_t)trem : (uint32_t)kTileBytes;
   const uint32_t n_active = min((uint32_t)kWarpsPerCta, a.nchunks - tile * kWarpsPerCta);
-  const uint8_t* src0 = a.frames + toff;
+  const uint8_t* frames = a.call->frames;
+  const uint8_t* src0 = frames + toff;
 
   uint64_t pol = 0;
   if (tid < kFrameGroup) { acc_y[tid] = 0; acc_f[tid] = 0; }
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     if (valid) load_env(e, elo, elo + a.env_plane);
     else zero_env(e);
     uint32_t fr[12];
-    load48(a.frames + (uint64_t)f * a.frame_bytes + coff + 48 * lane, valid, fr);
+    load48(frames + (uint64_t)f * a.frame_bytes + coff + 48 * lane, valid, fr);
     uint32_t bits = slow_bits16(fr, e, a.skin);
     bits = valid ? bits : 0u;
     const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
@@ -444,6 +444,7 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
   }
   __syncthreads();
   uint32_t phase = 0;
+  const uint8_t* frames = a.call->frames;
   for (uint64_t it = blockIdx.x; it < items; it += gridDim.x, phase ^= 1u) {
     const uint32_t f = a.fix[1 + it / a.tiles];
     const uint32_t tile = (uint32_t)(it % a.tiles);
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
     const uint32_t tile_bytes = rem < (uint64_t)kTileBytes ? (uint32_t)rem : (uint32_t)kTileBytes;
     if (tid == 0) {
       mbar_arrive_expect_tx(&bar, tile_bytes);
-      bulk_g2s(sm, a.frames + (uint64_t)f * a.frame_bytes + tile_off, tile_bytes, &bar, pol);
+      bulk_g2s(sm, frames + (uint64_t)f * a.frame_bytes + tile_off, tile_bytes, &bar, pol);
     }
     const uint64_t mean = (a.luma[f] + 500ull * a.N) / (1000ull * a.N);
     if (tid < 64)
@@ -498,8 +499,9 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
 // ------------------------------------------------------------- generic path
 // Any width: thread per pixel for the luma sum, warp per 32-pixel word of a
 // bit-mask row for the branch tests (ballot), after the means are known.
-__global__ void luma_generic_kernel(const uint8_t* __restrict__ frames, uint64_t N, uint32_t f0,
+__global__ void luma_generic_kernel(const CallPtrs* call, uint64_t N, uint32_t f0,
                                     unsigned long long* __restrict__ luma) {
+  const uint8_t* frames = call->frames;
   const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint32_t f = f0 + blockIdx.y;
   uint32_t y = 0;
@@ -525,7 +527,7 @@ __global__ void mask_generic_kernel(SegArgs a, uint32_t W, uint32_t H, uint32_t 
   uint32_t bit = 0;
   if (x < W) {
     const uint64_t q = (uint64_t)yrow * W + x;
-    const uint8_t* p = a.frames + ((uint64_t)f * a.N + q) * 3;
+    const uint8_t* p = a.call->frames + ((uint64_t)f * a.N + q) * 3;
     const uint32_t stream = a.frame_stream[f];
     const uint8_t* lo = a.env + (uint64_t)stream * 2 * a.env_plane + q * 3;
     const uint8_t* hi = lo + a.env_plane;
@@ -547,7 +549,7 @@ __global__ void finalize_kernel(uint32_t f0, uint32_t n, uint64_t N,
                                 uint32_t* __restrict__ fg, const double* __restrict__ gtab,
                                 const uint8_t* __restrict__ ctab,
                                 const uint32_t* __restrict__ frame_stream,
-                                const int64_t* __restrict__ frame_t, fizi_result* __restrict__ res,
+                                const int64_t* __restrict__ frame_t, const CallPtrs* call,
                                 uint32_t* __restrict__ fix) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -561,7 +563,7 @@ __global__ void finalize_kernel(uint32_t f0, uint32_t n, uint64_t N,
   r.mean_luma = (uint8_t)mean;
   r.corrected = ctab[mean];
   r.gamma = gtab[mean];
-  res[f] = r;
+  call->res[f] = r;
   if (r.corrected) {
     const uint32_t pos = atomicAdd(&fix[0], 1u);
     fix[1 + pos] = f;
@@ -569,10 +571,9 @@ __global__ void finalize_kernel(uint32_t f0, uint32_t n, uint64_t N,
   }
 }
 
-static SegArgs seg_args(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t g0,
-                        uint32_t sub) {
+static SegArgs seg_args(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32_t sub) {
   SegArgs a;
-  a.frames = frames;
+  a.call = c.call;
   a.frame_bytes = c.N * 3;
   a.N = c.N;
   a.nchunks = c.nchunks;
@@ -601,15 +602,13 @@ static SegArgs seg_args(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, 
   a.gtab = c.gamma_tab;
   a.ctab = c.corr_tab;
   a.frame_t = c.frame_t;
-  a.res = nullptr;
   return a;
 }
 
 // a2 + a3 main pass over frames [f0, f0+n) (same-stream groups g0 .. g0+ng-1).
-cudaError_t launch_seg_main(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t g0,
-                            uint32_t ng, uint32_t sub, fizi_result* res, cudaStream_t st) {
-  SegArgs a = seg_args(c, frames, f0, n, g0, sub);
-  a.res = res;
+cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32_t ng,
+                            uint32_t sub, cudaStream_t st) {
+  SegArgs a = seg_args(c, f0, n, g0, sub);
   prof_begin(c, st);
   if (c.fast) {
     if (c.seg_variant == 3)
@@ -617,7 +616,7 @@ cudaError_t launch_seg_main(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t
     else
       seg_fast_kernel<2><<<dim3(a.tiles, ng), 256, kStages * kTileBytes, st>>>(a);
   } else {
-    luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(frames, c.N, f0,
+    luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(c.call, c.N, f0,
                                                                                 c.luma);
   }
   prof_end(c, FIZI_PROF_SEGMENT, st);
@@ -627,9 +626,8 @@ cudaError_t launch_seg_main(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t
 
 // a2 finalisation (mean -> gamma, record header) and the LUT re-test of the
 // sub-batch's corrected frames (fast path) / the branch tests (generic path).
-cudaError_t launch_seg_fix(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t n, uint32_t sub,
-                           fizi_result* res, cudaStream_t st) {
-  SegArgs a = seg_args(c, frames, f0, n, 0, sub);
+cudaError_t launch_seg_fix(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st) {
+  SegArgs a = seg_args(c, f0, n, 0, sub);
   prof_begin(c, st);
   if (c.fast) {                      // finalisation already done by the fused kernel
     fix_fast_kernel<<<c.sms, 256, kTileBytes, st>>>(a);
@@ -637,7 +635,7 @@ cudaError_t launch_seg_fix(Ctx& c, const uint8_t* frames, uint32_t f0, uint32_t 
   } else {
     const unsigned fin_blocks = (n + 255) / 256;
     finalize_kernel<<<fin_blocks, 256, 0, st>>>(f0, n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
-                                                 c.frame_stream, c.frame_t, res,
+                                                 c.frame_stream, c.frame_t, c.call,
                                                  const_cast<uint32_t*>(a.fix));
     const uint64_t warps = (uint64_t)c.H * c.P * n;
     mask_generic_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a, c.W, c.H, c.P, n);

@@ -89,7 +89,9 @@ def lib() -> ctypes.CDLL:
         L.fizi_status_string.argtypes = [i32]
         L.fizi_status_string.restype = ctypes.c_char_p
         L.fizi_destroy.argtypes = [vp]
-        for name in ("fizi_params_default", "fizi_create", "fizi_learn_background",
+        L.fizi_set_pipeline.argtypes = [vp, i32]
+        L.fizi_flush.argtypes = [vp, vp]
+        for name in ("fizi_set_pipeline", "fizi_flush", "fizi_params_default", "fizi_create", "fizi_learn_background",
                      "fizi_process_frames", "fizi_segment_frames", "fizi_process_frames_host",
                      "fizi_track", "fizi_reset_tracker", "fizi_debug_stage",
                      "fizi_get_background", "fizi_set_background"):
@@ -131,6 +133,8 @@ class Fizi:
             raise RuntimeError("libfizi needs a CUDA device (no CPU fallback)")
         self.W, self.H = int(width), int(height)
         self.n_streams, self.max_batch = int(n_streams), int(max_batch)
+        self._zeros_u32 = np.zeros(self.max_batch, np.uint32)
+        self._zeros_i64 = np.zeros(self.max_batch, np.int64)
         self.device = torch.device("cuda", device)
         self.params = default_params(self.W, self.H, **params)
         self._h = ctypes.c_void_p()
@@ -180,9 +184,17 @@ class Fizi:
         frames = self._frames(frames)
         n = frames.shape[0]
         if streams is None:
-            streams = np.zeros(n, np.uint32)
-        streams = _u32(np.broadcast_to(np.asarray(streams, np.uint32), (n,)))
-        t = _i64(np.zeros(n) if t_ms is None else t_ms)
+            streams = self._zeros_u32[:n] if n <= self.max_batch else np.zeros(n, np.uint32)
+        else:
+            streams = _u32(np.broadcast_to(np.asarray(streams, np.uint32), (n,)))
+        if t_ms is None:
+            t = self._zeros_i64[:n] if n <= self.max_batch else np.zeros(n, np.int64)
+        elif not (isinstance(t_ms, np.ndarray) and t_ms.dtype == np.int64 and t_ms.flags.c_contiguous):
+            t = _i64(t_ms)
+        else:
+            t = t_ms
+        if t.shape != (n,):
+            raise ValueError("t_ms must have one timestamp per frame")
         if masks is True:
             masks = torch.empty((n, self.H, self.W), dtype=torch.uint8, device=self.device)
         if results is None:
@@ -249,6 +261,15 @@ class Fizi:
     def set_background(self, lo, hi, stream: int = 0):
         self._check(lib().fizi_set_background(self._h, stream, lo.data_ptr(), hi.data_ptr(),
                                               _stream_handle(self.device)), "fizi_set_background")
+
+    def set_pipeline(self, enable: bool = True):
+        """Pipelined mode (include/fizi.h): a call's tail overlaps the next call;
+        outputs are complete on the current stream after flush()."""
+        self._check(lib().fizi_set_pipeline(self._h, int(bool(enable))), "fizi_set_pipeline")
+
+    def flush(self):
+        """Join every outstanding call tail into the current stream."""
+        self._check(lib().fizi_flush(self._h, _stream_handle(self.device)), "fizi_flush")
 
     def profile_enable(self, mode=True):
         """mode True/1: every stage; 2: the fused segmentation kernel only; False/0: off."""

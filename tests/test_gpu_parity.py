@@ -327,6 +327,66 @@ def test_batch_size_invariance_and_sharded_track():
     b.close()
 
 
+def test_pipelined_graph_calls_match_oracle():
+    """Pipelined mode (tails overlap the next call, double-buffered slots)
+    and CUDA-graph replay vs direct launches: the same outputs, call after
+    call, with the fold running across calls; sampled frames vs the oracle."""
+    import os
+    cfg = synth.CONFIGS[3]
+    learn = synth.learning_frames_host(cfg)
+    ks = list(range(40, 40 + 30))
+    frames = _t(synth.frames_host(cfg, 0, ks))
+    t = np.array([synth.t_ms(k) for k in ks], np.int64)
+    calls = [(0, 7), (7, 14), (14, 21), (21, 24), (24, 30)]   # ragged: several graph shapes
+    os.environ["FIZI_NO_GRAPH"] = "1"
+    try:
+        ref = _ctx(cfg.W, cfg.H, max_batch=8)                 # direct launches, joined tails
+    finally:
+        del os.environ["FIZI_NO_GRAPH"]
+    ref.learn_background(_t(learn), margin=synth.MARGIN)
+    pip = _ctx(cfg.W, cfg.H, max_batch=8)
+    pip.learn_background(_t(learn), margin=synth.MARGIN)
+    pip.set_pipeline(True)
+    bufs = [(torch.empty((8, cfg.H, cfg.W), dtype=torch.uint8, device=DEV),
+             torch.empty((8, 128), dtype=torch.uint8, device=DEV)) for _ in range(2)]
+    out_ref, out_pip = [], []
+    for j, (a, b) in enumerate(calls):
+        mr, rr = ref.process_frames(frames[a:b], t_ms=t[a:b])
+        out_ref.append((mr.cpu().numpy(), results_numpy(rr)))
+        mk, rs = bufs[j & 1]
+        pip.process_frames(frames[a:b], t_ms=t[a:b], masks=mk[: b - a], results=rs[: b - a])
+        if j & 1:                      # both slots in flight, then collect them
+            pip.flush()
+            torch.cuda.synchronize()
+            for jj in (j - 1, j):
+                aa, bb = calls[jj]
+                m2, r2 = bufs[jj & 1]
+                out_pip.append((m2[: bb - aa].cpu().numpy(), results_numpy(r2[: bb - aa])))
+    pip.flush()
+    torch.cuda.synchronize()
+    j = len(calls) - 1
+    m2, r2 = bufs[j & 1]
+    out_pip.append((m2[: calls[j][1] - calls[j][0]].cpu().numpy(),
+                    results_numpy(r2[: calls[j][1] - calls[j][0]])))
+    for (ma, ra), (mb, rb) in zip(out_ref, out_pip):
+        assert np.array_equal(ma, mb)
+        assert ra.tobytes() == rb.tobytes()
+    # sampled frames of the pipelined run against the oracle (fold included)
+    p = oracle.make_params(cfg.W, cfg.H)
+    lo, hi = oracle.learn(learn, synth.MARGIN)
+    tr = oracle.Tracker(p)
+    fr_h = frames.cpu().numpy()
+    flat = [(m, r) for (mm, rr) in out_pip for m, r in zip(mm, rr)]
+    for i in range(len(ks)):
+        rec, st = oracle.segment(p, fr_h[i], lo, hi, t_ms=int(t[i]), stages=i in (3, 22))
+        tr.update(rec)
+        compare_record(flat[i][1], rec, ks[i], track=True)
+        if i in (3, 22):
+            assert np.array_equal(flat[i][0], st["final_mask"])
+    ref.close()
+    pip.close()
+
+
 def test_host_entry_matches_device_entry():
     cfg = synth.CONFIGS[1]
     learn = synth.learning_frames_host(cfg)
