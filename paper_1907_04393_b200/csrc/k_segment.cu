@@ -233,6 +233,60 @@ __device__ __forceinline__ bool all_inside16(const uint32_t (&fr)[12], const Env
   return ((am | ~bm) & 0x80008000u) == 0u;
 }
 
+// The same test from the raw envelope bytes with the byte-SIMD
+// sum-of-absolute-differences instruction (VABSDIFF4.U8.ACC): for lo <= hi,
+// |v - lo| + |v - hi| >= hi - lo with equality iff lo <= v <= hi, so the 48
+// bytes are all inside iff sum(|v - lo| + |v - hi|) == sum(hi - lo) =: W.
+// W and the lo <= hi check (sum|hi - lo| == sum hi - sum lo) are computed once
+// per thread when the envelope is loaded.
+struct EnvRaw {
+  uint32_t lo[12], hi[12];
+  uint32_t W;
+  bool ordered;                               // lo <= hi for all 48 bytes
+};
+
+__device__ __forceinline__ uint32_t sad4(uint32_t a, uint32_t b, uint32_t acc) {
+  uint32_t d;
+  asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(acc));
+  return d;
+}
+
+__device__ __forceinline__ void load_env_raw(EnvRaw& e, const uint8_t* elo, const uint8_t* ehi) {
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    const uint4 l = __ldg(reinterpret_cast<const uint4*>(elo + 512 * k));
+    const uint4 h = __ldg(reinterpret_cast<const uint4*>(ehi + 512 * k));
+    e.lo[4 * k + 0] = l.x; e.lo[4 * k + 1] = l.y; e.lo[4 * k + 2] = l.z; e.lo[4 * k + 3] = l.w;
+    e.hi[4 * k + 0] = h.x; e.hi[4 * k + 1] = h.y; e.hi[4 * k + 2] = h.z; e.hi[4 * k + 3] = h.w;
+  }
+  uint32_t w = 0, slo = 0, shi = 0;
+#pragma unroll
+  for (int i = 0; i < 12; i++) {
+    w = sad4(e.lo[i], e.hi[i], w);
+    slo = sad4(e.lo[i], 0u, slo);
+    shi = sad4(e.hi[i], 0u, shi);
+  }
+  e.W = w;
+  e.ordered = w == shi - slo;
+}
+
+__device__ __forceinline__ void full_env_raw(EnvRaw& e) {
+#pragma unroll
+  for (int i = 0; i < 12; i++) { e.lo[i] = 0u; e.hi[i] = 0xFFFFFFFFu; }
+  e.W = 48u * 255u;
+  e.ordered = true;
+}
+
+__device__ __forceinline__ bool all_inside_sad(const uint32_t (&fr)[12], const EnvRaw& e) {
+  uint32_t acc[2] = {0u, 0u};
+#pragma unroll
+  for (int i = 0; i < 12; i++) {
+    acc[i & 1] = sad4(fr[i], e.lo[i], acc[i & 1]);
+    acc[i & 1] = sad4(fr[i], e.hi[i], acc[i & 1]);
+  }
+  return e.ordered && acc[0] + acc[1] == e.W;
+}
+
 // Per-pixel R1 & R2 & R3 of the thread's 16 pixels (bit p = pixel p):
 // R1 per byte from the envelope lanes, R2 & R3 from the colour table.
 __device__ __forceinline__ uint32_t slow_bits16(const uint32_t (&fr)[12], const EnvRegs& e,
@@ -293,8 +347,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   __shared__ uint32_t empty_cnt[kStages];
   // per-frame partial sums of the CTA: luma <= 8 warps * 512 px * 255000 < 2^32
   __shared__ uint32_t acc_y[kFrameGroup], acc_f[kFrameGroup];
-  // deferred (frame, warp) items whose chunk has non-background pixels
-  __shared__ uint16_t q_item[kFrameGroup * kWarpsPerCta];
+  // deferred (frame, warp, word) items: 32-pixel mask words with a pixel
+  // outside the envelope (the rest of the chunk is background)
+  __shared__ uint16_t q_item[kFrameGroup * kWarpsPerCta * 16];
   __shared__ uint32_t q_tail, q_head;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -337,12 +392,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   if (c < a.nchunks) {
     const uint64_t coff = (uint64_t)c * kChunkBytes;
     const bool valid = coff + 48u * lane < a.frame_bytes;
-    EnvRegs e;
+    EnvRaw e;
     if (valid) {
       const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * lane;
-      load_env(e, elo, elo + a.env_plane);
+      load_env_raw(e, elo, elo + a.env_plane);
     } else {
-      zero_env(e);
+      full_env_raw(e);
     }
     if (warp != 0) pol = policy_evict_first();
     const uint8_t* my = sm + warp * kChunkBytes + 48 * lane;
@@ -354,8 +409,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
       uint32_t fr[12];
       load48(my + s * kTileBytes, valid, fr);
       uint32_t y = luma16(fr);
-      const bool inside = all_inside16(fr, e) || !valid;
-      const bool slow = __any_sync(0xFFFFFFFFu, !inside);
+      const bool inside = all_inside_sad(fr, e) || !valid;
+      const uint32_t out_lanes = __ballot_sync(0xFFFFFFFFu, !inside);
       const uint32_t fnext = __shfl_sync(0xFFFFFFFFu, fid_lane, (i + kStages) & 31);
       __syncwarp();                                          // this warp is done with stage s
       if (lane == 0 && atomicAdd(&empty_cnt[s], 1u) == n_active - 1) {
@@ -369,46 +424,62 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
       y = warp_sum_u32(y);
       if ((uint32_t)lane == i) luma_lane = y;
       // background chunks write nothing: their words are implied zero by the
-      // frame's dirty bitmap (only chunks with non-zero words are marked)
-      if (slow && lane == 0) q_item[atomicAdd(&q_tail, 1u)] = (uint16_t)((i << 3) | warp);
-      if (!slow && a.write_zero && !(lane & 1) && valid)
+      // frame's dirty bitmap (only chunks with non-zero words are marked).  In
+      // a chunk touching the foreground, the words with a pixel outside the
+      // envelope are deferred (one item each) and the others written as 0.
+      if (out_lanes) {
+        const uint32_t slow_words = (out_lanes | (out_lanes >> 1)) & 0x55555555u;   // bit 2k
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&q_tail, (uint32_t)__popc(slow_words));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (!(lane & 1)) {
+          if ((slow_words >> lane) & 1u)
+            q_item[base + __popc(slow_words & ((1u << lane) - 1u))] =
+                (uint16_t)((i << 7) | (warp << 4) | (lane >> 1));
+          else if (valid)
+            a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
+        }
+      } else if (a.write_zero && !(lane & 1) && valid) {
         a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
+      }
     }
     if ((uint32_t)lane < nf) atomicAdd(&acc_y[lane], luma_lane);
   }
   __syncthreads();
-  // deferred per-pixel work (chunks touching the hand), shared by all warps
-  // of the CTA: re-read the chunk and its envelope (L2) and test per pixel
+  // deferred per-pixel work (words touching the hand), shared by all warps
+  // of the CTA: a pair of lanes per item re-reads the word's 32 pixels and
+  // their envelope (L2) and tests them per pixel
   const uint32_t nq = q_tail;
   while (true) {
-    uint32_t item = 0;
-    if (lane == 0) item = atomicAdd(&q_head, 1u);
-    item = __shfl_sync(0xFFFFFFFFu, item, 0);
-    if (item >= nq) break;
-    const uint32_t it = q_item[item];
-    const uint32_t i = it >> 3, w = it & 7u;
+    uint32_t item0 = 0;
+    if (lane == 0) item0 = atomicAdd(&q_head, 16u);
+    item0 = __shfl_sync(0xFFFFFFFFu, item0, 0);
+    if (item0 >= nq) break;
+    const uint32_t item = item0 + (lane >> 1);
+    const bool act = item < nq;
+    const uint32_t it = act ? q_item[item] : 0u;
+    const uint32_t i = it >> 7, w = (it >> 4) & 7u, k = it & 15u;
     const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
     const uint32_t cq = tile * kWarpsPerCta + w;
+    const uint32_t L = 2 * k + (lane & 1);                   // lane of the chunk
     const uint64_t coff = (uint64_t)cq * kChunkBytes;
-    const bool valid = coff + 48u * lane < a.frame_bytes;
+    const bool valid = act && coff + 48u * L < a.frame_bytes;
     EnvRegs e;
-    const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * lane;
+    const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * L;
     if (valid) load_env(e, elo, elo + a.env_plane);
     else zero_env(e);
     uint32_t fr[12];
-    load48(frames + (uint64_t)f * a.frame_bytes + coff + 48 * lane, valid, fr);
+    load48(frames + (uint64_t)f * a.frame_bytes + coff + 48 * L, valid, fr);
     uint32_t bits = slow_bits16(fr, e, a.skin);
     bits = valid ? bits : 0u;
     const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
-    uint32_t pc = 0;
     if (!(lane & 1) && valid) {
-      a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)cq * 16 + (lane >> 1)] = word;
-      pc = __popc(word);
-    }
-    pc = warp_sum_u32(pc);
-    if (lane == 0 && pc) {
-      atomicAdd(&acc_f[i], pc);
-      atomicOr(a.dirty + (uint64_t)f * a.dirty_words + (cq >> 5), 1u << (cq & 31));
+      a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)cq * 16 + k] = word;
+      const uint32_t pc = __popc(word);
+      if (pc) {
+        atomicAdd(&acc_f[i], pc);
+        atomicOr(a.dirty + (uint64_t)f * a.dirty_words + (cq >> 5), 1u << (cq & 31));
+      }
     }
   }
   __syncthreads();                                           // flush the CTA's sums
