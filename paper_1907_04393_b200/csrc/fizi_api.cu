@@ -158,6 +158,9 @@ void free_all(Ctx& c) {
     if (c.ev_tail[i]) cudaEventDestroy(c.ev_tail[i]);
   }
   if (c.side) cudaStreamDestroy(c.side);
+  if (c.side2) cudaStreamDestroy(c.side2);
+  if (c.ev_zfork) cudaEventDestroy(c.ev_zfork);
+  if (c.ev_zjoin) cudaEventDestroy(c.ev_zjoin);
   for (auto& r : c.prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c.prof_free) cudaEventDestroy(e);
   if (c.prof_open) cudaEventDestroy(c.prof_open);
@@ -262,9 +265,13 @@ int enqueue_head(Ctx& c, const CallPlan& pl, cudaStream_t st) {
   return FIZI_OK;
 }
 
-int enqueue_tail(Ctx& c, const CallPlan& pl, const SubBatch& b, uint32_t k, cudaStream_t sd) {
-  cudaError_t e = fizi::launch_seg_fix(c, b.f0, b.n, k, sd);
-  if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
+int enqueue_tail(Ctx& c, const CallPlan& pl, const SubBatch& b, uint32_t k, cudaStream_t sd,
+                 cudaEvent_t before_ccl, bool with_fix) {
+  cudaError_t e = cudaSuccess;
+  if (with_fix) {
+    e = fizi::launch_seg_fix(c, b.f0, b.n, k, sd);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
+  }
   prof_begin(c, sd);
   e = fizi::launch_morph(c, b.f0, b.n, nullptr, pl.premask, sd);
   prof_end(c, FIZI_PROF_MORPH, sd);
@@ -274,6 +281,10 @@ int enqueue_tail(Ctx& c, const CallPlan& pl, const SubBatch& b, uint32_t k, cuda
     e = cudaMemcpyAsync(c.bitOC + b.f0 * w, c.bitO + b.f0 * w, (size_t)b.n * w * 4,
                         cudaMemcpyDeviceToDevice, sd);
     if (e != cudaSuccess) return cuda_fail(c, e, "debug copy");
+  }
+  if (before_ccl) {
+    e = cudaStreamWaitEvent(sd, before_ccl, 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "join");
   }
   prof_begin(c, sd);
   e = fizi::launch_ccl(c, b.f0, b.n, k, pl.premask, pl.fold, sd);
@@ -298,14 +309,24 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
     rc = enqueue_head(c, pl, st);
     if (rc) return rc;
     e = fizi::launch_seg_main(c, 0, pl.n, 0, pl.subs[0].ng, 0, st);
-    return e == cudaSuccess ? FIZI_OK : cuda_fail(c, e, "segment");
+    if (e != cudaSuccess) return cuda_fail(c, e, "segment");
+    // the LUT re-test of corrected frames closes the head: it starts while
+    // the SMs drain after segmentation instead of queueing behind the next
+    // call's segmentation CTAs
+    e = fizi::launch_seg_fix(c, 0, pl.n, 0, st);
+    return e == cudaSuccess ? FIZI_OK : cuda_fail(c, e, "fixup");
   }
   if (part == kTail) {
+    // the u8 mask target is zeroed on a second internal stream, off the
+    // critical path fix -> morph -> labelling; the labelling waits for it
     if (pl.premask) {
-      e = fizi::launch_zero_masks(c, pl.n, st);
+      e = cudaEventRecord(c.ev_zfork, st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side2, c.ev_zfork, 0);
+      if (e == cudaSuccess) e = fizi::launch_zero_masks(c, pl.n, c.side2);
+      if (e == cudaSuccess) e = cudaEventRecord(c.ev_zjoin, c.side2);
       if (e != cudaSuccess) return cuda_fail(c, e, "mask zero");
     }
-    return enqueue_tail(c, pl, pl.subs[0], 0, st);
+    return enqueue_tail(c, pl, pl.subs[0], 0, st, pl.premask ? c.ev_zjoin : nullptr, false);
   }
   rc = enqueue_head(c, pl, st);
   if (rc) return rc;
@@ -327,7 +348,7 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
     e = cudaEventRecord(c.ev_seg[k], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, c.ev_seg[k], 0);
     if (e != cudaSuccess) return cuda_fail(c, e, "event");
-    rc = enqueue_tail(c, pl, b, (uint32_t)k, sd);
+    rc = enqueue_tail(c, pl, b, (uint32_t)k, sd, nullptr, true);
     if (rc) return rc;
   }
   e = cudaEventRecord(c.ev_join, sd);
@@ -599,6 +620,11 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
     const char* sp = getenv("FIZI_SIDE_PRIO");
     e = cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking,
                                      (sp && atoi(sp) == 0) ? lo_prio : hi_prio);
+    if (e == cudaSuccess)
+      e = cudaStreamCreateWithPriority(&c.side2, cudaStreamNonBlocking,
+                                       (sp && atoi(sp) == 0) ? lo_prio : hi_prio);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_zfork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_zjoin, cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.cap, cudaStreamNonBlocking);
   for (uint32_t k = 0; k < fizi::kMaxSub && e == cudaSuccess; k++)

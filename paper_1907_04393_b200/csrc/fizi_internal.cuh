@@ -26,7 +26,6 @@ constexpr int kChunkBytes = 3 * kChunkPx;
 constexpr int kWarpsPerCta = 8;          // chunks per CTA tile
 constexpr int kTileBytes = kChunkBytes * kWarpsPerCta;   // 12 KiB frame bytes per tile
 constexpr int kFrameGroup = 32;          // frames sharing one envelope load (<= 32)
-constexpr int kStages = 8;               // bulk-copy ring depth in frames (power of 2)
 constexpr int kMaxRadius = 8;
 constexpr size_t kMorphSmem = 200 * 1024;  // dynamic smem budget of the morphology CTA
 constexpr uint32_t kCclSmemRuns = 4096;     // runs labelled in shared memory (else global)
@@ -108,6 +107,8 @@ struct Ctx {
   uint32_t* fix_count = nullptr;         // kMaxSub x (1 + max_batch): per sub-batch count + list
   uint8_t* tstate = nullptr;             // n_streams tracker states
   cudaStream_t side = nullptr;           // internal stream for the per-sub-batch tail
+  cudaStream_t side2 = nullptr;          // pipelined tail: u8 mask zeroing
+  cudaEvent_t ev_zfork = nullptr, ev_zjoin = nullptr;
   cudaEvent_t ev_seg[kMaxSub] = {};      // segment(k) done on the caller's stream
   cudaEvent_t ev_join = nullptr;         // tail of the call done on the side stream
   cudaEvent_t ev_start = nullptr;        // call start on the caller's stream

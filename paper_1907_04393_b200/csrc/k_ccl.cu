@@ -557,7 +557,7 @@ cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, bool masks
   a.cap_runs = c.cap_runs;
   a.fg = c.fg;
   a.ppm = c.p.min_blob_ppm;
-  static const int threads = getenv("FIZI_CCL_THREADS") ? atoi(getenv("FIZI_CCL_THREADS")) : 1024;
+  static const int threads = getenv("FIZI_CCL_THREADS") ? atoi(getenv("FIZI_CCL_THREADS")) : 512;
   ccl_kernel<<<n, threads, kCclSmem, st>>>(a);
   c.launches += 1;
   return cudaGetLastError();

@@ -340,8 +340,9 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
 // mbarrier completion).  Warps consume independently: each warp counts
 // itself out of stage s when done (shared atomic); the last one re-issues
 // the stage for frame i + kStages.  No block barrier inside the frame loop.
-template <int kMinBlocks>
+template <int kMinBlocks, int kStages>
 __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
+  static_assert((kStages & (kStages - 1)) == 0 && kStages <= kFrameGroup, "ring depth");
   extern __shared__ __align__(128) uint8_t sm[];          // kStages x 12 KiB tiles
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ uint32_t empty_cnt[kStages];
@@ -682,10 +683,14 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
   SegArgs a = seg_args(c, f0, n, g0, sub);
   prof_begin(c, st);
   if (c.fast) {
-    if (c.seg_variant == 3)
-      seg_fast_kernel<3><<<dim3(a.tiles, ng), 256, kStages * kTileBytes, st>>>(a);
-    else
-      seg_fast_kernel<2><<<dim3(a.tiles, ng), 256, kStages * kTileBytes, st>>>(a);
+    const dim3 grid(a.tiles, ng);
+    switch (c.seg_variant) {                        // CTAs per SM x ring depth
+      case 3: seg_fast_kernel<3, 4><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
+      case 4: seg_fast_kernel<2, 4><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
+      case 5: seg_fast_kernel<3, 2><<<grid, 256, 2 * kTileBytes, st>>>(a); break;
+      case 6: seg_fast_kernel<4, 2><<<grid, 256, 2 * kTileBytes, st>>>(a); break;
+      default: seg_fast_kernel<2, 8><<<grid, 256, 8 * kTileBytes, st>>>(a); break;
+    }
   } else {
     luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(c.call, c.N, f0,
                                                                                 c.luma);
@@ -718,13 +723,22 @@ cudaError_t launch_seg_fix(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaSt
 
 cudaError_t init_segment(Ctx& c) {
   (void)c;
-  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kStages * kTileBytes);
+  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       8 * kTileBytes);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_fast_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kStages * kTileBytes);
+    e = cudaFuncSetAttribute(seg_fast_kernel<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             4 * kTileBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(seg_fast_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             4 * kTileBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(seg_fast_kernel<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             2 * kTileBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(seg_fast_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             2 * kTileBytes);
   const char* v = getenv("FIZI_SEG_VARIANT");           // experiment switch (default 2)
-  c.seg_variant = v ? atoi(v) : 2;
+  c.seg_variant = v ? atoi(v) : 3;
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(fix_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes);
   return e;
