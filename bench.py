@@ -244,13 +244,14 @@ def main():
 
     fz = Fizi(cfg.W, cfg.H, n_streams=1, max_batch=B, device=local)
     fz.learn_background(learn, margin=synth.MARGIN)
-    # N = 1: pipelined calls (a call's tail overlaps the next call's
-    # segmentation), so outputs alternate between two buffers and the timed
+    # N = 1: pipelined calls (a call's tail overlaps the next calls'
+    # segmentation), so outputs rotate over three buffers and the timed
     # region ends with fz.flush(); N > 1 gathers every step's records at once
     pipelined = world == 1 and not args.no_pipeline
     fz.set_pipeline(pipelined)
-    masks2 = [torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=dev) for _ in range(2)]
-    res2 = [torch.empty((B, RESULT_BYTES), dtype=torch.uint8, device=dev) for _ in range(2)]
+    NBUF = 3                             # = the context's call slots (include/fizi.h)
+    masks2 = [torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
+    res2 = [torch.empty((B, RESULT_BYTES), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
     res = res2[0]
     gathered = torch.empty((world * B, RESULT_BYTES), dtype=torch.uint8, device=dev)
     del learn
@@ -272,7 +273,7 @@ def main():
         n = 0
         if v is not None:
             n, fr_n, mks, ress, t_base = v
-            mk, res_n = mks[i & 1], ress[i & 1]
+            mk, res_n = mks[i % NBUF], ress[i % NBUF]
             # timestamps keep increasing across passes over the resident rounds
             t = t_base + (i // need) * t_pass
             if world == 1:             # the whole path in one call (fold fused into labelling)

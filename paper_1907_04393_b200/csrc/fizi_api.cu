@@ -137,14 +137,18 @@ cudaError_t dalloc(T** p, size_t bytes) {
 void destroy_graphs(Ctx& c);
 
 void free_all(Ctx& c) {
-  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.zero_blocks[0], c.zero_blocks[1],
-                  c.bitAs[0], c.bitAs[1], c.bitO, c.bitOC, c.calls[0], c.calls[1],
-                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats,
+  for (uint32_t i = 0; i < fizi::kSlots; i++) {
+    if (c.zero_blocks[i]) cudaFree(c.zero_blocks[i]);
+    if (c.bitAs[i]) cudaFree(c.bitAs[i]);
+    if (c.calls[i]) cudaFree(c.calls[i]);
+  }
+  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.bitO, c.bitOC,
+                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.tl,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   destroy_graphs(c);
-  for (int i = 0; i < 2; i++) {
+  for (uint32_t i = 0; i < fizi::kSlots; i++) {
     if (c.pinned[i]) cudaFreeHost(c.pinned[i]);
     if (c.pinned_ev[i]) cudaEventDestroy(c.pinned_ev[i]);
   }
@@ -153,7 +157,7 @@ void free_all(Ctx& c) {
     if (ev) cudaEventDestroy(ev);
   if (c.ev_join) cudaEventDestroy(c.ev_join);
   if (c.ev_start) cudaEventDestroy(c.ev_start);
-  for (int i = 0; i < 2; i++) {
+  for (uint32_t i = 0; i < fizi::kSlots; i++) {
     if (c.ev_head[i]) cudaEventDestroy(c.ev_head[i]);
     if (c.ev_tail[i]) cudaEventDestroy(c.ev_tail[i]);
   }
@@ -451,16 +455,16 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   pl.masks = masks;
   const bool pipelined = c.pipeline && !c.p.debug;
   pl.slot = c.pinned_next;
-  c.pinned_next ^= 1u;
+  c.pinned_next = (c.pinned_next + 1) % fizi::kSlots;
   cudaError_t e = cudaEventSynchronize(c.pinned_ev[pl.slot]);   // slot's last upload consumed
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventSynchronize");
-  fizi::CallPtrs cp{frames, pl.fused_mask ? masks : nullptr, res, n};
+  fizi::CallPtrs cp{frames, pl.fused_mask ? masks : nullptr, res, n, c.call_counter++, c.tl};
   const uint32_t sub_frames = c.sub_frames;
   if (pipelined) c.sub_frames = 65535;                 // one sub-batch: the tail is the overlap
   fill_call(c, pl.slot, cp, sof, t, n, pl.subs);
   c.sub_frames = sub_frames;
   select_slot(c, pl.slot);
-  // the slot's previous call (two calls back) must be complete
+  // the slot's previous call (kSlots calls back) must be complete
   e = cudaStreamWaitEvent(st, c.ev_tail[pl.slot], 0);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamWaitEvent");
   int rc;
@@ -591,12 +595,10 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
     const uint64_t zb = mb * 8 + mb * 4 * 3 + fizi::kMaxSub * 4 + fizi::kMaxSub * (mb + 2) * 4 +
                         fizi::kMaxSub * (mb + 1) * 4 + mb * c.dirty_words * 4;
     c.zero_bytes = zb;
-    A(dalloc(&c.zero_blocks[0], zb));
-    A(dalloc(&c.zero_blocks[1], zb));
+    for (uint32_t i = 0; i < fizi::kSlots; i++) A(dalloc(&c.zero_blocks[i], zb));
   }
 
-  A(dalloc(&c.bitAs[0], mb * wpf * 4));
-  A(dalloc(&c.bitAs[1], mb * wpf * 4));
+  for (uint32_t i = 0; i < fizi::kSlots; i++) A(dalloc(&c.bitAs[i], mb * wpf * 4));
   A(dalloc(&c.bitO, mb * wpf * 4));
   if (c.p.debug) A(dalloc(&c.bitOC, mb * wpf * 4));
   A(dalloc(&c.row_cnt, mb * c.H * 4));
@@ -605,10 +607,9 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.parent, mb * c.cap_runs * 4));
   A(dalloc(&c.stats, mb * c.cap_runs * sizeof(fizi::RootStats)));
   const size_t table_bytes = sizeof(fizi::CallPtrs) + mb * 8 + mb * 4 * 2 + (mb + 1) * 4;
-  A(dalloc(&c.calls[0], table_bytes));
-  A(dalloc(&c.calls[1], table_bytes));
+  for (uint32_t i = 0; i < fizi::kSlots; i++) A(dalloc(&c.calls[i], table_bytes));
   A(dalloc(&c.tstate, (uint64_t)n_streams * sizeof(fizi::TrackState)));
-  for (int i = 0; i < 2 && e == cudaSuccess; i++) {
+  for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
     e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned[i]), table_bytes);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.pinned_ev[i], cudaEventDisableTiming);
   }
@@ -631,11 +632,17 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
     e = cudaEventCreateWithFlags(&c.ev_seg[k], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_start, cudaEventDisableTiming);
-  for (int i = 0; i < 2 && e == cudaSuccess; i++) {
+  for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
     e = cudaEventCreateWithFlags(&c.ev_head[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_tail[i], cudaEventDisableTiming);
   }
   c.use_graphs = getenv("FIZI_NO_GRAPH") == nullptr;
+  if (getenv("FIZI_TIMELINE") && e == cudaSuccess) {
+    const size_t tb = 2ull * fizi::kTlKinds * fizi::kTlCalls * 8;
+    e = cudaMalloc(reinterpret_cast<void**>(&c.tl), tb);
+    if (e == cudaSuccess) e = cudaMemset(c.tl, 0xFF, tb / 2);
+    if (e == cudaSuccess) e = cudaMemset(c.tl + fizi::kTlKinds * fizi::kTlCalls, 0, tb / 2);
+  }
   if (const char* sf = getenv("FIZI_SUB_FRAMES")) c.sub_frames = (uint32_t)atoi(sf) > 0 ? (uint32_t)atoi(sf) : 65535;
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -905,3 +912,11 @@ void fizi_destroy(fizi_ctx* ctx) {
 }
 
 }  // extern "C"
+
+// diagnostics (not part of include/fizi.h): copy the timeline (start array,
+// then end array, kTlKinds x kTlCalls each) to host memory
+extern "C" int fizi_diag_timeline(fizi_ctx* ctx, unsigned long long* host) {
+  if (!ctx || !ctx->c.tl) return FIZI_E_ARG;
+  return (int)cudaMemcpy(host, ctx->c.tl, 2ull * fizi::kTlKinds * fizi::kTlCalls * 8,
+                         cudaMemcpyDeviceToHost);
+}

@@ -30,6 +30,7 @@ constexpr int kMaxRadius = 8;
 constexpr size_t kMorphSmem = 200 * 1024;  // dynamic smem budget of the morphology CTA
 constexpr uint32_t kCclSmemRuns = 4096;     // runs labelled in shared memory (else global)
 constexpr uint32_t kMaxSub = 8;             // sub-batches per call (stream pipeline)
+constexpr uint32_t kSlots = 3;              // per-call state slots (pipelined calls in flight)
 
 struct Run {                             // one horizontal run of foreground pixels
   uint16_t x0, x1, y, pad;
@@ -42,7 +43,25 @@ struct CallPtrs {
   uint8_t* masks;                        // u8 mask target of the fused path, or nullptr
   fizi_result* res;                      // n records (device)
   uint64_t n;
+  uint64_t call_id;                      // diagnostics: timeline slot (FIZI_TIMELINE)
+  unsigned long long* tl;                // diagnostics: timeline buffer or nullptr
 };
+
+// Diagnostics timeline (env FIZI_TIMELINE=1): per kernel kind and call, the
+// earliest CTA start and the latest CTA end (globaltimer ns).
+constexpr int kTlKinds = 8, kTlCalls = 256;
+enum { kTlSeg = 0, kTlFix = 1, kTlZero = 2, kTlMorph = 3, kTlCcl = 4 };
+#ifdef __CUDACC__
+__device__ __forceinline__ void tl_mark(const CallPtrs* call, int kind, int end) {
+  unsigned long long* tl = call->tl;
+  if (!tl) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  const uint64_t i = (uint64_t)kind * kTlCalls + call->call_id % kTlCalls;
+  if (end) atomicMax(tl + kTlKinds * kTlCalls + i, t);
+  else atomicMin(tl + i, t);
+}
+#endif
 
 struct RootStats {                       // per component (indexed by its root run)
   uint32_t area;
@@ -66,6 +85,8 @@ struct Ctx {
   bool use_dirty = false;                // clean chunks of A are not written (dirty bitmap)
   uint32_t morph_tr = 0;                 // output rows per morphology CTA
   uint64_t launches = 0;
+  unsigned long long* tl = nullptr;      // diagnostics timeline (FIZI_TIMELINE)
+  uint64_t call_counter = 0;
   std::string err;
   bool sticky = false;
 
@@ -78,9 +99,9 @@ struct Ctx {
   // Per-call state lives in two slots (calls alternate between them) so that
   // a call's tail can still run while the next call segments (pipelined
   // mode).  The pointers below are views of the current slot (select_slot).
-  uint8_t* zero_blocks[2] = {};          // per-call counters (cleared each call)
-  uint32_t* bitAs[2] = {};               // merged masks A
-  CallPtrs* calls[2] = {};               // per-call tables
+  uint8_t* zero_blocks[kSlots] = {};          // per-call counters (cleared each call)
+  uint32_t* bitAs[kSlots] = {};               // merged masks A
+  CallPtrs* calls[kSlots] = {};               // per-call tables
   uint8_t* zero_block = nullptr;         // views of the current slot's block below
   uint64_t zero_bytes = 0;
   unsigned long long* luma = nullptr;    // max_batch
@@ -112,8 +133,8 @@ struct Ctx {
   cudaEvent_t ev_seg[kMaxSub] = {};      // segment(k) done on the caller's stream
   cudaEvent_t ev_join = nullptr;         // tail of the call done on the side stream
   cudaEvent_t ev_start = nullptr;        // call start on the caller's stream
-  cudaEvent_t ev_head[2] = {};           // pipelined: slot's segmentation done
-  cudaEvent_t ev_tail[2] = {};           // slot's last call fully done (slot reusable)
+  cudaEvent_t ev_head[kSlots] = {};           // pipelined: slot's segmentation done
+  cudaEvent_t ev_tail[kSlots] = {};           // slot's last call fully done (slot reusable)
   bool pipeline = false;                 // fizi_set_pipeline: tails not joined per call
   bool tail_pending = false;             // some pipelined tail may be outstanding
   uint32_t last_slot = 0;
@@ -126,14 +147,14 @@ struct Ctx {
   std::vector<uint8_t> env_valid;
   std::vector<int64_t> last_t;
   std::vector<uint8_t> has_t;
-  uint8_t* pinned[2] = {};               // staging for the per-call upload (ring of 2)
+  uint8_t* pinned[kSlots] = {};               // staging for the per-call upload (one per slot)
   size_t pinned_bytes = 0;
-  cudaEvent_t pinned_ev[2] = {};
+  cudaEvent_t pinned_ev[kSlots] = {};
   uint32_t pinned_next = 0;
   // captured launch sequences, one per call shape and pinned slot
   struct GraphEntry {
     std::vector<uint32_t> key;
-    cudaGraphExec_t exec[2] = {};
+    cudaGraphExec_t exec[kSlots] = {};
     uint64_t kernels = 0;                // kernel nodes per replay
     uint64_t used = 0;
   };

@@ -409,6 +409,11 @@ __device__ __forceinline__ unsigned long long gtimer_ccl() {
 
 __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   const unsigned long long g_t0 = a.trace ? gtimer_ccl() : 0ull;
+  if (threadIdx.x == 0) tl_mark(a.call, kTlCcl, 0);
+  struct TlEnd {
+    const CallPtrs* call;
+    __device__ ~TlEnd() { if (threadIdx.x == 0) tl_mark(call, kTlCcl, 1); }
+  } tl_end{a.call};
   extern __shared__ __align__(16) uint8_t smc[];
   const uint32_t f = a.f0 + blockIdx.x;
   const uint32_t T = a.frame_runs[f];
@@ -608,6 +613,7 @@ cudaError_t launch_expand_from(Ctx& c, const uint32_t* bits, uint32_t n, uint8_t
 // zero the call's u8 mask target (call->masks, call->n frames); runs on the
 // side stream while the fused segmentation kernel streams the frames
 __global__ void __launch_bounds__(512) zero_masks_kernel(const CallPtrs* call, uint64_t N) {
+  if (threadIdx.x == 0) tl_mark(call, kTlZero, 0);
   uint8_t* m = call->masks;
   if (!m) return;
   const uint64_t total = call->n * N;
@@ -621,6 +627,7 @@ __global__ void __launch_bounds__(512) zero_masks_kernel(const CallPtrs* call, u
   for (uint64_t i = gt; i < nb; i += stride) body[i] = z;
   const uint64_t tail = head + nb * 16;
   if (gt < total - tail) m[tail + gt] = 0;
+  if (threadIdx.x == 0) tl_mark(call, kTlZero, 1);
 }
 
 cudaError_t launch_zero_masks(Ctx& c, uint32_t n, cudaStream_t st) {

@@ -25,6 +25,7 @@ namespace fizi {
 
 
 struct MorphArgs {
+  const CallPtrs* call;         // diagnostics timeline only
   uint32_t f0;                  // first frame of the launch (sub-batch)
   uint8_t* masks;               // u8 final-mask output (fast path) or nullptr
   bool masks_zeroed;            // masks pre-zeroed: all-zero bands skip their rows
@@ -454,10 +455,12 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
   const int y0 = (int)(blockIdx.x * kBandRows);
   if (y0 >= (int)a.H) return;
   const unsigned long long t_start = a.trace ? gtimer() : 0ull;
+  if (threadIdx.x == 0) tl_mark(a.call, kTlMorph, 0);
   struct TraceEnd {
     const MorphArgs& a; unsigned long long t0; int nz = 0;
     unsigned long long t_staged = 0, t_piped = 0;
     __device__ ~TraceEnd() {
+      if (threadIdx.x == 0) tl_mark(a.call, kTlMorph, 1);
       if (a.trace && threadIdx.x == 0) {
         const uint32_t id = blockIdx.y * gridDim.x + blockIdx.x;
         if (id < 16384) {
@@ -583,6 +586,7 @@ cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, bool m
                          cudaStream_t st) {
   MorphArgs a;
   a.f0 = f0;
+  a.call = c.call;
   a.masks = masks;
   a.masks_zeroed = masks_zeroed;
   a.dirty = c.fast ? c.dirty : nullptr;

@@ -354,6 +354,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   __shared__ uint32_t q_tail, q_head;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) tl_mark(a.call, kTlSeg, 0);
   const uint32_t tile = blockIdx.x, grp = blockIdx.y;
   const uint32_t f_begin = a.group_off[grp];
   const uint32_t nf = a.group_off[grp + 1] - f_begin;
@@ -495,6 +496,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
       finalize_frame(a, f, sum, const_cast<uint32_t*>(a.fix), a.fg);
     }
   }
+  if (tid == 0) tl_mark(a.call, kTlSeg, 1);
 }
 
 // Frames whose mean luma is outside [luma_lo, luma_hi]: recompute their tiles
@@ -505,9 +507,13 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
   __shared__ __align__(16) uint8_t lut_s[256];
   __shared__ uint32_t red_f[kWarpsPerCta];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) tl_mark(a.call, kTlFix, 0);
   const uint32_t count = a.fix[0];
   const uint64_t items = (uint64_t)count * a.tiles;
-  if (blockIdx.x >= items) return;
+  if (blockIdx.x >= items) {
+    if (tid == 0) tl_mark(a.call, kTlFix, 1);
+    return;
+  }
   uint64_t pol = 0;
   if (tid == 0) {
     pol = policy_evict_first();
@@ -566,6 +572,7 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
     }
     __syncthreads();                          // smem tile + LUT reused next item
   }
+  if (tid == 0) tl_mark(a.call, kTlFix, 1);
 }
 
 // ------------------------------------------------------------- generic path

@@ -1,0 +1,52 @@
+"""Diagnostics: device timeline of pipelined calls (FIZI_TIMELINE=1).
+
+Per call: first-CTA start / last-CTA end of each kernel kind (globaltimer),
+relative to the call's segmentation start, plus the per-call period."""
+import ctypes, os, sys
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["FIZI_TIMELINE"] = "1"
+import synth
+from paper_1907_04393_b200 import Fizi, lib
+
+cid = int(os.environ.get("TL_CONFIG", "3"))
+B = int(os.environ.get("TL_BATCH", "64"))
+pipelined = os.environ.get("TL_PIPELINE", "1") == "1"
+cfg = synth.CONFIGS[cid]
+dev = torch.device("cuda", 0)
+fz = Fizi(cfg.W, cfg.H, max_batch=B)
+fz.learn_background(synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True), margin=synth.MARGIN)
+fz.set_pipeline(pipelined)
+nb = 4
+frames = [synth.frames_dev(cfg, 0, range(b * B, (b + 1) * B)) for b in range(nb)]
+masks = [torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=dev) for _ in range(3)]
+res = [torch.empty((B, 128), dtype=torch.uint8, device=dev) for _ in range(3)]
+ncalls = 48
+for i in range(ncalls):
+    t = np.arange(B, dtype=np.int64) * 33 + i * B * 33
+    fz.process_frames(frames[i % nb], t_ms=t, masks=masks[i % 3], results=res[i % 3])
+fz.flush()
+torch.cuda.synchronize()
+L = lib()
+L.fizi_diag_timeline.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+buf = np.zeros(2 * 8 * 256, np.uint64)
+rc = L.fizi_diag_timeline(fz._h, buf.ctypes.data)
+assert rc == 0, rc
+st = buf[:8 * 256].reshape(8, 256).astype(np.float64)
+en = buf[8 * 256:].reshape(8, 256).astype(np.float64)
+names = ["seg", "fix", "zero", "morph", "ccl"]
+print("pipelined" if pipelined else "joined", "C%d B=%d" % (cid, B))
+print("call " + " ".join("%17s" % n for n in names) + "   period")
+for k in range(ncalls - 12, ncalls):
+    t0 = st[0, k]
+    cells = []
+    for j, n in enumerate(names):
+        if st[j, k] > 1e19:
+            cells.append("%17s" % "-")
+        else:
+            cells.append("%7.1f..%7.1f" % ((st[j, k] - t0) / 1e3, (en[j, k] - t0) / 1e3))
+    per = (st[0, k] - st[0, k - 1]) / 1e3
+    print("%4d " % k + " ".join(cells) + "   %6.1f" % per)
+per = (st[0, ncalls - 1] - st[0, 8]) / 1e3 / (ncalls - 9)
+print("mean period %.1f us -> %.0f frames/s" % (per, B / per * 1e6))
