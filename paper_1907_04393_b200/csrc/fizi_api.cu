@@ -4,6 +4,7 @@
 //   -> final u8 mask (a6 output) -> Mouse fold (a8)
 // on the caller's CUDA stream.  No pixel is touched on the host.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -163,6 +164,12 @@ void free_all(Ctx& c) {
   }
   if (c.side) cudaStreamDestroy(c.side);
   if (c.side2) cudaStreamDestroy(c.side2);
+  if (c.side3) cudaStreamDestroy(c.side3);
+  if (c.head) cudaStreamDestroy(c.head);
+  for (uint32_t i = 0; i < fizi::kSlots; i++)
+    if (c.ev_in[i]) cudaEventDestroy(c.ev_in[i]);
+  for (uint32_t i = 0; i < fizi::kSlots; i++)
+    if (c.ev_ccl[i]) cudaEventDestroy(c.ev_ccl[i]);
   if (c.ev_zfork) cudaEventDestroy(c.ev_zfork);
   if (c.ev_zjoin) cudaEventDestroy(c.ev_zjoin);
   for (auto& r : c.prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -330,7 +337,9 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
       if (e == cudaSuccess) e = cudaEventRecord(c.ev_zjoin, c.side2);
       if (e != cudaSuccess) return cuda_fail(c, e, "mask zero");
     }
-    return enqueue_tail(c, pl, pl.subs[0], 0, st, pl.premask ? c.ev_zjoin : nullptr, false);
+    CallPlan nofold = pl;                             // the fold runs on its own stream
+    nofold.fold = -2;
+    return enqueue_tail(c, nofold, pl.subs[0], 0, st, pl.premask ? c.ev_zjoin : nullptr, false);
   }
   rc = enqueue_head(c, pl, st);
   if (rc) return rc;
@@ -456,7 +465,10 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   const bool pipelined = c.pipeline && !c.p.debug;
   pl.slot = c.pinned_next;
   c.pinned_next = (c.pinned_next + 1) % fizi::kSlots;
+  const auto h0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaEventSynchronize(c.pinned_ev[pl.slot]);   // slot's last upload consumed
+  const auto h1 = std::chrono::steady_clock::now();
+  c.host_sync_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(h1 - h0).count();
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventSynchronize");
   fizi::CallPtrs cp{frames, pl.fused_mask ? masks : nullptr, res, n, c.call_counter++, c.tl};
   const uint32_t sub_frames = c.sub_frames;
@@ -469,24 +481,47 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamWaitEvent");
   int rc;
   if (!pipelined) {
+    e = join_tail(c, st);                               // earlier pipelined tails (fold order)
+    if (e != cudaSuccess) return cuda_fail(c, e, "join");
     rc = run_part(c, pl, kWhole, st);
     if (rc) return rc;
     e = cudaEventRecord(c.pinned_ev[pl.slot], st);
     if (e == cudaSuccess) e = cudaEventRecord(c.ev_tail[pl.slot], st);
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
   } else {
-    rc = run_part(c, pl, kHead, st);
+    // the head runs on the context's head stream (ordered after the caller's
+    // earlier work on st); st itself is not joined (fizi_flush does that)
+    cudaStream_t hs = c.head;
+    e = cudaEventRecord(c.ev_in[pl.slot], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, c.ev_in[pl.slot], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, c.ev_tail[pl.slot], 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fork");
+    rc = run_part(c, pl, kHead, hs);
     if (rc) return rc;
-    e = cudaEventRecord(c.pinned_ev[pl.slot], st);
-    if (e == cudaSuccess) e = cudaEventRecord(c.ev_head[pl.slot], st);
+    e = cudaEventRecord(c.pinned_ev[pl.slot], hs);
+    if (e == cudaSuccess) e = cudaEventRecord(c.ev_head[pl.slot], hs);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side, c.ev_head[pl.slot], 0);
     if (e != cudaSuccess) return cuda_fail(c, e, "fork");
     rc = run_part(c, pl, kTail, c.side);
     if (rc) return rc;
-    e = cudaEventRecord(c.ev_tail[pl.slot], c.side);
-    if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
+    if (pl.fold != -2) {
+      // the a8 fold of this call follows its labelling on the fold stream,
+      // so the next call's labelling does not wait for it
+      e = cudaEventRecord(c.ev_ccl[pl.slot], c.side);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side3, c.ev_ccl[pl.slot], 0);
+      if (e == cudaSuccess) e = fizi::launch_track_call(c, pl.fold, c.side3);
+      if (e == cudaSuccess) e = cudaEventRecord(c.ev_tail[pl.slot], c.side3);
+    } else {
+      // still ordered after the fold stream's earlier work
+      e = cudaEventRecord(c.ev_ccl[pl.slot], c.side);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side3, c.ev_ccl[pl.slot], 0);
+      if (e == cudaSuccess) e = cudaEventRecord(c.ev_tail[pl.slot], c.side3);
+    }
+    if (e != cudaSuccess) return cuda_fail(c, e, "fold");
   }
   c.tail_pending = true;
+  c.host_call_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                        std::chrono::steady_clock::now() - h0).count();
   c.last_slot = pl.slot;
   c.last_frames = frames;
   c.last_n = n;
@@ -624,6 +659,17 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&c.side2, cudaStreamNonBlocking,
                                        (sp && atoi(sp) == 0) ? lo_prio : hi_prio);
+    if (e == cudaSuccess)
+      e = cudaStreamCreateWithPriority(&c.side3, cudaStreamNonBlocking,
+                                       (sp && atoi(sp) == 0) ? lo_prio : hi_prio);
+    for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
+      e = cudaEventCreateWithFlags(&c.ev_ccl[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_in[i], cudaEventDisableTiming);
+    }
+    const char* hp = getenv("FIZI_HEAD_PRIO");
+    if (e == cudaSuccess)
+      e = cudaStreamCreateWithPriority(&c.head, cudaStreamNonBlocking,
+                                       (hp && atoi(hp) == 0) ? lo_prio : hi_prio);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_zfork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_zjoin, cudaEventDisableTiming);
   }
@@ -919,4 +965,12 @@ extern "C" int fizi_diag_timeline(fizi_ctx* ctx, unsigned long long* host) {
   if (!ctx || !ctx->c.tl) return FIZI_E_ARG;
   return (int)cudaMemcpy(host, ctx->c.tl, 2ull * fizi::kTlKinds * fizi::kTlCalls * 8,
                          cudaMemcpyDeviceToHost);
+}
+
+// diagnostics: host nanoseconds spent in run_call and in its slot wait
+extern "C" int fizi_diag_host_ns(fizi_ctx* ctx, unsigned long long* call_ns, unsigned long long* sync_ns) {
+  if (!ctx) return FIZI_E_ARG;
+  *call_ns = ctx->c.host_call_ns;
+  *sync_ns = ctx->c.host_sync_ns;
+  return FIZI_OK;
 }

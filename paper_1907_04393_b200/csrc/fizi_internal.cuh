@@ -87,6 +87,7 @@ struct Ctx {
   uint64_t launches = 0;
   unsigned long long* tl = nullptr;      // diagnostics timeline (FIZI_TIMELINE)
   uint64_t call_counter = 0;
+  uint64_t host_call_ns = 0, host_sync_ns = 0;   // diagnostics
   std::string err;
   bool sticky = false;
 
@@ -129,6 +130,10 @@ struct Ctx {
   uint8_t* tstate = nullptr;             // n_streams tracker states
   cudaStream_t side = nullptr;           // internal stream for the per-sub-batch tail
   cudaStream_t side2 = nullptr;          // pipelined tail: u8 mask zeroing
+  cudaStream_t side3 = nullptr;          // pipelined tail: a8 fold (in call order)
+  cudaStream_t head = nullptr;           // pipelined head (segmentation)
+  cudaEvent_t ev_in[kSlots] = {};        // pipelined: caller's stream reached the call
+  cudaEvent_t ev_ccl[kSlots] = {};       // pipelined: slot's labelling done
   cudaEvent_t ev_zfork = nullptr, ev_zjoin = nullptr;
   cudaEvent_t ev_seg[kMaxSub] = {};      // segment(k) done on the caller's stream
   cudaEvent_t ev_join = nullptr;         // tail of the call done on the side stream
@@ -221,6 +226,8 @@ cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaS
 cudaError_t launch_track_batch(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st);
 cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,
                                 cudaStream_t st);
+// a8 fold of the current call's records (c.call) on st; fold >= 0: one stream
+cudaError_t launch_track_call(Ctx& c, int fold, cudaStream_t st);
 cudaError_t launch_tstate_reset(Ctx& c, uint32_t first, uint32_t count, cudaStream_t st);
 cudaError_t launch_debug_stage(Ctx& c, int stage, uint32_t frame, void* out, cudaStream_t st);
 

@@ -440,8 +440,9 @@ __device__ __forceinline__ void unrolled_steps(MorphPipe<R, WPL>& mp, int yi, in
   }
 }
 
-// One warp per CTA (the band depends on blockIdx only, so every branch is
-// warp-uniform and shuffles need no divergence handling).
+// kWarps independent warps per CTA, one band each (a warp's band depends on
+// blockIdx and its warp index only, so every branch is warp-uniform and the
+// warps never synchronise with each other).
 __device__ unsigned long long g_morph_trace[16384][5];      // diagnostics (FIZI_MORPH_TRACE)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -449,27 +450,30 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int R, int WPL>
-__global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
-  extern __shared__ uint32_t band[];                          // (kBandRows + 8R) x P words
-  const int y0 = (int)(blockIdx.x * kBandRows);
+template <int R, int WPL, int kWarps>
+__global__ void __launch_bounds__(32 * kWarps) morph_rows_kernel(MorphArgs a) {
+  extern __shared__ uint32_t band_all[];                      // kWarps x (kBandRows + 8R) x P words
+  const int warp = (int)(threadIdx.x >> 5);
+  const uint32_t band_id = blockIdx.x * kWarps + warp;
+  uint32_t* band = band_all + (size_t)warp * (kBandRows + 8 * R) * a.P;
+  const int y0 = (int)(band_id * kBandRows);
   if (y0 >= (int)a.H) return;
   const unsigned long long t_start = a.trace ? gtimer() : 0ull;
-  if (threadIdx.x == 0) tl_mark(a.call, kTlMorph, 0);
+  if ((threadIdx.x & 31) == 0) tl_mark(a.call, kTlMorph, 0);
   struct TraceEnd {
-    const MorphArgs& a; unsigned long long t0; int nz = 0;
+    const MorphArgs& a; unsigned long long t0; uint32_t band_id; int nz = 0;
     unsigned long long t_staged = 0, t_piped = 0;
     __device__ ~TraceEnd() {
-      if (threadIdx.x == 0) tl_mark(a.call, kTlMorph, 1);
-      if (a.trace && threadIdx.x == 0) {
-        const uint32_t id = blockIdx.y * gridDim.x + blockIdx.x;
+      if ((threadIdx.x & 31) == 0) tl_mark(a.call, kTlMorph, 1);
+      if (a.trace && (threadIdx.x & 31) == 0) {
+        const uint32_t id = blockIdx.y * ((a.H + kBandRows - 1) / kBandRows) + band_id;
         if (id < 16384) {
           g_morph_trace[id][0] = t0; g_morph_trace[id][1] = gtimer(); g_morph_trace[id][2] = nz;
           g_morph_trace[id][3] = t_staged; g_morph_trace[id][4] = t_piped;
         }
       }
     }
-  } trace_end{a, t_start};
+  } trace_end{a, t_start, band_id};
   MorphPipe<R, WPL> mp(a, a.f0 + blockIdx.y, y0);
   const int first = y0 - 4 * R, last = mp.y_end + 4 * R;     // input rows [first, last)
   mp.band = band;
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
     const uint32_t c0 = (uint32_t)((uint64_t)r0 * a.P / 16);
     const uint32_t c1 = (uint32_t)(((uint64_t)r1 * a.P - 1) / 16);
     bool any = false;
-    for (uint32_t wi = (c0 >> 5) + threadIdx.x; wi <= (c1 >> 5); wi += 32) {
+    for (uint32_t wi = (c0 >> 5) + (threadIdx.x & 31); wi <= (c1 >> 5); wi += 32) {
       uint32_t m = __ldg(dmap + wi);
       if (wi == (c0 >> 5)) m &= 0xFFFFFFFFu << (c0 & 31);
       if (wi == (c1 >> 5) && (c1 & 31) != 31) m &= (2u << (c1 & 31)) - 1u;
@@ -492,7 +496,8 @@ __global__ void __launch_bounds__(32) morph_rows_kernel(MorphArgs a) {
     }
   }
   if (dmap && (a.P & 3u) == 0) {        // TMA: the band's rows are one contiguous range
-    __shared__ __align__(8) uint64_t sbar;
+    __shared__ __align__(8) uint64_t sbars[kWarps];
+    uint64_t& sbar = sbars[warp];
     const uint32_t P = a.P;
     const int r0 = max(first, 0), r1 = min(first + kBandRows + 8 * R, (int)a.H);
     const uint32_t bytes = (uint32_t)(r1 - r0) * P * 4u;
@@ -604,9 +609,20 @@ cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, bool m
   a.runs = c.runs;
   const uint32_t r = c.p.se_radius;
   if (c.P <= 128 && r <= 4) {
-    const dim3 grid((c.H + kBandRows - 1) / kBandRows, n);
-    const size_t band_smem = (size_t)(kBandRows + 8 * r) * c.P * sizeof(uint32_t);
-#define FIZI_MORPH_ROWS(RR, WW) morph_rows_kernel<RR, WW><<<grid, 32, band_smem, st>>>(a)
+    static const int kw_env = getenv("FIZI_MORPH_WARPS") ? atoi(getenv("FIZI_MORPH_WARPS")) : 4;
+    const int kw = (kw_env == 1 || kw_env == 2 || kw_env == 8) ? kw_env : 4;
+    const uint32_t nbands = (c.H + kBandRows - 1) / kBandRows;
+    const dim3 grid((nbands + kw - 1) / kw, n);
+    const size_t band_smem = (size_t)kw * (kBandRows + 8 * r) * c.P * sizeof(uint32_t);
+#define FIZI_MORPH_ROWS(RR, WW)                                                        \
+    do {                                                                               \
+      switch (kw) {                                                                    \
+        case 1: morph_rows_kernel<RR, WW, 1><<<grid, 32, band_smem, st>>>(a); break;   \
+        case 2: morph_rows_kernel<RR, WW, 2><<<grid, 64, band_smem, st>>>(a); break;   \
+        case 8: morph_rows_kernel<RR, WW, 8><<<grid, 256, band_smem, st>>>(a); break;  \
+        default: morph_rows_kernel<RR, WW, 4><<<grid, 128, band_smem, st>>>(a); break; \
+      }                                                                                \
+    } while (0)
 #define FIZI_MORPH_WPL(RR)                                    \
     if (c.P <= 32) FIZI_MORPH_ROWS(RR, 1);                    \
     else if (c.P <= 64) FIZI_MORPH_ROWS(RR, 2);               \
@@ -644,6 +660,16 @@ cudaError_t init_morph(Ctx& c) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMorphSmem);
   };
+  // register-pipelined kernel: up to 8 warps x (kBandRows + 32) rows x 128 words
+#define FIZI_MORPH_SET_W(RR, WW)                                   \
+  set((const void*)morph_rows_kernel<RR, WW, 1>);                  \
+  set((const void*)morph_rows_kernel<RR, WW, 2>);                  \
+  set((const void*)morph_rows_kernel<RR, WW, 4>);                  \
+  set((const void*)morph_rows_kernel<RR, WW, 8>);
+#define FIZI_MORPH_SET(RR) FIZI_MORPH_SET_W(RR, 1) FIZI_MORPH_SET_W(RR, 2) FIZI_MORPH_SET_W(RR, 4)
+  FIZI_MORPH_SET(1) FIZI_MORPH_SET(2) FIZI_MORPH_SET(3) FIZI_MORPH_SET(4)
+#undef FIZI_MORPH_SET
+#undef FIZI_MORPH_SET_W
   set((const void*)morph_runs_kernel<1>);
   set((const void*)morph_runs_kernel<2>);
   set((const void*)morph_runs_kernel<3>);

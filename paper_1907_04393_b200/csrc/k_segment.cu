@@ -340,11 +340,16 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
 // mbarrier completion).  Warps consume independently: each warp counts
 // itself out of stage s when done (shared atomic); the last one re-issues
 // the stage for frame i + kStages.  No block barrier inside the frame loop.
-template <int kMinBlocks, int kStages>
+//
+// kWarpRing: every warp streams its own chunk through a private kStages-deep
+// ring (1.5 KiB bulk copies, one mbarrier per stage), so a warp never waits
+// for the other warps of the CTA before its next copy is issued.
+template <int kMinBlocks, int kStages, bool kWarpRing>
 __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   static_assert((kStages & (kStages - 1)) == 0 && kStages <= kFrameGroup, "ring depth");
   extern __shared__ __align__(128) uint8_t sm[];          // kStages x 12 KiB tiles
-  __shared__ __align__(8) uint64_t full[kStages];
+  constexpr int kBars = kWarpRing ? kStages * kWarpsPerCta : kStages;
+  __shared__ __align__(8) uint64_t full[kBars];
   __shared__ uint32_t empty_cnt[kStages];
   // per-frame partial sums of the CTA: luma <= 8 warps * 512 px * 255000 < 2^32
   __shared__ uint32_t acc_y[kFrameGroup], acc_f[kFrameGroup];
@@ -375,11 +380,31 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     q_tail = 0;
     q_head = 0;
 #pragma unroll
-    for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
+    for (int s = 0; s < kBars; s++) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == 0) {                                           // prologue: fill the ring
+  const uint32_t c = tile * kWarpsPerCta + warp;
+  const uint64_t coff_w = (uint64_t)c * kChunkBytes;
+  // private ring of this warp: stage s at sm + (warp * kStages + s) * 1536
+  const uint32_t cbytes = (c < a.nchunks)
+      ? (uint32_t)min((uint64_t)kChunkBytes, a.frame_bytes - coff_w) : 0u;
+  uint64_t* wfull = full + (kWarpRing ? warp * kStages : 0);
+  uint8_t* wring = sm + (kWarpRing ? warp * kStages * kChunkBytes : 0);
+  if (kWarpRing) {
+    if (cbytes) {
+      pol = policy_evict_first();
+#pragma unroll
+      for (int s = 0; s < kStages; s++) {
+        const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, s);
+        if (lane == 0 && (uint32_t)s < nf) {
+          mbar_arrive_expect_tx(&wfull[s], cbytes);
+          bulk_g2s(wring + s * kChunkBytes, frames + (uint64_t)f * a.frame_bytes + coff_w, cbytes,
+                   &wfull[s], pol);
+        }
+      }
+    }
+  } else if (warp == 0) {                                    // prologue: fill the ring
     pol = policy_evict_first();
 #pragma unroll
     for (int s = 0; s < kStages; s++) {
@@ -390,9 +415,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
       }
     }
   }
-  const uint32_t c = tile * kWarpsPerCta + warp;
   if (c < a.nchunks) {
-    const uint64_t coff = (uint64_t)c * kChunkBytes;
+    const uint64_t coff = coff_w;
     const bool valid = coff + 48u * lane < a.frame_bytes;
     EnvRaw e;
     if (valid) {
@@ -401,21 +425,29 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     } else {
       full_env_raw(e);
     }
-    if (warp != 0) pol = policy_evict_first();
-    const uint8_t* my = sm + warp * kChunkBytes + 48 * lane;
+    if (warp != 0 && !kWarpRing) pol = policy_evict_first();
+    const uint8_t* my = kWarpRing ? wring + 48 * lane : sm + warp * kChunkBytes + 48 * lane;
+    constexpr uint32_t kStageStride = kWarpRing ? kChunkBytes : kTileBytes;
     uint32_t luma_lane = 0;                                  // lane i: this warp's luma of frame i
     for (uint32_t i = 0; i < nf; i++) {
       const uint32_t s = i & (kStages - 1);
       const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
-      mbar_wait(&full[s], (i / kStages) & 1u);
+      mbar_wait(&wfull[s], (i / kStages) & 1u);
       uint32_t fr[12];
-      load48(my + s * kTileBytes, valid, fr);
-      uint32_t y = luma16(fr);
+      load48(my + s * kStageStride, valid, fr);
+      // the envelope test consumes all 12 words, so once every lane has it
+      // the stage can be released (the luma is computed after the release)
       const bool inside = all_inside_sad(fr, e) || !valid;
       const uint32_t out_lanes = __ballot_sync(0xFFFFFFFFu, !inside);
       const uint32_t fnext = __shfl_sync(0xFFFFFFFFu, fid_lane, (i + kStages) & 31);
-      __syncwarp();                                          // this warp is done with stage s
-      if (lane == 0 && atomicAdd(&empty_cnt[s], 1u) == n_active - 1) {
+      if (kWarpRing) {
+        __syncwarp();                                        // every lane has its 48 bytes
+        if (lane == 0 && i + kStages < nf) {
+          mbar_arrive_expect_tx(&wfull[s], cbytes);
+          bulk_g2s(wring + s * kChunkBytes, frames + (uint64_t)fnext * a.frame_bytes + coff, cbytes,
+                   &wfull[s], pol);
+        }
+      } else if (lane == 0 && atomicAdd(&empty_cnt[s], 1u) == n_active - 1) {
         empty_cnt[s] = 0;                                    // last warp out: refill stage s
         if (i + kStages < nf) {
           mbar_arrive_expect_tx(&full[s], tbytes);
@@ -423,7 +455,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
                    pol);
         }
       }
-      y = warp_sum_u32(y);
+      const uint32_t y = warp_sum_u32(luma16(fr));
       if ((uint32_t)lane == i) luma_lane = y;
       // background chunks write nothing: their words are implied zero by the
       // frame's dirty bitmap (only chunks with non-zero words are marked).  In
@@ -691,12 +723,11 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
   prof_begin(c, st);
   if (c.fast) {
     const dim3 grid(a.tiles, ng);
-    switch (c.seg_variant) {                        // CTAs per SM x ring depth
-      case 3: seg_fast_kernel<3, 4><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
-      case 4: seg_fast_kernel<2, 4><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
-      case 5: seg_fast_kernel<3, 2><<<grid, 256, 2 * kTileBytes, st>>>(a); break;
-      case 6: seg_fast_kernel<4, 2><<<grid, 256, 2 * kTileBytes, st>>>(a); break;
-      default: seg_fast_kernel<2, 8><<<grid, 256, 8 * kTileBytes, st>>>(a); break;
+    switch (c.seg_variant) {                        // CTAs per SM x ring depth (x per-warp ring)
+      case 2: seg_fast_kernel<2, 8, false><<<grid, 256, 8 * kTileBytes, st>>>(a); break;
+      case 7: seg_fast_kernel<3, 4, true><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
+      case 8: seg_fast_kernel<2, 8, true><<<grid, 256, 8 * kTileBytes, st>>>(a); break;
+      default: seg_fast_kernel<3, 4, false><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
     }
   } else {
     luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(c.call, c.N, f0,
@@ -730,20 +761,17 @@ cudaError_t launch_seg_fix(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaSt
 
 cudaError_t init_segment(Ctx& c) {
   (void)c;
-  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       8 * kTileBytes);
+  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<2, 8, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * kTileBytes);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_fast_kernel<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             4 * kTileBytes);
+    e = cudaFuncSetAttribute(seg_fast_kernel<3, 4, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTileBytes);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_fast_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             4 * kTileBytes);
+    e = cudaFuncSetAttribute(seg_fast_kernel<2, 8, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * kTileBytes);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_fast_kernel<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             2 * kTileBytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_fast_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             2 * kTileBytes);
+    e = cudaFuncSetAttribute(seg_fast_kernel<3, 4, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTileBytes);
   const char* v = getenv("FIZI_SEG_VARIANT");           // experiment switch (default 2)
   c.seg_variant = v ? atoi(v) : 3;
   if (e == cudaSuccess)

@@ -88,6 +88,71 @@ __global__ void __launch_bounds__(256) track_stream_kernel(fizi_params p, uint32
   if (threadIdx.x == 0) *ts = st;
 }
 
+// Fold of one call's records (pointers from the uploaded call table): a
+// single stream (fold >= 0) staged through shared memory, else one thread
+// per stream.  Runs on its own stream after the labelling in pipelined mode.
+__global__ void __launch_bounds__(256) track_call_kernel(fizi_params p, const CallPtrs* call,
+                                                         int fold, uint32_t n_streams,
+                                                         const uint32_t* __restrict__ frame_stream,
+                                                         TrackState* __restrict__ ts) {
+  fizi_result* res = call->res;
+  const uint32_t n = (uint32_t)call->n;
+  if (fold < 0) {
+    for (uint32_t s = threadIdx.x; s < n_streams; s += blockDim.x) {
+      bool any = false;
+      TrackState st;
+      for (uint32_t f = 0; f < n; f++) {
+        if (frame_stream[f] != s) continue;
+        if (!any) { st = ts[s]; any = true; }
+        fizi_result r;
+        r.t_ms = res[f].t_ms; r.blob_area = res[f].blob_area; r.cx = res[f].cx; r.cy = res[f].cy;
+        track_one(p, st, r);
+        res[f].visible = r.visible; res[f].clicked = r.clicked;
+        res[f].px = r.px; res[f].py = r.py; res[f].dwell_ms = r.dwell_ms;
+      }
+      if (any) ts[s] = st;
+    }
+    return;
+  }
+  __shared__ int64_t t_s[kTrackChunk];
+  __shared__ double cx_s[kTrackChunk], cy_s[kTrackChunk];
+  __shared__ uint32_t ar_s[kTrackChunk];
+  TrackState st;
+  if (threadIdx.x == 0) st = ts[fold];
+  for (uint32_t base = 0; base < n; base += kTrackChunk) {
+    const uint32_t m = min((uint32_t)kTrackChunk, n - base);
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const fizi_result& r = res[base + i];
+      t_s[i] = r.t_ms; ar_s[i] = r.blob_area; cx_s[i] = r.cx; cy_s[i] = r.cy;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (uint32_t i = 0; i < m; i++) {
+        fizi_result r;
+        r.t_ms = t_s[i]; r.blob_area = ar_s[i]; r.cx = cx_s[i]; r.cy = cy_s[i];
+        track_one(p, st, r);
+        t_s[i] = r.dwell_ms; cx_s[i] = r.px; cy_s[i] = r.py;
+        ar_s[i] = (uint32_t)r.visible | ((uint32_t)r.clicked << 1);
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      fizi_result& r = res[base + i];
+      r.visible = (uint8_t)(ar_s[i] & 1u); r.clicked = (uint8_t)(ar_s[i] >> 1);
+      r.px = cx_s[i]; r.py = cy_s[i]; r.dwell_ms = t_s[i];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ts[fold] = st;
+}
+
+cudaError_t launch_track_call(Ctx& c, int fold, cudaStream_t st) {
+  track_call_kernel<<<1, 256, 0, st>>>(c.p, c.call, fold, c.n_streams, c.frame_stream,
+                                       reinterpret_cast<TrackState*>(c.tstate));
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
 __global__ void tstate_reset_kernel(TrackState* ts, uint32_t count) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) {
