@@ -144,7 +144,7 @@ void free_all(Ctx& c) {
     if (c.calls[i]) cudaFree(c.calls[i]);
   }
   void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.bitO, c.bitOC,
-                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.tl,
+                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.tl, c.slow_items,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -166,6 +166,9 @@ void free_all(Ctx& c) {
   if (c.side2) cudaStreamDestroy(c.side2);
   if (c.side3) cudaStreamDestroy(c.side3);
   if (c.head) cudaStreamDestroy(c.head);
+  if (c.prep) cudaStreamDestroy(c.prep);
+  for (uint32_t i = 0; i < fizi::kSlots; i++)
+    if (c.ev_prep[i]) cudaEventDestroy(c.ev_prep[i]);
   for (uint32_t i = 0; i < fizi::kSlots; i++)
     if (c.ev_in[i]) cudaEventDestroy(c.ev_in[i]);
   for (uint32_t i = 0; i < fizi::kSlots; i++)
@@ -189,6 +192,8 @@ void select_slot(Ctx& c, uint32_t s) {
   c.sub_done = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * 4;
   c.fold_sync = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * (mb + 2) * 4;
   c.fix_count = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * (mb + 1) * 4;
+  c.item_counter = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * 4;
+  c.slow_count = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * 4;
   c.dirty = reinterpret_cast<uint32_t*>(z);
   c.bitA = c.bitAs[s];
   c.call = c.calls[s];
@@ -316,10 +321,9 @@ int enqueue_tail(Ctx& c, const CallPlan& pl, const SubBatch& b, uint32_t k, cuda
 int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   int rc = FIZI_OK;
-  if (part == kHead) {
-    rc = enqueue_head(c, pl, st);
-    if (rc) return rc;
+  if (part == kHead) {                                  // (table + counters: prep stream)
     e = fizi::launch_seg_main(c, 0, pl.n, 0, pl.subs[0].ng, 0, st);
+    if (e == cudaSuccess && c.fast) e = fizi::launch_slow_words(c, 0, pl.n, 0, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "segment");
     // the LUT re-test of corrected frames closes the head: it starts while
     // the SMs drain after segmentation instead of queueing behind the next
@@ -357,6 +361,7 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
   for (size_t k = 0; k < pl.subs.size(); k++) {
     const SubBatch& b = pl.subs[k];
     e = fizi::launch_seg_main(c, b.f0, b.n, b.g0, b.ng, (uint32_t)k, st);
+    if (e == cudaSuccess && c.fast) e = fizi::launch_slow_words(c, b.f0, b.n, (uint32_t)k, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "segment");
     e = cudaEventRecord(c.ev_seg[k], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, c.ev_seg[k], 0);
@@ -492,14 +497,21 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
     // the head runs on the context's head stream (ordered after the caller's
     // earlier work on st); st itself is not joined (fizi_flush does that)
     cudaStream_t hs = c.head;
-    e = cudaEventRecord(c.ev_in[pl.slot], st);
+    // the slot's table upload and counter clear run on the prep stream as
+    // soon as the slot is free, ahead of the segmentation that needs them
+    e = cudaStreamWaitEvent(c.prep, c.ev_tail[pl.slot], 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "prep");
+    rc = enqueue_head(c, pl, c.prep);
+    if (rc) return rc;
+    e = cudaEventRecord(c.pinned_ev[pl.slot], c.prep);
+    if (e == cudaSuccess) e = cudaEventRecord(c.ev_prep[pl.slot], c.prep);
+    if (e == cudaSuccess) e = cudaEventRecord(c.ev_in[pl.slot], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, c.ev_in[pl.slot], 0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, c.ev_tail[pl.slot], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, c.ev_prep[pl.slot], 0);
     if (e != cudaSuccess) return cuda_fail(c, e, "fork");
     rc = run_part(c, pl, kHead, hs);
     if (rc) return rc;
-    e = cudaEventRecord(c.pinned_ev[pl.slot], hs);
-    if (e == cudaSuccess) e = cudaEventRecord(c.ev_head[pl.slot], hs);
+    e = cudaEventRecord(c.ev_head[pl.slot], hs);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side, c.ev_head[pl.slot], 0);
     if (e != cudaSuccess) return cuda_fail(c, e, "fork");
     rc = run_part(c, pl, kTail, c.side);
@@ -628,7 +640,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   c.dirty_words = (c.nchunks + 31) / 32;
   {
     const uint64_t zb = mb * 8 + mb * 4 * 3 + fizi::kMaxSub * 4 + fizi::kMaxSub * (mb + 2) * 4 +
-                        fizi::kMaxSub * (mb + 1) * 4 + mb * c.dirty_words * 4;
+                        fizi::kMaxSub * (mb + 1) * 4 + fizi::kMaxSub * 4 * 2 + mb * c.dirty_words * 4;
     c.zero_bytes = zb;
     for (uint32_t i = 0; i < fizi::kSlots; i++) A(dalloc(&c.zero_blocks[i], zb));
   }
@@ -636,6 +648,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   for (uint32_t i = 0; i < fizi::kSlots; i++) A(dalloc(&c.bitAs[i], mb * wpf * 4));
   A(dalloc(&c.bitO, mb * wpf * 4));
   if (c.p.debug) A(dalloc(&c.bitOC, mb * wpf * 4));
+  if (c.fast) A(dalloc(&c.slow_items, mb * c.nchunks * 16 * sizeof(unsigned long long)));
   A(dalloc(&c.row_cnt, mb * c.H * 4));
   A(dalloc(&c.row_base, mb * c.H * 4));
   A(dalloc(&c.runs, mb * c.cap_runs * sizeof(fizi::Run)));
@@ -665,7 +678,9 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
     for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
       e = cudaEventCreateWithFlags(&c.ev_ccl[i], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_in[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_prep[i], cudaEventDisableTiming);
     }
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.prep, cudaStreamNonBlocking, hi_prio);
     const char* hp = getenv("FIZI_HEAD_PRIO");
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&c.head, cudaStreamNonBlocking,

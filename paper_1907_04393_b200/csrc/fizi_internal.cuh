@@ -50,7 +50,7 @@ struct CallPtrs {
 // Diagnostics timeline (env FIZI_TIMELINE=1): per kernel kind and call, the
 // earliest CTA start and the latest CTA end (globaltimer ns).
 constexpr int kTlKinds = 8, kTlCalls = 256;
-enum { kTlSeg = 0, kTlFix = 1, kTlZero = 2, kTlMorph = 3, kTlCcl = 4 };
+enum { kTlSeg = 0, kTlFix = 1, kTlZero = 2, kTlMorph = 3, kTlCcl = 4, kTlFold = 5, kTlSlow = 6 };
 #ifdef __CUDACC__
 __device__ __forceinline__ void tl_mark(const CallPtrs* call, int kind, int end) {
   unsigned long long* tl = call->tl;
@@ -81,7 +81,8 @@ struct Ctx {
   uint64_t cap_runs = 0;                 // run capacity per frame
   bool fast = false;                     // W % 32 == 0: fused bulk-copy kernels
   int sms = 148;
-  int seg_variant = 2;                   // min CTAs/SM of the fused kernel
+  int seg_variant = 3;                   // fused kernel: CTAs/SM x ring depth variant
+  uint32_t seg_persist = 2;              // persistent fused kernel: CTAs per SM (0: off)
   bool use_dirty = false;                // clean chunks of A are not written (dirty bitmap)
   uint32_t morph_tr = 0;                 // output rows per morphology CTA
   uint64_t launches = 0;
@@ -127,11 +128,16 @@ struct Ctx {
   uint32_t* group_frames = nullptr;      // max_batch (frame ids ordered by group)
   uint32_t* group_off = nullptr;         // max_batch + 1
   uint32_t* fix_count = nullptr;         // kMaxSub x (1 + max_batch): per sub-batch count + list
+  uint32_t* item_counter = nullptr;      // kMaxSub: fused-kernel work items taken
+  uint32_t* slow_count = nullptr;        // kMaxSub: words queued for the per-pixel kernel
+  unsigned long long* slow_items = nullptr;   // max_batch x nchunks x 16 queue (one call)
   uint8_t* tstate = nullptr;             // n_streams tracker states
   cudaStream_t side = nullptr;           // internal stream for the per-sub-batch tail
   cudaStream_t side2 = nullptr;          // pipelined tail: u8 mask zeroing
   cudaStream_t side3 = nullptr;          // pipelined tail: a8 fold (in call order)
   cudaStream_t head = nullptr;           // pipelined head (segmentation)
+  cudaStream_t prep = nullptr;           // pipelined: per-call table upload + counter clear
+  cudaEvent_t ev_prep[kSlots] = {};
   cudaEvent_t ev_in[kSlots] = {};        // pipelined: caller's stream reached the call
   cudaEvent_t ev_ccl[kSlots] = {};       // pipelined: slot's labelling done
   cudaEvent_t ev_zfork = nullptr, ev_zjoin = nullptr;
@@ -213,6 +219,8 @@ cudaError_t launch_env_export(Ctx& c, uint32_t stream, uint8_t* lo, uint8_t* hi,
 cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32_t ng, uint32_t sub,
                             cudaStream_t st);
 cudaError_t launch_seg_fix(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st);
+// per-pixel R1 & R2 & R3 of the words the fused kernel queued (fast path)
+cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st);
 // the segment launcher marks the SEGMENT -> FIXUP boundary through this hook
 void prof_begin(Ctx& c, cudaStream_t st);
 void prof_end(Ctx& c, int slot, cudaStream_t st);

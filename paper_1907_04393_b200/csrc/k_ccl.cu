@@ -62,6 +62,15 @@ struct CclArgs {
   fizi_params p;
 };
 
+// max over the warp of a 64-bit key: the high words first, then the low
+// words of the lanes holding the maximal high word (two REDUX instructions)
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+  const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+  const uint32_t mh = __reduce_max_sync(0xFFFFFFFFu, hi);
+  const uint32_t ml = __reduce_max_sync(0xFFFFFFFFu, hi == mh ? lo : 0u);
+  return ((unsigned long long)mh << 32) | ml;
+}
+
 __device__ __forceinline__ bool kept_area(uint32_t area, uint32_t ppm, uint64_t N) {
   return (uint64_t)area * 1000000ull >= (uint64_t)ppm * N;
 }
@@ -105,8 +114,8 @@ __device__ __forceinline__ void unite(uint32_t* par, const Run* R, uint32_t W, u
 #define CCL_MARK(k) if (a.trace && threadIdx.x == 0) t_mark[k] = clock64();
 
 template <bool kShared>
-__device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, uint32_t T,
-                          long long* t_mark) {
+__device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, uint32_t* s_area,
+                          uint32_t T, long long* t_mark) {
   __shared__ unsigned long long s_best[32];
   __shared__ uint32_t s_cnt[3][32];
   __shared__ unsigned long long s_key;
@@ -120,9 +129,14 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   RootStats* stats = a.stats + (uint64_t)f * a.cap_runs;
 
   CCL_MARK(0)
+  const uint32_t fg_merged = a.fg[f];                   // loaded early, written in phase 4
+  // component area of root i: shared memory for frames labelled in shared memory
+  auto area_of = [&](uint32_t i) -> uint32_t {
+    return kShared ? s_area[i] : __ldcg(&stats[i].area);
+  };
   // 0. load
   for (uint32_t i = tid; i < T; i += nthr) {
-    if (kShared) R[i] = gruns[i];
+    if (kShared) { R[i] = gruns[i]; s_area[i] = 0u; }
     par[i] = i;
     RootStats z;
     z.area = 0; z.xmin = 0xFFFFFFFFu; z.xmax = 0; z.ymin = 0xFFFFFFFFu; z.ymax = 0;
@@ -132,10 +146,15 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   __syncthreads();
 
   CCL_MARK(1)
-  // 1. union with the previous row
-  for (uint32_t y = tid + 1; y < H; y += nthr) {
+  // 1. union of every run with the 8-connected runs of the previous row.
+  //    Rows are taken in blocks of kRowBlock: one thread unites the row pairs
+  //    inside a block in order (no contention, runs end up one link from the
+  //    block's top component), then the block boundaries are united in
+  //    parallel, so trees stay shallow even for tall components.
+  constexpr uint32_t kRowBlock = 8;
+  auto unite_rows = [&](uint32_t y) {                  // row pair (y - 1, y)
     const uint32_t n = cnt[y], np = cnt[y - 1];
-    if (!n || !np) continue;
+    if (!n || !np) return;
     const uint32_t cb = rb[y], pb = rb[y - 1];
     uint32_t h = 0;
     for (uint32_t j = 0; j < n; j++) {
@@ -144,27 +163,58 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
       for (uint32_t h2 = h; h2 < np && R[pb + h2].x0 <= (uint32_t)rc.x1 + 1; h2++)
         unite<kShared>(par, R, W, cb + j, pb + h2);
     }
+  };
+  for (uint32_t blk = tid; blk * kRowBlock < H; blk += nthr) {
+    const uint32_t y1 = min(blk * kRowBlock + kRowBlock, H);
+    for (uint32_t y = blk * kRowBlock + 1; y < y1; y++) unite_rows(y);
   }
+  __syncthreads();
+  for (uint32_t blk = tid + 1; blk * kRowBlock < H; blk += nthr) unite_rows(blk * kRowBlock);
   __syncthreads();
 
   CCL_MARK(2)
-  // 2. flatten by lockstep pointer jumping (the forest depth halves every
-  //    round; concurrent unions can leave long chains along tall components)
-  int rounds = 0;
-  while (true) {
-    rounds++;
-    int changed = 0;
-    for (uint32_t i = tid; i < T; i += nthr) {
-      const uint32_t p = ld_par<kShared>(par + i);
-      const uint32_t gp = ld_par<kShared>(par + p);
-      if (gp != p) {
-        par[i] = gp;
-        changed = 1;
+  // 2. flatten: every run walks to its root, halving the path as it goes
+  //    (the forest no longer changes shape, so plain stores of an ancestor
+  //    are safe while other threads walk); once every walk is over, each
+  //    run points at its root
+  constexpr uint32_t kMaxPer = 8;                        // runs per thread kept in registers
+  uint32_t roots[kMaxPer];
+  const bool in_regs = T <= kMaxPer * (uint32_t)nthr;
+#pragma unroll
+  for (uint32_t k = 0; k < kMaxPer; k++) {
+    const uint32_t i = tid + k * nthr;
+    uint32_t x = i;
+    if (i < T) {
+      while (true) {
+        const uint32_t p = ld_par<kShared>(par + x);
+        if (p == x) break;
+        const uint32_t gp = ld_par<kShared>(par + p);
+        if (gp == p) { x = p; break; }
+        par[x] = gp;
+        x = gp;
       }
     }
-    if (!__syncthreads_or(changed)) break;
+    roots[k] = x;
   }
-  if (a.trace && tid == 0) t_mark[8] = rounds;
+  __syncthreads();
+  if (in_regs) {
+#pragma unroll
+    for (uint32_t k = 0; k < kMaxPer; k++) {
+      const uint32_t i = tid + k * nthr;
+      if (i < T) par[i] = roots[k];
+    }
+  } else {                                  // large frames: lockstep pointer jumping
+    while (true) {
+      int changed = 0;
+      for (uint32_t i = tid; i < T; i += nthr) {
+        const uint32_t p = ld_par<kShared>(par + i);
+        const uint32_t gp = ld_par<kShared>(par + p);
+        if (gp != p) { par[i] = gp; changed = 1; }
+      }
+      if (!__syncthreads_or(changed)) break;
+    }
+  }
+  __syncthreads();
   CCL_MARK(3)
 
   // 3. statistics, aggregated over lanes of a warp that share a root
@@ -215,6 +265,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     }
     if (act && (uint32_t)lane == (uint32_t)(__ffs(m) - 1)) {
       RootStats* st = stats + root;
+      if (kShared) atomicAdd(&s_area[root], g_area);
       atomicAdd(&st->area, g_area);
       atomicAdd(&st->sx, g_sx);
       atomicAdd(&st->sy, g_sy);
@@ -233,7 +284,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   for (uint32_t i = tid; i < T; i += nthr) {
     if (ld_par<kShared>(par + i) != i) continue;
     n_tot++;
-    const uint32_t area = __ldcg(&stats[i].area);
+    const uint32_t area = area_of(i);
     if (!kept_area(area, a.ppm, a.N)) continue;
     n_kept++;
     fg_final += area;
@@ -241,14 +292,10 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     const unsigned long long key = ((unsigned long long)area << 32) | (0xFFFFFFFFu - label);
     best = key > best ? key : best;
   }
-  n_tot = warp_sum_u32(n_tot);
-  n_kept = warp_sum_u32(n_kept);
-  fg_final = warp_sum_u32(fg_final);
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, best, d);
-    best = o > best ? o : best;
-  }
+  n_tot = __reduce_add_sync(0xFFFFFFFFu, n_tot);
+  n_kept = __reduce_add_sync(0xFFFFFFFFu, n_kept);
+  fg_final = __reduce_add_sync(0xFFFFFFFFu, fg_final);
+  best = warp_max_u64(best);
   if (lane == 0) {
     s_cnt[0][warp] = n_tot;
     s_cnt[1][warp] = n_kept;
@@ -258,18 +305,13 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   __syncthreads();
   if (warp == 0) {
     const int nw = nthr >> 5;
-    n_tot = warp_sum_u32(lane < nw ? s_cnt[0][lane] : 0u);
-    n_kept = warp_sum_u32(lane < nw ? s_cnt[1][lane] : 0u);
-    fg_final = warp_sum_u32(lane < nw ? s_cnt[2][lane] : 0u);
-    best = lane < nw ? s_best[lane] : 0ull;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, best, d);
-      best = o > best ? o : best;
-    }
+    n_tot = __reduce_add_sync(0xFFFFFFFFu, lane < nw ? s_cnt[0][lane] : 0u);
+    n_kept = __reduce_add_sync(0xFFFFFFFFu, lane < nw ? s_cnt[1][lane] : 0u);
+    fg_final = __reduce_add_sync(0xFFFFFFFFu, lane < nw ? s_cnt[2][lane] : 0u);
+    best = warp_max_u64(lane < nw ? s_best[lane] : 0ull);
     if (lane == 0) {
       fizi_result* r = a.call->res + f;
-      r->fg_merged = a.fg[f];
+      r->fg_merged = fg_merged;
       r->fg_final = fg_final;
       r->n_comp_total = n_tot;
       r->n_comp_kept = n_kept;
@@ -302,28 +344,57 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     for (uint32_t i = tid; i < T; i += nthr) gpar[i] = par[i];
 
   CCL_MARK(6)
-  // 5a. pre-zeroed u8 mask: write the bytes of every run of a kept component
-  if (a.call->masks && a.masks_zeroed) {
-    for (uint32_t i = tid; i < T; i += nthr) {
-      const uint32_t root = ld_par<kShared>(par + i);
-      if (!kept_area(__ldcg(&stats[root].area), a.ppm, a.N)) continue;
-      const Run rg = R[i];
-      uint8_t* p = a.call->masks + ((uint64_t)f * H + rg.y) * W;
-      uint32_t x = rg.x0;
-      const uint32_t xe = (uint32_t)rg.x1 + 1;
-      for (; x < xe && (x & 15u); x++) p[x] = 1;
-      for (; x + 16 <= xe; x += 16)
-        *reinterpret_cast<uint4*>(p + x) = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
-      for (; x < xe; x++) p[x] = 1;
+  // 5a. pre-zeroed u8 mask: write the bytes of every run of a kept component,
+  //     one warp per run, lanes over the run's 16-byte segments
+  uint8_t* const masks = a.call->masks;
+  if (masks && a.masks_zeroed) {
+    const int nwarps = nthr >> 5;
+    // runs in batches of 32 per warp: lane j loads run i0 + j * nwarps (one
+    // round of shared-memory loads per batch), then the warp writes them one
+    // by one
+    for (uint32_t i0 = (uint32_t)warp; i0 < T; i0 += (uint32_t)nwarps * 32u) {
+     const uint32_t my = i0 + (uint32_t)lane * (uint32_t)nwarps;
+     bool my_kept = false;
+     Run my_run{};
+     if (my < T) {
+       my_kept = kept_area(area_of(ld_par<kShared>(par + my)), a.ppm, a.N);
+       my_run = R[my];
+     }
+     uint32_t kept_mask = __ballot_sync(0xFFFFFFFFu, my_kept);
+     while (kept_mask) {
+      const int j = __ffs(kept_mask) - 1;
+      kept_mask &= kept_mask - 1u;
+      Run rg;
+      rg.x0 = (uint16_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)my_run.x0, j);
+      rg.x1 = (uint16_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)my_run.x1, j);
+      rg.y = (uint16_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)my_run.y, j);
+      uint8_t* p = masks + ((uint64_t)f * H + rg.y) * W;
+      const uint32_t x0 = rg.x0, xe = (uint32_t)rg.x1 + 1;
+      if ((reinterpret_cast<uintptr_t>(p) & 15u) != 0u) {     // unaligned rows: lane per byte
+        for (uint32_t x = x0 + lane; x < xe; x += 32) p[x] = 1;
+        continue;
+      }
+      // first and last 16-byte segment: one lane per byte (lanes 0-15 and
+      // 16-31, a single store instruction); full segments in between: 16-byte
+      // stores, one lane per segment
+      const uint32_t s0 = x0 >> 4, s1 = (xe - 1) >> 4;
+      const uint32_t xb = (lane < 16 ? s0 : s1) * 16u + (lane & 15u);
+      if (a.trace == 2) continue;                          // diagnostics: loop without stores
+      if (xb >= x0 && xb < xe && (lane < 16 || s1 != s0)) __stcg(p + xb, (unsigned char)1);
+      for (uint32_t sg = s0 + 1 + lane; sg < s1; sg += 32)
+        __stcg(reinterpret_cast<uint4*>(p + sg * 16u),
+               make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u));
+     }
     }
   }
 
+  if (a.trace && tid == 0) t_mark[8] = clock64();
   // 5. clear the runs of dropped components from the bit mask (final mask F)
   if (s_drop == 0) return;
   uint32_t* Of = a.O + (uint64_t)f * H * P;
   for (uint32_t i = tid; i < T; i += nthr) {
     const uint32_t root = ld_par<kShared>(par + i);
-    if (kept_area(__ldcg(&stats[root].area), a.ppm, a.N)) continue;
+    if (kept_area(area_of(root), a.ppm, a.N)) continue;
     const Run rg = R[i];
     uint32_t* row = Of + (uint64_t)rg.y * P;
     for (uint32_t k = rg.x0 >> 5; k <= (uint32_t)(rg.x1 >> 5); k++) {
@@ -422,16 +493,17 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   if (T <= kCclSmemRuns) {
     Run* R = reinterpret_cast<Run*>(smc);
     uint32_t* par = reinterpret_cast<uint32_t*>(smc + sizeof(Run) * kCclSmemRuns);
-    ccl_frame<true>(a, f, R, par, T, t_mark);
+    uint32_t* s_area = par + kCclSmemRuns;
+    ccl_frame<true>(a, f, R, par, s_area, T, t_mark);
   } else {
     ccl_frame<false>(a, f, const_cast<Run*>(a.runs + (uint64_t)f * a.cap_runs),
-                     a.parent + (uint64_t)f * a.cap_runs, T, t_mark);
+                     a.parent + (uint64_t)f * a.cap_runs, nullptr, T, t_mark);
   }
   if (a.trace && threadIdx.x == 0 && blockIdx.x < 4096) {
     t_mark[7] = clock64();
     g_ccl_trace[blockIdx.x][0] = g_t0;
     g_ccl_trace[blockIdx.x][1] = gtimer_ccl();
-    g_ccl_trace[blockIdx.x][2] = T | ((unsigned long long)t_mark[8] << 32);
+    g_ccl_trace[blockIdx.x][2] = T | ((unsigned long long)(t_mark[8] - t_mark[6]) << 32);
     for (int k = 0; k < 8; k++) g_ccl_trace[blockIdx.x][4 + k] = (unsigned long long)(t_mark[k] - t_mark[9]);
   }
   if (a.track_stream == -2) return;
@@ -525,7 +597,7 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   }
 }
 
-constexpr size_t kCclSmem = (sizeof(Run) + sizeof(uint32_t)) * kCclSmemRuns;
+constexpr size_t kCclSmem = (sizeof(Run) + 2 * sizeof(uint32_t)) * kCclSmemRuns;
 static_assert(kCclSmem >= 512 * 28, "fold staging fits the labelling shared memory");
 
 cudaError_t init_ccl(Ctx& c) {
@@ -548,7 +620,7 @@ cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, bool masks
   a.frame_stream = c.frame_stream;
   a.tstate = reinterpret_cast<TrackState*>(c.tstate);
   a.p = c.p;
-  static const int trace = getenv("FIZI_CCL_TRACE") ? 1 : 0;
+  static const int trace = getenv("FIZI_CCL_TRACE") ? atoi(getenv("FIZI_CCL_TRACE")) : 0;
   a.trace = trace;
   a.O = c.bitO;
   a.W = c.W; a.H = c.H; a.P = c.P;

@@ -52,6 +52,11 @@ struct SegArgs {
   uint32_t dirty_words;         // words per frame of the dirty bitmap
   bool write_zero;              // background chunks still write their zero words
   uint32_t f0, n;               // frame range of this launch (sub-batch)
+  uint32_t n_groups;            // same-stream groups of this launch (items = tiles x groups)
+  unsigned long long* slow_items;   // deferred words: f << 32 | (chunk * 16 + word)
+  uint32_t* slow_count;             // deferred words queued by this launch
+  bool persist;                 // persistent grid: CTAs take items from *item_counter
+  uint32_t* item_counter;
   // in-kernel finalisation (fast path): the last CTA of a frame writes its record
   uint32_t* frame_done;         // per-frame count of finished CTAs
   const double* gtab;
@@ -76,13 +81,11 @@ __device__ __forceinline__ void finalize_frame(const SegArgs& a, uint32_t f,
   r.corrected = a.ctab[mean];
   r.gamma = a.gtab[mean];
   a.call->res[f] = r;
-  if (r.corrected) {
+  if (r.corrected) {             // the LUT re-test rewrites every word of the frame
     const uint32_t pos = atomicAdd(&fix[0], 1u);
     fix[1 + pos] = f;
-    fg[f] = 0;
-    // the identity-LUT mask is void: the LUT re-test rewrites every word
-    for (uint32_t w = 0; w < a.dirty_words; w++) a.dirty[(uint64_t)f * a.dirty_words + w] = 0u;
   }
+  (void)fg;
 }
 
 // Rec.601 weights split so every dp4a weight fits a byte:
@@ -334,171 +337,180 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
 }
 
 // ---------------------------------------------------------------- fast path
-// Fast path.  CTA = 8 warps = one 12 KiB tile (8 chunks of 512 pixels) of
-// every frame of a same-stream group.  Tiles stream through a kStages-deep
-// ring of shared-memory buffers filled by the TMA engine (cp.async.bulk,
-// mbarrier completion).  Warps consume independently: each warp counts
-// itself out of stage s when done (shared atomic); the last one re-issues
-// the stage for frame i + kStages.  No block barrier inside the frame loop.
+// Fast path.  Work item = one 12 KiB tile (8 chunks of 512 pixels) of every
+// frame of a same-stream group; CTA = 8 warps, one chunk each.  Tiles stream
+// through a kStages-deep ring of shared-memory buffers filled by the TMA
+// engine (cp.async.bulk, mbarrier completion).  Warps consume independently:
+// each warp counts itself out of stage s when done (shared atomic); the last
+// one re-issues the stage for frame i + kStages.  No block barrier inside the
+// frame loop.
 //
-// kWarpRing: every warp streams its own chunk through a private kStages-deep
-// ring (1.5 KiB bulk copies, one mbarrier per stage), so a warp never waits
-// for the other warps of the CTA before its next copy is issued.
-template <int kMinBlocks, int kStages, bool kWarpRing>
+// The grid is persistent when a.persist is set: a fixed number of CTAs per
+// SM take items from a per-call counter, so the kernel holds a fixed share
+// of every SM for its whole duration and the pipelined tail kernels of the
+// previous call run beside it in the rest.  The ring's stage / parity run on
+// across items (g0 counts the frames this CTA has streamed so far).
+template <int kMinBlocks, int kStages>
 __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   static_assert((kStages & (kStages - 1)) == 0 && kStages <= kFrameGroup, "ring depth");
   extern __shared__ __align__(128) uint8_t sm[];          // kStages x 12 KiB tiles
-  constexpr int kBars = kWarpRing ? kStages * kWarpsPerCta : kStages;
-  __shared__ __align__(8) uint64_t full[kBars];
+  __shared__ __align__(8) uint64_t full[kStages];
   __shared__ uint32_t empty_cnt[kStages];
-  // per-frame partial sums of the CTA: luma <= 8 warps * 512 px * 255000 < 2^32
-  __shared__ uint32_t acc_y[kFrameGroup], acc_f[kFrameGroup];
-  // deferred (frame, warp, word) items: 32-pixel mask words with a pixel
-  // outside the envelope (the rest of the chunk is background)
-  __shared__ uint16_t q_item[kFrameGroup * kWarpsPerCta * 16];
-  __shared__ uint32_t q_tail, q_head;
+  // per-frame partial luma sums of the CTA: <= 8 warps * 512 px * 255000 < 2^32
+  __shared__ uint32_t acc_y[kFrameGroup];
+  __shared__ uint32_t s_item;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) tl_mark(a.call, kTlSeg, 0);
-  const uint32_t tile = blockIdx.x, grp = blockIdx.y;
-  const uint32_t f_begin = a.group_off[grp];
-  const uint32_t nf = a.group_off[grp + 1] - f_begin;
-  // frame ids of the group, lane i holds frame i (nf <= kFrameGroup <= 32)
-  const uint32_t fid_lane = (uint32_t)lane < nf ? a.group_frames[f_begin + lane] : 0u;
-  const uint32_t stream = a.frame_stream[__shfl_sync(0xFFFFFFFFu, fid_lane, 0)];
-  const uint64_t toff = (uint64_t)tile * kTileBytes;
-  const uint64_t trem = a.frame_bytes - toff;
-  const uint32_t tbytes = trem < (uint64_t)kTileBytes ? (uint32_t)trem : (uint32_t)kTileBytes;
-  const uint32_t n_active = min((uint32_t)kWarpsPerCta, a.nchunks - tile * kWarpsPerCta);
   const uint8_t* frames = a.call->frames;
-  const uint8_t* src0 = frames + toff;
-
-  uint64_t pol = 0;
-  if (tid < kFrameGroup) { acc_y[tid] = 0; acc_f[tid] = 0; }
+  const uint32_t n_items = a.tiles * a.n_groups;
   if (tid < kStages) empty_cnt[tid] = 0;
   if (tid == 0) {
-    q_tail = 0;
-    q_head = 0;
 #pragma unroll
-    for (int s = 0; s < kBars; s++) mbar_init(&full[s], 1);
+    for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
-  __syncthreads();
-  const uint32_t c = tile * kWarpsPerCta + warp;
-  const uint64_t coff_w = (uint64_t)c * kChunkBytes;
-  // private ring of this warp: stage s at sm + (warp * kStages + s) * 1536
-  const uint32_t cbytes = (c < a.nchunks)
-      ? (uint32_t)min((uint64_t)kChunkBytes, a.frame_bytes - coff_w) : 0u;
-  uint64_t* wfull = full + (kWarpRing ? warp * kStages : 0);
-  uint8_t* wring = sm + (kWarpRing ? warp * kStages * kChunkBytes : 0);
-  if (kWarpRing) {
-    if (cbytes) {
+  uint32_t g0 = 0;                                           // frames streamed by this CTA
+  for (uint32_t item = blockIdx.x;;) {
+    if (a.persist) {
+      if (tid == 0) s_item = atomicAdd(a.item_counter, 1u);
+      __syncthreads();
+      item = s_item;
+    }
+    if (item >= n_items) break;
+    const uint32_t tile = item % a.tiles, grp = item / a.tiles;
+    const uint32_t f_begin = a.group_off[grp];
+    const uint32_t nf = a.group_off[grp + 1] - f_begin;
+    // frame ids of the group, lane i holds frame i (nf <= kFrameGroup <= 32)
+    const uint32_t fid_lane = (uint32_t)lane < nf ? a.group_frames[f_begin + lane] : 0u;
+    const uint32_t stream = a.frame_stream[__shfl_sync(0xFFFFFFFFu, fid_lane, 0)];
+    const uint64_t toff = (uint64_t)tile * kTileBytes;
+    const uint64_t trem = a.frame_bytes - toff;
+    const uint32_t tbytes = trem < (uint64_t)kTileBytes ? (uint32_t)trem : (uint32_t)kTileBytes;
+    const uint32_t n_active = min((uint32_t)kWarpsPerCta, a.nchunks - tile * kWarpsPerCta);
+    const uint8_t* src0 = frames + toff;
+    if (tid < kFrameGroup) acc_y[tid] = 0;
+    __syncthreads();
+    uint64_t pol = 0;
+    if (warp == 0) {                                         // prologue: fill the ring
       pol = policy_evict_first();
 #pragma unroll
-      for (int s = 0; s < kStages; s++) {
-        const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, s);
-        if (lane == 0 && (uint32_t)s < nf) {
-          mbar_arrive_expect_tx(&wfull[s], cbytes);
-          bulk_g2s(wring + s * kChunkBytes, frames + (uint64_t)f * a.frame_bytes + coff_w, cbytes,
-                   &wfull[s], pol);
-        }
-      }
-    }
-  } else if (warp == 0) {                                    // prologue: fill the ring
-    pol = policy_evict_first();
-#pragma unroll
-    for (int s = 0; s < kStages; s++) {
-      const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, s);
-      if (lane == 0 && (uint32_t)s < nf) {
-        mbar_arrive_expect_tx(&full[s], tbytes);
-        bulk_g2s(sm + s * kTileBytes, src0 + (uint64_t)f * a.frame_bytes, tbytes, &full[s], pol);
-      }
-    }
-  }
-  if (c < a.nchunks) {
-    const uint64_t coff = coff_w;
-    const bool valid = coff + 48u * lane < a.frame_bytes;
-    EnvRaw e;
-    if (valid) {
-      const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * lane;
-      load_env_raw(e, elo, elo + a.env_plane);
-    } else {
-      full_env_raw(e);
-    }
-    if (warp != 0 && !kWarpRing) pol = policy_evict_first();
-    const uint8_t* my = kWarpRing ? wring + 48 * lane : sm + warp * kChunkBytes + 48 * lane;
-    constexpr uint32_t kStageStride = kWarpRing ? kChunkBytes : kTileBytes;
-    uint32_t luma_lane = 0;                                  // lane i: this warp's luma of frame i
-    for (uint32_t i = 0; i < nf; i++) {
-      const uint32_t s = i & (kStages - 1);
-      const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
-      mbar_wait(&wfull[s], (i / kStages) & 1u);
-      uint32_t fr[12];
-      load48(my + s * kStageStride, valid, fr);
-      // the envelope test consumes all 12 words, so once every lane has it
-      // the stage can be released (the luma is computed after the release)
-      const bool inside = all_inside_sad(fr, e) || !valid;
-      const uint32_t out_lanes = __ballot_sync(0xFFFFFFFFu, !inside);
-      const uint32_t fnext = __shfl_sync(0xFFFFFFFFu, fid_lane, (i + kStages) & 31);
-      if (kWarpRing) {
-        __syncwarp();                                        // every lane has its 48 bytes
-        if (lane == 0 && i + kStages < nf) {
-          mbar_arrive_expect_tx(&wfull[s], cbytes);
-          bulk_g2s(wring + s * kChunkBytes, frames + (uint64_t)fnext * a.frame_bytes + coff, cbytes,
-                   &wfull[s], pol);
-        }
-      } else if (lane == 0 && atomicAdd(&empty_cnt[s], 1u) == n_active - 1) {
-        empty_cnt[s] = 0;                                    // last warp out: refill stage s
-        if (i + kStages < nf) {
+      for (int k = 0; k < kStages; k++) {
+        const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, k);
+        const uint32_t s = (g0 + k) & (kStages - 1);
+        if (lane == 0 && (uint32_t)k < nf) {
           mbar_arrive_expect_tx(&full[s], tbytes);
-          bulk_g2s(sm + s * kTileBytes, src0 + (uint64_t)fnext * a.frame_bytes, tbytes, &full[s],
-                   pol);
+          bulk_g2s(sm + s * kTileBytes, src0 + (uint64_t)f * a.frame_bytes, tbytes, &full[s], pol);
         }
-      }
-      const uint32_t y = warp_sum_u32(luma16(fr));
-      if ((uint32_t)lane == i) luma_lane = y;
-      // background chunks write nothing: their words are implied zero by the
-      // frame's dirty bitmap (only chunks with non-zero words are marked).  In
-      // a chunk touching the foreground, the words with a pixel outside the
-      // envelope are deferred (one item each) and the others written as 0.
-      if (out_lanes) {
-        const uint32_t slow_words = (out_lanes | (out_lanes >> 1)) & 0x55555555u;   // bit 2k
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&q_tail, (uint32_t)__popc(slow_words));
-        base = __shfl_sync(0xFFFFFFFFu, base, 0);
-        if (!(lane & 1)) {
-          if ((slow_words >> lane) & 1u)
-            q_item[base + __popc(slow_words & ((1u << lane) - 1u))] =
-                (uint16_t)((i << 7) | (warp << 4) | (lane >> 1));
-          else if (valid)
-            a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
-        }
-      } else if (a.write_zero && !(lane & 1) && valid) {
-        a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
       }
     }
-    if ((uint32_t)lane < nf) atomicAdd(&acc_y[lane], luma_lane);
+    const uint32_t c = tile * kWarpsPerCta + warp;
+    if (c < a.nchunks) {
+      const uint64_t coff = (uint64_t)c * kChunkBytes;
+      const bool valid = coff + 48u * lane < a.frame_bytes;
+      EnvRaw e;
+      if (valid) {
+        const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * lane;
+        load_env_raw(e, elo, elo + a.env_plane);
+      } else {
+        full_env_raw(e);
+      }
+      if (warp != 0) pol = policy_evict_first();
+      const uint8_t* my = sm + warp * kChunkBytes + 48 * lane;
+      uint32_t luma_lane = 0;                                // lane i: this warp's luma of frame i
+      for (uint32_t i = 0; i < nf; i++) {
+        const uint32_t gi = g0 + i;
+        const uint32_t s = gi & (kStages - 1);
+        const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
+        mbar_wait(&full[s], (gi / kStages) & 1u);
+        uint32_t fr[12];
+        load48(my + s * kTileBytes, valid, fr);
+        // the envelope test consumes all 12 words, so once every lane has it
+        // the stage can be released (the luma is computed after the release)
+        const bool inside = all_inside_sad(fr, e) || !valid;
+        const uint32_t out_lanes = __ballot_sync(0xFFFFFFFFu, !inside);
+        const uint32_t fnext = __shfl_sync(0xFFFFFFFFu, fid_lane, (i + kStages) & 31);
+        if (lane == 0 && atomicAdd(&empty_cnt[s], 1u) == n_active - 1) {
+          empty_cnt[s] = 0;                                  // last warp out: refill stage s
+          if (i + kStages < nf) {
+            mbar_arrive_expect_tx(&full[s], tbytes);
+            bulk_g2s(sm + s * kTileBytes, src0 + (uint64_t)fnext * a.frame_bytes, tbytes,
+                     &full[s], pol);
+          }
+        }
+        const uint32_t y = warp_sum_u32(luma16(fr));
+        if ((uint32_t)lane == i) luma_lane = y;
+        // background chunks write nothing: their words are implied zero by
+        // the frame's dirty bitmap (only chunks with non-zero words are
+        // marked).  In a chunk touching the foreground, the words with a pixel
+        // outside the envelope are queued for the per-pixel kernel (one item
+        // each) and the others written as 0.
+        if (out_lanes) {
+          const uint32_t slow_words = (out_lanes | (out_lanes >> 1)) & 0x55555555u;   // bit 2k
+          uint32_t base = 0;
+          if (lane == 0) base = atomicAdd(a.slow_count, (uint32_t)__popc(slow_words));
+          base = __shfl_sync(0xFFFFFFFFu, base, 0);
+          if (!(lane & 1)) {
+            if ((slow_words >> lane) & 1u)
+              a.slow_items[base + __popc(slow_words & ((1u << lane) - 1u))] =
+                  ((unsigned long long)f << 32) | (c * 16u + (lane >> 1));
+            else if (valid)
+              a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
+          }
+        } else if (a.write_zero && !(lane & 1) && valid) {
+          a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
+        }
+      }
+      if ((uint32_t)lane < nf) atomicAdd(&acc_y[lane], luma_lane);
+    }
+    g0 += nf;
+    __syncthreads();                                         // flush the CTA's sums
+    if (tid < (int)nf) {
+      const uint32_t f = a.group_frames[f_begin + tid];
+      atomicAdd(&a.luma[f], (unsigned long long)acc_y[tid]);
+      __threadfence();
+      if (atomicAdd(&a.frame_done[f], 1u) == a.tiles - 1) {   // last CTA of frame f
+        __threadfence();
+        const unsigned long long sum = atomicAdd(&a.luma[f], 0ull);
+        finalize_frame(a, f, sum, const_cast<uint32_t*>(a.fix), a.fg);
+      }
+    }
+    if (!a.persist) break;
   }
-  __syncthreads();
-  // deferred per-pixel work (words touching the hand), shared by all warps
-  // of the CTA: a pair of lanes per item re-reads the word's 32 pixels and
-  // their envelope (L2) and tests them per pixel
-  const uint32_t nq = q_tail;
-  while (true) {
-    uint32_t item0 = 0;
-    if (lane == 0) item0 = atomicAdd(&q_head, 16u);
-    item0 = __shfl_sync(0xFFFFFFFFu, item0, 0);
-    if (item0 >= nq) break;
-    const uint32_t item = item0 + (lane >> 1);
-    const bool act = item < nq;
-    const uint32_t it = act ? q_item[item] : 0u;
-    const uint32_t i = it >> 7, w = (it >> 4) & 7u, k = it & 15u;
-    const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
-    const uint32_t cq = tile * kWarpsPerCta + w;
+  if (tid == 0) tl_mark(a.call, kTlSeg, 1);
+}
+
+// The words queued by the fused kernel (a pixel outside the envelope): a pair
+// of lanes per word re-reads its 32 pixels and their envelope and applies R1
+// per byte and R2 & R3 through the colour table.  Words of frames that get
+// the LUT re-test are skipped (that kernel rewrites the whole frame).
+// Grid-stride over the queue, foreground counts aggregated per frame.
+__global__ void __launch_bounds__(256) slow_words_kernel(SegArgs a) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) tl_mark(a.call, kTlSlow, 0);
+  struct TlEnd {
+    const CallPtrs* call;
+    __device__ ~TlEnd() { if (threadIdx.x == 0) tl_mark(call, kTlSlow, 1); }
+  } tl_end{a.call};
+  const uint32_t count = *a.slow_count;
+  const uint8_t* frames = a.call->frames;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t q0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 16u; q0 < count;
+       q0 += warps * 16u) {
+    const uint32_t qi = q0 + (lane >> 1);
+    bool act = qi < count;
+    const unsigned long long it = act ? a.slow_items[qi] : 0ull;
+    const uint32_t f = (uint32_t)(it >> 32), wd = (uint32_t)it;
+    const uint32_t cq = wd >> 4, k = wd & 15u;
+    if (act) {
+      const uint64_t mean = (a.luma[f] + 500ull * a.N) / (1000ull * a.N);
+      act = a.ctab[mean] == 0;
+    }
     const uint32_t L = 2 * k + (lane & 1);                   // lane of the chunk
     const uint64_t coff = (uint64_t)cq * kChunkBytes;
     const bool valid = act && coff + 48u * L < a.frame_bytes;
     EnvRegs e;
+    const uint32_t stream = act ? a.frame_stream[f] : 0u;
     const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * L;
     if (valid) load_env(e, elo, elo + a.env_plane);
     else zero_env(e);
@@ -507,29 +519,19 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     uint32_t bits = slow_bits16(fr, e, a.skin);
     bits = valid ? bits : 0u;
     const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
-    if (!(lane & 1) && valid) {
-      a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)cq * 16 + k] = word;
-      const uint32_t pc = __popc(word);
-      if (pc) {
-        atomicAdd(&acc_f[i], pc);
-        atomicOr(a.dirty + (uint64_t)f * a.dirty_words + (cq >> 5), 1u << (cq & 31));
-      }
-    }
+    const bool writer = !(lane & 1) && valid;
+    const uint32_t pc = writer ? __popc(word) : 0u;
+    if (writer) a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)cq * 16 + k] = word;
+    if (pc) atomicOr(a.dirty + (uint64_t)f * a.dirty_words + (cq >> 5), 1u << (cq & 31));
+    // foreground pixels per frame: one atomic per distinct frame of the warp
+    const uint32_t key = pc ? f : 0xFFFFFFFFu;
+    const uint32_t grp = __match_any_sync(0xFFFFFFFFu, key);
+    const uint32_t tot = __reduce_add_sync(grp, pc);
+    if (pc && lane == __ffs(grp) - 1) atomicAdd(&a.fg[f], tot);
   }
-  __syncthreads();                                           // flush the CTA's sums
-  if (tid < (int)nf) {
-    const uint32_t f = a.group_frames[f_begin + tid];
-    atomicAdd(&a.luma[f], (unsigned long long)acc_y[tid]);
-    if (acc_f[tid]) atomicAdd(&a.fg[f], acc_f[tid]);
-    __threadfence();
-    if (atomicAdd(&a.frame_done[f], 1u) == a.tiles - 1) {   // last CTA of frame f
-      __threadfence();
-      const unsigned long long sum = atomicAdd(&a.luma[f], 0ull);
-      finalize_frame(a, f, sum, const_cast<uint32_t*>(a.fix), a.fg);
-    }
-  }
-  if (tid == 0) tl_mark(a.call, kTlSeg, 1);
 }
+
+cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st);
 
 // Frames whose mean luma is outside [luma_lo, luma_hi]: recompute their tiles
 // with the frame's gamma LUT (persistent grid over fix-list x tiles).
@@ -700,6 +702,8 @@ static SegArgs seg_args(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32_t s
   a.fg = c.fg;
   a.lut_table = c.lut;
   a.fix = c.fix_count + (uint64_t)sub * (c.max_batch + 1);
+  a.slow_items = c.slow_items + (uint64_t)f0 * c.nchunks * 16;
+  a.slow_count = c.slow_count + sub;
   a.S = c.p.gray_tol_S;
   a.a1 = c.p.hue_lo_deg;
   a.a2 = c.p.hue_hi_deg;
@@ -722,18 +726,29 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
   SegArgs a = seg_args(c, f0, n, g0, sub);
   prof_begin(c, st);
   if (c.fast) {
-    const dim3 grid(a.tiles, ng);
-    switch (c.seg_variant) {                        // CTAs per SM x ring depth (x per-warp ring)
-      case 2: seg_fast_kernel<2, 8, false><<<grid, 256, 8 * kTileBytes, st>>>(a); break;
-      case 7: seg_fast_kernel<3, 4, true><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
-      case 8: seg_fast_kernel<2, 8, true><<<grid, 256, 8 * kTileBytes, st>>>(a); break;
-      default: seg_fast_kernel<3, 4, false><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
+    a.n_groups = ng;
+    a.item_counter = c.item_counter + sub;
+    const uint32_t items = a.tiles * ng;
+    // persistent grid of c.seg_persist CTAs per SM (0: one CTA per item)
+    const uint32_t per_sm = c.seg_persist;
+    a.persist = per_sm > 0 && items > (uint32_t)c.sms * per_sm;
+    const uint32_t grid = a.persist ? (uint32_t)c.sms * per_sm : items;
+    switch (c.seg_variant) {                        // CTAs per SM x ring depth
+      case 2: seg_fast_kernel<2, 8><<<grid, 256, 8 * kTileBytes, st>>>(a); break;
+      default: seg_fast_kernel<3, 4><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
     }
   } else {
     luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(c.call, c.N, f0,
                                                                                 c.luma);
   }
   prof_end(c, FIZI_PROF_SEGMENT, st);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st) {
+  SegArgs a = seg_args(c, f0, n, 0, sub);
+  slow_words_kernel<<<c.sms * 8, 256, 0, st>>>(a);
   c.launches += 1;
   return cudaGetLastError();
 }
@@ -761,17 +776,13 @@ cudaError_t launch_seg_fix(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaSt
 
 cudaError_t init_segment(Ctx& c) {
   (void)c;
-  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<2, 8, false>,
+  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<2, 8>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * kTileBytes);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_fast_kernel<3, 4, false>,
+    e = cudaFuncSetAttribute(seg_fast_kernel<3, 4>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTileBytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_fast_kernel<2, 8, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * kTileBytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_fast_kernel<3, 4, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTileBytes);
+  const char* ps = getenv("FIZI_SEG_PERSIST");          // experiment switch
+  c.seg_persist = ps ? (uint32_t)atoi(ps) : 0u;
   const char* v = getenv("FIZI_SEG_VARIANT");           // experiment switch (default 2)
   c.seg_variant = v ? atoi(v) : 3;
   if (e == cudaSuccess)

@@ -95,6 +95,11 @@ __global__ void __launch_bounds__(256) track_call_kernel(fizi_params p, const Ca
                                                          int fold, uint32_t n_streams,
                                                          const uint32_t* __restrict__ frame_stream,
                                                          TrackState* __restrict__ ts) {
+  if (threadIdx.x == 0) tl_mark(call, kTlFold, 0);
+  struct TlEnd {
+    const CallPtrs* call;
+    __device__ ~TlEnd() { if (threadIdx.x == 0) tl_mark(call, kTlFold, 1); }
+  } tl_end{call};
   fizi_result* res = call->res;
   const uint32_t n = (uint32_t)call->n;
   if (fold < 0) {

@@ -11,8 +11,9 @@ fz = Fizi(cfg.W, cfg.H, max_batch=64)
 fz.learn_background(synth.frames_dev(cfg, 0, range(30), learning=True))
 fr = synth.frames_dev(cfg, 0, range(64))
 masks = torch.empty((64, cfg.H, cfg.W), dtype=torch.uint8, device=dev)
+mk = None if os.environ.get("CT_NOMASK") else masks
 for it in range(3):
-    fz.process_frames(fr, t_ms=np.arange(64) * 33 + it * 10000, masks=masks)
+    fz.process_frames(fr, t_ms=np.arange(64) * 33 + it * 10000, masks=mk)
 torch.cuda.synchronize()
 n = 64
 buf = (ctypes.c_ulonglong * (12 * n))()
@@ -23,7 +24,7 @@ s, e = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3
 d = e - s
 rounds = a[:, 2] >> 32
 a[:, 2] &= 0xFFFFFFFF
-print("T", a[:, 2].min(), a[:, 2].max(), "flatten rounds min/p50/max", rounds.min(), np.median(rounds), rounds.max())
+print("T", a[:, 2].min(), a[:, 2].max(), "phase 5a (mask bytes) us p50/max", np.median(rounds) / 1965.0, rounds.max() / 1965.0)
 print("start us min %.2f max %.2f | dur us min %.2f p50 %.2f max %.2f | end max %.2f" % (s.min(), s.max(), d.min(), np.median(d), d.max(), e.max()))
 f = a[:, 3]
 if (f > 0).any():

@@ -46,17 +46,19 @@ rc = L.fizi_diag_timeline(fz._h, buf.ctypes.data)
 assert rc == 0, rc
 st = buf[:8 * 256].reshape(8, 256).astype(np.float64)
 en = buf[8 * 256:].reshape(8, 256).astype(np.float64)
-names = ["seg", "fix", "zero", "morph", "ccl"]
+names = ["seg", "slow", "fix", "zero", "morph", "ccl", "fold"]
 print("pipelined" if pipelined else "joined", "C%d B=%d" % (cid, B))
-print("call " + " ".join("%17s" % n for n in names) + "   period")
+print("call " + " ".join("%15s" % n for n in names) + "   period")
 for k in range(ncalls - 12, ncalls):
     t0 = st[0, k]
     cells = []
-    for j, n in enumerate(names):
+    kinds = {"seg": 0, "fix": 1, "zero": 2, "morph": 3, "ccl": 4, "fold": 5, "slow": 6}
+    for n in names:
+        j = kinds[n]
         if st[j, k] > 1e19:
-            cells.append("%17s" % "-")
+            cells.append("%15s" % "-")
         else:
-            cells.append("%7.1f..%7.1f" % ((st[j, k] - t0) / 1e3, (en[j, k] - t0) / 1e3))
+            cells.append("%6.1f..%6.1f" % ((st[j, k] - t0) / 1e3, (en[j, k] - t0) / 1e3))
     per = (st[0, k] - st[0, k - 1]) / 1e3
     print("%4d " % k + " ".join(cells) + "   %6.1f" % per)
 per = (st[0, ncalls - 1] - st[0, 8]) / 1e3 / (ncalls - 9)
