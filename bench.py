@@ -325,7 +325,10 @@ def main():
     fz.flush()
     torch.cuda.synchronize()
     prof = fz.profile_read(reset=True)
-    # per-stage breakdown: a separate, untimed pass with events around every stage
+    # per-stage breakdown: a separate, untimed pass with events around every
+    # stage, calls joined (not pipelined) so that each stage's events bracket
+    # that stage's own kernels
+    fz.set_pipeline(False)
     fz.profile_enable(1)
     nb = min(args.steps, 50)
     for i in range(nb):
@@ -334,6 +337,7 @@ def main():
     torch.cuda.synchronize()
     breakdown = fz.profile_read(reset=True)
     fz.profile_enable(False)
+    fz.set_pipeline(pipelined)
     tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
     tot = torch.tensor([frames_done], dtype=torch.float64, device=dev)
     if world > 1:
@@ -373,6 +377,7 @@ def main():
                  "frac": step_bytes / (step_ms / 1e3) / 1e9 / hbm,
                  "algorithmic_bytes_per_step": step_bytes},
         "stage_ms_per_step": {k: (v[0] / max(nb, 1)) for k, v in breakdown.items()},
+        "stage_breakdown": "separate pass, calls joined (not pipelined), events around each stage",
         "stage_share": {k: v[0] / max(sum(x[0] for x in breakdown.values()), 1e-9)
                         for k, v in breakdown.items()},
     }

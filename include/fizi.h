@@ -212,7 +212,9 @@ enum {
     FIZI_PROF_CCL = 3,        /* labelling, filter, hand blob (a5-a7)         */
     FIZI_PROF_EXPAND = 4,     /* final u8 mask write (a6 output)              */
     FIZI_PROF_TRACK = 5,      /* Mouse fold (a8)                              */
-    FIZI_PROF_SLOTS = 6
+    FIZI_PROF_SLOW = 6,       /* per-pixel R1/R2/R3 of the words queued by the fused kernel */
+    FIZI_PROF_MASKZERO = 7,   /* u8 mask target cleared before the labelling writes it */
+    FIZI_PROF_SLOTS = 8
 };
 int fizi_profile_enable(fizi_ctx *ctx, int mode);
 int fizi_profile_read(fizi_ctx *ctx, double *ms_out, uint64_t *count_out, int reset);

@@ -704,7 +704,9 @@ __global__ void __launch_bounds__(512) zero_masks_kernel(const CallPtrs* call, u
 
 cudaError_t launch_zero_masks(Ctx& c, uint32_t n, cudaStream_t st) {
   (void)n;
+  prof_begin(c, st);
   zero_masks_kernel<<<c.sms * 2, 512, 0, st>>>(c.call, c.N);
+  prof_end(c, FIZI_PROF_MASKZERO, st);
   c.launches += 1;
   return cudaGetLastError();
 }

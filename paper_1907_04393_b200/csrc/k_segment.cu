@@ -748,7 +748,9 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
 
 cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st) {
   SegArgs a = seg_args(c, f0, n, 0, sub);
+  prof_begin(c, st);
   slow_words_kernel<<<c.sms * 8, 256, 0, st>>>(a);
+  prof_end(c, FIZI_PROF_SLOW, st);
   c.launches += 1;
   return cudaGetLastError();
 }

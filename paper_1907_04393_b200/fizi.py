@@ -54,7 +54,7 @@ RESULT_DTYPE = np.dtype({
     "itemsize": 128,
 })
 RESULT_BYTES = 128
-PROF_NAMES = ("segment", "fixup", "morph", "ccl", "expand", "track")
+PROF_NAMES = ("segment", "fixup", "morph", "ccl", "expand", "track", "slow", "maskzero")
 PROF_SLOTS = len(PROF_NAMES)
 
 _lib = None
