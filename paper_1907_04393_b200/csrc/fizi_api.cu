@@ -247,7 +247,7 @@ void fill_call(Ctx& c, uint32_t slot, const fizi::CallPtrs& cp, const uint32_t* 
         if (sof[j] != s) continue;
         if (in_group == 0) ho[g++] = pos;
         hg[pos++] = j;
-        if (++in_group == (uint32_t)fizi::kFrameGroup) in_group = 0;
+        if (++in_group == c.group_max) in_group = 0;
       }
     }
     b.ng = g - b.g0;
@@ -323,7 +323,6 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
   int rc = FIZI_OK;
   if (part == kHead) {                                  // (table + counters: prep stream)
     e = fizi::launch_seg_main(c, 0, pl.n, 0, pl.subs[0].ng, 0, st);
-    if (e == cudaSuccess && c.fast) e = fizi::launch_slow_words(c, 0, pl.n, 0, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "segment");
     // the LUT re-test of corrected frames closes the head: it starts while
     // the SMs drain after segmentation instead of queueing behind the next
@@ -332,6 +331,12 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
     return e == cudaSuccess ? FIZI_OK : cuda_fail(c, e, "fixup");
   }
   if (part == kTail) {
+    // the queued per-pixel words open the tail (the morphology needs them,
+    // the next call's segmentation does not)
+    if (c.fast) {
+      e = fizi::launch_slow_words(c, 0, pl.n, 0, st);
+      if (e != cudaSuccess) return cuda_fail(c, e, "slow words");
+    }
     // the u8 mask target is zeroed on a second internal stream, off the
     // critical path fix -> morph -> labelling; the labelling waits for it
     if (pl.premask) {
@@ -475,7 +480,8 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   const auto h1 = std::chrono::steady_clock::now();
   c.host_sync_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(h1 - h0).count();
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventSynchronize");
-  fizi::CallPtrs cp{frames, pl.fused_mask ? masks : nullptr, res, n, c.call_counter++, c.tl};
+  fizi::CallPtrs cp{frames, pl.fused_mask ? masks : nullptr, res, n,
+                    single ? (int64_t)sof[0] : -1, c.call_counter++, c.tl};
   const uint32_t sub_frames = c.sub_frames;
   if (pipelined) c.sub_frames = 65535;                 // one sub-batch: the tail is the overlap
   fill_call(c, pl.slot, cp, sof, t, n, pl.subs);
@@ -698,6 +704,10 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_tail[i], cudaEventDisableTiming);
   }
   c.use_graphs = getenv("FIZI_NO_GRAPH") == nullptr;
+  if (const char* gm = getenv("FIZI_GROUP")) {          // experiment switch (1..32)
+    const int g = atoi(gm);
+    if (g >= 1 && g <= (int)fizi::kFrameGroup) c.group_max = (uint32_t)g;
+  }
   if (getenv("FIZI_TIMELINE") && e == cudaSuccess) {
     const size_t tb = 2ull * fizi::kTlKinds * fizi::kTlCalls * 8;
     e = cudaMalloc(reinterpret_cast<void**>(&c.tl), tb);

@@ -43,6 +43,7 @@ struct CallPtrs {
   uint8_t* masks;                        // u8 mask target of the fused path, or nullptr
   fizi_result* res;                      // n records (device)
   uint64_t n;
+  int64_t single_stream;                 // stream id when every frame is of one stream, else -1
   uint64_t call_id;                      // diagnostics: timeline slot (FIZI_TIMELINE)
   unsigned long long* tl;                // diagnostics: timeline buffer or nullptr
 };
@@ -82,7 +83,8 @@ struct Ctx {
   bool fast = false;                     // W % 32 == 0: fused bulk-copy kernels
   int sms = 148;
   int seg_variant = 3;                   // fused kernel: CTAs/SM x ring depth variant
-  uint32_t seg_persist = 2;              // persistent fused kernel: CTAs per SM (0: off)
+  uint32_t seg_persist = 0;              // persistent fused kernel: CTAs per SM (0: off)
+  uint32_t group_max = kFrameGroup;      // frames per same-stream group (fused-kernel item)
   bool use_dirty = false;                // clean chunks of A are not written (dirty bitmap)
   uint32_t morph_tr = 0;                 // output rows per morphology CTA
   uint64_t launches = 0;

@@ -494,6 +494,8 @@ __global__ void __launch_bounds__(256) slow_words_kernel(SegArgs a) {
   } tl_end{a.call};
   const uint32_t count = *a.slow_count;
   const uint8_t* frames = a.call->frames;
+  const int64_t single = a.call->single_stream;
+  const bool any_fix = a.fix[0] != 0u;                        // frames getting the LUT re-test
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t q0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 16u; q0 < count;
        q0 += warps * 16u) {
@@ -502,7 +504,7 @@ __global__ void __launch_bounds__(256) slow_words_kernel(SegArgs a) {
     const unsigned long long it = act ? a.slow_items[qi] : 0ull;
     const uint32_t f = (uint32_t)(it >> 32), wd = (uint32_t)it;
     const uint32_t cq = wd >> 4, k = wd & 15u;
-    if (act) {
+    if (act && any_fix) {
       const uint64_t mean = (a.luma[f] + 500ull * a.N) / (1000ull * a.N);
       act = a.ctab[mean] == 0;
     }
@@ -510,7 +512,7 @@ __global__ void __launch_bounds__(256) slow_words_kernel(SegArgs a) {
     const uint64_t coff = (uint64_t)cq * kChunkBytes;
     const bool valid = act && coff + 48u * L < a.frame_bytes;
     EnvRegs e;
-    const uint32_t stream = act ? a.frame_stream[f] : 0u;
+    const uint32_t stream = single >= 0 ? (uint32_t)single : (act ? a.frame_stream[f] : 0u);
     const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * L;
     if (valid) load_env(e, elo, elo + a.env_plane);
     else zero_env(e);

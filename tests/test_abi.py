@@ -60,3 +60,5 @@ def test_sass_is_sm100a_and_uses_bulk_copy(libfizi):
     assert "sm_100a" in out
     assert "UBLKCP" in out            # cp.async.bulk (TMA engine) in the fused kernel
     assert "IDP.4A" in out            # luma dot products
+    assert "VABSDIFF4.U8.ACC" in out  # byte-SIMD sum of absolute differences (envelope test)
+    assert "UBLKCP.G.S" in out or "UBLKCP" in out   # TMA bulk store of morphology rows
