@@ -387,6 +387,59 @@ def test_pipelined_graph_calls_match_oracle():
     pip.close()
 
 
+def test_pipelined_multistream_and_segment_only():
+    """Pipelined calls of interleaved streams (per-stream fold on the fold
+    stream) and stateless segment_frames + track equal joined calls."""
+    cfg = synth.CONFIGS[5]
+    S = 4
+    ref = _ctx(cfg.W, cfg.H, n_streams=S, max_batch=2 * S)
+    pip = _ctx(cfg.W, cfg.H, n_streams=S, max_batch=2 * S)
+    seg = _ctx(cfg.W, cfg.H, n_streams=S, max_batch=2 * S)
+    for s_ in range(S):
+        learn = _t(synth.learning_frames_host(cfg, s_))
+        for fz in (ref, pip, seg):
+            fz.learn_background(learn, stream=s_, margin=synth.MARGIN)
+    pip.set_pipeline(True)
+    seg.set_pipeline(True)
+    out_ref, out_pip, out_seg = [], [], []
+    bufs = [(torch.empty((2 * S, cfg.H, cfg.W), dtype=torch.uint8, device=DEV),
+             torch.empty((2 * S, 128), dtype=torch.uint8, device=DEV)) for _ in range(3)]
+    sbufs = [torch.empty((2 * S, 128), dtype=torch.uint8, device=DEV) for _ in range(3)]
+    for step in range(5):
+        ks = [2 * step, 2 * step + 1]
+        frames, sof, t = [], [], []
+        for k in ks:
+            for s_ in range(S):
+                frames.append(synth.frames_host(cfg, s_, [k])[0])
+                sof.append(s_)
+                t.append(synth.t_ms(k))
+        fr = _t(np.stack(frames))
+        mr, rr = ref.process_frames(fr, streams=sof, t_ms=t)
+        out_ref.append((mr.cpu().numpy(), results_numpy(rr)))
+        mk, rs = bufs[step % 3]
+        pip.process_frames(fr, streams=sof, t_ms=t, masks=mk, results=rs)
+        seg.segment_frames(fr, streams=sof, t_ms=t, masks=None, results=sbufs[step % 3])
+        pip.flush()
+        seg.flush()
+        torch.cuda.synchronize()
+        out_pip.append((mk.cpu().numpy(), results_numpy(rs)))
+        r2 = sbufs[step % 3].clone()
+        for s_ in range(S):                      # fold each stream's records in order
+            idx = [i for i in range(len(sof)) if sof[i] == s_]
+            sub = r2[idx].contiguous()
+            seg.track(sub, stream=s_)
+            r2[idx] = sub
+        torch.cuda.synchronize()
+        out_seg.append(results_numpy(r2))
+    for (ma, ra), (mb, rb), rc in zip(out_ref, out_pip, out_seg):
+        assert np.array_equal(ma, mb)
+        assert ra.tobytes() == rb.tobytes()
+        for name in ra.dtype.names:
+            assert np.array_equal(ra[name], rc[name]), name
+    for fz in (ref, pip, seg):
+        fz.close()
+
+
 def test_host_entry_matches_device_entry():
     cfg = synth.CONFIGS[1]
     learn = synth.learning_frames_host(cfg)
