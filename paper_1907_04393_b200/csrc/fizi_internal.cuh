@@ -83,7 +83,7 @@ struct Ctx {
   bool fast = false;                     // W % 32 == 0: fused bulk-copy kernels
   int sms = 148;
   int seg_variant = 3;                   // fused kernel: CTAs/SM x ring depth variant
-  uint32_t seg_persist = 0;              // persistent fused kernel: CTAs per SM (0: off)
+  uint32_t seg_persist = 5;              // persistent fused kernel: half-CTAs per SM (0: off)
   uint32_t group_max = kFrameGroup;      // frames per same-stream group (fused-kernel item)
   bool use_dirty = false;                // clean chunks of A are not written (dirty bitmap)
   uint32_t morph_tr = 0;                 // output rows per morphology CTA

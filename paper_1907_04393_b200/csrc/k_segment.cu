@@ -733,8 +733,12 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
     const uint32_t items = a.tiles * ng;
     // persistent grid of c.seg_persist CTAs per SM (0: one CTA per item)
     const uint32_t per_sm = c.seg_persist;
-    a.persist = per_sm > 0 && items > (uint32_t)c.sms * per_sm;
-    const uint32_t grid = a.persist ? (uint32_t)c.sms * per_sm : items;
+    static const uint32_t grid_env = getenv("FIZI_SEG_GRID") ? (uint32_t)atoi(getenv("FIZI_SEG_GRID")) : 0u;
+    // default: 2.5 CTAs per SM (half of the SMs keep room for the previous
+    // call's tail kernels beside the fused kernel)
+    const uint32_t pgrid = grid_env ? grid_env : (uint32_t)c.sms * per_sm / 2u;
+    a.persist = pgrid > 0 && items > pgrid;
+    const uint32_t grid = a.persist ? pgrid : items;
     switch (c.seg_variant) {                        // CTAs per SM x ring depth
       case 2: seg_fast_kernel<2, 8><<<grid, 256, 8 * kTileBytes, st>>>(a); break;
       default: seg_fast_kernel<3, 4><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
@@ -786,7 +790,7 @@ cudaError_t init_segment(Ctx& c) {
     e = cudaFuncSetAttribute(seg_fast_kernel<3, 4>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTileBytes);
   const char* ps = getenv("FIZI_SEG_PERSIST");          // experiment switch
-  c.seg_persist = ps ? (uint32_t)atoi(ps) : 0u;
+  c.seg_persist = ps ? 2u * (uint32_t)atoi(ps) : 5u;      // in half CTAs per SM
   const char* v = getenv("FIZI_SEG_VARIANT");           // experiment switch (default 2)
   c.seg_variant = v ? atoi(v) : 3;
   if (e == cudaSuccess)
