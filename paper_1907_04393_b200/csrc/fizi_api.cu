@@ -672,15 +672,21 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
     // next call's segmentation CTAs retire
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
-    const char* sp = getenv("FIZI_SIDE_PRIO");
+    // stream priorities: head (segmentation) > tail (mask clear, per-pixel
+    // words, morphology, labelling, fold) > the caller's streams.  Experiment
+    // switches: FIZI_SIDE_PRIO=0/1/2 -> tail at lowest / highest / one below
+    // highest (default 2); FIZI_HEAD_PRIO=0 -> head at lowest.
+    const int mid_prio = hi_prio < lo_prio ? hi_prio + 1 : hi_prio;
+    const char* spe = getenv("FIZI_SIDE_PRIO");
+    const int side_prio = !spe ? mid_prio : atoi(spe) == 0 ? lo_prio : atoi(spe) == 1 ? hi_prio : mid_prio;
     e = cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking,
-                                     (sp && atoi(sp) == 0) ? lo_prio : hi_prio);
+                                     side_prio);
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&c.side2, cudaStreamNonBlocking,
-                                       (sp && atoi(sp) == 0) ? lo_prio : hi_prio);
+                                       side_prio);
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&c.side3, cudaStreamNonBlocking,
-                                       (sp && atoi(sp) == 0) ? lo_prio : hi_prio);
+                                       side_prio);
     for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
       e = cudaEventCreateWithFlags(&c.ev_ccl[i], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_in[i], cudaEventDisableTiming);
