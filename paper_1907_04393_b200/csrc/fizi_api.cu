@@ -167,6 +167,10 @@ void free_all(Ctx& c) {
   if (c.side3) cudaStreamDestroy(c.side3);
   if (c.head) cudaStreamDestroy(c.head);
   if (c.prep) cudaStreamDestroy(c.prep);
+  if (c.pinned_results) cudaFreeHost(c.pinned_results);
+  if (c.h2d) cudaStreamDestroy(c.h2d);
+  if (c.d2h) cudaStreamDestroy(c.d2h);
+  for (auto ev : c.host_ev) cudaEventDestroy(ev);
   for (uint32_t i = 0; i < fizi::kSlots; i++)
     if (c.ev_prep[i]) cudaEventDestroy(c.ev_prep[i]);
   for (uint32_t i = 0; i < fizi::kSlots; i++)
@@ -839,28 +843,85 @@ int fizi_process_frames_host(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* 
     e = dalloc(&c.stage_frames, (uint64_t)c.max_batch * c.N * 3);
     if (e == cudaSuccess) e = dalloc(&c.stage_masks, (uint64_t)c.max_batch * c.N);
     if (e == cudaSuccess) e = dalloc(&c.stage_results, (uint64_t)c.max_batch * sizeof(fizi_result));
+    if (e == cudaSuccess)
+      e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned_results),
+                         (uint64_t)c.max_batch * sizeof(fizi_result));
     if (e != cudaSuccess) {
       cudaGetLastError();
       return fail(c, FIZI_E_OOM, "staging allocation failed");
     }
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
-  e = cudaMemcpyAsync(c.stage_frames, frames_host, (size_t)n * c.N * 3, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return cuda_fail(c, e, "H2D frames");
-  int rc = fizi_process_frames(ctx, sof, c.stage_frames, n, width, height, t_ms,
-                               masks_host ? c.stage_masks : nullptr, c.stage_results, cuda_stream);
-  if (rc) return rc;
-  e = join_tail(c, st);
-  if (e != cudaSuccess) return cuda_fail(c, e, "join");
+  // The batch moves in chunks of ~32 MB of frames: chunk j+1 is copied in
+  // (copy stream h2d) while chunk j is processed (st) and chunk j-1's masks
+  // and records are copied out (copy stream d2h), so the two PCIe directions
+  // and the path overlap.  Chunks are processed in order on st, so the
+  // tracker sees the frames in index order.
+  const uint64_t fb = c.N * 3;
+  const uint32_t m = std::max<uint32_t>(1u, std::min<uint64_t>(n, (32ull << 20) / fb));
+  const uint32_t nchunk = (n + m - 1) / m;
+  if (!c.h2d) {
+    e = cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(c, e, "copy streams");
+  }
+  while (c.host_ev.size() < 2ull * nchunk + 1) {
+    cudaEvent_t ev = nullptr;
+    e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventCreate");
+    c.host_ev.push_back(ev);
+  }
+  // a pageable mask buffer is filled by one copy at the end (a pageable
+  // destination makes every copy synchronous)
+  bool masks_pinned = false;
   if (masks_host) {
-    e = cudaMemcpyAsync(masks_host, c.stage_masks, (size_t)n * c.N, cudaMemcpyDeviceToHost, st);
+    cudaPointerAttributes pa{};
+    masks_pinned = cudaPointerGetAttributes(&pa, masks_host) == cudaSuccess &&
+                   pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+  }
+  // the copies start after the caller's earlier work on st
+  e = cudaEventRecord(c.host_ev[2 * nchunk], st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c.h2d, c.host_ev[2 * nchunk], 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c.d2h, c.host_ev[2 * nchunk], 0);
+  if (e != cudaSuccess) return cuda_fail(c, e, "fork");
+  for (uint32_t j = 0; j < nchunk; j++) {
+    const uint32_t j0 = j * m, mj = std::min(m, n - j0);
+    cudaEvent_t ev_in = c.host_ev[2 * j], ev_out = c.host_ev[2 * j + 1];
+    e = cudaMemcpyAsync(c.stage_frames + (uint64_t)j0 * fb, frames_host + (uint64_t)j0 * fb,
+                        (size_t)mj * fb, cudaMemcpyHostToDevice, c.h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_in, c.h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_in, 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "H2D frames");
+    int rc = fizi_process_frames(ctx, sof + j0, c.stage_frames + (uint64_t)j0 * fb, mj, width, height,
+                                 t_ms ? t_ms + j0 : nullptr,
+                                 masks_host ? c.stage_masks + (uint64_t)j0 * c.N : nullptr,
+                                 c.stage_results + j0, cuda_stream);
+    if (rc) return rc;
+    e = join_tail(c, st);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_out, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.d2h, ev_out, 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "join");
+    if (masks_pinned) {
+      e = cudaMemcpyAsync(masks_host + (uint64_t)j0 * c.N, c.stage_masks + (uint64_t)j0 * c.N,
+                          (size_t)mj * c.N, cudaMemcpyDeviceToHost, c.d2h);
+      if (e != cudaSuccess) return cuda_fail(c, e, "D2H masks");
+    }
+    // records go through a pinned staging buffer (a pageable destination
+    // would make the copy synchronous and serialise the chunks)
+    e = cudaMemcpyAsync(c.pinned_results + j0, c.stage_results + j0, (size_t)mj * sizeof(fizi_result),
+                        cudaMemcpyDeviceToHost, c.d2h);
+    if (e != cudaSuccess) return cuda_fail(c, e, "D2H results");
+  }
+  if (masks_host && !masks_pinned) {
+    e = cudaMemcpyAsync(masks_host, c.stage_masks, (size_t)n * c.N, cudaMemcpyDeviceToHost, c.d2h);
     if (e != cudaSuccess) return cuda_fail(c, e, "D2H masks");
   }
-  e = cudaMemcpyAsync(results_host, c.stage_results, (size_t)n * sizeof(fizi_result),
-                      cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return cuda_fail(c, e, "D2H results");
-  e = cudaStreamSynchronize(st);
+  e = cudaStreamSynchronize(c.d2h);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamSynchronize");
+  memcpy(results_host, c.pinned_results, (size_t)n * sizeof(fizi_result));
+  for (uint32_t i = 0; i < n; i++) results_host[i].frame_idx = i;   // index in this call
   return FIZI_OK;
 }
 

@@ -139,6 +139,9 @@ struct Ctx {
   cudaStream_t side3 = nullptr;          // pipelined tail: a8 fold (in call order)
   cudaStream_t head = nullptr;           // pipelined head (segmentation)
   cudaStream_t prep = nullptr;           // pipelined: per-call table upload + counter clear
+  cudaStream_t h2d = nullptr, d2h = nullptr;   // fizi_process_frames_host copy streams
+  std::vector<cudaEvent_t> host_ev;            // fizi_process_frames_host chunk events
+  fizi_result* pinned_results = nullptr;       // fizi_process_frames_host record staging
   cudaEvent_t ev_prep[kSlots] = {};
   cudaEvent_t ev_in[kSlots] = {};        // pipelined: caller's stream reached the call
   cudaEvent_t ev_ccl[kSlots] = {};       // pipelined: slot's labelling done

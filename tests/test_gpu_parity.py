@@ -440,17 +440,21 @@ def test_pipelined_multistream_and_segment_only():
         fz.close()
 
 
-def test_host_entry_matches_device_entry():
-    cfg = synth.CONFIGS[1]
+@pytest.mark.parametrize("cid,n", [(1, None), (3, 12)])
+def test_host_entry_matches_device_entry(cid, n):
+    """fizi_process_frames_host (chunked H2D / path / D2H overlap; C3 frames
+    give several ~32 MB chunks) equals the device entry point."""
+    cfg = synth.CONFIGS[cid]
     learn = synth.learning_frames_host(cfg)
-    frames = synth.frames_host(cfg, 0, range(cfg.n_proc))
-    t = np.array([synth.t_ms(k) for k in range(cfg.n_proc)], np.int64)
+    n = n or cfg.n_proc
+    frames = synth.frames_host(cfg, 0, range(n))
+    t = np.array([synth.t_ms(k) for k in range(n)], np.int64)
     a = _ctx(cfg.W, cfg.H, max_batch=20)
     a.learn_background(_t(learn))
     ma, ra = a.process_frames(_t(frames), t_ms=t)
     b = _ctx(cfg.W, cfg.H, max_batch=20)
     b.learn_background(_t(learn))
-    mh = np.empty((cfg.n_proc, cfg.H, cfg.W), np.uint8)
+    mh = np.empty((n, cfg.H, cfg.W), np.uint8)
     _, rh = b.process_frames_host(frames, t_ms=t, masks=mh)
     assert np.array_equal(ma.cpu().numpy(), mh)
     assert results_numpy(ra).tobytes() == rh.tobytes()
