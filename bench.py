@@ -179,7 +179,7 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(out), flush=True)
 
 
-def cpu_baseline(cfg, n_frames=0):
+def cpu_baseline(cfg, n_frames=0, target_s=10.0):
     import oracle
     import synth
     cores = os.cpu_count() or 1
@@ -188,15 +188,22 @@ def cpu_baseline(cfg, n_frames=0):
     lo, hi = oracle.learn(learn, synth.MARGIN)
     frames = synth.frames_host(cfg, 0, range(n))
     p = oracle.make_params(cfg.W, cfg.H)
-    t0 = time.perf_counter()
-    recs, _ = oracle.segment_batch(p, frames, lo, hi, nthreads=cores)
+    # passes over the same n frames until ~10 s of CPU work (bounded sample)
+    passes, done, t0 = 0, 0, time.perf_counter()
     tr = oracle.Tracker(p)
-    for r in recs:
-        tr.update(r)
-    dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "frames/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {n} frames of C{cfg.cid} ({cfg.W}x{cfg.H}), frame-parallel "
-                      f"oracle over {cores} host threads, {dt:.1f} s"}
+    while True:
+        recs, _ = oracle.segment_batch(p, frames, lo, hi, nthreads=cores, want_masks=True)
+        for r in recs:
+            tr.update(r)
+        passes += 1
+        done += n
+        dt = time.perf_counter() - t0
+        if dt >= target_s or passes >= 200:
+            break
+    return {"value": done / dt, "unit": "frames/s", "cores": cores, "kind": "oracle",
+            "sample": f"{passes} passes over the first {n} frames of C{cfg.cid} ({cfg.W}x{cfg.H}) "
+                      f"= {done} frames, frame-parallel oracle (masks + records + fold) over "
+                      f"{cores} host threads, {dt:.1f} s"}
 
 
 # ------------------------------------------------------------------ GPU arm
