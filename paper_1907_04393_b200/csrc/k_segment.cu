@@ -352,13 +352,18 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
 // across items (g0 counts the frames this CTA has streamed so far).
 template <int kMinBlocks, int kStages>
 __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
-  static_assert((kStages & (kStages - 1)) == 0 && kStages <= kFrameGroup, "ring depth");
+  static_assert(kStages >= 2 && kStages <= kFrameGroup, "ring depth");
   extern __shared__ __align__(128) uint8_t sm[];          // kStages x 12 KiB tiles
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ uint32_t empty_cnt[kStages];
   // per-frame partial luma sums of the CTA: <= 8 warps * 512 px * 255000 < 2^32
   __shared__ uint32_t acc_y[kFrameGroup];
   __shared__ uint32_t s_item;
+  // words queued for the per-pixel kernel, staged per work item: (frame
+  // index in the group, warp, word); moved to the global queue at the end of
+  // the item with one reservation
+  __shared__ uint16_t q_item[kFrameGroup * kWarpsPerCta * 16];
+  __shared__ uint32_t q_tail, q_base;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) tl_mark(a.call, kTlSeg, 0);
@@ -390,6 +395,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     const uint32_t n_active = min((uint32_t)kWarpsPerCta, a.nchunks - tile * kWarpsPerCta);
     const uint8_t* src0 = frames + toff;
     if (tid < kFrameGroup) acc_y[tid] = 0;
+    if (tid == 0) q_tail = 0;
     __syncthreads();
     uint64_t pol = 0;
     if (warp == 0) {                                         // prologue: fill the ring
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
 #pragma unroll
       for (int k = 0; k < kStages; k++) {
         const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, k);
-        const uint32_t s = (g0 + k) & (kStages - 1);
+        const uint32_t s = (g0 + k) % kStages;
         if (lane == 0 && (uint32_t)k < nf) {
           mbar_arrive_expect_tx(&full[s], tbytes);
           bulk_g2s(sm + s * kTileBytes, src0 + (uint64_t)f * a.frame_bytes, tbytes, &full[s], pol);
@@ -420,7 +426,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
       uint32_t luma_lane = 0;                                // lane i: this warp's luma of frame i
       for (uint32_t i = 0; i < nf; i++) {
         const uint32_t gi = g0 + i;
-        const uint32_t s = gi & (kStages - 1);
+        const uint32_t s = gi % kStages;
         const uint32_t f = __shfl_sync(0xFFFFFFFFu, fid_lane, i);
         mbar_wait(&full[s], (gi / kStages) & 1u);
         uint32_t fr[12];
@@ -448,12 +454,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
         if (out_lanes) {
           const uint32_t slow_words = (out_lanes | (out_lanes >> 1)) & 0x55555555u;   // bit 2k
           uint32_t base = 0;
-          if (lane == 0) base = atomicAdd(a.slow_count, (uint32_t)__popc(slow_words));
+          if (lane == 0) base = atomicAdd(&q_tail, (uint32_t)__popc(slow_words));
           base = __shfl_sync(0xFFFFFFFFu, base, 0);
           if (!(lane & 1)) {
             if ((slow_words >> lane) & 1u)
-              a.slow_items[base + __popc(slow_words & ((1u << lane) - 1u))] =
-                  ((unsigned long long)f << 32) | (c * 16u + (lane >> 1));
+              q_item[base + __popc(slow_words & ((1u << lane) - 1u))] =
+                  (uint16_t)((i << 7) | (warp << 4) | (lane >> 1));
             else if (valid)
               a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
           }
@@ -464,7 +470,19 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
       if ((uint32_t)lane < nf) atomicAdd(&acc_y[lane], luma_lane);
     }
     g0 += nf;
-    __syncthreads();                                         // flush the CTA's sums
+    __syncthreads();                                         // flush the CTA's sums and queue
+    const uint32_t nq = q_tail;
+    if (nq) {
+      if (tid == 0) q_base = atomicAdd(a.slow_count, nq);
+      __syncthreads();
+      const uint32_t qb = q_base;
+      for (uint32_t q = tid; q < nq; q += blockDim.x) {
+        const uint32_t it = q_item[q];
+        const uint32_t i = it >> 7, w = (it >> 4) & 7u, k = it & 15u;
+        const uint32_t f = a.group_frames[f_begin + i];
+        a.slow_items[qb + q] = ((unsigned long long)f << 32) | ((tile * kWarpsPerCta + w) * 16u + k);
+      }
+    }
     if (tid < (int)nf) {
       const uint32_t f = a.group_frames[f_begin + tid];
       atomicAdd(&a.luma[f], (unsigned long long)acc_y[tid]);
@@ -741,6 +759,7 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
     const uint32_t grid = a.persist ? pgrid : items;
     switch (c.seg_variant) {                        // CTAs per SM x ring depth
       case 2: seg_fast_kernel<2, 8><<<grid, 256, 8 * kTileBytes, st>>>(a); break;
+      case 6: seg_fast_kernel<3, 6><<<grid, 256, 6 * kTileBytes, st>>>(a); break;
       default: seg_fast_kernel<3, 4><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
     }
   } else {
@@ -789,6 +808,9 @@ cudaError_t init_segment(Ctx& c) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(seg_fast_kernel<3, 4>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTileBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(seg_fast_kernel<3, 6>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * kTileBytes);
   const char* ps = getenv("FIZI_SEG_PERSIST");          // experiment switch
   c.seg_persist = ps ? 2u * (uint32_t)atoi(ps) : 5u;      // in half CTAs per SM
   const char* v = getenv("FIZI_SEG_VARIANT");           // experiment switch (default 2)
