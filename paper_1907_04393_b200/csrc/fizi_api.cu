@@ -175,8 +175,10 @@ void free_all(Ctx& c) {
     if (c.ev_prep[i]) cudaEventDestroy(c.ev_prep[i]);
   for (uint32_t i = 0; i < fizi::kSlots; i++)
     if (c.ev_in[i]) cudaEventDestroy(c.ev_in[i]);
-  for (uint32_t i = 0; i < fizi::kSlots; i++)
+  for (uint32_t i = 0; i < fizi::kSlots; i++) {
     if (c.ev_ccl[i]) cudaEventDestroy(c.ev_ccl[i]);
+    if (c.ev_zj[i]) cudaEventDestroy(c.ev_zj[i]);
+  }
   if (c.ev_zfork) cudaEventDestroy(c.ev_zfork);
   if (c.ev_zjoin) cudaEventDestroy(c.ev_zjoin);
   for (auto& r : c.prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -341,18 +343,10 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
       e = fizi::launch_slow_words(c, 0, pl.n, 0, st);
       if (e != cudaSuccess) return cuda_fail(c, e, "slow words");
     }
-    // the u8 mask target is zeroed on a second internal stream, off the
-    // critical path fix -> morph -> labelling; the labelling waits for it
-    if (pl.premask) {
-      e = cudaEventRecord(c.ev_zfork, st);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side2, c.ev_zfork, 0);
-      if (e == cudaSuccess) e = fizi::launch_zero_masks(c, pl.n, c.side2);
-      if (e == cudaSuccess) e = cudaEventRecord(c.ev_zjoin, c.side2);
-      if (e != cudaSuccess) return cuda_fail(c, e, "mask zero");
-    }
+    // (the u8 mask target was cleared beside the segmentation, run_call)
     CallPlan nofold = pl;                             // the fold runs on its own stream
     nofold.fold = -2;
-    return enqueue_tail(c, nofold, pl.subs[0], 0, st, pl.premask ? c.ev_zjoin : nullptr, false);
+    return enqueue_tail(c, nofold, pl.subs[0], 0, st, nullptr, false);
   }
   rc = enqueue_head(c, pl, st);
   if (rc) return rc;
@@ -519,10 +513,21 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
     if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, c.ev_in[pl.slot], 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, c.ev_prep[pl.slot], 0);
     if (e != cudaSuccess) return cuda_fail(c, e, "fork");
+    // the u8 mask target is cleared on its own stream beside this call's
+    // segmentation (it needs only the caller's buffer and the table); the
+    // tail waits for it before labelling writes the kept runs
+    if (pl.premask) {
+      e = cudaStreamWaitEvent(c.side2, c.ev_in[pl.slot], 0);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side2, c.ev_prep[pl.slot], 0);
+      if (e == cudaSuccess) e = fizi::launch_zero_masks(c, pl.n, c.side2);
+      if (e == cudaSuccess) e = cudaEventRecord(c.ev_zj[pl.slot], c.side2);
+      if (e != cudaSuccess) return cuda_fail(c, e, "mask zero");
+    }
     rc = run_part(c, pl, kHead, hs);
     if (rc) return rc;
     e = cudaEventRecord(c.ev_head[pl.slot], hs);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side, c.ev_head[pl.slot], 0);
+    if (e == cudaSuccess && pl.premask) e = cudaStreamWaitEvent(c.side, c.ev_zj[pl.slot], 0);
     if (e != cudaSuccess) return cuda_fail(c, e, "fork");
     rc = run_part(c, pl, kTail, c.side);
     if (rc) return rc;
@@ -693,6 +698,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
                                        side_prio);
     for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
       e = cudaEventCreateWithFlags(&c.ev_ccl[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_zj[i], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_in[i], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_prep[i], cudaEventDisableTiming);
     }

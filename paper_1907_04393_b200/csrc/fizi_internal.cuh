@@ -145,6 +145,7 @@ struct Ctx {
   cudaEvent_t ev_prep[kSlots] = {};
   cudaEvent_t ev_in[kSlots] = {};        // pipelined: caller's stream reached the call
   cudaEvent_t ev_ccl[kSlots] = {};       // pipelined: slot's labelling done
+  cudaEvent_t ev_zj[kSlots] = {};        // pipelined: slot's u8 mask target cleared
   cudaEvent_t ev_zfork = nullptr, ev_zjoin = nullptr;
   cudaEvent_t ev_seg[kMaxSub] = {};      // segment(k) done on the caller's stream
   cudaEvent_t ev_join = nullptr;         // tail of the call done on the side stream
