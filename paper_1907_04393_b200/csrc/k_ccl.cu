@@ -129,7 +129,11 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   RootStats* stats = a.stats + (uint64_t)f * a.cap_runs;
 
   CCL_MARK(0)
-  const uint32_t fg_merged = a.fg[f];                   // loaded early, written in phase 4
+  // loaded early (their loads would otherwise sit on the critical path of
+  // phases 4 and 5): merged foreground count, record and mask pointers
+  const uint32_t fg_merged = a.fg[f];
+  fizi_result* const res = a.call->res;
+  uint8_t* const masks = a.call->masks;
   // component area of root i: shared memory for frames labelled in shared memory
   auto area_of = [&](uint32_t i) -> uint32_t {
     return kShared ? s_area[i] : __ldcg(&stats[i].area);
@@ -151,7 +155,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   //    inside a block in order (no contention, runs end up one link from the
   //    block's top component), then the block boundaries are united in
   //    parallel, so trees stay shallow even for tall components.
-  constexpr uint32_t kRowBlock = 8;
+  constexpr uint32_t kRowBlock = 4;
   auto unite_rows = [&](uint32_t y) {                  // row pair (y - 1, y)
     const uint32_t n = cnt[y], np = cnt[y - 1];
     if (!n || !np) return;
@@ -310,7 +314,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     fg_final = __reduce_add_sync(0xFFFFFFFFu, lane < nw ? s_cnt[2][lane] : 0u);
     best = warp_max_u64(lane < nw ? s_best[lane] : 0ull);
     if (lane == 0) {
-      fizi_result* r = a.call->res + f;
+      fizi_result* r = res + f;
       r->fg_merged = fg_merged;
       r->fg_final = fg_final;
       r->n_comp_total = n_tot;
@@ -326,7 +330,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     const uint32_t blabel = 0xFFFFFFFFu - (uint32_t)(bk & 0xFFFFFFFFu);
     for (uint32_t i = tid; i < T; i += nthr) {
       if (ld_par<kShared>(par + i) != i || 1u + run_key(R, i, W) != blabel) continue;
-      fizi_result* r = a.call->res + f;
+      fizi_result* r = res + f;
       const RootStats* st = stats + i;
       const uint32_t area = __ldcg(&st->area);
       const unsigned long long sx = __ldcg(&st->sx), sy = __ldcg(&st->sy);
@@ -345,46 +349,22 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
 
   CCL_MARK(6)
   // 5a. pre-zeroed u8 mask: write the bytes of every run of a kept component,
-  //     one warp per run, lanes over the run's 16-byte segments
-  uint8_t* const masks = a.call->masks;
-  if (masks && a.masks_zeroed) {
-    const int nwarps = nthr >> 5;
-    // runs in batches of 32 per warp: lane j loads run i0 + j * nwarps (one
-    // round of shared-memory loads per batch), then the warp writes them one
-    // by one
-    for (uint32_t i0 = (uint32_t)warp; i0 < T; i0 += (uint32_t)nwarps * 32u) {
-     const uint32_t my = i0 + (uint32_t)lane * (uint32_t)nwarps;
-     bool my_kept = false;
-     Run my_run{};
-     if (my < T) {
-       my_kept = kept_area(area_of(ld_par<kShared>(par + my)), a.ppm, a.N);
-       my_run = R[my];
-     }
-     uint32_t kept_mask = __ballot_sync(0xFFFFFFFFu, my_kept);
-     while (kept_mask) {
-      const int j = __ffs(kept_mask) - 1;
-      kept_mask &= kept_mask - 1u;
-      Run rg;
-      rg.x0 = (uint16_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)my_run.x0, j);
-      rg.x1 = (uint16_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)my_run.x1, j);
-      rg.y = (uint16_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)my_run.y, j);
+  //     one thread per run: bytes up to 4-byte alignment, words up to 16-byte
+  //     alignment, 16-byte stores, then words and bytes (runs are disjoint,
+  //     so no two threads write the same byte)
+  if (masks && a.masks_zeroed && a.trace != 2) {
+    const uint32_t k1 = 0x01010101u;
+    for (uint32_t i = tid; i < T; i += nthr) {
+      if (!kept_area(area_of(ld_par<kShared>(par + i)), a.ppm, a.N)) continue;
+      const Run rg = R[i];
       uint8_t* p = masks + ((uint64_t)f * H + rg.y) * W;
-      const uint32_t x0 = rg.x0, xe = (uint32_t)rg.x1 + 1;
-      if ((reinterpret_cast<uintptr_t>(p) & 15u) != 0u) {     // unaligned rows: lane per byte
-        for (uint32_t x = x0 + lane; x < xe; x += 32) p[x] = 1;
-        continue;
-      }
-      // first and last 16-byte segment: one lane per byte (lanes 0-15 and
-      // 16-31, a single store instruction); full segments in between: 16-byte
-      // stores, one lane per segment
-      const uint32_t s0 = x0 >> 4, s1 = (xe - 1) >> 4;
-      const uint32_t xb = (lane < 16 ? s0 : s1) * 16u + (lane & 15u);
-      if (a.trace == 2) continue;                          // diagnostics: loop without stores
-      if (xb >= x0 && xb < xe && (lane < 16 || s1 != s0)) __stcg(p + xb, (unsigned char)1);
-      for (uint32_t sg = s0 + 1 + lane; sg < s1; sg += 32)
-        __stcg(reinterpret_cast<uint4*>(p + sg * 16u),
-               make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u));
-     }
+      uintptr_t x = reinterpret_cast<uintptr_t>(p) + rg.x0;
+      const uintptr_t xe = reinterpret_cast<uintptr_t>(p) + (uint32_t)rg.x1 + 1;
+      for (; x < xe && (x & 3u); x++) __stcg(reinterpret_cast<uint8_t*>(x), (uint8_t)1);
+      for (; x + 4 <= xe && (x & 15u); x += 4) __stcg(reinterpret_cast<uint32_t*>(x), k1);
+      for (; x + 16 <= xe; x += 16) __stcg(reinterpret_cast<uint4*>(x), make_uint4(k1, k1, k1, k1));
+      for (; x + 4 <= xe; x += 4) __stcg(reinterpret_cast<uint32_t*>(x), k1);
+      for (; x < xe; x++) __stcg(reinterpret_cast<uint8_t*>(x), (uint8_t)1);
     }
   }
 
@@ -403,8 +383,8 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
       const uint32_t m = (b1 == 31u ? 0xFFFFFFFFu : ((1u << (b1 + 1)) - 1u)) & ~((1u << b0) - 1u);
       atomicAnd(row + k, ~m);
     }
-    if (a.call->masks && !a.masks_zeroed) {
-      uint8_t* mrow = a.call->masks + ((uint64_t)f * H + rg.y) * W;
+    if (masks && !a.masks_zeroed) {
+      uint8_t* mrow = masks + ((uint64_t)f * H + rg.y) * W;
       for (uint32_t x = rg.x0; x <= rg.x1; x++) mrow[x] = 0;
     }
   }

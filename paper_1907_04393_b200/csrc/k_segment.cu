@@ -320,6 +320,30 @@ __device__ __forceinline__ uint32_t slow_bits16(const uint32_t (&fr)[12], const 
   return bits;
 }
 
+// The same per-pixel result with R2 & R3 evaluated arithmetically
+// (gray_and_skin, the definition the colour table is built from) instead of
+// looked up: no dependent memory round trip in the per-pixel kernel.
+__device__ __forceinline__ uint32_t slow_bits16_alu(const uint32_t (&fr)[12], const EnvRegs& e,
+                                                    int S, int a1, int a2) {
+  uint64_t inside = 0;
+#pragma unroll
+  for (int i = 0; i < 12; i++) {
+    uint32_t tE, tO;
+    r1_lanes(fr[i], e, i, tE, tO);
+    const uint32_t f4 = ((tE >> 15) & 1u) | ((tO >> 14) & 2u) | ((tE >> 29) & 4u) | ((tO >> 28) & 8u);
+    inside |= (uint64_t)f4 << (4 * i);
+  }
+  uint32_t bits = 0;
+#pragma unroll
+  for (int p = 0; p < 16; p++) {
+    const int b0 = 3 * p;
+    const int r = (int)byte_of(fr, b0), g = (int)byte_of(fr, b0 + 1), b = (int)byte_of(fr, b0 + 2);
+    const uint32_t bit = ((inside >> b0) & 7u) == 7u ? 0u : gray_and_skin(r, g, b, S, a1, a2);
+    bits |= bit << p;
+  }
+  return bits;
+}
+
 // Process this thread's 16 pixels of one frame in one go (LUT re-test path).
 template <bool kLut>
 __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e, bool valid,
@@ -503,6 +527,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
 // per byte and R2 & R3 through the colour table.  Words of frames that get
 // the LUT re-test are skipped (that kernel rewrites the whole frame).
 // Grid-stride over the queue, foreground counts aggregated per frame.
+template <bool kAluSkin>
 __global__ void __launch_bounds__(256) slow_words_kernel(SegArgs a) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) tl_mark(a.call, kTlSlow, 0);
@@ -536,7 +561,8 @@ __global__ void __launch_bounds__(256) slow_words_kernel(SegArgs a) {
     else zero_env(e);
     uint32_t fr[12];
     load48(frames + (uint64_t)f * a.frame_bytes + coff + 48 * L, valid, fr);
-    uint32_t bits = slow_bits16(fr, e, a.skin);
+    uint32_t bits = kAluSkin ? slow_bits16_alu(fr, e, (int)a.S, (int)a.a1, (int)a.a2)
+                             : slow_bits16(fr, e, a.skin);
     bits = valid ? bits : 0u;
     const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
     const bool writer = !(lane & 1) && valid;
@@ -774,7 +800,9 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
 cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st) {
   SegArgs a = seg_args(c, f0, n, 0, sub);
   prof_begin(c, st);
-  slow_words_kernel<<<c.sms * 8, 256, 0, st>>>(a);
+  static const int alu = getenv("FIZI_SKIN_TABLE") ? 0 : 1;      // experiment switch
+  if (alu) slow_words_kernel<true><<<c.sms * 8, 256, 0, st>>>(a);
+  else slow_words_kernel<false><<<c.sms * 8, 256, 0, st>>>(a);
   prof_end(c, FIZI_PROF_SLOW, st);
   c.launches += 1;
   return cudaGetLastError();
