@@ -133,6 +133,7 @@ class Fizi:
             raise RuntimeError("libfizi needs a CUDA device (no CPU fallback)")
         self.W, self.H = int(width), int(height)
         self.n_streams, self.max_batch = int(n_streams), int(max_batch)
+        self._learned = {}                 # stream -> (frames learned, margin), for FIZIBG1
         self._zeros_u32 = np.zeros(self.max_batch, np.uint32)
         self._zeros_i64 = np.zeros(self.max_batch, np.int64)
         self.device = torch.device("cuda", device)
@@ -174,6 +175,7 @@ class Fizi:
     def learn_background(self, frames, stream: int = 0, margin: int = 10):
         frames = self._frames(frames)
         n = frames.shape[0]
+        self._learned[stream] = (n, margin)
         self._check(lib().fizi_learn_background(self._h, stream, frames.data_ptr(), n,
                                                 frames.shape[2], frames.shape[1], margin,
                                                 _stream_handle(self.device)),
@@ -261,6 +263,32 @@ class Fizi:
     def set_background(self, lo, hi, stream: int = 0):
         self._check(lib().fizi_set_background(self._h, stream, lo.data_ptr(), hi.data_ptr(),
                                               _stream_handle(self.device)), "fizi_set_background")
+
+    def save_background(self, dst, stream: int = 0, frames_learned: int | None = None,
+                        margin: int | None = None):
+        """Write stream's envelope as a FIZIBG1 file (persist.py, NEXT-4)."""
+        import torch
+        from .persist import BackgroundModel, save_background
+        lo, hi = self.get_background(stream)
+        torch.cuda.current_stream(self.device).synchronize()
+        n0, m0 = self._learned.get(stream, (0, 0))
+        save_background(dst, BackgroundModel(lo.cpu().numpy(), hi.cpu().numpy(),
+                                             n0 if frames_learned is None else frames_learned,
+                                             m0 if margin is None else margin))
+
+    def load_background(self, src, stream: int = 0):
+        """Install a FIZIBG1 file as stream's envelope; returns the model."""
+        import torch
+        from .persist import load_background
+        m = load_background(src)
+        if (m.width, m.height) != (self.W, self.H):
+            raise ValueError(f"model is {m.width}x{m.height}, context is {self.W}x{self.H}")
+        lo = torch.from_numpy(m.lo).to(self.device)
+        hi = torch.from_numpy(m.hi).to(self.device)
+        self.set_background(lo, hi, stream)
+        torch.cuda.current_stream(self.device).synchronize()
+        self._learned[stream] = (m.frames_learned, m.margin)
+        return m
 
     def set_pipeline(self, enable: bool = True):
         """Pipelined mode (include/fizi.h): a call's tail overlaps the next call;
