@@ -162,6 +162,41 @@ int fizi_process_frames_host(fizi_ctx *ctx, const uint32_t *stream_of_frame_host
 /* Reset stream `stream`'s tracker to its initial state (invisible). */
 int fizi_reset_tracker(fizi_ctx *ctx, uint32_t stream);
 
+/* ---- NEXT-2: drive mapping ("a rotation around an imaginary
+ * wheel"; SPEC module drive S:376-403).  The pointer of a8 is mapped to a
+ * signed steering value on a virtual wheel and folded into one command per
+ * frame.  Readings L32/L33. */
+typedef struct fizi_wheel {
+    double   cx, cy;               /* wheel centre, pixels                                  */
+    double   radius;               /* > 0                                                   */
+    double   theta_max_deg;        /* 90: |theta| at full lock, (0, 180]                    */
+    double   inner, outer;         /* 0.6, 1.4: annulus in fractions of the radius, inner<1<outer */
+    double   dead_zone_deg;        /* 3: |theta| <= dead zone steers 0, >= 0                */
+    int64_t  hold_ms;              /* 200: steering held after the last reading, then x0.8/frame */
+} fizi_wheel;
+
+typedef struct fizi_command {      /* 32 bytes per frame                                    */
+    double   steering;             /* [-1, 1], negative = left                              */
+    double   throttle;             /* [0, 1] (no slider source yet: stays 0)                */
+    int64_t  t_ms;                 /* the frame's timestamp                                 */
+    uint32_t has_steering;         /* 1 iff the pointer was on the wheel in this frame      */
+    uint32_t _pad;
+} fizi_command;
+
+/* Fill *w with the defaults above for a wheel at (cx, cy) of the given radius. */
+int fizi_wheel_default(fizi_wheel *w, double cx, double cy, double radius);
+
+/* Install (validated: FIZI_E_ARG) the wheel of stream `stream` and reset its
+ * drive state to the neutral command (0, 0) with no reading. */
+int fizi_set_wheel(fizi_ctx *ctx, uint32_t stream, const fizi_wheel *wheel);
+
+/* Fold n records of stream `stream` (device; fields visible, px, py, t_ms as
+ * written by a8), in order, through the stream's drive state; writes n
+ * commands to commands_dev (device).  FIZI_E_NOMODEL if no wheel was set.
+ * Joins outstanding pipelined tails into cuda_stream first. */
+int fizi_drive(fizi_ctx *ctx, uint32_t stream, const fizi_result *results_dev, uint32_t n,
+               fizi_command *commands_dev, fizi_stream_t cuda_stream);
+
 /* Parity/debug: write stage `stage` of frame `frame_in_last_batch` of the last
  * fizi_process_frames / fizi_segment_frames call to out_dev (u8 per pixel;
  * u32 per pixel for FIZI_STAGE_LABELS).  Needs params.debug = 1 and, for

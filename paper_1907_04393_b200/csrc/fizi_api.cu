@@ -144,7 +144,7 @@ void free_all(Ctx& c) {
     if (c.calls[i]) cudaFree(c.calls[i]);
   }
   void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.bitO, c.bitOC,
-                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.tl, c.slow_items,
+                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.tl, c.slow_items, c.dstate,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -672,6 +672,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   const size_t table_bytes = sizeof(fizi::CallPtrs) + mb * 8 + mb * 4 * 2 + (mb + 1) * 4;
   for (uint32_t i = 0; i < fizi::kSlots; i++) A(dalloc(&c.calls[i], table_bytes));
   A(dalloc(&c.tstate, (uint64_t)n_streams * sizeof(fizi::TrackState)));
+  A(dalloc(&c.dstate, (uint64_t)n_streams * sizeof(fizi::DriveState)));
   for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
     e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned[i]), table_bytes);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.pinned_ev[i], cudaEventDisableTiming);
@@ -746,6 +747,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   if (e == cudaSuccess) e = fizi::init_morph(c);
   if (e == cudaSuccess) e = fizi::init_ccl(c);
   if (e == cudaSuccess) e = cudaMemset(c.env, 0, (uint64_t)n_streams * 2 * c.env_plane);
+  if (e == cudaSuccess) e = cudaMemset(c.dstate, 0, (uint64_t)n_streams * sizeof(fizi::DriveState));
   if (e == cudaSuccess) e = fizi::launch_lut_table(c, 0);
   if (e == cudaSuccess) e = fizi::launch_skin_table(c, 0);
   if (e == cudaSuccess) e = fizi::launch_tstate_reset(c, 0, n_streams, 0);
@@ -987,6 +989,56 @@ int fizi_set_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* lo_dev,
   if (e != cudaSuccess) return cuda_fail(c, e, "set_background");
   c.env_valid[stream] = 1;
   c.has_t[stream] = 0;
+  return FIZI_OK;
+}
+
+int fizi_wheel_default(fizi_wheel* w, double cx, double cy, double radius) {
+  if (!w) return FIZI_E_ARG;
+  w->cx = cx;
+  w->cy = cy;
+  w->radius = radius;
+  w->theta_max_deg = 90.0;
+  w->inner = 0.6;
+  w->outer = 1.4;
+  w->dead_zone_deg = 3.0;
+  w->hold_ms = 200;
+  return FIZI_OK;
+}
+
+int fizi_set_wheel(fizi_ctx* ctx, uint32_t stream, const fizi_wheel* w) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (!w) return fail(c, FIZI_E_ARG, "wheel is NULL");
+  const bool ok = std::isfinite(w->cx) && std::isfinite(w->cy) && w->radius > 0.0 &&
+                  std::isfinite(w->radius) && w->theta_max_deg > 0.0 && w->theta_max_deg <= 180.0 &&
+                  w->inner >= 0.0 && w->inner < 1.0 && w->outer > 1.0 && std::isfinite(w->outer) &&
+                  w->dead_zone_deg >= 0.0 && w->hold_ms >= 0;
+  if (!ok) return fail(c, FIZI_E_ARG, "wheel: need radius > 0, 0 < theta_max <= 180, 0 <= inner < 1 < outer, dead zone >= 0, hold >= 0");
+  DeviceGuard guard(c.device);
+  cudaError_t e = fizi::launch_drive_set(c, stream, *w, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(c, e, "set_wheel");
+  if (c.has_wheel.size() < c.n_streams) c.has_wheel.assign(c.n_streams, 0);
+  c.has_wheel[stream] = 1;
+  return FIZI_OK;
+}
+
+int fizi_drive(fizi_ctx* ctx, uint32_t stream, const fizi_result* results_dev, uint32_t n,
+               fizi_command* commands_dev, fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (c.has_wheel.size() <= stream || !c.has_wheel[stream])
+    return fail(c, FIZI_E_NOMODEL, "no wheel set for this stream (fizi_set_wheel)");
+  if (n == 0) return FIZI_OK;
+  if (!results_dev || !commands_dev) return fail(c, FIZI_E_ARG, "NULL pointer argument");
+  DeviceGuard guard(c.device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  cudaError_t e = join_tail(c, st);
+  if (e == cudaSuccess) e = fizi::launch_drive(c, stream, results_dev, n, commands_dev, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "drive");
   return FIZI_OK;
 }
 

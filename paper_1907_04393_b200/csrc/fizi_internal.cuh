@@ -134,6 +134,7 @@ struct Ctx {
   uint32_t* slow_count = nullptr;        // kMaxSub: words queued for the per-pixel kernel
   unsigned long long* slow_items = nullptr;   // max_batch x nchunks x 16 queue (one call)
   uint8_t* tstate = nullptr;             // n_streams tracker states
+  uint8_t* dstate = nullptr;             // n_streams drive states (NEXT-2)
   cudaStream_t side = nullptr;           // internal stream for the per-sub-batch tail
   cudaStream_t side2 = nullptr;          // pipelined tail: u8 mask zeroing
   cudaStream_t side3 = nullptr;          // pipelined tail: a8 fold (in call order)
@@ -162,6 +163,7 @@ struct Ctx {
 
   // host
   std::vector<uint8_t> env_valid;
+  std::vector<uint8_t> has_wheel;        // NEXT-2: fizi_set_wheel called per stream
   std::vector<int64_t> last_t;
   std::vector<uint8_t> has_t;
   uint8_t* pinned[kSlots] = {};               // staging for the per-call upload (one per slot)
@@ -192,6 +194,13 @@ struct Ctx {
   // last call (debug)
   const uint8_t* last_frames = nullptr;
   uint32_t last_n = 0;
+};
+
+struct DriveState {                      // NEXT-2 make_command fold state
+  double steering, throttle;
+  int64_t last_reading;                  // t_ms of the last steering reading
+  int32_t has_reading, has_wheel;
+  fizi_wheel wheel;
 };
 
 struct TrackState {                      // Mouse fold state (c1 step 11)
@@ -242,6 +251,10 @@ cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint3
                                 cudaStream_t st);
 // a8 fold of the current call's records (c.call) on st; fold >= 0: one stream
 cudaError_t launch_track_call(Ctx& c, int fold, cudaStream_t st);
+// NEXT-2: install a wheel (resets the drive state) / fold records into commands
+cudaError_t launch_drive_set(Ctx& c, uint32_t stream, const fizi_wheel& w, cudaStream_t st);
+cudaError_t launch_drive(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
+                         fizi_command* out, cudaStream_t st);
 cudaError_t launch_tstate_reset(Ctx& c, uint32_t first, uint32_t count, cudaStream_t st);
 cudaError_t launch_debug_stage(Ctx& c, int stage, uint32_t frame, void* out, cudaStream_t st);
 

@@ -158,6 +158,77 @@ cudaError_t launch_track_call(Ctx& c, int fold, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------ NEXT-2 drive mapping
+// steering_from_cursor and the make_command fold for
+// one stream, in frame order, one thread.  Every product / sum is a separate
+// correctly rounded operation (no FMA contraction); the angle is atan2 in
+// double, converted to degrees with the factor 180/pi.
+__device__ __forceinline__ bool steering_from_cursor(const fizi_wheel& w, bool visible, double px,
+                                                     double py, double& steering) {
+  if (!visible) return false;
+  const double dx = __dadd_rn(px, -w.cx), dy = __dadd_rn(py, -w.cy);
+  const double d = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+  if (d < __dmul_rn(w.inner, w.radius) || d > __dmul_rn(w.outer, w.radius)) return false;
+  double theta = __dmul_rn(atan2(dx, -dy), 57.29577951308232);   // 12 o'clock 0, clockwise > 0
+  if (theta == -180.0) theta = 180.0;                              // (-180, 180]
+  if (fabs(theta) <= w.dead_zone_deg) { steering = 0.0; return true; }
+  steering = fmin(1.0, fmax(-1.0, __ddiv_rn(theta, w.theta_max_deg)));
+  return true;
+}
+
+__global__ void drive_kernel(DriveState* ds, const fizi_result* __restrict__ res, uint32_t n,
+                             fizi_command* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  DriveState s = *ds;
+  for (uint32_t i = 0; i < n; i++) {
+    const fizi_result& r = res[i];
+    const int64_t t = r.t_ms;
+    double st = 0.0;
+    const bool on = steering_from_cursor(s.wheel, r.visible != 0, r.px, r.py, st);
+    if (on) {
+      s.last_reading = t;
+      s.has_reading = 1;
+    } else {
+      st = s.steering;
+      if (!s.has_reading || t - s.last_reading > s.wheel.hold_ms) st = __dmul_rn(st, 0.8);
+    }
+    s.steering = fmin(1.0, fmax(-1.0, st));
+    s.throttle = fmin(1.0, fmax(0.0, s.throttle));       // no slider source (NEXT-3)
+    fizi_command c;
+    c.steering = s.steering;
+    c.throttle = s.throttle;
+    c.t_ms = t;
+    c.has_steering = on ? 1u : 0u;
+    c._pad = 0;
+    out[i] = c;
+  }
+  *ds = s;
+}
+
+__global__ void drive_set_kernel(DriveState* ds, fizi_wheel w) {
+  DriveState s;
+  s.steering = 0.0;
+  s.throttle = 0.0;
+  s.last_reading = 0;
+  s.has_reading = 0;
+  s.has_wheel = 1;
+  s.wheel = w;
+  *ds = s;
+}
+
+cudaError_t launch_drive_set(Ctx& c, uint32_t stream, const fizi_wheel& w, cudaStream_t st) {
+  drive_set_kernel<<<1, 1, 0, st>>>(reinterpret_cast<DriveState*>(c.dstate) + stream, w);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_drive(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
+                         fizi_command* out, cudaStream_t st) {
+  drive_kernel<<<1, 32, 0, st>>>(reinterpret_cast<DriveState*>(c.dstate) + stream, res, n, out);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
 __global__ void tstate_reset_kernel(TrackState* ts, uint32_t count) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) {

@@ -54,6 +54,21 @@ RESULT_DTYPE = np.dtype({
     "itemsize": 128,
 })
 RESULT_BYTES = 128
+
+
+class Wheel(ctypes.Structure):
+    """fizi_wheel (NEXT-2 drive mapping, include/fizi.h)."""
+    _fields_ = [("cx", ctypes.c_double), ("cy", ctypes.c_double), ("radius", ctypes.c_double),
+                ("theta_max_deg", ctypes.c_double), ("inner", ctypes.c_double),
+                ("outer", ctypes.c_double), ("dead_zone_deg", ctypes.c_double),
+                ("hold_ms", ctypes.c_int64)]
+
+
+# fizi_command (32 bytes)
+COMMAND_DTYPE = np.dtype({"names": ["steering", "throttle", "t_ms", "has_steering"],
+                          "formats": ["<f8", "<f8", "<i8", "<u4"],
+                          "offsets": [0, 8, 16, 24], "itemsize": 32})
+COMMAND_BYTES = 32
 PROF_NAMES = ("segment", "fixup", "morph", "ccl", "expand", "track", "slow", "maskzero")
 PROF_SLOTS = len(PROF_NAMES)
 
@@ -90,8 +105,13 @@ def lib() -> ctypes.CDLL:
         L.fizi_status_string.restype = ctypes.c_char_p
         L.fizi_destroy.argtypes = [vp]
         L.fizi_set_pipeline.argtypes = [vp, i32]
+        L.fizi_wheel_default.argtypes = [ctypes.POINTER(Wheel), ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_double]
+        L.fizi_set_wheel.argtypes = [vp, u32, ctypes.POINTER(Wheel)]
+        L.fizi_drive.argtypes = [vp, u32, vp, u32, vp, vp]
         L.fizi_flush.argtypes = [vp, vp]
-        for name in ("fizi_set_pipeline", "fizi_flush", "fizi_params_default", "fizi_create", "fizi_learn_background",
+        for name in ("fizi_set_pipeline", "fizi_flush", "fizi_wheel_default", "fizi_set_wheel",
+                     "fizi_drive", "fizi_params_default", "fizi_create", "fizi_learn_background",
                      "fizi_process_frames", "fizi_segment_frames", "fizi_process_frames_host",
                      "fizi_track", "fizi_reset_tracker", "fizi_debug_stage",
                      "fizi_get_background", "fizi_set_background"):
@@ -290,6 +310,27 @@ class Fizi:
         self._learned[stream] = (m.frames_learned, m.margin)
         return m
 
+    def set_wheel(self, cx: float, cy: float, radius: float, stream: int = 0, **kw):
+        """NEXT-2: install the virtual steering wheel of `stream` (fizi_set_wheel);
+        keyword overrides: theta_max_deg, inner, outer, dead_zone_deg, hold_ms."""
+        w = Wheel()
+        self._check(lib().fizi_wheel_default(ctypes.byref(w), cx, cy, radius), "fizi_wheel_default")
+        for k, v in kw.items():
+            setattr(w, k, v)
+        self._check(lib().fizi_set_wheel(self._h, stream, ctypes.byref(w)), "fizi_set_wheel")
+        return w
+
+    def drive(self, results, stream: int = 0, commands=None):
+        """NEXT-2: fold records (device (n,128) uint8) into drive commands
+        (device (n,32) uint8 tensor of fizi_command)."""
+        import torch
+        n = results.shape[0]
+        if commands is None:
+            commands = torch.empty((n, COMMAND_BYTES), dtype=torch.uint8, device=self.device)
+        self._check(lib().fizi_drive(self._h, stream, results.data_ptr(), n, commands.data_ptr(),
+                                     _stream_handle(self.device)), "fizi_drive")
+        return commands
+
     def set_pipeline(self, enable: bool = True):
         """Pipelined mode (include/fizi.h): a call's tail overlaps the next call;
         outputs are complete on the current stream after flush()."""
@@ -326,3 +367,14 @@ def results_numpy(results) -> np.ndarray:
     if a.dtype == RESULT_DTYPE:
         return a
     return a.view(np.uint8).reshape(-1, RESULT_BYTES).view(RESULT_DTYPE).reshape(-1)
+
+
+def commands_numpy(commands) -> np.ndarray:
+    """(n,32) uint8 tensor/array of fizi_command -> numpy structured array."""
+    try:
+        import torch
+        if isinstance(commands, torch.Tensor):
+            commands = commands.cpu().numpy()
+    except ImportError:
+        pass
+    return np.ascontiguousarray(commands).view(COMMAND_DTYPE).reshape(-1)
