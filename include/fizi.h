@@ -162,6 +162,17 @@ int fizi_process_frames_host(fizi_ctx *ctx, const uint32_t *stream_of_frame_host
 /* Reset stream `stream`'s tracker to its initial state (invisible). */
 int fizi_reset_tracker(fizi_ctx *ctx, uint32_t stream);
 
+/* ---- NEXT-1: relearn trigger ("re-initiate partly the machine
+ * learning techniques" on a luminosity change).  Folds the
+ * a2 mean luma of n records of stream `stream` (device), in order, through
+ * the stream's trigger state and writes flags_dev[i] (device u8) = 1 iff
+ * |mean_i - mean_prev| > threshold (strict; the first frame after a reset
+ * has no previous mean and gives 0).  The caller re-learns the envelope from
+ * later frames (fizi_learn_background swaps the model between calls, and
+ * resets this state).  threshold <= 255. */
+int fizi_relearn_flags(fizi_ctx *ctx, uint32_t stream, const fizi_result *results_dev, uint32_t n,
+                       uint32_t threshold, uint8_t *flags_dev, fizi_stream_t cuda_stream);
+
 /* ---- NEXT-2: drive mapping ("a rotation around an imaginary
  * wheel"; SPEC module drive S:376-403).  The pointer of a8 is mapped to a
  * signed steering value on a virtual wheel and folded into one command per

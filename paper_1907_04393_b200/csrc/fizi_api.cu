@@ -145,6 +145,7 @@ void free_all(Ctx& c) {
   }
   void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.bitO, c.bitOC,
                   c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.tl, c.slow_items, c.dstate,
+                  c.prev_mean,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -673,6 +674,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   for (uint32_t i = 0; i < fizi::kSlots; i++) A(dalloc(&c.calls[i], table_bytes));
   A(dalloc(&c.tstate, (uint64_t)n_streams * sizeof(fizi::TrackState)));
   A(dalloc(&c.dstate, (uint64_t)n_streams * sizeof(fizi::DriveState)));
+  A(dalloc(&c.prev_mean, (uint64_t)n_streams * sizeof(int32_t)));
   for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
     e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned[i]), table_bytes);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.pinned_ev[i], cudaEventDisableTiming);
@@ -748,6 +750,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   if (e == cudaSuccess) e = fizi::init_ccl(c);
   if (e == cudaSuccess) e = cudaMemset(c.env, 0, (uint64_t)n_streams * 2 * c.env_plane);
   if (e == cudaSuccess) e = cudaMemset(c.dstate, 0, (uint64_t)n_streams * sizeof(fizi::DriveState));
+  if (e == cudaSuccess) e = fizi::launch_relearn_reset(c, 0, n_streams, 0);
   if (e == cudaSuccess) e = fizi::launch_lut_table(c, 0);
   if (e == cudaSuccess) e = fizi::launch_skin_table(c, 0);
   if (e == cudaSuccess) e = fizi::launch_tstate_reset(c, 0, n_streams, 0);
@@ -781,6 +784,7 @@ int fizi_learn_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* frames_
   e = fizi::launch_learn(c, stream, frames_dev, n_frames, margin, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "learn");
   e = fizi::launch_tstate_reset(c, stream, 1, st);
+  if (e == cudaSuccess) e = fizi::launch_relearn_reset(c, stream, 1, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "tracker reset");
   c.env_valid[stream] = 1;
   c.has_t[stream] = 0;
@@ -989,6 +993,23 @@ int fizi_set_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* lo_dev,
   if (e != cudaSuccess) return cuda_fail(c, e, "set_background");
   c.env_valid[stream] = 1;
   c.has_t[stream] = 0;
+  return FIZI_OK;
+}
+
+int fizi_relearn_flags(fizi_ctx* ctx, uint32_t stream, const fizi_result* results_dev, uint32_t n,
+                       uint32_t threshold, uint8_t* flags_dev, fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (threshold > 255) return fail(c, FIZI_E_ARG, "threshold must be <= 255");
+  if (n == 0) return FIZI_OK;
+  if (!results_dev || !flags_dev) return fail(c, FIZI_E_ARG, "NULL pointer argument");
+  DeviceGuard guard(c.device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  cudaError_t e = join_tail(c, st);
+  if (e == cudaSuccess) e = fizi::launch_relearn_flags(c, stream, results_dev, n, threshold, flags_dev, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "relearn flags");
   return FIZI_OK;
 }
 

@@ -135,6 +135,7 @@ struct Ctx {
   unsigned long long* slow_items = nullptr;   // max_batch x nchunks x 16 queue (one call)
   uint8_t* tstate = nullptr;             // n_streams tracker states
   uint8_t* dstate = nullptr;             // n_streams drive states (NEXT-2)
+  int32_t* prev_mean = nullptr;          // n_streams relearn-trigger states (NEXT-1), -1 = none
   cudaStream_t side = nullptr;           // internal stream for the per-sub-batch tail
   cudaStream_t side2 = nullptr;          // pipelined tail: u8 mask zeroing
   cudaStream_t side3 = nullptr;          // pipelined tail: a8 fold (in call order)
@@ -251,6 +252,10 @@ cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint3
                                 cudaStream_t st);
 // a8 fold of the current call's records (c.call) on st; fold >= 0: one stream
 cudaError_t launch_track_call(Ctx& c, int fold, cudaStream_t st);
+// NEXT-1: relearn-trigger flags of a stream's records / reset of the state
+cudaError_t launch_relearn_flags(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
+                                 uint32_t threshold, uint8_t* flags, cudaStream_t st);
+cudaError_t launch_relearn_reset(Ctx& c, uint32_t first, uint32_t count, cudaStream_t st);
 // NEXT-2: install a wheel (resets the drive state) / fold records into commands
 cudaError_t launch_drive_set(Ctx& c, uint32_t stream, const fizi_wheel& w, cudaStream_t st);
 cudaError_t launch_drive(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,

@@ -158,6 +158,39 @@ cudaError_t launch_track_call(Ctx& c, int fold, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ----------------------------------------------------- NEXT-1 relearn trigger
+// relearn_trigger(prev, cur, threshold) = |cur - prev| > threshold
+// over the stream's frames in order; one thread.
+__global__ void relearn_kernel(int32_t* prev_mean, const fizi_result* __restrict__ res, uint32_t n,
+                               int32_t threshold, uint8_t* __restrict__ flags) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int32_t prev = *prev_mean;
+  for (uint32_t i = 0; i < n; i++) {
+    const int32_t cur = res[i].mean_luma;
+    flags[i] = (prev >= 0 && abs(cur - prev) > threshold) ? 1u : 0u;
+    prev = cur;
+  }
+  *prev_mean = prev;
+}
+
+__global__ void relearn_reset_kernel(int32_t* prev_mean, uint32_t count) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) prev_mean[i] = -1;
+}
+
+cudaError_t launch_relearn_flags(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
+                                 uint32_t threshold, uint8_t* flags, cudaStream_t st) {
+  relearn_kernel<<<1, 32, 0, st>>>(c.prev_mean + stream, res, n, (int32_t)threshold, flags);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_relearn_reset(Ctx& c, uint32_t first, uint32_t count, cudaStream_t st) {
+  relearn_reset_kernel<<<(count + 255) / 256, 256, 0, st>>>(c.prev_mean + first, count);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------ NEXT-2 drive mapping
 // steering_from_cursor and the make_command fold for
 // one stream, in frame order, one thread.  Every product / sum is a separate

@@ -109,9 +109,10 @@ def lib() -> ctypes.CDLL:
                                          ctypes.c_double]
         L.fizi_set_wheel.argtypes = [vp, u32, ctypes.POINTER(Wheel)]
         L.fizi_drive.argtypes = [vp, u32, vp, u32, vp, vp]
+        L.fizi_relearn_flags.argtypes = [vp, u32, vp, u32, u32, vp, vp]
         L.fizi_flush.argtypes = [vp, vp]
         for name in ("fizi_set_pipeline", "fizi_flush", "fizi_wheel_default", "fizi_set_wheel",
-                     "fizi_drive", "fizi_params_default", "fizi_create", "fizi_learn_background",
+                     "fizi_drive", "fizi_relearn_flags", "fizi_params_default", "fizi_create", "fizi_learn_background",
                      "fizi_process_frames", "fizi_segment_frames", "fizi_process_frames_host",
                      "fizi_track", "fizi_reset_tracker", "fizi_debug_stage",
                      "fizi_get_background", "fizi_set_background"):
@@ -309,6 +310,17 @@ class Fizi:
         torch.cuda.current_stream(self.device).synchronize()
         self._learned[stream] = (m.frames_learned, m.margin)
         return m
+
+    def relearn_flags(self, results, stream: int = 0, threshold: int = 40):
+        """NEXT-1: u8 flag per record, 1 iff the mean luma jumped by more than
+        `threshold` since the stream's previous frame (device (n,) tensor)."""
+        import torch
+        n = results.shape[0]
+        flags = torch.empty(n, dtype=torch.uint8, device=self.device)
+        self._check(lib().fizi_relearn_flags(self._h, stream, results.data_ptr(), n, threshold,
+                                             flags.data_ptr(), _stream_handle(self.device)),
+                    "fizi_relearn_flags")
+        return flags
 
     def set_wheel(self, cx: float, cy: float, radius: float, stream: int = 0, **kw):
         """NEXT-2: install the virtual steering wheel of `stream` (fizi_set_wheel);
