@@ -173,6 +173,39 @@ int fizi_reset_tracker(fizi_ctx *ctx, uint32_t stream);
 int fizi_relearn_flags(fizi_ctx *ctx, uint32_t stream, const fizi_result *results_dev, uint32_t n,
                        uint32_t threshold, uint8_t *flags_dev, fizi_stream_t cuda_stream);
 
+/* ---- NEXT-3: interface hit-test ("determines the interface zone
+ * activated by the pointer").  Zones of a stream's layout
+ * (parsed on the host) are tested against the a8 pointer of each frame, in
+ * order; per frame and zone the membership and its events are written.
+ * Readings L34/L35. */
+enum { FIZI_ZONE_BUTTON = 0, FIZI_ZONE_SLIDER = 1, FIZI_ZONE_WHEEL = 2 };
+enum { FIZI_EV_ENTER = 1, FIZI_EV_LEAVE = 2, FIZI_EV_CLICK = 4, FIZI_EV_VALUE = 8 };
+
+typedef struct fizi_zone {         /* 72 bytes                                            */
+    uint32_t kind;                 /* FIZI_ZONE_*                                          */
+    uint32_t _pad;
+    double   x, y, w, h;           /* button / slider rectangle, inclusive edges, w,h > 0  */
+    double   cx, cy, r;            /* wheel circle (membership: squared distance <= r^2)   */
+    double   theta_max_deg;        /* wheel: full lock angle, (0, 180]                     */
+} fizi_zone;
+
+typedef struct fizi_zone_event {   /* 16 bytes, one per frame and zone                     */
+    uint8_t  inside;               /* membership after this frame                          */
+    uint8_t  events;               /* FIZI_EV_* bits                                       */
+    uint8_t  _pad[6];
+    double   value;                /* slider [0,1] / wheel steering [-1,1] when FIZI_EV_VALUE, else 0 */
+} fizi_zone_event;
+
+/* Install the layout of stream `stream` (host array of n_zones <= 64 zones,
+ * validated: FIZI_E_ARG) and reset its hit state (no zone entered). */
+int fizi_set_zones(fizi_ctx *ctx, uint32_t stream, const fizi_zone *zones_host, uint32_t n_zones);
+
+/* Hit-test n records of stream `stream` (device; visible, clicked, px, py),
+ * in order; writes n * n_zones events (frame-major) to events_dev (device).
+ * FIZI_E_NOMODEL if no layout was set. */
+int fizi_hit_test(fizi_ctx *ctx, uint32_t stream, const fizi_result *results_dev, uint32_t n,
+                  fizi_zone_event *events_dev, fizi_stream_t cuda_stream);
+
 /* ---- NEXT-2: drive mapping ("a rotation around an imaginary
  * wheel"; SPEC module drive S:376-403).  The pointer of a8 is mapped to a
  * signed steering value on a virtual wheel and folded into one command per

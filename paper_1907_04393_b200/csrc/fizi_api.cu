@@ -145,7 +145,7 @@ void free_all(Ctx& c) {
   }
   void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.bitO, c.bitOC,
                   c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.tl, c.slow_items, c.dstate,
-                  c.prev_mean,
+                  c.prev_mean, c.hstate,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -675,6 +675,7 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.tstate, (uint64_t)n_streams * sizeof(fizi::TrackState)));
   A(dalloc(&c.dstate, (uint64_t)n_streams * sizeof(fizi::DriveState)));
   A(dalloc(&c.prev_mean, (uint64_t)n_streams * sizeof(int32_t)));
+  A(dalloc(&c.hstate, (uint64_t)n_streams * sizeof(fizi::HitState)));
   for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
     e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned[i]), table_bytes);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.pinned_ev[i], cudaEventDisableTiming);
@@ -993,6 +994,56 @@ int fizi_set_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* lo_dev,
   if (e != cudaSuccess) return cuda_fail(c, e, "set_background");
   c.env_valid[stream] = 1;
   c.has_t[stream] = 0;
+  return FIZI_OK;
+}
+
+int fizi_set_zones(fizi_ctx* ctx, uint32_t stream, const fizi_zone* zones, uint32_t n_zones) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (n_zones > fizi::kMaxZones) return fail(c, FIZI_E_CAPACITY, "more than 64 zones");
+  if (n_zones && !zones) return fail(c, FIZI_E_ARG, "zones is NULL");
+  fizi::HitState h;
+  memset(&h, 0, sizeof(h));
+  h.n_zones = n_zones;
+  for (uint32_t k = 0; k < n_zones; k++) {
+    const fizi_zone& z = zones[k];
+    bool ok = false;
+    if (z.kind == FIZI_ZONE_BUTTON || z.kind == FIZI_ZONE_SLIDER)
+      ok = std::isfinite(z.x) && std::isfinite(z.y) && z.w > 0.0 && z.h > 0.0 &&
+           std::isfinite(z.w) && std::isfinite(z.h);
+    else if (z.kind == FIZI_ZONE_WHEEL)
+      ok = std::isfinite(z.cx) && std::isfinite(z.cy) && z.r > 0.0 && std::isfinite(z.r) &&
+           z.theta_max_deg > 0.0 && z.theta_max_deg <= 180.0;
+    if (!ok) return fail(c, FIZI_E_ARG, "zone " + std::to_string(k) + ": bad kind or geometry");
+    h.zones[k] = z;
+  }
+  DeviceGuard guard(c.device);
+  cudaError_t e = cudaDeviceSynchronize();              // no hit test of this stream in flight
+  if (e == cudaSuccess)
+    e = cudaMemcpy(reinterpret_cast<fizi::HitState*>(c.hstate) + stream, &h, sizeof(h),
+                   cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(c, e, "set_zones");
+  if (c.n_zones.size() < c.n_streams) c.n_zones.assign(c.n_streams, 0);
+  c.n_zones[stream] = n_zones;
+  return FIZI_OK;
+}
+
+int fizi_hit_test(fizi_ctx* ctx, uint32_t stream, const fizi_result* results_dev, uint32_t n,
+                  fizi_zone_event* events_dev, fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (c.n_zones.size() <= stream || c.n_zones[stream] == 0)
+    return fail(c, FIZI_E_NOMODEL, "no layout set for this stream (fizi_set_zones)");
+  if (n == 0) return FIZI_OK;
+  if (!results_dev || !events_dev) return fail(c, FIZI_E_ARG, "NULL pointer argument");
+  DeviceGuard guard(c.device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  cudaError_t e = join_tail(c, st);
+  if (e == cudaSuccess) e = fizi::launch_hit_test(c, stream, results_dev, n, events_dev, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "hit test");
   return FIZI_OK;
 }
 

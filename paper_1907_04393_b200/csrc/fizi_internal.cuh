@@ -136,6 +136,7 @@ struct Ctx {
   uint8_t* tstate = nullptr;             // n_streams tracker states
   uint8_t* dstate = nullptr;             // n_streams drive states (NEXT-2)
   int32_t* prev_mean = nullptr;          // n_streams relearn-trigger states (NEXT-1), -1 = none
+  uint8_t* hstate = nullptr;             // n_streams hit-test states (NEXT-3)
   cudaStream_t side = nullptr;           // internal stream for the per-sub-batch tail
   cudaStream_t side2 = nullptr;          // pipelined tail: u8 mask zeroing
   cudaStream_t side3 = nullptr;          // pipelined tail: a8 fold (in call order)
@@ -165,6 +166,7 @@ struct Ctx {
   // host
   std::vector<uint8_t> env_valid;
   std::vector<uint8_t> has_wheel;        // NEXT-2: fizi_set_wheel called per stream
+  std::vector<uint32_t> n_zones;         // NEXT-3: zones per stream (0: no layout)
   std::vector<int64_t> last_t;
   std::vector<uint8_t> has_t;
   uint8_t* pinned[kSlots] = {};               // staging for the per-call upload (one per slot)
@@ -202,6 +204,15 @@ struct DriveState {                      // NEXT-2 make_command fold state
   int64_t last_reading;                  // t_ms of the last steering reading
   int32_t has_reading, has_wheel;
   fizi_wheel wheel;
+};
+
+constexpr uint32_t kMaxZones = 64;
+struct HitState {                        // NEXT-3 layout + per-zone state of one stream
+  uint32_t n_zones, pad;
+  fizi_zone zones[kMaxZones];
+  uint8_t inside[kMaxZones];
+  uint8_t has_value[kMaxZones];
+  double last_value[kMaxZones];
 };
 
 struct TrackState {                      // Mouse fold state (c1 step 11)
@@ -256,6 +267,9 @@ cudaError_t launch_track_call(Ctx& c, int fold, cudaStream_t st);
 cudaError_t launch_relearn_flags(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
                                  uint32_t threshold, uint8_t* flags, cudaStream_t st);
 cudaError_t launch_relearn_reset(Ctx& c, uint32_t first, uint32_t count, cudaStream_t st);
+// NEXT-3: hit-test of a stream's records against its layout (state in c.hstate)
+cudaError_t launch_hit_test(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
+                            fizi_zone_event* out, cudaStream_t st);
 // NEXT-2: install a wheel (resets the drive state) / fold records into commands
 cudaError_t launch_drive_set(Ctx& c, uint32_t stream, const fizi_wheel& w, cudaStream_t st);
 cudaError_t launch_drive(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,

@@ -191,6 +191,76 @@ cudaError_t launch_relearn_reset(Ctx& c, uint32_t first, uint32_t count, cudaStr
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------- NEXT-3 interface hit-test
+// One thread per zone, frames in order (zones are independent; S:350 all
+// containing zones receive events).  Membership needs a visible pointer;
+// rectangles have inclusive edges, circles use squared distance <= r^2.
+__device__ __forceinline__ bool wheel_steering(const fizi_zone& z, double px, double py,
+                                               double& steering);
+
+__global__ void hit_test_kernel(HitState* hs, const fizi_result* __restrict__ res, uint32_t n,
+                                fizi_zone_event* __restrict__ out) {
+  const uint32_t nz = hs->n_zones;
+  const uint32_t k = threadIdx.x;
+  if (k >= nz) return;
+  const fizi_zone z = hs->zones[k];
+  bool inside = hs->inside[k] != 0, has_value = hs->has_value[k] != 0;
+  double last = hs->last_value[k];
+  for (uint32_t i = 0; i < n; i++) {
+    const fizi_result& r = res[i];
+    const bool vis = r.visible != 0;
+    const double px = r.px, py = r.py;
+    bool in = false;
+    if (vis) {
+      if (z.kind == FIZI_ZONE_WHEEL) {
+        const double dx = __dadd_rn(px, -z.cx), dy = __dadd_rn(py, -z.cy);
+        in = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) <= __dmul_rn(z.r, z.r);
+      } else {
+        in = px >= z.x && px <= __dadd_rn(z.x, z.w) && py >= z.y && py <= __dadd_rn(z.y, z.h);
+      }
+    }
+    uint8_t ev = 0;
+    if (in && !inside) ev |= FIZI_EV_ENTER;
+    if (!in && inside) ev |= FIZI_EV_LEAVE;
+    if (in && r.clicked) ev |= FIZI_EV_CLICK;
+    double value = 0.0;
+    if (in) {
+      double v = 0.0;
+      bool have = false;
+      if (z.kind == FIZI_ZONE_SLIDER) {
+        v = fmin(1.0, fmax(0.0, __dadd_rn(1.0, -__ddiv_rn(__dadd_rn(py, -z.y), z.h))));
+        have = true;
+      } else if (z.kind == FIZI_ZONE_WHEEL) {
+        have = wheel_steering(z, px, py, v);
+      }
+      if (have && (!has_value || fabs(__dadd_rn(v, -last)) >= 0.01)) {
+        ev |= FIZI_EV_VALUE;
+        value = v;
+        last = v;
+        has_value = true;
+      }
+    }
+    inside = in;
+    fizi_zone_event e;
+    e.inside = in ? 1u : 0u;
+    e.events = ev;
+    for (int j = 0; j < 6; j++) e._pad[j] = 0;
+    e.value = value;
+    out[(uint64_t)i * nz + k] = e;
+  }
+  hs->inside[k] = inside ? 1u : 0u;
+  hs->has_value[k] = has_value ? 1u : 0u;
+  hs->last_value[k] = last;
+}
+
+cudaError_t launch_hit_test(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
+                            fizi_zone_event* out, cudaStream_t st) {
+  hit_test_kernel<<<1, kMaxZones, 0, st>>>(reinterpret_cast<HitState*>(c.hstate) + stream, res, n,
+                                           out);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------ NEXT-2 drive mapping
 // steering_from_cursor and the make_command fold for
 // one stream, in frame order, one thread.  Every product / sum is a separate
@@ -207,6 +277,16 @@ __device__ __forceinline__ bool steering_from_cursor(const fizi_wheel& w, bool v
   if (fabs(theta) <= w.dead_zone_deg) { steering = 0.0; return true; }
   steering = fmin(1.0, fmax(-1.0, __ddiv_rn(theta, w.theta_max_deg)));
   return true;
+}
+
+// a wheel zone steers like a wheel of the drive module with the default
+// annulus and dead zone (reading L35)
+__device__ __forceinline__ bool wheel_steering(const fizi_zone& z, double px, double py,
+                                               double& steering) {
+  fizi_wheel w;
+  w.cx = z.cx; w.cy = z.cy; w.radius = z.r; w.theta_max_deg = z.theta_max_deg;
+  w.inner = 0.6; w.outer = 1.4; w.dead_zone_deg = 3.0; w.hold_ms = 200;
+  return steering_from_cursor(w, true, px, py, steering);
 }
 
 __global__ void drive_kernel(DriveState* ds, const fizi_result* __restrict__ res, uint32_t n,

@@ -64,6 +64,19 @@ class Wheel(ctypes.Structure):
                 ("hold_ms", ctypes.c_int64)]
 
 
+class Zone(ctypes.Structure):
+    """fizi_zone (NEXT-3 interface hit-test, include/fizi.h)."""
+    _fields_ = [("kind", ctypes.c_uint32), ("_pad", ctypes.c_uint32),
+                ("x", ctypes.c_double), ("y", ctypes.c_double), ("w", ctypes.c_double),
+                ("h", ctypes.c_double), ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+                ("r", ctypes.c_double), ("theta_max_deg", ctypes.c_double)]
+
+
+ZONE_BUTTON, ZONE_SLIDER, ZONE_WHEEL = 0, 1, 2
+EV_ENTER, EV_LEAVE, EV_CLICK, EV_VALUE = 1, 2, 4, 8
+ZONE_EVENT_DTYPE = np.dtype({"names": ["inside", "events", "value"], "formats": ["u1", "u1", "<f8"],
+                             "offsets": [0, 1, 8], "itemsize": 16})
+
 # fizi_command (32 bytes)
 COMMAND_DTYPE = np.dtype({"names": ["steering", "throttle", "t_ms", "has_steering"],
                           "formats": ["<f8", "<f8", "<i8", "<u4"],
@@ -110,9 +123,11 @@ def lib() -> ctypes.CDLL:
         L.fizi_set_wheel.argtypes = [vp, u32, ctypes.POINTER(Wheel)]
         L.fizi_drive.argtypes = [vp, u32, vp, u32, vp, vp]
         L.fizi_relearn_flags.argtypes = [vp, u32, vp, u32, u32, vp, vp]
+        L.fizi_set_zones.argtypes = [vp, u32, vp, u32]
+        L.fizi_hit_test.argtypes = [vp, u32, vp, u32, vp, vp]
         L.fizi_flush.argtypes = [vp, vp]
         for name in ("fizi_set_pipeline", "fizi_flush", "fizi_wheel_default", "fizi_set_wheel",
-                     "fizi_drive", "fizi_relearn_flags", "fizi_params_default", "fizi_create", "fizi_learn_background",
+                     "fizi_drive", "fizi_relearn_flags", "fizi_set_zones", "fizi_hit_test", "fizi_params_default", "fizi_create", "fizi_learn_background",
                      "fizi_process_frames", "fizi_segment_frames", "fizi_process_frames_host",
                      "fizi_track", "fizi_reset_tracker", "fizi_debug_stage",
                      "fizi_get_background", "fizi_set_background"):
@@ -155,6 +170,7 @@ class Fizi:
         self.W, self.H = int(width), int(height)
         self.n_streams, self.max_batch = int(n_streams), int(max_batch)
         self._learned = {}                 # stream -> (frames learned, margin), for FIZIBG1
+        self._nz = {}                      # stream -> zones of its layout (NEXT-3)
         self._zeros_u32 = np.zeros(self.max_batch, np.uint32)
         self._zeros_i64 = np.zeros(self.max_batch, np.int64)
         self.device = torch.device("cuda", device)
@@ -321,6 +337,23 @@ class Fizi:
                                              flags.data_ptr(), _stream_handle(self.device)),
                     "fizi_relearn_flags")
         return flags
+
+    def set_zones(self, zones, stream: int = 0):
+        """NEXT-3: install a layout (sequence of Zone) for `stream`."""
+        arr = (Zone * max(len(zones), 1))(*zones)
+        self._check(lib().fizi_set_zones(self._h, stream, ctypes.cast(arr, ctypes.c_void_p),
+                                         len(zones)), "fizi_set_zones")
+        self._nz[stream] = len(zones)
+
+    def hit_test(self, results, stream: int = 0):
+        """NEXT-3: per frame and zone membership + events (device (n, n_zones, 16) uint8)."""
+        import torch
+        n = results.shape[0]
+        nz = self._nz.get(stream, 0)
+        out = torch.empty((n, max(nz, 1), 16), dtype=torch.uint8, device=self.device)
+        self._check(lib().fizi_hit_test(self._h, stream, results.data_ptr(), n, out.data_ptr(),
+                                        _stream_handle(self.device)), "fizi_hit_test")
+        return out
 
     def set_wheel(self, cx: float, cy: float, radius: float, stream: int = 0, **kw):
         """NEXT-2: install the virtual steering wheel of `stream` (fizi_set_wheel);
