@@ -464,8 +464,6 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   bool single = true;
   for (uint32_t i = 1; i < n && single; i++) single = sof[i] == sof[0];
   pl.fold = !track ? -2 : (single ? (int)sof[0] : -1);
-  static const bool kNoFoldDiag = getenv("FIZI_DIAG_NO_FOLD") != nullptr;   // timing experiments only
-  if (kNoFoldDiag) pl.fold = -2;
   // the u8 mask is written by the labelling kernel when the register-pipelined
   // morphology runs; otherwise it is expanded from the final bit mask
   pl.fused_mask = c.fast && c.P <= 128 && c.p.se_radius <= 4;

@@ -82,7 +82,6 @@ struct Ctx {
   uint64_t cap_runs = 0;                 // run capacity per frame
   bool fast = false;                     // W % 32 == 0: fused bulk-copy kernels
   int sms = 148;
-  int seg_variant = 3;                   // fused kernel: CTAs/SM x ring depth variant
   uint32_t seg_persist = 5;              // persistent fused kernel: half-CTAs per SM (0: off)
   uint32_t group_max = kFrameGroup;      // frames per same-stream group (fused-kernel item)
   bool use_dirty = false;                // clean chunks of A are not written (dirty bitmap)

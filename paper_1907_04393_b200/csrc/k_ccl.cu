@@ -352,7 +352,7 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
   //     one thread per run: bytes up to 4-byte alignment, words up to 16-byte
   //     alignment, 16-byte stores, then words and bytes (runs are disjoint,
   //     so no two threads write the same byte)
-  if (masks && a.masks_zeroed && a.trace != 2) {
+  if (masks && a.masks_zeroed) {
     const uint32_t k1 = 0x01010101u;
     for (uint32_t i = tid; i < T; i += nthr) {
       if (!kept_area(area_of(ld_par<kShared>(par + i)), a.ppm, a.N)) continue;

@@ -783,11 +783,7 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
     const uint32_t pgrid = grid_env ? grid_env : (uint32_t)c.sms * per_sm / 2u;
     a.persist = pgrid > 0 && items > pgrid;
     const uint32_t grid = a.persist ? pgrid : items;
-    switch (c.seg_variant) {                        // CTAs per SM x ring depth
-      case 2: seg_fast_kernel<2, 8><<<grid, 256, 8 * kTileBytes, st>>>(a); break;
-      case 6: seg_fast_kernel<3, 6><<<grid, 256, 6 * kTileBytes, st>>>(a); break;
-      default: seg_fast_kernel<3, 4><<<grid, 256, 4 * kTileBytes, st>>>(a); break;
-    }
+    seg_fast_kernel<3, 4><<<grid, 256, 4 * kTileBytes, st>>>(a);   // 3 CTAs/SM x 4-deep ring
   } else {
     luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(c.call, c.N, f0,
                                                                                 c.luma);
@@ -800,9 +796,7 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
 cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st) {
   SegArgs a = seg_args(c, f0, n, 0, sub);
   prof_begin(c, st);
-  static const int alu = getenv("FIZI_SKIN_TABLE") ? 0 : 1;      // experiment switch
-  if (alu) slow_words_kernel<true><<<c.sms * 8, 256, 0, st>>>(a);
-  else slow_words_kernel<false><<<c.sms * 8, 256, 0, st>>>(a);
+  slow_words_kernel<true><<<c.sms * 8, 256, 0, st>>>(a);
   prof_end(c, FIZI_PROF_SLOW, st);
   c.launches += 1;
   return cudaGetLastError();
@@ -831,18 +825,10 @@ cudaError_t launch_seg_fix(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaSt
 
 cudaError_t init_segment(Ctx& c) {
   (void)c;
-  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<2, 8>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * kTileBytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_fast_kernel<3, 4>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTileBytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_fast_kernel<3, 6>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * kTileBytes);
+  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<3, 4>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTileBytes);
   const char* ps = getenv("FIZI_SEG_PERSIST");          // experiment switch
   c.seg_persist = ps ? 2u * (uint32_t)atoi(ps) : 5u;      // in half CTAs per SM
-  const char* v = getenv("FIZI_SEG_VARIANT");           // experiment switch (default 2)
-  c.seg_variant = v ? atoi(v) : 3;
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(fix_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes);
   return e;
