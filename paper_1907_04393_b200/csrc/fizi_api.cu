@@ -330,20 +330,18 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
   int rc = FIZI_OK;
   if (part == kHead) {                                  // (table + counters: prep stream)
     e = fizi::launch_seg_main(c, 0, pl.n, 0, pl.subs[0].ng, 0, st);
-    if (e != cudaSuccess) return cuda_fail(c, e, "segment");
-    // the LUT re-test of corrected frames closes the head: it starts while
-    // the SMs drain after segmentation instead of queueing behind the next
-    // call's segmentation CTAs
-    e = fizi::launch_seg_fix(c, 0, pl.n, 0, st);
-    return e == cudaSuccess ? FIZI_OK : cuda_fail(c, e, "fixup");
+    return e == cudaSuccess ? FIZI_OK : cuda_fail(c, e, "segment");
   }
   if (part == kTail) {
-    // the queued per-pixel words open the tail (the morphology needs them,
-    // the next call's segmentation does not)
+    // the queued per-pixel words and the LUT re-test of corrected frames
+    // open the tail (the morphology needs them, the next call's
+    // segmentation does not, so the head is the fused kernel alone)
     if (c.fast) {
       e = fizi::launch_slow_words(c, 0, pl.n, 0, st);
       if (e != cudaSuccess) return cuda_fail(c, e, "slow words");
     }
+    e = fizi::launch_seg_fix(c, 0, pl.n, 0, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
     // (the u8 mask target was cleared beside the segmentation, run_call)
     CallPlan nofold = pl;                             // the fold runs on its own stream
     nofold.fold = -2;
