@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(512) zero_masks_kernel(const CallPtrs* call, u
   uint4* body = reinterpret_cast<uint4*>(m + head);
   const uint64_t nb = (total - head) / 16;
   const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-  for (uint64_t i = gt; i < nb; i += stride) body[i] = z;
+  for (uint64_t i = gt; i < nb; i += stride) __stcs(body + i, z);   // streaming: evict first
   const uint64_t tail = head + nb * 16;
   if (gt < total - tail) m[tail + gt] = 0;
   if (threadIdx.x == 0) tl_mark(call, kTlZero, 1);
