@@ -122,6 +122,9 @@ __global__ void __launch_bounds__(256) track_call_kernel(fizi_params p, const Ca
   __shared__ int64_t t_s[kTrackChunk];
   __shared__ double cx_s[kTrackChunk], cy_s[kTrackChunk];
   __shared__ uint32_t ar_s[kTrackChunk];
+  __shared__ int64_t dw_o[kTrackChunk];
+  __shared__ double px_o[kTrackChunk], py_o[kTrackChunk];
+  __shared__ uint8_t vc_o[kTrackChunk];
   TrackState st;
   if (threadIdx.x == 0) st = ts[fold];
   for (uint32_t base = 0; base < n; base += kTrackChunk) {
@@ -132,19 +135,25 @@ __global__ void __launch_bounds__(256) track_call_kernel(fizi_params p, const Ca
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+      // the next record's inputs are loaded before the current fold step
+      // (separate output arrays: no aliasing between the two)
+      int64_t t_n = t_s[0];
+      uint32_t a_n = ar_s[0];
+      double x_n = cx_s[0], y_n = cy_s[0];
       for (uint32_t i = 0; i < m; i++) {
         fizi_result r;
-        r.t_ms = t_s[i]; r.blob_area = ar_s[i]; r.cx = cx_s[i]; r.cy = cy_s[i];
+        r.t_ms = t_n; r.blob_area = a_n; r.cx = x_n; r.cy = y_n;
+        if (i + 1 < m) { t_n = t_s[i + 1]; a_n = ar_s[i + 1]; x_n = cx_s[i + 1]; y_n = cy_s[i + 1]; }
         track_one(p, st, r);
-        t_s[i] = r.dwell_ms; cx_s[i] = r.px; cy_s[i] = r.py;
-        ar_s[i] = (uint32_t)r.visible | ((uint32_t)r.clicked << 1);
+        dw_o[i] = r.dwell_ms; px_o[i] = r.px; py_o[i] = r.py;
+        vc_o[i] = (uint8_t)(r.visible | (r.clicked << 1));
       }
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
       fizi_result& r = res[base + i];
-      r.visible = (uint8_t)(ar_s[i] & 1u); r.clicked = (uint8_t)(ar_s[i] >> 1);
-      r.px = cx_s[i]; r.py = cy_s[i]; r.dwell_ms = t_s[i];
+      r.visible = (uint8_t)(vc_o[i] & 1u); r.clicked = (uint8_t)(vc_o[i] >> 1);
+      r.px = px_o[i]; r.py = py_o[i]; r.dwell_ms = dw_o[i];
     }
     __syncthreads();
   }
