@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="frames per launch (default: config's)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps (capped)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather-every", type=int, default=16,
+                    help="sharded path: steps per record gather + fold window")
+    ap.add_argument("--force-gather", action="store_true",
+                    help="N=1: run the sharded path (segment + NCCL gather + fold) on a one-rank group")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="N=1: join every call's tail into the stream (no cross-call overlap)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -224,8 +228,16 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    # sharded path (segment + gather + fold): N > 1, or N = 1 with --force-gather
+    # (a one-rank NCCL group, to exercise the multi-GPU code path on one GPU)
+    sharded = world > 1 or args.force_gather
+    if sharded:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            dist.init_process_group("nccl", device_id=dev, rank=0, world_size=1)
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     B = args.batch or cfg.batch
     from paper_1907_04393_b200 import shard
@@ -253,14 +265,20 @@ def main():
     fz.learn_background(learn, margin=synth.MARGIN)
     # N = 1: pipelined calls (a call's tail overlaps the next calls'
     # segmentation), so outputs rotate over three buffers and the timed
-    # region ends with fz.flush(); N > 1 gathers every step's records at once
-    pipelined = world == 1 and not args.no_pipeline
+    # region ends with fz.flush() (N > 1: segment_frames, windowed gather + fold)
+    pipelined = not args.no_pipeline
     fz.set_pipeline(pipelined)
+    # sharded path: the records of G steps are gathered and folded together on
+    # a fold stream (one NCCL all_gather per window), while the next window's
+    # calls run; the folds of every rank cover every frame, in frame order
+    G = max(1, args.gather_every) if sharded else 1
+    resw = torch.empty((G, B, RESULT_BYTES), dtype=torch.uint8, device=dev)
+    gathered_w = torch.empty((world * G * B, RESULT_BYTES), dtype=torch.uint8, device=dev)
+    fold_stream = torch.cuda.Stream(device=dev)
+    window = []
     NBUF = 3                             # = the context's call slots (include/fizi.h)
     masks2 = [torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
     res2 = [torch.empty((B, RESULT_BYTES), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
-    res = res2[0]
-    gathered = torch.empty((world * B, RESULT_BYTES), dtype=torch.uint8, device=dev)
     del learn
     # per-round views, made once (the step itself only enqueues work)
     views = []
@@ -283,20 +301,43 @@ def main():
             mk, res_n = mks[i % NBUF], ress[i % NBUF]
             # timestamps keep increasing across passes over the resident rounds
             t = t_base + (i // need) * t_pass
-            if world == 1:             # the whole path in one call (fold fused into labelling)
+            if not sharded:            # the whole path in one call (fold fused into labelling)
                 fz.process_frames(fr_n, t_ms=t, masks=mk, results=res_n)
                 return n
-            fz.segment_frames(fr_n, t_ms=t, masks=mk, results=res_n)
-        # a8 across ranks: gather the step's records (frame order = rank order)
-        # and fold them on every rank
-        dist.all_gather_into_tensor(gathered, res)
-        for off, cnt in shard.gathered_slices(cfg.n_proc, B, world, rnd):
-            fz.track(gathered[off: off + cnt])
+            fz.segment_frames(fr_n, t_ms=t, masks=mk, results=resw[len(window)][:n])
+        window.append(rnd)
+        if len(window) == G:
+            drain()
         return n
+
+    def drain():
+        # a8 across ranks: gather the window's records (frame order = step
+        # order, then rank order) and fold them on every rank
+        if not window:
+            return
+        main = torch.cuda.current_stream(dev)
+        fold_stream.wait_stream(main)
+        with torch.cuda.stream(fold_stream):
+            fz.flush()                      # the window's tails, joined into the fold stream
+            dist.all_gather_into_tensor(gathered_w, resw)
+            gathered_ev = torch.cuda.Event()
+            gathered_ev.record(fold_stream)
+            for j, rnd_j in enumerate(window):
+                for off, cnt in shard.gathered_slices(cfg.n_proc, B, world, rnd_j):
+                    o = (off // B) * G * B + j * B
+                    fz.track(gathered_w[o: o + cnt])
+        main.wait_event(gathered_ev)        # resw is free for the next window
+        window.clear()
+
+    def finish():
+        # the last (partial) window, its folds, and every outstanding tail
+        drain()
+        torch.cuda.current_stream(dev).wait_stream(fold_stream)
+        fz.flush()
 
     for i in range(args.warmup):
         step(i)
-    fz.flush()
+    finish()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -314,7 +355,7 @@ def main():
         h0 = time.perf_counter()
         for i in range(args.steps):
             frames_done += step(args.warmup + i)
-        fz.flush()                       # every tail of the timed calls is inside
+        finish()                         # every tail (and fold) of the timed calls is inside
         host_ms = (time.perf_counter() - h0) * 1e3
         e1.record(st)
         torch.cuda.synchronize()
@@ -329,7 +370,7 @@ def main():
     fz.profile_read(reset=True)
     for i in range(args.steps):
         step(args.warmup + args.steps + i)
-    fz.flush()
+    finish()
     torch.cuda.synchronize()
     prof = fz.profile_read(reset=True)
     # per-stage breakdown: a separate, untimed pass with events around every
@@ -340,7 +381,7 @@ def main():
     nb = min(args.steps, 50)
     for i in range(nb):
         step(args.warmup + 2 * args.steps + i)
-    fz.flush()
+    finish()
     torch.cuda.synchronize()
     breakdown = fz.profile_read(reset=True)
     fz.profile_enable(False)
@@ -397,7 +438,8 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": f"C{cfg.cid}: {cfg.W}x{cfg.H} stream, {cfg.n_proc} frames, "
                                f"batches of {B} per launch (BASELINE.json configs[{cfg.cid - 1}])",
-                   "frames_per_step_per_gpu": B, "pipelined_calls": pipelined, "resident_batches_per_gpu": need,
+                   "frames_per_step_per_gpu": B, "pipelined_calls": pipelined,
+                   "sharded_path": sharded, "resident_batches_per_gpu": need,
                    "l2": f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step",
                    "parallelism": f"frames sharded by batch, dp{world}"},
         "gpu_launches": launches,
@@ -455,7 +497,7 @@ def main():
     if rank == 0:
         print(json.dumps(out), flush=True)
     fz.close()
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 
