@@ -322,10 +322,8 @@ def main():
             dist.all_gather_into_tensor(gathered_w, resw)
             gathered_ev = torch.cuda.Event()
             gathered_ev.record(fold_stream)
-            for j, rnd_j in enumerate(window):
-                for off, cnt in shard.gathered_slices(cfg.n_proc, B, world, rnd_j):
-                    o = (off // B) * G * B + j * B
-                    fz.track(gathered_w[o: o + cnt])
+            for o, cnt in shard.window_slices(cfg.n_proc, B, world, window, G):
+                fz.track(gathered_w[o: o + cnt])
         main.wait_event(gathered_ev)        # resw is free for the next window
         window.clear()
 

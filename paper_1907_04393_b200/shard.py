@@ -57,3 +57,16 @@ def gathered_slices(n_frames: int, batch: int, world: int, rnd: int):
     """(offset, n) of each rank's records inside the gathered buffer of
     world * batch records, in frame order."""
     return [(r * batch, n) for r, n in enumerate(round_sizes(n_frames, batch, world, rnd)) if n]
+
+
+def window_slices(n_frames: int, batch: int, world: int, rounds, window: int):
+    """(offset, n) of the records, in frame order, inside the buffer gathered
+    from every rank's window of `window` steps x `batch` records (rank r's
+    block at r * window * batch, step j of the window at + j * batch);
+    `rounds` are the rounds of the window's steps, in order."""
+    out = []
+    for j, rnd in enumerate(rounds):
+        for off, n in gathered_slices(n_frames, batch, world, rnd):
+            r = off // batch
+            out.append((r * window * batch + j * batch, n))
+    return out

@@ -89,6 +89,71 @@ def _worker(rank, world, port, cid, n_frames, batch, q):
     dist.destroy_process_group()
 
 
+def _worker_windowed(rank, world, port, cid, n_frames, batch, window, q):
+    """bench.py's sharded path: records of `window` steps gathered at once
+    (one all_gather of window x batch records per rank), folded in frame order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg, lo, hi, frames = _stream(cid, n_frames)
+    p = oracle.make_params(cfg.W, cfg.H)
+    tr = oracle.Tracker(p)
+    folded = []
+    resw = torch.zeros(window, batch, RESULT_BYTES, dtype=torch.uint8)
+    rounds = []
+
+    def drain():
+        parts = [torch.zeros(window * batch, RESULT_BYTES, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(parts, resw.reshape(window * batch, RESULT_BYTES))
+        rows = torch.cat(parts).numpy().view(RESULT_DTYPE).reshape(-1)
+        for off, n in shard.window_slices(n_frames, batch, world, rounds, window):
+            for row in rows[off: off + n]:
+                rec = oracle.record_from_blob(int(row["t_ms"]), int(row["blob_area"]),
+                                              float(row["cx"]), float(row["cy"]))
+                tr.update(rec)
+                folded.append((int(row["frame_idx"]), rec.visible, rec.clicked, rec.px, rec.py,
+                               rec.dwell_ms))
+        rounds.clear()
+
+    for rnd in range(shard.n_rounds(n_frames, batch, world)):
+        b = shard.round_batch(n_frames, batch, world, rank, rnd)
+        if b is not None:
+            ks = list(range(b.k0, b.k1))
+            recs = [oracle.segment(p, frames[k], lo, hi, t_ms=synth.t_ms(k), stages=False)[0]
+                    for k in ks]
+            resw[len(rounds), : b.n] = torch.from_numpy(_to_result_bytes(recs, ks))
+        rounds.append(rnd)
+        if len(rounds) == window:
+            drain()
+    if rounds:
+        drain()
+    q.put((rank, folded))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("window", [1, 2, 3])
+def test_two_ranks_windowed_gather_matches_single_process(window):
+    world, cid, n_frames, batch = 2, 1, 20, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_windowed,
+                         args=(r, world, port, cid, n_frames, batch, window, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = dict(q.get(timeout=600) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    cfg, lo, hi, frames = _stream(cid, n_frames)
+    p = oracle.make_params(cfg.W, cfg.H)
+    recs = [oracle.segment(p, frames[k], lo, hi, t_ms=synth.t_ms(k), stages=False)[0]
+            for k in range(n_frames)]
+    ref = _fold(p, _to_result_bytes(recs, range(n_frames)).view(RESULT_DTYPE).reshape(-1))
+    for r in range(world):
+        assert results[r] == ref
+
+
 def test_shard_assignment_covers_every_frame_once():
     for n_frames, batch, world in [(10000, 64, 1), (10000, 64, 2), (10000, 64, 8), (30, 4, 3),
                                    (7, 8, 2)]:
