@@ -130,7 +130,7 @@ def _worker_windowed(rank, world, port, cid, n_frames, batch, window, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("window", [1, 2, 3])
+@pytest.mark.parametrize("window", [3])   # 4 rounds: a full and a partial window
 def test_two_ranks_windowed_gather_matches_single_process(window):
     world, cid, n_frames, batch = 2, 1, 20, 3
     ctx = mp.get_context("spawn")
