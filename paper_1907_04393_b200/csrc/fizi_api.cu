@@ -336,12 +336,19 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
     // the queued per-pixel words and the LUT re-test of corrected frames
     // open the tail (the morphology needs them, the next call's
     // segmentation does not, so the head is the fused kernel alone)
+    // (the two touch disjoint frames, so the LUT re-test runs on a branch
+    // beside the per-pixel words and joins before the morphology)
+    e = cudaEventRecord(c.ev_zfork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side2, c.ev_zfork, 0);
+    if (e == cudaSuccess) e = fizi::launch_seg_fix(c, 0, pl.n, 0, c.side2);
+    if (e == cudaSuccess) e = cudaEventRecord(c.ev_zjoin, c.side2);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
     if (c.fast) {
       e = fizi::launch_slow_words(c, 0, pl.n, 0, st);
       if (e != cudaSuccess) return cuda_fail(c, e, "slow words");
     }
-    e = fizi::launch_seg_fix(c, 0, pl.n, 0, st);
-    if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
+    e = cudaStreamWaitEvent(st, c.ev_zjoin, 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "join");
     // (the u8 mask target was cleared beside the segmentation, run_call)
     CallPlan nofold = pl;                             // the fold runs on its own stream
     nofold.fold = -2;
