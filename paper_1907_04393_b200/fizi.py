@@ -327,6 +327,15 @@ class Fizi:
         self._learned[stream] = (m.frames_learned, m.margin)
         return m
 
+    def dump_stages(self, directory, frame_no: int, frame: int = 0):
+        """Write frame `frame` of the last batch's stage masks as
+        <frame_no>_{r1,r2,r3,merged,final}.pgm (needs debug=1)."""
+        import torch
+        from .persist import DUMP_STAGES, dump_stages
+        st = {s: self.debug_stage(s, frame) for s in DUMP_STAGES}
+        torch.cuda.current_stream(self.device).synchronize()
+        return dump_stages(directory, frame_no, {s: m.cpu().numpy() for s, m in st.items()})
+
     def relearn_flags(self, results, stream: int = 0, threshold: int = 40):
         """NEXT-1: u8 flag per record, 1 iff the mean luma jumped by more than
         `threshold` since the stream's previous frame (device (n,) tensor)."""

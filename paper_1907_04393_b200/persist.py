@@ -152,3 +152,92 @@ def model_bytes(model: BackgroundModel) -> bytes:
     buf = io.BytesIO()
     save_background(buf, model)
     return buf.getvalue()
+
+
+# ---- PGM / PPM debug dumps ("Mask debug dump: binary PGM (P5),
+# 0 -> 0, 1 -> 255. Frame dump: binary PPM (P6)"; "Debug flag emits
+# per-stage masks as PGM files named <frame#>_{r1,r2,r3,merged,final}.pgm").
+
+DUMP_STAGES = ("r1", "r2", "r3", "merged", "final")
+
+
+def write_pgm(dst, mask: np.ndarray) -> None:
+    """Write an (H, W) {0,1} mask as binary PGM (P5, maxval 255): 0 -> 0, 1 -> 255."""
+    m = np.asarray(mask)
+    if m.ndim != 2:
+        raise ValueError("mask must be (H, W)")
+    if m.size and (m.min() < 0 or m.max() > 1):
+        raise ValueError("mask values must be 0 or 1")
+    body = (m.astype(np.uint8) * np.uint8(255)).tobytes()
+    f, own = _open(dst, "wb")
+    try:
+        f.write(b"P5\n%d %d\n255\n" % (m.shape[1], m.shape[0]))
+        f.write(body)
+    finally:
+        if own:
+            f.close()
+
+
+def write_ppm(dst, frame: np.ndarray) -> None:
+    """Write an (H, W, 3) u8 interleaved-RGB frame as binary PPM (P6, maxval 255)."""
+    fr = np.ascontiguousarray(frame, np.uint8)
+    if fr.ndim != 3 or fr.shape[2] != 3:
+        raise ValueError("frame must be (H, W, 3) uint8")
+    f, own = _open(dst, "wb")
+    try:
+        f.write(b"P6\n%d %d\n255\n" % (fr.shape[1], fr.shape[0]))
+        f.write(fr.tobytes())
+    finally:
+        if own:
+            f.close()
+
+
+def read_pnm(src) -> np.ndarray:
+    """Read a binary P5 / P6 file (maxval 255) written by write_pgm / write_ppm:
+    (H, W) u8 for P5, (H, W, 3) u8 for P6 (raw values, no 255 -> 1 mapping)."""
+    f, own = _open(src, "rb")
+    try:
+        data = f.read()
+    finally:
+        if own:
+            f.close()
+    toks, pos = [], 0
+    while len(toks) < 4:
+        while pos < len(data) and data[pos:pos + 1].isspace():
+            pos += 1
+        if pos < len(data) and data[pos:pos + 1] == b"#":
+            while pos < len(data) and data[pos:pos + 1] != b"\n":
+                pos += 1
+            continue
+        start = pos
+        while pos < len(data) and not data[pos:pos + 1].isspace():
+            pos += 1
+        if start == pos:
+            raise FormatError(f"truncated PNM header (at byte offset {pos})")
+        toks.append(data[start:pos])
+    pos += 1                                      # the single whitespace before the raster
+    magic = toks[0]
+    if magic not in (b"P5", b"P6"):
+        raise FormatError(f"bad magic {magic!r} at byte offset 0 (expected b'P5' or b'P6')")
+    w, h, maxval = (int(t) for t in toks[1:])
+    if maxval != 255:
+        raise FormatError(f"maxval {maxval} unsupported (expected 255)")
+    ch = 1 if magic == b"P5" else 3
+    need = w * h * ch
+    if len(data) - pos != need:
+        raise FormatError(f"raster of {len(data) - pos} bytes at byte offset {pos}, expected {need}")
+    a = np.frombuffer(data, np.uint8, need, pos)
+    return a.reshape(h, w).copy() if ch == 1 else a.reshape(h, w, 3).copy()
+
+
+def dump_stages(directory, frame_no: int, stages: dict) -> list:
+    """Write `stages` ({name: (H, W) {0,1} array}, names from DUMP_STAGES) as
+    <frame_no>_<name>.pgm under `directory`; returns the paths."""
+    os.makedirs(directory, exist_ok=True)
+    paths = []
+    for name in DUMP_STAGES:
+        if name in stages:
+            p = os.path.join(directory, f"{frame_no}_{name}.pgm")
+            write_pgm(p, np.asarray(stages[name]))
+            paths.append(p)
+    return paths

@@ -111,3 +111,79 @@ def test_device_envelope_round_trip_through_fizibg1(tmp_path):
     assert torch.equal(lo_a, lo_b) and torch.equal(hi_a, hi_b)
     a.close()
     b.close()
+
+
+# ---- PGM / PPM dumps
+from paper_1907_04393_b200.persist import (DUMP_STAGES, dump_stages, read_pnm,  # noqa: E402
+                                           write_pgm, write_ppm)
+
+# S:115 "binary PGM (P5), 0 -> 0, 1 -> 255" for the 3x2 mask [[1,0,1],[0,1,0]]
+PGM_FIXTURE = b"P5\n3 2\n255\n" + bytes([255, 0, 255, 0, 255, 0])
+# S:115 "Frame dump: binary PPM (P6)" for the 2x1 frame [(1,2,3), (4,5,6)]
+PPM_FIXTURE = b"P6\n2 1\n255\n" + bytes([1, 2, 3, 4, 5, 6])
+
+
+def test_pgm_bytes_match_the_format_text():
+    buf = io.BytesIO()
+    write_pgm(buf, np.array([[1, 0, 1], [0, 1, 0]], np.uint8))
+    assert buf.getvalue() == PGM_FIXTURE
+    assert np.array_equal(read_pnm(io.BytesIO(PGM_FIXTURE)),
+                          np.array([[255, 0, 255], [0, 255, 0]], np.uint8))
+
+
+def test_ppm_bytes_match_the_format_text():
+    buf = io.BytesIO()
+    frame = np.array([[[1, 2, 3], [4, 5, 6]]], np.uint8)
+    write_ppm(buf, frame)
+    assert buf.getvalue() == PPM_FIXTURE
+    assert np.array_equal(read_pnm(io.BytesIO(PPM_FIXTURE)), frame)
+
+
+def test_pnm_round_trip_and_errors(tmp_path):
+    rng = np.random.default_rng(7)
+    m = rng.integers(0, 2, (17, 32), dtype=np.uint8)
+    write_pgm(tmp_path / "m.pgm", m)
+    assert np.array_equal(read_pnm(tmp_path / "m.pgm") // 255, m)
+    f = rng.integers(0, 256, (5, 8, 3), dtype=np.uint8)
+    write_ppm(tmp_path / "f.ppm", f)
+    assert np.array_equal(read_pnm(tmp_path / "f.ppm"), f)
+    with pytest.raises(ValueError):
+        write_pgm(io.BytesIO(), np.array([[0, 2]], np.uint8))
+    with pytest.raises(FormatError, match="byte offset 0"):
+        read_pnm(io.BytesIO(b"P4\n2 1\n255\n\x00\x00"))
+    with pytest.raises(FormatError, match="expected 6"):
+        read_pnm(io.BytesIO(PGM_FIXTURE[:-1]))
+
+
+def test_dump_stages_names(tmp_path):
+    st = {s: np.full((2, 4), i % 2, np.uint8) for i, s in enumerate(DUMP_STAGES)}
+    paths = dump_stages(tmp_path, 42, st)
+    assert [p.rsplit("/", 1)[1] for p in paths] == [f"42_{s}.pgm" for s in
+                                                    ("r1", "r2", "r3", "merged", "final")]
+    for i, s in enumerate(DUMP_STAGES):
+        assert np.array_equal(read_pnm(tmp_path / f"42_{s}.pgm"), st[s] * 255)
+
+
+@pytest.mark.gpu
+def test_device_stage_dumps_match_oracle(tmp_path):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import oracle
+    import synth
+    from paper_1907_04393_b200 import Fizi
+    cfg = synth.CONFIGS[1]
+    learn = synth.learning_frames_host(cfg)
+    frames = synth.frames_host(cfg, 0, range(4))
+    fz = Fizi(cfg.W, cfg.H, max_batch=4, debug=1)
+    fz.learn_background(torch.from_numpy(learn).cuda(), margin=synth.MARGIN)
+    fz.process_frames(torch.from_numpy(frames).cuda(),
+                      t_ms=np.array([synth.t_ms(k) for k in range(4)], np.int64))
+    lo, hi = oracle.learn(learn, synth.MARGIN)
+    p = oracle.make_params(cfg.W, cfg.H)
+    _, st = oracle.segment(p, frames[3], lo, hi, t_ms=synth.t_ms(3))
+    fz.dump_stages(tmp_path, 3, frame=3)
+    names = {"r1": "r1", "r2": "r2", "r3": "r3", "merged": "merged", "final": "final_mask"}
+    for s, o in names.items():
+        assert np.array_equal(read_pnm(tmp_path / f"3_{s}.pgm"), st[o].astype(np.uint8) * 255), s
+    fz.close()
