@@ -221,7 +221,7 @@ typedef struct fizi_wheel {
 
 typedef struct fizi_command {      /* 32 bytes per frame                                    */
     double   steering;             /* [-1, 1], negative = left                              */
-    double   throttle;             /* [0, 1] (no slider source yet: stays 0)                */
+    double   throttle;             /* [0, 1]: last slider value (fizi_drive_throttle), 0 at start */
     int64_t  t_ms;                 /* the frame's timestamp                                 */
     uint32_t has_steering;         /* 1 iff the pointer was on the wheel in this frame      */
     uint32_t _pad;
@@ -240,6 +240,18 @@ int fizi_set_wheel(fizi_ctx *ctx, uint32_t stream, const fizi_wheel *wheel);
  * Joins outstanding pipelined tails into cuda_stream first. */
 int fizi_drive(fizi_ctx *ctx, uint32_t stream, const fizi_result *results_dev, uint32_t n,
                fizi_command *commands_dev, fizi_stream_t cuda_stream);
+
+/* As fizi_drive, with the throttle source of make_command (S:396-399:
+ * "throttle: slider value when present, else previous throttle"): events_dev
+ * (device) holds the n * n_zones events fizi_hit_test wrote for the same n
+ * records of this stream (frame-major); the slider value of frame i is
+ * events_dev[i * n_zones + slider_zone].value when that event carries
+ * FIZI_EV_VALUE, else absent.  FIZI_E_NOMODEL without a wheel or a layout;
+ * FIZI_E_ARG if n_zones is not the layout's zone count or slider_zone is not
+ * a FIZI_ZONE_SLIDER of it.  Reading L36. */
+int fizi_drive_throttle(fizi_ctx *ctx, uint32_t stream, const fizi_result *results_dev, uint32_t n,
+                        const fizi_zone_event *events_dev, uint32_t n_zones, uint32_t slider_zone,
+                        fizi_command *commands_dev, fizi_stream_t cuda_stream);
 
 /* Parity/debug: write stage `stage` of frame `frame_in_last_batch` of the last
  * fizi_process_frames / fizi_segment_frames call to out_dev (u8 per pixel;

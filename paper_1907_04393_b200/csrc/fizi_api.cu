@@ -1028,7 +1028,11 @@ int fizi_set_zones(fizi_ctx* ctx, uint32_t stream, const fizi_zone* zones, uint3
                    cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(c, e, "set_zones");
   if (c.n_zones.size() < c.n_streams) c.n_zones.assign(c.n_streams, 0);
+  if (c.slider_zones.size() < c.n_streams) c.slider_zones.assign(c.n_streams, 0);
   c.n_zones[stream] = n_zones;
+  c.slider_zones[stream] = 0;
+  for (uint32_t k = 0; k < n_zones; k++)
+    if (zones[k].kind == FIZI_ZONE_SLIDER) c.slider_zones[stream] |= 1ull << k;
   return FIZI_OK;
 }
 
@@ -1112,8 +1116,36 @@ int fizi_drive(fizi_ctx* ctx, uint32_t stream, const fizi_result* results_dev, u
   DeviceGuard guard(c.device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
   cudaError_t e = join_tail(c, st);
-  if (e == cudaSuccess) e = fizi::launch_drive(c, stream, results_dev, n, commands_dev, st);
+  if (e == cudaSuccess)
+    e = fizi::launch_drive(c, stream, results_dev, n, nullptr, 0, 0, commands_dev, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "drive");
+  return FIZI_OK;
+}
+
+int fizi_drive_throttle(fizi_ctx* ctx, uint32_t stream, const fizi_result* results_dev, uint32_t n,
+                        const fizi_zone_event* events_dev, uint32_t n_zones, uint32_t slider_zone,
+                        fizi_command* commands_dev, fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (c.has_wheel.size() <= stream || !c.has_wheel[stream])
+    return fail(c, FIZI_E_NOMODEL, "no wheel set for this stream (fizi_set_wheel)");
+  if (c.n_zones.size() <= stream || c.n_zones[stream] == 0)
+    return fail(c, FIZI_E_NOMODEL, "no layout set for this stream (fizi_set_zones)");
+  if (n_zones != c.n_zones[stream])
+    return fail(c, FIZI_E_ARG, "n_zones differs from the stream's layout");
+  if (slider_zone >= n_zones || !((c.slider_zones[stream] >> slider_zone) & 1))
+    return fail(c, FIZI_E_ARG, "slider_zone is not a slider zone of the stream's layout");
+  if (n == 0) return FIZI_OK;
+  if (!results_dev || !events_dev || !commands_dev) return fail(c, FIZI_E_ARG, "NULL pointer argument");
+  DeviceGuard guard(c.device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  cudaError_t e = join_tail(c, st);
+  if (e == cudaSuccess)
+    e = fizi::launch_drive(c, stream, results_dev, n, events_dev, n_zones, slider_zone,
+                           commands_dev, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "drive_throttle");
   return FIZI_OK;
 }
 

@@ -166,6 +166,7 @@ struct Ctx {
   std::vector<uint8_t> env_valid;
   std::vector<uint8_t> has_wheel;        // NEXT-2: fizi_set_wheel called per stream
   std::vector<uint32_t> n_zones;         // NEXT-3: zones per stream (0: no layout)
+  std::vector<uint64_t> slider_zones;    // NEXT-3: bit k set iff zone k of the stream is a slider
   std::vector<int64_t> last_t;
   std::vector<uint8_t> has_t;
   uint8_t* pinned[kSlots] = {};               // staging for the per-call upload (one per slot)
@@ -272,7 +273,8 @@ cudaError_t launch_hit_test(Ctx& c, uint32_t stream, const fizi_result* res, uin
 // NEXT-2: install a wheel (resets the drive state) / fold records into commands
 cudaError_t launch_drive_set(Ctx& c, uint32_t stream, const fizi_wheel& w, cudaStream_t st);
 cudaError_t launch_drive(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
-                         fizi_command* out, cudaStream_t st);
+                         const fizi_zone_event* ev, uint32_t nz, uint32_t zi, fizi_command* out,
+                         cudaStream_t st);
 cudaError_t launch_tstate_reset(Ctx& c, uint32_t first, uint32_t count, cudaStream_t st);
 cudaError_t launch_debug_stage(Ctx& c, int stage, uint32_t frame, void* out, cudaStream_t st);
 

@@ -298,7 +298,11 @@ __device__ __forceinline__ bool wheel_steering(const fizi_zone& z, double px, do
   return steering_from_cursor(w, true, px, py, steering);
 }
 
+// ev == nullptr: no throttle source (make_command's slider_throttle_opt is
+// always absent).  Else the slider value of frame i is ev[i * nz + zi].value
+// when that event carries FIZI_EV_VALUE (fizi_hit_test's output, L36).
 __global__ void drive_kernel(DriveState* ds, const fizi_result* __restrict__ res, uint32_t n,
+                             const fizi_zone_event* __restrict__ ev, uint32_t nz, uint32_t zi,
                              fizi_command* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   DriveState s = *ds;
@@ -315,7 +319,11 @@ __global__ void drive_kernel(DriveState* ds, const fizi_result* __restrict__ res
       if (!s.has_reading || t - s.last_reading > s.wheel.hold_ms) st = __dmul_rn(st, 0.8);
     }
     s.steering = fmin(1.0, fmax(-1.0, st));
-    s.throttle = fmin(1.0, fmax(0.0, s.throttle));       // no slider source (NEXT-3)
+    if (ev != nullptr) {
+      const fizi_zone_event& e = ev[(size_t)i * nz + zi];
+      if (e.events & FIZI_EV_VALUE) s.throttle = e.value;
+    }
+    s.throttle = fmin(1.0, fmax(0.0, s.throttle));
     fizi_command c;
     c.steering = s.steering;
     c.throttle = s.throttle;
@@ -345,8 +353,10 @@ cudaError_t launch_drive_set(Ctx& c, uint32_t stream, const fizi_wheel& w, cudaS
 }
 
 cudaError_t launch_drive(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
-                         fizi_command* out, cudaStream_t st) {
-  drive_kernel<<<1, 32, 0, st>>>(reinterpret_cast<DriveState*>(c.dstate) + stream, res, n, out);
+                         const fizi_zone_event* ev, uint32_t nz, uint32_t zi, fizi_command* out,
+                         cudaStream_t st) {
+  drive_kernel<<<1, 32, 0, st>>>(reinterpret_cast<DriveState*>(c.dstate) + stream, res, n, ev, nz,
+                                 zi, out);
   c.launches += 1;
   return cudaGetLastError();
 }

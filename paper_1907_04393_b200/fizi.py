@@ -122,12 +122,13 @@ def lib() -> ctypes.CDLL:
                                          ctypes.c_double]
         L.fizi_set_wheel.argtypes = [vp, u32, ctypes.POINTER(Wheel)]
         L.fizi_drive.argtypes = [vp, u32, vp, u32, vp, vp]
+        L.fizi_drive_throttle.argtypes = [vp, u32, vp, u32, vp, u32, u32, vp, vp]
         L.fizi_relearn_flags.argtypes = [vp, u32, vp, u32, u32, vp, vp]
         L.fizi_set_zones.argtypes = [vp, u32, vp, u32]
         L.fizi_hit_test.argtypes = [vp, u32, vp, u32, vp, vp]
         L.fizi_flush.argtypes = [vp, vp]
         for name in ("fizi_set_pipeline", "fizi_flush", "fizi_wheel_default", "fizi_set_wheel",
-                     "fizi_drive", "fizi_relearn_flags", "fizi_set_zones", "fizi_hit_test", "fizi_params_default", "fizi_create", "fizi_learn_background",
+                     "fizi_drive", "fizi_drive_throttle", "fizi_relearn_flags", "fizi_set_zones", "fizi_hit_test", "fizi_params_default", "fizi_create", "fizi_learn_background",
                      "fizi_process_frames", "fizi_segment_frames", "fizi_process_frames_host",
                      "fizi_track", "fizi_reset_tracker", "fizi_debug_stage",
                      "fizi_get_background", "fizi_set_background"):
@@ -374,15 +375,25 @@ class Fizi:
         self._check(lib().fizi_set_wheel(self._h, stream, ctypes.byref(w)), "fizi_set_wheel")
         return w
 
-    def drive(self, results, stream: int = 0, commands=None):
+    def drive(self, results, stream: int = 0, commands=None, events=None, slider_zone=None):
         """NEXT-2: fold records (device (n,128) uint8) into drive commands
-        (device (n,32) uint8 tensor of fizi_command)."""
+        (device (n,32) uint8 tensor of fizi_command).  With `events` (the
+        hit_test output for the same records) and `slider_zone`, the throttle
+        follows that slider (fizi_drive_throttle)."""
         import torch
         n = results.shape[0]
         if commands is None:
             commands = torch.empty((n, COMMAND_BYTES), dtype=torch.uint8, device=self.device)
-        self._check(lib().fizi_drive(self._h, stream, results.data_ptr(), n, commands.data_ptr(),
-                                     _stream_handle(self.device)), "fizi_drive")
+        if events is None:
+            self._check(lib().fizi_drive(self._h, stream, results.data_ptr(), n,
+                                         commands.data_ptr(), _stream_handle(self.device)),
+                        "fizi_drive")
+        else:
+            nz = events.numel() // (16 * n) if n else 0
+            self._check(lib().fizi_drive_throttle(self._h, stream, results.data_ptr(), n,
+                                                  events.data_ptr(), nz, int(slider_zone),
+                                                  commands.data_ptr(), _stream_handle(self.device)),
+                        "fizi_drive_throttle")
         return commands
 
     def set_pipeline(self, enable: bool = True):

@@ -99,3 +99,69 @@ def test_fizi_drive_matches_oracle():
         assert abs(out[i]["steering"] - c.steering) <= 1e-9, (i, out[i]["steering"], c.steering)
         assert out[i]["throttle"] == c.throttle and out[i]["t_ms"] == c.t_ms
     fz.close()
+
+
+# ---- throttle from a NEXT-3 slider zone (reading L36)
+def test_throttle_follows_slider_value_events():
+    from oracle.interface import SLIDER, VALUE, HitTest, Zone
+    slider = Zone(SLIDER, 500, 100, 40, 200)                 # value = 1 - (py - 100) / 200
+    ht = HitTest([slider])
+    d = Drive(W)
+    seq = [(True, 520.0, 140.0), (True, 520.0, 140.0), (False, 0.0, 0.0), (True, 520.0, 300.0),
+           (True, *_rim(90))]
+    want = [0.8, 0.8, 0.8, 0.0, 0.0]                          # value, unchanged, held, bottom, off
+    for k, ((vis, x, y), w) in enumerate(zip(seq, want)):
+        (_, ev, v), = ht.update(vis, False, x, y)
+        c = d.update(vis, x, y, 33 * k, v if ev & VALUE else None)
+        assert c.throttle == w, (k, c.throttle)
+    assert c.steering == 1.0 and c.has_steering                 # S:393 3 o'clock on the rim
+
+
+@pytest.mark.gpu
+def test_fizi_drive_throttle_matches_oracle():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from oracle.interface import BUTTON, SLIDER, VALUE, HitTest, Zone
+    from paper_1907_04393_b200 import RESULT_DTYPE, Fizi, FiziError, commands_numpy
+    from paper_1907_04393_b200.fizi import Zone as CZone
+    layout = [Zone(BUTTON, 20, 20, 60, 60), Zone(SLIDER, 480, 60, 80, 360)]
+    rng = np.random.default_rng(11)
+    n = 300
+    rec = np.zeros(n, RESULT_DTYPE)
+    t = np.cumsum(rng.integers(20, 60, n)).astype(np.int64)
+    vis = rng.random(n) < 0.85
+    px = np.clip(np.cumsum(rng.normal(0, 30, n)) + 450, 0, 639)
+    py = np.clip(np.cumsum(rng.normal(0, 30, n)) + 240, 0, 479)
+    rec["t_ms"], rec["visible"], rec["px"], rec["py"] = t, vis, px, py
+    fz = Fizi(640, 480, max_batch=16)
+    cz = []
+    for z in layout:
+        c = CZone()
+        c.kind, c.x, c.y, c.w, c.h = z.kind, z.x, z.y, z.w, z.h
+        cz.append(c)
+    fz.set_zones(cz)
+    fz.set_wheel(W.cx, W.cy, W.radius, theta_max_deg=W.theta_max, hold_ms=W.hold_ms)
+    dev = torch.from_numpy(rec.view(np.uint8).reshape(n, 128).copy()).cuda()
+    ev0 = fz.hit_test(dev[:1])
+    with pytest.raises(FiziError):
+        fz.drive(dev[:1], events=ev0, slider_zone=0)          # zone 0 is a button
+    fz.set_zones(cz)                                           # reset the hit state
+    fz.set_wheel(W.cx, W.cy, W.radius, theta_max_deg=W.theta_max, hold_ms=W.hold_ms)
+    out = []
+    for i in range(0, n, 64):
+        ev = fz.hit_test(dev[i:i + 64])
+        out.append(commands_numpy(fz.drive(dev[i:i + 64], events=ev, slider_zone=1)))
+    out = np.concatenate(out)
+    ht, d = HitTest(layout), Drive(W)
+    moved = 0
+    for i in range(n):
+        _, (_, ev, v) = ht.update(bool(vis[i]), False, float(px[i]), float(py[i]))
+        c = d.update(bool(vis[i]), float(px[i]), float(py[i]), int(t[i]),
+                     v if ev & VALUE else None)
+        moved += bool(ev & VALUE)
+        assert abs(out[i]["steering"] - c.steering) <= 1e-9, i
+        assert abs(out[i]["throttle"] - c.throttle) <= 1e-9, (i, out[i]["throttle"], c.throttle)
+        assert bool(out[i]["has_steering"]) == c.has_steering and out[i]["t_ms"] == c.t_ms
+    assert moved > 5
+    fz.close()
