@@ -240,12 +240,28 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
 
     B = args.batch or cfg.batch
+    S = cfg.streams
+    if S > 1 and sharded:
+        raise SystemExit("bench: the multi-stream config (C5) is measured at N = 1 only")
     from paper_1907_04393_b200 import shard
     # round r: rank takes batch r*world + rank (weak scaling, B frames per rank
     # per step); the resident rounds are cycled if warmup + steps exceeds them
     need = min(shard.n_rounds(cfg.n_proc, B, world), args.warmup + args.steps)
     frames_by_round = []
-    for rnd in range(need):
+    if S > 1:
+        # C5: round r = frame k = r // G of the streams of group g = r % G
+        # (G groups of B consecutive streams): every call holds B streams,
+        # one frame each, with per-stream envelopes and per-stream folds
+        G5 = -(-S // B)
+        need = min(G5 * cfg.n_proc, args.warmup + args.steps)
+    for rnd in range(need if S > 1 else 0):
+        g, k = rnd % G5, rnd // G5
+        sids = list(range(g * B, min(S, (g + 1) * B)))
+        fr = torch.empty((len(sids), cfg.H, cfg.W, 3), dtype=torch.uint8, device=dev)
+        for j, sid in enumerate(sids):
+            synth.frames_dev(cfg, sid, [k], out=fr[j:j + 1], device=dev)
+        frames_by_round.append((sids, fr, np.full(len(sids), synth.t_ms(k), np.int64)))
+    for rnd in range(need if S == 1 else 0):
         b = shard.round_batch(cfg.n_proc, B, world, rank, rnd)
         if b is None:
             frames_by_round.append(None)
@@ -259,10 +275,10 @@ def main():
         else:
             fr = synth.frames_dev(cfg, 0, ks, device=dev)
         frames_by_round.append((ks, fr, t_base))
-    learn = synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True, device=dev)
-
-    fz = Fizi(cfg.W, cfg.H, n_streams=1, max_batch=B, device=local)
-    fz.learn_background(learn, margin=synth.MARGIN)
+    fz = Fizi(cfg.W, cfg.H, n_streams=S, max_batch=B, device=local)
+    for sid in range(S):
+        learn = synth.frames_dev(cfg, sid, range(cfg.n_learn), learning=True, device=dev)
+        fz.learn_background(learn, stream=sid, margin=synth.MARGIN)
     # N = 1: pipelined calls (a call's tail overlaps the next calls'
     # segmentation), so outputs rotate over three buffers and the timed
     # region ends with fz.flush() (N > 1: segment_frames, windowed gather + fold)
@@ -289,7 +305,7 @@ def main():
         ks, fr, t_base = item
         n = len(ks)
         views.append((n, fr[:n], [None if args.diag_no_masks else m[:n] for m in masks2],
-                      [r[:n] for r in res2], t_base))
+                      [r[:n] for r in res2], t_base, np.asarray(ks, np.uint32) if S > 1 else None))
     t_pass = synth.t_ms(cfg.n_proc)
 
     def step(i):
@@ -297,12 +313,12 @@ def main():
         v = views[rnd]
         n = 0
         if v is not None:
-            n, fr_n, mks, ress, t_base = v
+            n, fr_n, mks, ress, t_base, sids = v
             mk, res_n = mks[i % NBUF], ress[i % NBUF]
             # timestamps keep increasing across passes over the resident rounds
             t = t_base + (i // need) * t_pass
             if not sharded:            # the whole path in one call (fold fused into labelling)
-                fz.process_frames(fr_n, t_ms=t, masks=mk, results=res_n)
+                fz.process_frames(fr_n, streams=sids, t_ms=t, masks=mk, results=res_n)
                 return n
             fz.segment_frames(fr_n, t_ms=t, masks=mk, results=resw[len(window)][:n])
         window.append(rnd)
@@ -401,10 +417,10 @@ def main():
     # read (3N each), the stream's envelope once (6N), B bit masks written
     # (N/8 each); a step may issue several launches (sub-batches), so the
     # achieved rate is total algorithmic bytes / total kernel time
-    seg_bytes = B * (3 * N + N / 8) + 6 * N
+    seg_bytes = B * (3 * N + N / 8) + 6 * N * min(S, B)   # C5: one envelope per frame
     launches_per_step = seg_n / max(args.steps, 1)
     seg_gbs = seg_bytes * args.steps / (seg_ms / 1e3) / 1e9 if seg_n else None
-    step_bytes = B * (3 * N + N) + 6 * N       # whole-path algorithmic bytes per step
+    step_bytes = B * (3 * N + N) + 6 * N * min(S, B)   # whole-path algorithmic bytes per step
     step_ms = ms_max / args.steps
     traffic, traffic_src = ncu_traffic(seg_bytes) if launches_per_step == 1 else (None, None)
     roofline = {
@@ -434,11 +450,18 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
         "host_enqueue_ms_per_step": host_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"C{cfg.cid}: {cfg.W}x{cfg.H} stream, {cfg.n_proc} frames, "
-                               f"batches of {B} per launch (BASELINE.json configs[{cfg.cid - 1}])",
+        "config": {"workload": (f"C{cfg.cid}: {cfg.W}x{cfg.H} stream, {cfg.n_proc} frames, "
+                                f"batches of {B} per launch (BASELINE.json configs[{cfg.cid - 1}])"
+                                if S == 1 else
+                                f"C{cfg.cid}: {S} streams of {cfg.W}x{cfg.H}, {cfg.n_proc} frames "
+                                f"each, per-stream envelopes; batches of one frame from each of "
+                                f"{B} streams (BASELINE.json configs[{cfg.cid - 1}])"),
                    "frames_per_step_per_gpu": B, "pipelined_calls": pipelined,
                    "sharded_path": sharded, "resident_batches_per_gpu": need,
-                   "l2": f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step",
+                   "l2": (f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step"
+                          if B * 3 * N > 126e6 else
+                          f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step, "
+                          f"cycled over {need} resident batches ({need * B * 3 * N / 1e9:.1f} GB)"),
                    "parallelism": f"frames sharded by batch, dp{world}"},
         "gpu_launches": launches,
         "roofline": roofline,
@@ -446,7 +469,7 @@ def main():
     }
 
     # --------------------------------------------------------------- e2e
-    if not args.no_e2e:
+    if not args.no_e2e and S == 1:
         k2 = args.e2e_steps or min(args.steps, 40)
         fe = Fizi(cfg.W, cfg.H, n_streams=1, max_batch=B, device=local)
         learn = synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True, device=dev)
@@ -490,7 +513,7 @@ def main():
                       "steps": k2, "api": "fizi_process_frames_host (pinned host buffers)"}
         fe.close()
 
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and S == 1:
         out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample_frames)
     if rank == 0:
         print(json.dumps(out), flush=True)
