@@ -796,10 +796,13 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
 cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st) {
   SegArgs a = seg_args(c, f0, n, 0, sub);
   prof_begin(c, st);
-#ifdef FIZI_SLOW_TABLE
-  slow_words_kernel<false><<<c.sms * 8, 256, 0, st>>>(a);   // A/B build: colour-table test
+  // colour-table test by default: the ALU test keeps the ALU pipe 83 % busy
+  // on C4 (profiles/r01_slow_words_c4_ncu.txt); the table is 223 vs 290 us
+  // per C4 call and 19 vs 21 us per C3 call (gpurun_out A/B)
+#ifdef FIZI_SLOW_ALU
+  slow_words_kernel<true><<<c.sms * 8, 256, 0, st>>>(a);    // A/B build: arithmetic test
 #else
-  slow_words_kernel<true><<<c.sms * 8, 256, 0, st>>>(a);
+  slow_words_kernel<false><<<c.sms * 8, 256, 0, st>>>(a);
 #endif
   prof_end(c, FIZI_PROF_SLOW, st);
   c.launches += 1;
