@@ -527,8 +527,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
 // per byte and R2 & R3 through the colour table.  Words of frames that get
 // the LUT re-test are skipped (that kernel rewrites the whole frame).
 // Grid-stride over the queue, foreground counts aggregated per frame.
+#ifndef FIZI_SLOW_MINB
+#define FIZI_SLOW_MINB 1
+#endif
 template <bool kAluSkin>
-__global__ void __launch_bounds__(256) slow_words_kernel(SegArgs a) {
+__global__ void __launch_bounds__(256, FIZI_SLOW_MINB) slow_words_kernel(SegArgs a) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) tl_mark(a.call, kTlSlow, 0);
   struct TlEnd {
