@@ -239,8 +239,10 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=dev)
 
-    B = args.batch or cfg.batch
     S = cfg.streams
+    # C5: each call takes the current frame of every stream (256 per call;
+    # 32 per call is 1.9x slower: scripts/gpu_c5_batch.sh)
+    B = args.batch or (S if S > 1 else cfg.batch)
     if S > 1 and sharded:
         raise SystemExit("bench: the multi-stream config (C5) is measured at N = 1 only")
     from paper_1907_04393_b200 import shard

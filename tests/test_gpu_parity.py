@@ -301,6 +301,39 @@ def test_config5_multi_stream_batch():
     fz.close()
 
 
+def test_config5_all_streams_one_call_sampled():
+    """bench.py's C5 launch configuration: one call holds the current frame of
+    all 256 streams (device-learned per-stream envelopes, device-generated
+    frames); 12 sampled streams are checked against the oracle (envelope,
+    record with the fold, final mask)."""
+    cfg = synth.CONFIGS[5]
+    S = cfg.streams
+    fz = _ctx(cfg.W, cfg.H, n_streams=S, max_batch=S)
+    for s in range(S):
+        fz.learn_background(synth.frames_dev(cfg, s, range(cfg.n_learn), learning=True,
+                                             device=DEV), stream=s, margin=synth.MARGIN)
+    k = 7
+    fr = torch.empty((S, cfg.H, cfg.W, 3), dtype=torch.uint8, device=DEV)
+    for s in range(S):
+        synth.frames_dev(cfg, s, [k], out=fr[s:s + 1], device=DEV)
+    t = np.full(S, synth.t_ms(k), np.int64)
+    masks, res = fz.process_frames(fr, streams=np.arange(S, dtype=np.uint32), t_ms=t)
+    res = results_numpy(res)
+    p = oracle.make_params(cfg.W, cfg.H)
+    for s in [0, 1, 31, 32, 63, 64, 100, 127, 128, 200, 254, 255]:
+        lo, hi = oracle.learn(synth.learning_frames_host(cfg, s), synth.MARGIN)
+        glo, ghi = fz.get_background(s)
+        assert np.array_equal(glo.cpu().numpy(), lo) and np.array_equal(ghi.cpu().numpy(), hi), s
+        frame = synth.frames_host(cfg, s, [k])[0]
+        assert np.array_equal(fr[s].cpu().numpy(), frame), s
+        rec, st = oracle.segment(p, frame, lo, hi, t_ms=int(t[s]))
+        oracle.Tracker(p).update(rec)
+        compare_record(res[s], rec, s, track=True)
+        assert int(res[s]["stream"]) == s
+        assert np.array_equal(masks[s].cpu().numpy(), st["final_mask"]), s
+    fz.close()
+
+
 # ------------------------------------------------------------ invariances
 def test_batch_size_invariance_and_sharded_track():
     cfg = synth.CONFIGS[3]
