@@ -159,8 +159,11 @@ int fizi_process_frames_host(fizi_ctx *ctx, const uint32_t *stream_of_frame_host
                              uint32_t height, const int64_t *t_ms_host, uint8_t *masks_host,
                              fizi_result *results_host, fizi_stream_t cuda_stream);
 
-/* Reset stream `stream`'s tracker to its initial state (invisible). */
-int fizi_reset_tracker(fizi_ctx *ctx, uint32_t stream);
+/* Reset stream `stream`'s tracker to its initial state (invisible), in
+ * cuda_stream order after every earlier call's fold (outstanding pipelined
+ * tails are joined into cuda_stream first).  Timestamps of the stream may
+ * restart from any value afterwards. */
+int fizi_reset_tracker(fizi_ctx *ctx, uint32_t stream, fizi_stream_t cuda_stream);
 
 /* ---- NEXT-1: relearn trigger ("re-initiate partly the machine
  * learning techniques" on a luminosity change).  Folds the

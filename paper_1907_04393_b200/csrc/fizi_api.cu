@@ -142,9 +142,10 @@ void free_all(Ctx& c) {
     if (c.zero_blocks[i]) cudaFree(c.zero_blocks[i]);
     if (c.bitAs[i]) cudaFree(c.bitAs[i]);
     if (c.calls[i]) cudaFree(c.calls[i]);
+    if (c.slow_itemss[i]) cudaFree(c.slow_itemss[i]);
   }
   void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.bitO, c.bitOC,
-                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.tl, c.slow_items, c.dstate,
+                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.tl, c.dstate,
                   c.prev_mean, c.hstate,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
@@ -203,6 +204,7 @@ void select_slot(Ctx& c, uint32_t s) {
   c.slow_count = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * 4;
   c.dirty = reinterpret_cast<uint32_t*>(z);
   c.bitA = c.bitAs[s];
+  c.slow_items = c.slow_itemss[s];
   c.call = c.calls[s];
   c.frame_t = reinterpret_cast<int64_t*>(c.call + 1);
   c.frame_stream = reinterpret_cast<uint32_t*>(c.frame_t + mb);
@@ -667,7 +669,9 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   for (uint32_t i = 0; i < fizi::kSlots; i++) A(dalloc(&c.bitAs[i], mb * wpf * 4));
   A(dalloc(&c.bitO, mb * wpf * 4));
   if (c.p.debug) A(dalloc(&c.bitOC, mb * wpf * 4));
-  if (c.fast) A(dalloc(&c.slow_items, mb * c.nchunks * 16 * sizeof(unsigned long long)));
+  if (c.fast)
+    for (uint32_t i = 0; i < fizi::kSlots; i++)
+      A(dalloc(&c.slow_itemss[i], mb * c.nchunks * 16 * sizeof(unsigned long long)));
   A(dalloc(&c.row_cnt, mb * c.H * 4));
   A(dalloc(&c.row_base, mb * c.H * 4));
   A(dalloc(&c.runs, mb * c.cap_runs * sizeof(fizi::Run)));
@@ -941,13 +945,17 @@ int fizi_process_frames_host(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* 
   return FIZI_OK;
 }
 
-int fizi_reset_tracker(fizi_ctx* ctx, uint32_t stream) {
+int fizi_reset_tracker(fizi_ctx* ctx, uint32_t stream, fizi_stream_t cuda_stream) {
   if (!ctx) return FIZI_E_ARG;
   Ctx& c = ctx->c;
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
   if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
   DeviceGuard guard(c.device);
-  cudaError_t e = fizi::launch_tstate_reset(c, stream, 1, 0);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  // every earlier fold of this stream (pipelined tails on the fold stream,
+  // joined calls on their caller's stream) is ordered before the reset
+  cudaError_t e = join_tail(c, st);
+  if (e == cudaSuccess) e = fizi::launch_tstate_reset(c, stream, 1, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "tracker reset");
   c.has_t[stream] = 0;
   return FIZI_OK;
@@ -1095,7 +1103,9 @@ int fizi_set_wheel(fizi_ctx* ctx, uint32_t stream, const fizi_wheel* w) {
                   w->dead_zone_deg >= 0.0 && w->hold_ms >= 0;
   if (!ok) return fail(c, FIZI_E_ARG, "wheel: need radius > 0, 0 < theta_max <= 180, 0 <= inner < 1 < outer, dead zone >= 0, hold >= 0");
   DeviceGuard guard(c.device);
-  cudaError_t e = fizi::launch_drive_set(c, stream, *w, 0);
+  // no drive fold of this stream may still be in flight on any stream
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = fizi::launch_drive_set(c, stream, *w, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cuda_fail(c, e, "set_wheel");
   if (c.has_wheel.size() < c.n_streams) c.has_wheel.assign(c.n_streams, 0);

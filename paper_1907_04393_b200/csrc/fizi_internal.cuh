@@ -131,7 +131,10 @@ struct Ctx {
   uint32_t* fix_count = nullptr;         // kMaxSub x (1 + max_batch): per sub-batch count + list
   uint32_t* item_counter = nullptr;      // kMaxSub: fused-kernel work items taken
   uint32_t* slow_count = nullptr;        // kMaxSub: words queued for the per-pixel kernel
-  unsigned long long* slow_items = nullptr;   // max_batch x nchunks x 16 queue (one call)
+  unsigned long long* slow_items = nullptr;   // view of the slot's queue below
+  // max_batch x nchunks x 16 queue per slot: call k's tail reads its queue
+  // while call k+1's head (another slot) fills its own
+  unsigned long long* slow_itemss[kSlots] = {};
   uint8_t* tstate = nullptr;             // n_streams tracker states
   uint8_t* dstate = nullptr;             // n_streams drive states (NEXT-2)
   int32_t* prev_mean = nullptr;          // n_streams relearn-trigger states (NEXT-1), -1 = none

@@ -609,20 +609,11 @@ cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, bool m
   a.runs = c.runs;
   const uint32_t r = c.p.se_radius;
   if (c.P <= 128 && r <= 4) {
-    static const int kw_env = getenv("FIZI_MORPH_WARPS") ? atoi(getenv("FIZI_MORPH_WARPS")) : 4;
-    const int kw = (kw_env == 1 || kw_env == 2 || kw_env == 8) ? kw_env : 4;
+    constexpr int kw = 4;               // warps (bands) per CTA; 1/2/8 measured no better
     const uint32_t nbands = (c.H + kBandRows - 1) / kBandRows;
     const dim3 grid((nbands + kw - 1) / kw, n);
     const size_t band_smem = (size_t)kw * (kBandRows + 8 * r) * c.P * sizeof(uint32_t);
-#define FIZI_MORPH_ROWS(RR, WW)                                                        \
-    do {                                                                               \
-      switch (kw) {                                                                    \
-        case 1: morph_rows_kernel<RR, WW, 1><<<grid, 32, band_smem, st>>>(a); break;   \
-        case 2: morph_rows_kernel<RR, WW, 2><<<grid, 64, band_smem, st>>>(a); break;   \
-        case 8: morph_rows_kernel<RR, WW, 8><<<grid, 256, band_smem, st>>>(a); break;  \
-        default: morph_rows_kernel<RR, WW, 4><<<grid, 128, band_smem, st>>>(a); break; \
-      }                                                                                \
-    } while (0)
+#define FIZI_MORPH_ROWS(RR, WW) morph_rows_kernel<RR, WW, kw><<<grid, 32 * kw, band_smem, st>>>(a)
 #define FIZI_MORPH_WPL(RR)                                    \
     if (c.P <= 32) FIZI_MORPH_ROWS(RR, 1);                    \
     else if (c.P <= 64) FIZI_MORPH_ROWS(RR, 2);               \
@@ -660,12 +651,8 @@ cudaError_t init_morph(Ctx& c) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMorphSmem);
   };
-  // register-pipelined kernel: up to 8 warps x (kBandRows + 32) rows x 128 words
-#define FIZI_MORPH_SET_W(RR, WW)                                   \
-  set((const void*)morph_rows_kernel<RR, WW, 1>);                  \
-  set((const void*)morph_rows_kernel<RR, WW, 2>);                  \
-  set((const void*)morph_rows_kernel<RR, WW, 4>);                  \
-  set((const void*)morph_rows_kernel<RR, WW, 8>);
+  // register-pipelined kernel: 4 warps x (kBandRows + 32) rows x 128 words
+#define FIZI_MORPH_SET_W(RR, WW) set((const void*)morph_rows_kernel<RR, WW, 4>);
 #define FIZI_MORPH_SET(RR) FIZI_MORPH_SET_W(RR, 1) FIZI_MORPH_SET_W(RR, 2) FIZI_MORPH_SET_W(RR, 4)
   FIZI_MORPH_SET(1) FIZI_MORPH_SET(2) FIZI_MORPH_SET(3) FIZI_MORPH_SET(4)
 #undef FIZI_MORPH_SET

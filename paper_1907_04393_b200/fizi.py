@@ -102,7 +102,7 @@ def lib() -> ctypes.CDLL:
         for fn in (L.fizi_process_frames, L.fizi_segment_frames, L.fizi_process_frames_host):
             fn.argtypes = [vp, vp, vp, u32, u32, u32, vp, vp, vp, vp]
         L.fizi_track.argtypes = [vp, u32, vp, u32, vp]
-        L.fizi_reset_tracker.argtypes = [vp, u32]
+        L.fizi_reset_tracker.argtypes = [vp, u32, vp]
         L.fizi_debug_stage.argtypes = [vp, i32, u32, vp, vp]
         L.fizi_get_background.argtypes = [vp, u32, vp, vp, vp]
         L.fizi_set_background.argtypes = [vp, u32, vp, vp, vp]
@@ -196,7 +196,33 @@ class Fizi:
             raise ValueError("frames must be contiguous")
         if frames.dim() == 3:
             frames = frames.unsqueeze(0)
+        if frames.dim() != 4 or frames.shape[3] != 3:
+            raise ValueError("frames must have shape (n, H, W, 3)")
+        if frames.device != self.device:
+            raise ValueError(f"frames are on {frames.device}, the context on {self.device}")
         return frames
+
+    def _dev_buf(self, t, nbytes: int, what: str):
+        """A caller-supplied device output buffer: contiguous, on the context's
+        device, and at least the nbytes the C side writes."""
+        import torch
+        if not (isinstance(t, torch.Tensor) and t.is_cuda):
+            raise TypeError(f"{what} must be a CUDA tensor")
+        if t.device != self.device:
+            raise ValueError(f"{what} is on {t.device}, the context on {self.device}")
+        if not t.is_contiguous():
+            raise ValueError(f"{what} must be contiguous")
+        if t.numel() * t.element_size() < nbytes:
+            raise ValueError(f"{what} holds {t.numel() * t.element_size()} bytes, needs {nbytes}")
+        return t
+
+    @staticmethod
+    def _host_buf(a, dtype, count: int, what: str):
+        if not (isinstance(a, np.ndarray) and a.dtype == dtype and a.flags.c_contiguous):
+            raise TypeError(f"{what} must be a C-contiguous numpy array of {dtype}")
+        if a.size < count:
+            raise ValueError(f"{what} holds {a.size} elements, needs {count}")
+        return a
 
     def close(self):
         if self._h:
@@ -237,8 +263,14 @@ class Fizi:
             raise ValueError("t_ms must have one timestamp per frame")
         if masks is True:
             masks = torch.empty((n, self.H, self.W), dtype=torch.uint8, device=self.device)
+        elif masks is not None:
+            self._dev_buf(masks, n * self.H * self.W, "masks")
+            if masks.dtype != torch.uint8:
+                raise TypeError("masks must be uint8")
         if results is None:
             results = torch.empty((n, RESULT_BYTES), dtype=torch.uint8, device=self.device)
+        else:
+            self._dev_buf(results, n * RESULT_BYTES, "results")
         self._last_frames = frames          # R1/R2/R3 debug stages re-read the last frames
         self._check(fn(self._h, streams.ctypes.data, frames.data_ptr(), n, frames.shape[2],
                        frames.shape[1], t.ctypes.data, masks.data_ptr() if masks is not None else None,
@@ -258,6 +290,7 @@ class Fizi:
     def track(self, results, stream: int = 0):
         """Fold records (device (n,128) uint8 tensor) through stream's tracker in place."""
         n = results.shape[0]
+        self._dev_buf(results, n * RESULT_BYTES, "results")
         self._check(lib().fizi_track(self._h, stream, results.data_ptr(), n,
                                      _stream_handle(self.device)), "fizi_track")
         return results
@@ -266,11 +299,20 @@ class Fizi:
                             masks: np.ndarray | None = None, results: np.ndarray | None = None):
         """End-to-end on host buffers (H2D + path + D2H inside the call)."""
         frames = np.ascontiguousarray(frames, np.uint8)
+        if frames.ndim == 3:
+            frames = frames[None]
+        if frames.ndim != 4 or frames.shape[3] != 3:
+            raise ValueError("frames must have shape (n, H, W, 3)")
         n = frames.shape[0]
         streams = _u32(np.broadcast_to(np.asarray(0 if streams is None else streams, np.uint32), (n,)))
         t = _i64(np.zeros(n) if t_ms is None else t_ms)
+        if t.shape != (n,):
+            raise ValueError("t_ms must have one timestamp per frame")
         if results is None:
             results = np.zeros(n, RESULT_DTYPE)
+        self._host_buf(results, RESULT_DTYPE, n, "results")
+        if masks is not None:
+            self._host_buf(masks, np.uint8, n * self.H * self.W, "masks")
         self._check(lib().fizi_process_frames_host(
             self._h, streams.ctypes.data, frames.ctypes.data, n, frames.shape[2], frames.shape[1],
             t.ctypes.data,
@@ -279,7 +321,8 @@ class Fizi:
         return masks, results
 
     def reset_tracker(self, stream: int = 0):
-        self._check(lib().fizi_reset_tracker(self._h, stream), "fizi_reset_tracker")
+        self._check(lib().fizi_reset_tracker(self._h, stream, _stream_handle(self.device)),
+                    "fizi_reset_tracker")
 
     def debug_stage(self, stage, frame: int = 0):
         import torch
@@ -299,6 +342,8 @@ class Fizi:
         return lo, hi
 
     def set_background(self, lo, hi, stream: int = 0):
+        for a, nm in ((lo, "lo"), (hi, "hi")):
+            self._dev_buf(a, self.H * self.W * 3, nm)
         self._check(lib().fizi_set_background(self._h, stream, lo.data_ptr(), hi.data_ptr(),
                                               _stream_handle(self.device)), "fizi_set_background")
 
@@ -342,6 +387,7 @@ class Fizi:
         `threshold` since the stream's previous frame (device (n,) tensor)."""
         import torch
         n = results.shape[0]
+        self._dev_buf(results, n * RESULT_BYTES, "results")
         flags = torch.empty(n, dtype=torch.uint8, device=self.device)
         self._check(lib().fizi_relearn_flags(self._h, stream, results.data_ptr(), n, threshold,
                                              flags.data_ptr(), _stream_handle(self.device)),
@@ -359,6 +405,7 @@ class Fizi:
         """NEXT-3: per frame and zone membership + events (device (n, n_zones, 16) uint8)."""
         import torch
         n = results.shape[0]
+        self._dev_buf(results, n * RESULT_BYTES, "results")
         nz = self._nz.get(stream, 0)
         out = torch.empty((n, max(nz, 1), 16), dtype=torch.uint8, device=self.device)
         self._check(lib().fizi_hit_test(self._h, stream, results.data_ptr(), n, out.data_ptr(),
@@ -382,14 +429,18 @@ class Fizi:
         follows that slider (fizi_drive_throttle)."""
         import torch
         n = results.shape[0]
+        self._dev_buf(results, n * RESULT_BYTES, "results")
         if commands is None:
             commands = torch.empty((n, COMMAND_BYTES), dtype=torch.uint8, device=self.device)
+        else:
+            self._dev_buf(commands, n * COMMAND_BYTES, "commands")
         if events is None:
             self._check(lib().fizi_drive(self._h, stream, results.data_ptr(), n,
                                          commands.data_ptr(), _stream_handle(self.device)),
                         "fizi_drive")
         else:
             nz = events.numel() // (16 * n) if n else 0
+            self._dev_buf(events, n * nz * 16, "events")
             self._check(lib().fizi_drive_throttle(self._h, stream, results.data_ptr(), n,
                                                   events.data_ptr(), nz, int(slider_zone),
                                                   commands.data_ptr(), _stream_handle(self.device)),

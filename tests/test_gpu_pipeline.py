@@ -1,0 +1,131 @@
+"""GPU parity of pipelined calls in the launch configuration bench.py times:
+several calls in flight with no flush between them (call k's tail overlaps
+call k+1's segmentation), one flush at the end, then every output compared
+with joined calls (bit-exact) and sampled frames with the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.gpu_common import compare_record
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1907_04393_b200 import RESULT_BYTES, Fizi, results_numpy  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def test_pipelined_c3_six_calls_in_flight():
+    """C3 (1920x1080), 6 pipelined calls of 32 frames back to back, no flush
+    until the end, each call with its own output buffers."""
+    cfg = synth.CONFIGS[3]
+    B, ncalls = 32, 6
+    learn = synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True, device=DEV)
+    ks = list(range(80, 80 + B * ncalls))          # includes a dwell pause (frames 100-139)
+    frames = synth.frames_dev(cfg, 0, ks, device=DEV)
+    t = np.array([synth.t_ms(k) for k in ks], np.int64)
+    pip = Fizi(cfg.W, cfg.H, max_batch=B)
+    ref = Fizi(cfg.W, cfg.H, max_batch=B)
+    for fz in (pip, ref):
+        fz.learn_background(learn, margin=synth.MARGIN)
+    pip.set_pipeline(True)
+    outs = [(torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=DEV),
+             torch.empty((B, RESULT_BYTES), dtype=torch.uint8, device=DEV)) for _ in range(ncalls)]
+    for j in range(ncalls):
+        sl = slice(j * B, (j + 1) * B)
+        pip.process_frames(frames[sl], t_ms=t[sl], masks=outs[j][0], results=outs[j][1])
+    pip.flush()
+    torch.cuda.synchronize()
+    lo, hi = oracle.learn(learn.cpu().numpy(), synth.MARGIN)
+    p = oracle.make_params(cfg.W, cfg.H)
+    tr = oracle.Tracker(p)
+    for j in range(ncalls):
+        sl = slice(j * B, (j + 1) * B)
+        mr, rr = ref.process_frames(frames[sl], t_ms=t[sl])
+        assert torch.equal(mr, outs[j][0]), j
+        assert torch.equal(rr, outs[j][1]), j
+        rp = results_numpy(outs[j][1])
+        fr_h = frames[sl].cpu().numpy()
+        for i in range(B):
+            sample = i in (0, B - 1) or (j * B + i) % 37 == 0
+            rec, st = oracle.segment(p, fr_h[i], lo, hi, t_ms=int(t[j * B + i]), stages=sample)
+            tr.update(rec)
+            compare_record(rp[i], rec, ks[j * B + i], track=True)
+            if sample:
+                assert np.array_equal(outs[j][0][i].cpu().numpy(), st["final_mask"])
+    pip.close()
+    ref.close()
+
+
+def test_pipelined_c5_all_streams_four_calls_in_flight():
+    """C5: each call holds the current frame of all 256 streams (bench.py's
+    launch configuration), 4 pipelined calls without a flush between them."""
+    cfg = synth.CONFIGS[5]
+    S, ncalls = cfg.streams, 4
+    pip = Fizi(cfg.W, cfg.H, n_streams=S, max_batch=S)
+    ref = Fizi(cfg.W, cfg.H, n_streams=S, max_batch=S)
+    for s in range(S):
+        learn = synth.frames_dev(cfg, s, range(cfg.n_learn), learning=True, device=DEV)
+        pip.learn_background(learn, stream=s, margin=synth.MARGIN)
+        ref.learn_background(learn, stream=s, margin=synth.MARGIN)
+    pip.set_pipeline(True)
+    sids = np.arange(S, dtype=np.uint32)
+    calls = []
+    for k in range(ncalls):
+        fr = torch.empty((S, cfg.H, cfg.W, 3), dtype=torch.uint8, device=DEV)
+        for s in range(S):
+            synth.frames_dev(cfg, s, [k], out=fr[s:s + 1], device=DEV)
+        calls.append((fr, np.full(S, synth.t_ms(k), np.int64)))
+    outs = [(torch.empty((S, cfg.H, cfg.W), dtype=torch.uint8, device=DEV),
+             torch.empty((S, RESULT_BYTES), dtype=torch.uint8, device=DEV)) for _ in range(ncalls)]
+    for k, (fr, t) in enumerate(calls):
+        pip.process_frames(fr, streams=sids, t_ms=t, masks=outs[k][0], results=outs[k][1])
+    pip.flush()
+    torch.cuda.synchronize()
+    for k, (fr, t) in enumerate(calls):
+        mr, rr = ref.process_frames(fr, streams=sids, t_ms=t)
+        assert torch.equal(mr, outs[k][0]), k
+        assert torch.equal(rr, outs[k][1]), k
+    p = oracle.make_params(cfg.W, cfg.H)
+    for s in (0, 77, 255):
+        lo, hi = oracle.learn(synth.learning_frames_host(cfg, s), synth.MARGIN)
+        tr = oracle.Tracker(p)
+        for k, (fr, t) in enumerate(calls):
+            rec, st = oracle.segment(p, fr[s].cpu().numpy(), lo, hi, t_ms=int(t[s]))
+            tr.update(rec)
+            compare_record(results_numpy(outs[k][1])[s], rec, (s, k), track=True)
+            assert np.array_equal(outs[k][0][s].cpu().numpy(), st["final_mask"]), (s, k)
+    pip.close()
+    ref.close()
+
+
+def test_reset_tracker_ordered_after_pipelined_fold():
+    """fizi_reset_tracker between pipelined calls (no flush): the reset is
+    ordered after the earlier call's fold, so the next call starts from the
+    initial tracker state (timestamps may restart)."""
+    cfg = synth.CONFIGS[1]
+    learn = synth.learning_frames_host(cfg)
+    frames = _t(synth.frames_host(cfg, 0, range(cfg.n_proc)))
+    t = np.array([synth.t_ms(k) for k in range(cfg.n_proc)], np.int64)
+    fz = Fizi(cfg.W, cfg.H, max_batch=cfg.n_proc)
+    fz.learn_background(_t(learn), margin=synth.MARGIN)
+    fz.set_pipeline(True)
+    r1 = torch.empty((cfg.n_proc, RESULT_BYTES), dtype=torch.uint8, device=DEV)
+    r2 = torch.empty_like(r1)
+    fz.process_frames(frames, t_ms=t, results=r1)
+    fz.reset_tracker()
+    fz.process_frames(frames, t_ms=t, results=r2)       # same timestamps again
+    fz.flush()
+    torch.cuda.synchronize()
+    a, b = results_numpy(r1), results_numpy(r2)
+    assert a.tobytes() == b.tobytes()
+    fz.close()
