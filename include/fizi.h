@@ -263,6 +263,14 @@ int fizi_drive_throttle(fizi_ctx *ctx, uint32_t stream, const fizi_result *resul
 int fizi_debug_stage(fizi_ctx *ctx, int stage, uint32_t frame_in_last_batch, void *out_dev,
                      fizi_stream_t cuda_stream);
 
+/* Parity/debug: copy the context's K0 brightness tables (a2, §3.2;
+ * readings L19-L21) to device memory: lut_dev (256 x 256 u8, row m = the
+ * per-channel LUT of integer mean luma m, identity rows for luma_lo <= m <=
+ * luma_hi), gamma_dev (256 doubles, gamma(m)) and corrected_dev (256 u8, 1
+ * iff row m is not the identity).  Any of the three may be NULL. */
+int fizi_get_lut_table(fizi_ctx *ctx, uint8_t *lut_dev, double *gamma_dev, uint8_t *corrected_dev,
+                       fizi_stream_t cuda_stream);
+
 /* Copy stream `stream`'s envelope out as two interleaved-RGB planes
  * (W*H*3 u8 each, the S:174 plane layout) to device memory. */
 int fizi_get_background(fizi_ctx *ctx, uint32_t stream, uint8_t *lo_dev, uint8_t *hi_dev,

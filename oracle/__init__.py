@@ -249,8 +249,10 @@ def segment(params: Params, frame: np.ndarray, lo: np.ndarray, hi: np.ndarray,
 
 
 def segment_batch(params: Params, frames: np.ndarray, lo, hi, t_ms=None, nthreads: int = 1,
-                  want_masks: bool = True):
-    """Frame-parallel batch (threads over frames; no tracking)."""
+                  want_masks: bool = True, as_array: bool = False):
+    """Frame-parallel batch (threads over frames; no tracking).  as_array:
+    the records as one numpy structured array (fields of Record) instead of
+    a list of Record."""
     frames, lo, hi = _c(frames), _c(lo), _c(hi)
     n = frames.shape[0]
     recs = (Record * max(n, 1))()
@@ -261,6 +263,8 @@ def segment_batch(params: Params, frames: np.ndarray, lo, hi, t_ms=None, nthread
     lib().or_segment_batch(ctypes.byref(params), _p(frames), n, _p(lo), _p(hi),
                            t_ms.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), nthreads,
                            recs, _p(masks) if masks is not None else None)
+    if as_array:
+        return np.ctypeslib.as_array(recs)[:n].copy(), masks
     return [recs[i] for i in range(n)], masks
 
 

@@ -977,6 +977,23 @@ int fizi_debug_stage(fizi_ctx* ctx, int stage, uint32_t frame, void* out_dev,
   return FIZI_OK;
 }
 
+int fizi_get_lut_table(fizi_ctx* ctx, uint8_t* lut_dev, double* gamma_dev, uint8_t* corrected_dev,
+                       fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
+  DeviceGuard guard(c.device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  cudaError_t e = cudaSuccess;
+  if (lut_dev) e = cudaMemcpyAsync(lut_dev, c.lut, 256 * 256, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && gamma_dev)
+    e = cudaMemcpyAsync(gamma_dev, c.gamma_tab, 256 * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && corrected_dev)
+    e = cudaMemcpyAsync(corrected_dev, c.corr_tab, 256, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "get_lut_table");
+  return FIZI_OK;
+}
+
 int fizi_get_background(fizi_ctx* ctx, uint32_t stream, uint8_t* lo_dev, uint8_t* hi_dev,
                         fizi_stream_t cuda_stream) {
   if (!ctx) return FIZI_E_ARG;

@@ -127,11 +127,12 @@ def lib() -> ctypes.CDLL:
         L.fizi_set_zones.argtypes = [vp, u32, vp, u32]
         L.fizi_hit_test.argtypes = [vp, u32, vp, u32, vp, vp]
         L.fizi_flush.argtypes = [vp, vp]
+        L.fizi_get_lut_table.argtypes = [vp, vp, vp, vp, vp]
         for name in ("fizi_set_pipeline", "fizi_flush", "fizi_wheel_default", "fizi_set_wheel",
                      "fizi_drive", "fizi_drive_throttle", "fizi_relearn_flags", "fizi_set_zones", "fizi_hit_test", "fizi_params_default", "fizi_create", "fizi_learn_background",
                      "fizi_process_frames", "fizi_segment_frames", "fizi_process_frames_host",
                      "fizi_track", "fizi_reset_tracker", "fizi_debug_stage",
-                     "fizi_get_background", "fizi_set_background"):
+                     "fizi_get_background", "fizi_set_background", "fizi_get_lut_table"):
             getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -332,6 +333,16 @@ class Fizi:
         self._check(lib().fizi_debug_stage(self._h, sid, frame, out.data_ptr(),
                                            _stream_handle(self.device)), "fizi_debug_stage")
         return out
+
+    def get_lut_table(self):
+        """K0 tables (device): LUT rows (256, 256) u8, gamma (256,) f64, corrected (256,) u8."""
+        import torch
+        lut = torch.empty((256, 256), dtype=torch.uint8, device=self.device)
+        gam = torch.empty(256, dtype=torch.float64, device=self.device)
+        cor = torch.empty(256, dtype=torch.uint8, device=self.device)
+        self._check(lib().fizi_get_lut_table(self._h, lut.data_ptr(), gam.data_ptr(), cor.data_ptr(),
+                                             _stream_handle(self.device)), "fizi_get_lut_table")
+        return lut, gam, cor
 
     def get_background(self, stream: int = 0):
         import torch

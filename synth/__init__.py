@@ -79,6 +79,11 @@ def _gain_q10(cfg: Config, k: int) -> int:
     # three abrupt exposure steps ("brutal changes")
     if any(s <= k < s + 30 for s in (150, 500, 800)):
         g *= 0.6
+    # an over-exposure ramp near the drift's peak ("over-exposed
+    # environment"): x1.0 .. x1.5 over frames 40-139, so the mean luma climbs
+    # through the unclamped gamma > 1 rows (191-193) into the clamped ones
+    if 40 <= k < 140:
+        g *= 1.0 + 0.5 * (k - 40) / 100.0
     return round_half_up(1024.0 * g)
 
 

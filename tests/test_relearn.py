@@ -26,12 +26,15 @@ def test_device_flags_match_oracle_on_drift_stream():
     cfg = synth.CONFIGS[2]
     fz = Fizi(cfg.W, cfg.H, max_batch=64)
     fz.learn_background(torch.from_numpy(synth.learning_frames_host(cfg)).cuda(), margin=synth.MARGIN)
+    import oracle
     means, flags = [], []
     for k0 in range(0, 640, 64):                  # flags fold across calls
         ks = range(k0, k0 + 64)
-        fr = torch.from_numpy(synth.frames_host(cfg, 0, ks)).cuda()
+        fh = synth.frames_host(cfg, 0, ks)
+        fr = torch.from_numpy(fh).cuda()
         _, res = fz.process_frames(fr, t_ms=np.array([synth.t_ms(k) for k in ks], np.int64))
-        means += [int(m) for m in results_numpy(res)["mean_luma"]]
+        # the oracle's own a2 mean of every frame (not the device's record field)
+        means += [oracle.mean_luma(f)[0] for f in fh]
         flags += [bool(f) for f in fz.relearn_flags(res, threshold=20).cpu().numpy()]
     ref = relearn_flags(means, 20)
     assert flags == ref
