@@ -224,7 +224,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_1907_04393_b200 import RESULT_BYTES, Fizi
+    from paper_1907_04393_b200 import CALL_SLOTS, RESULT_BYTES, Fizi
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -282,7 +282,7 @@ def main():
         learn = synth.frames_dev(cfg, sid, range(cfg.n_learn), learning=True, device=dev)
         fz.learn_background(learn, stream=sid, margin=synth.MARGIN)
     # N = 1: pipelined calls (a call's tail overlaps the next calls'
-    # segmentation), so outputs rotate over three buffers and the timed
+    # segmentation), so outputs rotate over CALL_SLOTS buffers and the timed
     # region ends with fz.flush() (N > 1: segment_frames, windowed gather + fold)
     pipelined = not args.no_pipeline
     fz.set_pipeline(pipelined)
@@ -294,7 +294,7 @@ def main():
     gathered_w = torch.empty((world * G * B, RESULT_BYTES), dtype=torch.uint8, device=dev)
     fold_stream = torch.cuda.Stream(device=dev)
     window = []
-    NBUF = 3                             # = the context's call slots (include/fizi.h)
+    NBUF = CALL_SLOTS                    # = the context's call slots (include/fizi.h)
     masks2 = [torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
     res2 = [torch.empty((B, RESULT_BYTES), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
     del learn

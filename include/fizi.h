@@ -286,14 +286,15 @@ int fizi_set_background(fizi_ctx *ctx, uint32_t stream, const uint8_t *lo_dev,
  * order when the call returns.  In pipelined mode a call's tail (LUT
  * re-test, a4-a7, the u8 mask, the a8 fold) runs on the context's internal
  * stream and is NOT joined into cuda_stream, so that it overlaps the next
- * call's segmentation; per-call state is double-buffered inside the context.
- * The context keeps 3 call slots: every write of call k+3 is ordered after
- * the tail of call k, so a caller may rotate 3 output buffers across calls
- * without waiting.  Outputs of a pipelined call are complete in a stream's
+ * call's segmentation; per-call state is multi-buffered inside the context.
+ * The context keeps FIZI_CALL_SLOTS call slots: every write of call
+ * k+FIZI_CALL_SLOTS is ordered after the tail of call k, so a caller may
+ * rotate FIZI_CALL_SLOTS output buffers across calls without waiting.  Outputs of a pipelined call are complete in a stream's
  * order after fizi_flush on that stream; until then the caller must not read
  * them, nor overwrite the call's frames.  Every other entry point
  * that touches the tail's state (learn / set_background / track / debug /
  * host entry) joins the outstanding tails into its stream itself. */
+#define FIZI_CALL_SLOTS 4
 int fizi_set_pipeline(fizi_ctx *ctx, int enable);
 
 /* Make cuda_stream wait for the tails of all previous calls (no-op when

@@ -141,11 +141,13 @@ void free_all(Ctx& c) {
   for (uint32_t i = 0; i < fizi::kSlots; i++) {
     if (c.zero_blocks[i]) cudaFree(c.zero_blocks[i]);
     if (c.bitAs[i]) cudaFree(c.bitAs[i]);
-    if (c.calls[i]) cudaFree(c.calls[i]);
     if (c.slow_itemss[i]) cudaFree(c.slow_itemss[i]);
+    for (void* q : {(void*)c.bitOs[i], (void*)c.row_cnts[i], (void*)c.row_bases[i], (void*)c.runss[i]})
+      if (q) cudaFree(q);
+    if (c.calls[i]) cudaFree(c.calls[i]);
   }
-  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.bitO, c.bitOC,
-                  c.row_cnt, c.row_base, c.runs, c.parent, c.stats, c.tl, c.dstate,
+  void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.bitOC,
+                  c.parent, c.stats, c.tl, c.dstate,
                   c.prev_mean, c.hstate,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
   for (void* p : ptrs)
@@ -162,27 +164,24 @@ void free_all(Ctx& c) {
   if (c.ev_start) cudaEventDestroy(c.ev_start);
   for (uint32_t i = 0; i < fizi::kSlots; i++) {
     if (c.ev_head[i]) cudaEventDestroy(c.ev_head[i]);
+    if (c.ev_morph[i]) cudaEventDestroy(c.ev_morph[i]);
+    if (c.ev_words[i]) cudaEventDestroy(c.ev_words[i]);
     if (c.ev_tail[i]) cudaEventDestroy(c.ev_tail[i]);
   }
   if (c.side) cudaStreamDestroy(c.side);
   if (c.side2) cudaStreamDestroy(c.side2);
   if (c.side3) cudaStreamDestroy(c.side3);
   if (c.head) cudaStreamDestroy(c.head);
-  if (c.prep) cudaStreamDestroy(c.prep);
+  if (c.cclst) cudaStreamDestroy(c.cclst);
+  if (c.morphst) cudaStreamDestroy(c.morphst);
   if (c.pinned_results) cudaFreeHost(c.pinned_results);
   if (c.h2d) cudaStreamDestroy(c.h2d);
   if (c.d2h) cudaStreamDestroy(c.d2h);
   for (auto ev : c.host_ev) cudaEventDestroy(ev);
   for (uint32_t i = 0; i < fizi::kSlots; i++)
-    if (c.ev_prep[i]) cudaEventDestroy(c.ev_prep[i]);
-  for (uint32_t i = 0; i < fizi::kSlots; i++)
     if (c.ev_in[i]) cudaEventDestroy(c.ev_in[i]);
-  for (uint32_t i = 0; i < fizi::kSlots; i++) {
-    if (c.ev_ccl[i]) cudaEventDestroy(c.ev_ccl[i]);
-    if (c.ev_zj[i]) cudaEventDestroy(c.ev_zj[i]);
-  }
-  if (c.ev_zfork) cudaEventDestroy(c.ev_zfork);
-  if (c.ev_zjoin) cudaEventDestroy(c.ev_zjoin);
+  for (cudaEvent_t ev : {c.ev_zfork, c.ev_zjoin, c.ev_hfork, c.ev_hjoin})
+    if (ev) cudaEventDestroy(ev);
   for (auto& r : c.prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c.prof_free) cudaEventDestroy(e);
   if (c.prof_open) cudaEventDestroy(c.prof_open);
@@ -204,7 +203,11 @@ void select_slot(Ctx& c, uint32_t s) {
   c.slow_count = reinterpret_cast<uint32_t*>(z); z += fizi::kMaxSub * 4;
   c.dirty = reinterpret_cast<uint32_t*>(z);
   c.bitA = c.bitAs[s];
+  c.bitO = c.bitOs[s];
   c.slow_items = c.slow_itemss[s];
+  c.row_cnt = c.row_cnts[s];
+  c.row_base = c.row_bases[s];
+  c.runs = c.runss[s];
   c.call = c.calls[s];
   c.frame_t = reinterpret_cast<int64_t*>(c.call + 1);
   c.frame_stream = reinterpret_cast<uint32_t*>(c.frame_t + mb);
@@ -270,7 +273,8 @@ struct CallPlan {
   std::vector<SubBatch> subs;
   int fold = -2;               // -2 no fold, -1 per-stream end fold, >= 0 single-stream fold
   bool fused_mask = false;     // the labelling kernel writes the u8 mask (pre-zeroed)
-  bool premask = false;
+  bool premask = false;        // u8 mask: zeroed beside the segmentation, kept runs by labelling
+  bool morphmask = false;      // u8 mask: rows of O by the morphology, dropped runs cleared
   uint8_t* masks = nullptr;    // caller's u8 masks (expand path only)
 };
 
@@ -280,7 +284,7 @@ struct CallPlan {
 // call into kHead (upload + counters + fused segmentation, on st) and kTail
 // (u8 mask zeroing, LUT re-test, a4 morphology, a5-a7 labelling + u8 mask,
 // a8 fold, on the side stream) so that call k's tail overlaps call k+1's head.
-enum Part { kWhole = 0, kHead = 1, kTail = 2 };
+enum Part { kWhole = 0, kHead = 1, kTail = 2, kTailCcl = 3, kTailMorph = 4 };
 
 int enqueue_head(Ctx& c, const CallPlan& pl, cudaStream_t st) {
   cudaError_t e = cudaMemcpyAsync(c.call, c.pinned[pl.slot], c.pinned_bytes, cudaMemcpyHostToDevice, st);
@@ -298,7 +302,7 @@ int enqueue_tail(Ctx& c, const CallPlan& pl, const SubBatch& b, uint32_t k, cuda
     if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
   }
   prof_begin(c, sd);
-  e = fizi::launch_morph(c, b.f0, b.n, nullptr, pl.premask, sd);
+  e = fizi::launch_morph(c, b.f0, b.n, pl.morphmask, sd);
   prof_end(c, FIZI_PROF_MORPH, sd);
   if (e != cudaSuccess) return cuda_fail(c, e, "morph");
   if (c.p.debug) {
@@ -330,31 +334,63 @@ int enqueue_tail(Ctx& c, const CallPlan& pl, const SubBatch& b, uint32_t k, cuda
 int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   int rc = FIZI_OK;
-  if (part == kHead) {                                  // (table + counters: prep stream)
+  if (part == kHead) {
+    // per-call table upload and counter clear, then the fused segmentation
+    // kernel beside the u8 mask clear (a branch on side2, joined back)
+    rc = enqueue_head(c, pl, st);
+    if (rc) return rc;
+    if (pl.premask) {
+      e = cudaEventRecord(c.ev_hfork, st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side2, c.ev_hfork, 0);
+      if (e == cudaSuccess) e = fizi::launch_zero_masks(c, pl.n, c.side2);
+      if (e == cudaSuccess) e = cudaEventRecord(c.ev_hjoin, c.side2);
+      if (e != cudaSuccess) return cuda_fail(c, e, "mask zero");
+    }
     e = fizi::launch_seg_main(c, 0, pl.n, 0, pl.subs[0].ng, 0, st);
-    return e == cudaSuccess ? FIZI_OK : cuda_fail(c, e, "segment");
+    if (e != cudaSuccess) return cuda_fail(c, e, "segment");
+    if (pl.premask) {
+      e = cudaStreamWaitEvent(st, c.ev_hjoin, 0);
+      if (e != cudaSuccess) return cuda_fail(c, e, "join");
+    }
+    return FIZI_OK;
   }
   if (part == kTail) {
     // the queued per-pixel words and the LUT re-test of corrected frames
     // open the tail (the morphology needs them, the next call's
-    // segmentation does not, so the head is the fused kernel alone)
-    // (the two touch disjoint frames, so the LUT re-test runs on a branch
-    // beside the per-pixel words and joins before the morphology)
+    // segmentation does not); the two touch disjoint frames, so the LUT
+    // re-test runs on a branch (side3) and joins before the morphology.
+    // The a8 fold runs inside the labelling kernel (the CTA holding the
+    // fold lock folds the ready records in order).
     e = cudaEventRecord(c.ev_zfork, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side2, c.ev_zfork, 0);
-    if (e == cudaSuccess) e = fizi::launch_seg_fix(c, 0, pl.n, 0, c.side2);
-    if (e == cudaSuccess) e = cudaEventRecord(c.ev_zjoin, c.side2);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side3, c.ev_zfork, 0);
+    if (e == cudaSuccess) e = fizi::launch_seg_fix(c, 0, pl.n, 0, c.side3);
+    if (e == cudaSuccess) e = cudaEventRecord(c.ev_zjoin, c.side3);
     if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
     if (c.fast) {
       e = fizi::launch_slow_words(c, 0, pl.n, 0, st);
       if (e != cudaSuccess) return cuda_fail(c, e, "slow words");
     }
     e = cudaStreamWaitEvent(st, c.ev_zjoin, 0);
-    if (e != cudaSuccess) return cuda_fail(c, e, "join");
-    // (the u8 mask target was cleared beside the segmentation, run_call)
-    CallPlan nofold = pl;                             // the fold runs on its own stream
-    nofold.fold = -2;
-    return enqueue_tail(c, nofold, pl.subs[0], 0, st, nullptr, false);
+    return e == cudaSuccess ? FIZI_OK : cuda_fail(c, e, "join");
+  }
+  if (part == kTailMorph) {
+    prof_begin(c, st);
+    e = fizi::launch_morph(c, 0, pl.n, pl.morphmask, st);
+    prof_end(c, FIZI_PROF_MORPH, st);
+    return e == cudaSuccess ? FIZI_OK : cuda_fail(c, e, "morph");
+  }
+  if (part == kTailCcl) {                  // a5-a7 + u8 mask + a8 fold (fused)
+    prof_begin(c, st);
+    e = fizi::launch_ccl(c, 0, pl.n, 0, pl.premask, pl.fold, st);
+    prof_end(c, FIZI_PROF_CCL, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "ccl");
+    if (pl.masks && !pl.fused_mask) {
+      prof_begin(c, st);
+      e = fizi::launch_expand(c, 0, pl.n, pl.masks, st);
+      prof_end(c, FIZI_PROF_EXPAND, st);
+      if (e != cudaSuccess) return cuda_fail(c, e, "expand");
+    }
+    return FIZI_OK;
   }
   rc = enqueue_head(c, pl, st);
   if (rc) return rc;
@@ -399,7 +435,7 @@ int run_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
   const bool graph = c.use_graphs && !c.prof && !(pl.masks && !pl.fused_mask);
   if (!graph) return enqueue_part(c, pl, part, st);
   std::vector<uint32_t> key = {(uint32_t)part, pl.n, (uint32_t)(pl.fold + 2), (uint32_t)pl.premask,
-                               (uint32_t)pl.fused_mask};
+                               (uint32_t)pl.fused_mask, (uint32_t)pl.morphmask};
   for (const SubBatch& b : pl.subs) {
     key.push_back(b.n);
     key.push_back(b.g0);
@@ -474,7 +510,8 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   // the u8 mask is written by the labelling kernel when the register-pipelined
   // morphology runs; otherwise it is expanded from the final bit mask
   pl.fused_mask = c.fast && c.P <= 128 && c.p.se_radius <= 4;
-  pl.premask = masks && pl.fused_mask;
+  pl.premask = masks && pl.fused_mask && !c.mask_by_morph;
+  pl.morphmask = masks && pl.fused_mask && c.mask_by_morph;
   pl.masks = masks;
   const bool pipelined = c.pipeline && !c.p.debug;
   pl.slot = c.pinned_next;
@@ -504,53 +541,41 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
     if (e == cudaSuccess) e = cudaEventRecord(c.ev_tail[pl.slot], st);
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
   } else {
-    // the head runs on the context's head stream (ordered after the caller's
-    // earlier work on st); st itself is not joined (fizi_flush does that)
+    // Four graph launches per call, each on a stream that runs its stage
+    // in call order: the head (table upload, counter clear, fused
+    // segmentation) on the head stream; the per-pixel words + LUT re-test on
+    // the side stream; the morphology (+ u8 mask rows) on the morphology
+    // stream; the labelling (+ the fused a8 fold) on the labelling stream.
+    // So call k's labelling, call k+1's morphology, call k+2's per-pixel
+    // words and call k+3's segmentation can run at once
+    // (every buffer a stage writes is per slot; the labelling scratch and the
+    // tracker state are only touched by the in-order labelling stage).  st
+    // itself is not joined (fizi_flush does that); st already waits for the
+    // slot's previous call (above), and every stage is ordered after st.
     cudaStream_t hs = c.head;
-    // the slot's table upload and counter clear run on the prep stream as
-    // soon as the slot is free, ahead of the segmentation that needs them
-    e = cudaStreamWaitEvent(c.prep, c.ev_tail[pl.slot], 0);
-    if (e != cudaSuccess) return cuda_fail(c, e, "prep");
-    rc = enqueue_head(c, pl, c.prep);
-    if (rc) return rc;
-    e = cudaEventRecord(c.pinned_ev[pl.slot], c.prep);
-    if (e == cudaSuccess) e = cudaEventRecord(c.ev_prep[pl.slot], c.prep);
-    if (e == cudaSuccess) e = cudaEventRecord(c.ev_in[pl.slot], st);
+    e = cudaEventRecord(c.ev_in[pl.slot], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, c.ev_in[pl.slot], 0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, c.ev_prep[pl.slot], 0);
     if (e != cudaSuccess) return cuda_fail(c, e, "fork");
-    // the u8 mask target is cleared on its own stream beside this call's
-    // segmentation (it needs only the caller's buffer and the table); the
-    // tail waits for it before labelling writes the kept runs
-    if (pl.premask) {
-      e = cudaStreamWaitEvent(c.side2, c.ev_in[pl.slot], 0);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side2, c.ev_prep[pl.slot], 0);
-      if (e == cudaSuccess) e = fizi::launch_zero_masks(c, pl.n, c.side2);
-      if (e == cudaSuccess) e = cudaEventRecord(c.ev_zj[pl.slot], c.side2);
-      if (e != cudaSuccess) return cuda_fail(c, e, "mask zero");
-    }
     rc = run_part(c, pl, kHead, hs);
     if (rc) return rc;
     e = cudaEventRecord(c.ev_head[pl.slot], hs);
+    if (e == cudaSuccess) e = cudaEventRecord(c.pinned_ev[pl.slot], hs);   // table consumed
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side, c.ev_head[pl.slot], 0);
-    if (e == cudaSuccess && pl.premask) e = cudaStreamWaitEvent(c.side, c.ev_zj[pl.slot], 0);
     if (e != cudaSuccess) return cuda_fail(c, e, "fork");
     rc = run_part(c, pl, kTail, c.side);
     if (rc) return rc;
-    if (pl.fold != -2) {
-      // the a8 fold of this call follows its labelling on the fold stream,
-      // so the next call's labelling does not wait for it
-      e = cudaEventRecord(c.ev_ccl[pl.slot], c.side);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side3, c.ev_ccl[pl.slot], 0);
-      if (e == cudaSuccess) e = fizi::launch_track_call(c, pl.fold, c.side3);
-      if (e == cudaSuccess) e = cudaEventRecord(c.ev_tail[pl.slot], c.side3);
-    } else {
-      // still ordered after the fold stream's earlier work
-      e = cudaEventRecord(c.ev_ccl[pl.slot], c.side);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side3, c.ev_ccl[pl.slot], 0);
-      if (e == cudaSuccess) e = cudaEventRecord(c.ev_tail[pl.slot], c.side3);
-    }
-    if (e != cudaSuccess) return cuda_fail(c, e, "fold");
+    e = cudaEventRecord(c.ev_words[pl.slot], c.side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.morphst, c.ev_words[pl.slot], 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fork");
+    rc = run_part(c, pl, kTailMorph, c.morphst);
+    if (rc) return rc;
+    e = cudaEventRecord(c.ev_morph[pl.slot], c.morphst);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.cclst, c.ev_morph[pl.slot], 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fork");
+    rc = run_part(c, pl, kTailCcl, c.cclst);
+    if (rc) return rc;
+    e = cudaEventRecord(c.ev_tail[pl.slot], c.cclst);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
   }
   c.tail_pending = true;
   c.host_call_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
@@ -667,14 +692,16 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   }
 
   for (uint32_t i = 0; i < fizi::kSlots; i++) A(dalloc(&c.bitAs[i], mb * wpf * 4));
-  A(dalloc(&c.bitO, mb * wpf * 4));
+  for (uint32_t i = 0; i < fizi::kSlots; i++) {
+    A(dalloc(&c.bitOs[i], mb * wpf * 4));
+    A(dalloc(&c.row_cnts[i], mb * c.H * 4));
+    A(dalloc(&c.row_bases[i], mb * c.H * 4));
+    A(dalloc(&c.runss[i], mb * c.cap_runs * sizeof(fizi::Run)));
+  }
   if (c.p.debug) A(dalloc(&c.bitOC, mb * wpf * 4));
   if (c.fast)
     for (uint32_t i = 0; i < fizi::kSlots; i++)
       A(dalloc(&c.slow_itemss[i], mb * c.nchunks * 16 * sizeof(unsigned long long)));
-  A(dalloc(&c.row_cnt, mb * c.H * 4));
-  A(dalloc(&c.row_base, mb * c.H * 4));
-  A(dalloc(&c.runs, mb * c.cap_runs * sizeof(fizi::Run)));
   A(dalloc(&c.parent, mb * c.cap_runs * 4));
   A(dalloc(&c.stats, mb * c.cap_runs * sizeof(fizi::RootStats)));
   const size_t table_bytes = sizeof(fizi::CallPtrs) + mb * 8 + mb * 4 * 2 + (mb + 1) * 4;
@@ -707,19 +734,16 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&c.side3, cudaStreamNonBlocking,
                                        side_prio);
-    for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
-      e = cudaEventCreateWithFlags(&c.ev_ccl[i], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_zj[i], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_in[i], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_prep[i], cudaEventDisableTiming);
-    }
-    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.prep, cudaStreamNonBlocking, hi_prio);
+    for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++)
+      e = cudaEventCreateWithFlags(&c.ev_in[i], cudaEventDisableTiming);
     const char* hp = getenv("FIZI_HEAD_PRIO");
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&c.head, cudaStreamNonBlocking,
                                        (hp && atoi(hp) == 0) ? lo_prio : hi_prio);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_zfork, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_zjoin, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.cclst, cudaStreamNonBlocking, side_prio);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.morphst, cudaStreamNonBlocking, side_prio);
+    for (cudaEvent_t* ev : {&c.ev_zfork, &c.ev_zjoin, &c.ev_hfork, &c.ev_hjoin})
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.cap, cudaStreamNonBlocking);
   for (uint32_t k = 0; k < fizi::kMaxSub && e == cudaSuccess; k++)
@@ -728,9 +752,13 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_start, cudaEventDisableTiming);
   for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
     e = cudaEventCreateWithFlags(&c.ev_head[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_morph[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_words[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_tail[i], cudaEventDisableTiming);
   }
   c.use_graphs = getenv("FIZI_NO_GRAPH") == nullptr;
+  if (const char* mm = getenv("FIZI_MASK_MODE"))       // experiment switch: zero | morph
+    c.mask_by_morph = std::strcmp(mm, "zero") != 0;
   if (const char* gm = getenv("FIZI_GROUP")) {          // experiment switch (1..32)
     const int g = atoi(gm);
     if (g >= 1 && g <= (int)fizi::kFrameGroup) c.group_max = (uint32_t)g;

@@ -30,7 +30,7 @@ constexpr int kMaxRadius = 8;
 constexpr size_t kMorphSmem = 200 * 1024;  // dynamic smem budget of the morphology CTA
 constexpr uint32_t kCclSmemRuns = 4096;     // runs labelled in shared memory (else global)
 constexpr uint32_t kMaxSub = 8;             // sub-batches per call (stream pipeline)
-constexpr uint32_t kSlots = 3;              // per-call state slots (pipelined calls in flight)
+constexpr uint32_t kSlots = FIZI_CALL_SLOTS;  // per-call state slots (pipelined calls in flight)
 
 struct Run {                             // one horizontal run of foreground pixels
   uint16_t x0, x1, y, pad;
@@ -85,6 +85,7 @@ struct Ctx {
   uint32_t seg_persist = 5;              // persistent fused kernel: half-CTAs per SM (0: off)
   uint32_t group_max = kFrameGroup;      // frames per same-stream group (fused-kernel item)
   bool use_dirty = false;                // clean chunks of A are not written (dirty bitmap)
+  bool mask_by_morph = true;             // u8 mask rows written by the morphology (else zero + kept runs)
   uint32_t morph_tr = 0;                 // output rows per morphology CTA
   uint64_t launches = 0;
   unsigned long long* tl = nullptr;      // diagnostics timeline (FIZI_TIMELINE)
@@ -104,6 +105,12 @@ struct Ctx {
   // mode).  The pointers below are views of the current slot (select_slot).
   uint8_t* zero_blocks[kSlots] = {};          // per-call counters (cleared each call)
   uint32_t* bitAs[kSlots] = {};               // merged masks A
+  // morphology outputs (O, runs) per slot: call k+1's morphology writes its
+  // own while call k's labelling reads call k's
+  uint32_t* bitOs[kSlots] = {};
+  uint32_t* row_cnts[kSlots] = {};
+  uint32_t* row_bases[kSlots] = {};
+  Run* runss[kSlots] = {};
   CallPtrs* calls[kSlots] = {};               // per-call tables
   uint8_t* zero_block = nullptr;         // views of the current slot's block below
   uint64_t zero_bytes = 0;
@@ -115,7 +122,7 @@ struct Ctx {
   uint32_t* sub_done = nullptr;          // kMaxSub (CCL CTAs finished per sub-batch)
   uint32_t* fold_sync = nullptr;         // kMaxSub x (2 + max_batch): fold lock / cursor / ready
   uint32_t* bitA = nullptr;              // max_batch * H * P
-  uint32_t* bitO = nullptr;              // max_batch * H * P
+  uint32_t* bitO = nullptr;              // max_batch * H * P (view of the slot's)
   uint32_t* bitOC = nullptr;             // debug copy of O
   uint32_t* row_cnt = nullptr;           // max_batch * H   (runs per row)
   uint32_t* row_base = nullptr;          // max_batch * H   (first run of the row)
@@ -139,23 +146,24 @@ struct Ctx {
   uint8_t* dstate = nullptr;             // n_streams drive states (NEXT-2)
   int32_t* prev_mean = nullptr;          // n_streams relearn-trigger states (NEXT-1), -1 = none
   uint8_t* hstate = nullptr;             // n_streams hit-test states (NEXT-3)
-  cudaStream_t side = nullptr;           // internal stream for the per-sub-batch tail
-  cudaStream_t side2 = nullptr;          // pipelined tail: u8 mask zeroing
-  cudaStream_t side3 = nullptr;          // pipelined tail: a8 fold (in call order)
-  cudaStream_t head = nullptr;           // pipelined head (segmentation)
-  cudaStream_t prep = nullptr;           // pipelined: per-call table upload + counter clear
+  cudaStream_t side = nullptr;           // tail: LUT re-test + morphology (joined: whole tail)
+  cudaStream_t cclst = nullptr;          // pipelined tail: labelling + u8 mask + fold, call order
+  cudaStream_t morphst = nullptr;        // pipelined tail: morphology, call order
+  cudaStream_t side2 = nullptr;          // head branch: u8 mask zeroing
+  cudaStream_t side3 = nullptr;          // tail branch: LUT re-test
+  cudaStream_t head = nullptr;           // pipelined head: upload, clear, segmentation (call order)
+  cudaEvent_t ev_hfork = nullptr, ev_hjoin = nullptr;   // head: u8 mask clear branch
   cudaStream_t h2d = nullptr, d2h = nullptr;   // fizi_process_frames_host copy streams
   std::vector<cudaEvent_t> host_ev;            // fizi_process_frames_host chunk events
   fizi_result* pinned_results = nullptr;       // fizi_process_frames_host record staging
-  cudaEvent_t ev_prep[kSlots] = {};
   cudaEvent_t ev_in[kSlots] = {};        // pipelined: caller's stream reached the call
-  cudaEvent_t ev_ccl[kSlots] = {};       // pipelined: slot's labelling done
-  cudaEvent_t ev_zj[kSlots] = {};        // pipelined: slot's u8 mask target cleared
-  cudaEvent_t ev_zfork = nullptr, ev_zjoin = nullptr;
+  cudaEvent_t ev_zfork = nullptr, ev_zjoin = nullptr;   // tail: LUT re-test branch
   cudaEvent_t ev_seg[kMaxSub] = {};      // segment(k) done on the caller's stream
   cudaEvent_t ev_join = nullptr;         // tail of the call done on the side stream
   cudaEvent_t ev_start = nullptr;        // call start on the caller's stream
   cudaEvent_t ev_head[kSlots] = {};           // pipelined: slot's segmentation done
+  cudaEvent_t ev_morph[kSlots] = {};          // pipelined: slot's morphology done
+  cudaEvent_t ev_words[kSlots] = {};          // pipelined: slot's per-pixel words + LUT re-test done
   cudaEvent_t ev_tail[kSlots] = {};           // slot's last call fully done (slot reusable)
   bool pipeline = false;                 // fizi_set_pipeline: tails not joined per call
   bool tail_pending = false;             // some pipelined tail may be outstanding
@@ -254,9 +262,12 @@ cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cud
 // the segment launcher marks the SEGMENT -> FIXUP boundary through this hook
 void prof_begin(Ctx& c, cudaStream_t st);
 void prof_end(Ctx& c, int slot, cudaStream_t st);
-cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, bool masks_zeroed,
-                         cudaStream_t st);
-// masks_zeroed: c.call->masks (if any) was zeroed by launch_zero_masks
+// write_masks: the morphology writes the u8 rows of O into c.call->masks
+// (the labelling then clears the dropped components' runs)
+cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, bool write_masks, cudaStream_t st);
+// masks_zeroed: c.call->masks (if any) was zeroed by launch_zero_masks (the
+// labelling writes the kept runs), else it holds O (the labelling clears the
+// dropped runs)
 cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, bool masks_zeroed,
                        int track_stream, cudaStream_t st);
 cudaError_t launch_zero_masks(Ctx& c, uint32_t n, cudaStream_t st);

@@ -27,8 +27,8 @@ namespace fizi {
 struct MorphArgs {
   const CallPtrs* call;         // diagnostics timeline only
   uint32_t f0;                  // first frame of the launch (sub-batch)
-  uint8_t* masks;               // u8 final-mask output (fast path) or nullptr
-  bool masks_zeroed;            // masks pre-zeroed: all-zero bands skip their rows
+  bool write_masks;             // write the u8 mask rows of O into call->masks (fast path)
+  bool masks_zeroed;            // (always false when write_masks)
   const uint32_t* dirty;        // per-frame chunk bitmap (fast path) or nullptr
   uint32_t dirty_words;
   bool write_zero_o;            // zero bands still write their O rows (debug / expand)
@@ -276,7 +276,7 @@ struct MorphPipe {
     }
     Af = a.A + (uint64_t)f * H * P;
     Of = a.O + (uint64_t)f * H * P;
-    Mf = a.masks ? a.masks + (uint64_t)f * H * a.W : nullptr;
+    Mf = (a.write_masks && a.call->masks) ? a.call->masks + (uint64_t)f * H * a.W : nullptr;
     runs = a.runs + (uint64_t)f * a.cap_runs;
     p1.init(); p2.init(); p3.init(); p4.init();
   }
@@ -587,13 +587,12 @@ static void launch_r(const MorphArgs& a, uint32_t n, size_t smem, cudaStream_t s
   morph_runs_kernel<R><<<dim3((a.H + a.TR - 1) / a.TR, n), 256, smem, st>>>(a);
 }
 
-cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, bool masks_zeroed,
-                         cudaStream_t st) {
+cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, bool write_masks, cudaStream_t st) {
   MorphArgs a;
   a.f0 = f0;
   a.call = c.call;
-  a.masks = masks;
-  a.masks_zeroed = masks_zeroed;
+  a.write_masks = write_masks;
+  a.masks_zeroed = false;
   a.dirty = c.fast ? c.dirty : nullptr;
   a.dirty_words = c.dirty_words;
   a.write_zero_o = c.p.debug != 0;

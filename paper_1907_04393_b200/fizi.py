@@ -54,6 +54,7 @@ RESULT_DTYPE = np.dtype({
     "itemsize": 128,
 })
 RESULT_BYTES = 128
+CALL_SLOTS = 4          # FIZI_CALL_SLOTS (include/fizi.h): output buffers a pipelined caller may rotate
 
 
 class Wheel(ctypes.Structure):

@@ -20,8 +20,8 @@ fz.learn_background(synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True),
 fz.set_pipeline(pipelined)
 nb = 4
 frames = [synth.frames_dev(cfg, 0, range(b * B, (b + 1) * B)) for b in range(nb)]
-masks = [torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=dev) for _ in range(3)]
-res = [torch.empty((B, 128), dtype=torch.uint8, device=dev) for _ in range(3)]
+masks = [torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=dev) for _ in range(4)]
+res = [torch.empty((B, 128), dtype=torch.uint8, device=dev) for _ in range(4)]
 ncalls = 48
 import time
 L0 = lib()
@@ -32,7 +32,8 @@ c0, s0 = hc.value, hsync.value
 tp0 = time.perf_counter()
 for i in range(ncalls):
     t = np.arange(B, dtype=np.int64) * 33 + i * B * 33
-    fz.process_frames(frames[i % nb], t_ms=t, masks=masks[i % 3], results=res[i % 3])
+    fz.process_frames(frames[i % nb], t_ms=t,
+                      masks=None if os.environ.get("TL_NOMASK") else masks[i % 4], results=res[i % 4])
 tp1 = time.perf_counter()
 L0.fizi_diag_host_ns(fz._h, ctypes.byref(hc), ctypes.byref(hsync))
 print("host per call: python+lib %.1f us, inside run_call %.1f us, of which slot wait %.1f us" % (
