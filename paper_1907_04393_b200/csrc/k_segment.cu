@@ -31,6 +31,11 @@
 
 namespace fizi {
 
+#ifndef FIZI_MULTI_STAGES
+#define FIZI_MULTI_STAGES 4
+#endif
+constexpr int kMultiStages = FIZI_MULTI_STAGES;   // ring depth of the multi-stream kernel
+
 struct SegArgs {
   const CallPtrs* call;         // frames / records of the call (device)
   uint64_t frame_bytes;         // 3N
@@ -522,6 +527,158 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   if (tid == 0) tl_mark(a.call, kTlSeg, 1);
 }
 
+// Multi-stream calls (every same-stream group holds one frame, e.g. C5: the
+// current frame of each of 256 camera streams): the envelope is read once per
+// frame, so it streams exactly like the frame.  Work item = one 12 KiB tile
+// of one frame; a kStages-deep ring of shared-memory stages each holds the
+// frame tile and its two envelope tiles (lo, hi planes: 3 x 12 KiB), all
+// three filled by TMA bulk copies on one mbarrier.  Each CTA owns a
+// contiguous range of items (consecutive tiles of consecutive frames), so
+// the ring is refilled without any claim: the last warp out of a stage
+// issues the copies of the item kStages rounds ahead at once, then does the
+// round's bookkeeping.  The luma of consecutive tiles of one frame is summed
+// in shared memory and flushed to the frame's global sum (with the frame-done
+// count, the last CTA of the frame finalises its record) when the frame
+// changes, once per frame and CTA.  An item past the range arrives on its
+// stage's barrier without data and ends the consumers.
+template <int kStages, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) seg_multi_kernel(SegArgs a) {
+  constexpr uint32_t kStageBytes = 3 * kTileBytes;
+  extern __shared__ __align__(128) uint8_t sm[];          // kStages x (frame, lo, hi) tiles
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ uint32_t empty_cnt[kStages];
+  __shared__ uint32_t acc_y[kStages];
+  __shared__ uint32_t cur_f, cur_n;                        // frame being summed, its tiles so far
+  __shared__ unsigned long long cur_sum;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) tl_mark(a.call, kTlSeg, 0);
+  const uint8_t* frames = a.call->frames;
+  const uint32_t n_items = a.tiles * a.n_groups;
+  const uint32_t per = (n_items + gridDim.x - 1) / gridDim.x;
+  const uint32_t it0 = min(n_items, blockIdx.x * per), it1 = min(n_items, it0 + per);
+  if (tid < kStages) { empty_cnt[tid] = 0; acc_y[tid] = 0; }
+  if (tid == 0) {
+    cur_f = 0xFFFFFFFFu;
+    cur_n = 0;
+    cur_sum = 0;
+#pragma unroll
+    for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // start the copies of item `it` into stage s (or end the ring there)
+  auto issue = [&](uint32_t s, uint32_t it) {
+    if (it < it1) {
+      const uint32_t tile = it % a.tiles, grp = it / a.tiles;
+      const uint32_t f = a.group_frames[a.group_off[grp]];
+      const uint32_t stream = a.frame_stream[f];
+      const uint64_t toff = (uint64_t)tile * kTileBytes;
+      const uint64_t trem = a.frame_bytes - toff;
+      const uint32_t tbytes = trem < (uint64_t)kTileBytes ? (uint32_t)trem : (uint32_t)kTileBytes;
+      const uint32_t ebytes = min((uint32_t)kWarpsPerCta, a.nchunks - tile * kWarpsPerCta) * kChunkBytes;
+      const uint64_t pol = policy_evict_first();
+      uint8_t* dst = sm + s * kStageBytes;
+      const uint8_t* env = a.env + (uint64_t)stream * 2 * a.env_plane + toff;
+      mbar_arrive_expect_tx(&full[s], tbytes + 2 * ebytes);
+      bulk_g2s(dst, frames + (uint64_t)f * a.frame_bytes + toff, tbytes, &full[s], pol);
+      bulk_g2s(dst + kTileBytes, env, ebytes, &full[s], pol);
+      bulk_g2s(dst + 2 * kTileBytes, env + a.env_plane, ebytes, &full[s], pol);
+    } else {
+      mbar_arrive(&full[s]);                     // no data: the end of the range
+    }
+  };
+  // a frame's summed tiles -> its global luma sum and done count
+  auto flush = [&](uint32_t f, unsigned long long sum, uint32_t ntiles) {
+    atomicAdd(&a.luma[f], sum);
+    __threadfence();
+    if (atomicAdd(&a.frame_done[f], ntiles) + ntiles == a.tiles) {   // frame f complete
+      __threadfence();
+      const unsigned long long tot = atomicAdd(&a.luma[f], 0ull);
+      finalize_frame(a, f, tot, const_cast<uint32_t*>(a.fix), a.fg);
+    }
+  };
+  if (tid == 0)
+    for (int s = 0; s < kStages; s++) issue(s, it0 + s);
+  for (uint32_t k = 0;; k++) {
+    const uint32_t s = k % kStages;
+    const uint32_t it = it0 + k;
+    mbar_wait(&full[s], (k / kStages) & 1u);
+    if (it >= it1) break;
+    const uint32_t tile = it % a.tiles, grp = it / a.tiles;
+    const uint32_t f = a.group_frames[a.group_off[grp]];
+    const uint32_t c = tile * kWarpsPerCta + warp;
+    if (c < a.nchunks) {
+      const uint64_t coff = (uint64_t)c * kChunkBytes;
+      const bool valid = coff + 48u * lane < a.frame_bytes;
+      const uint8_t* st0 = sm + s * kStageBytes + warp * kChunkBytes;
+      uint32_t fr[12];
+      load48(st0 + 48 * lane, valid, fr);
+      EnvRaw e;
+      if (valid) {
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+          const uint4 l = *reinterpret_cast<const uint4*>(st0 + kTileBytes + 512 * q + 16 * lane);
+          const uint4 h = *reinterpret_cast<const uint4*>(st0 + 2 * kTileBytes + 512 * q + 16 * lane);
+          e.lo[4 * q + 0] = l.x; e.lo[4 * q + 1] = l.y; e.lo[4 * q + 2] = l.z; e.lo[4 * q + 3] = l.w;
+          e.hi[4 * q + 0] = h.x; e.hi[4 * q + 1] = h.y; e.hi[4 * q + 2] = h.z; e.hi[4 * q + 3] = h.w;
+        }
+        uint32_t w = 0, slo = 0, shi = 0;
+#pragma unroll
+        for (int i = 0; i < 12; i++) {
+          w = sad4(e.lo[i], e.hi[i], w);
+          slo = sad4(e.lo[i], 0u, slo);
+          shi = sad4(e.hi[i], 0u, shi);
+        }
+        e.W = w;
+        e.ordered = w == shi - slo;
+      } else {
+        full_env_raw(e);
+      }
+      const bool inside = all_inside_sad(fr, e) || !valid;
+      const uint32_t out_lanes = __ballot_sync(0xFFFFFFFFu, !inside);
+      const uint32_t y = warp_sum_u32(luma16(fr));
+      if (out_lanes) {
+        // words with an outside pixel go to the per-pixel kernel, the others
+        // of the chunk are written as 0
+        const uint32_t slow_words = (out_lanes | (out_lanes >> 1)) & 0x55555555u;   // bit 2k
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(a.slow_count, (uint32_t)__popc(slow_words));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (!(lane & 1)) {
+          if ((slow_words >> lane) & 1u)
+            a.slow_items[base + __popc(slow_words & ((1u << lane) - 1u))] =
+                ((unsigned long long)f << 32) | (c * 16u + (lane >> 1));
+          else if (valid)
+            a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
+        }
+      } else if (a.write_zero && !(lane & 1) && valid) {
+        a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
+      }
+      if (lane == 0) atomicAdd(&acc_y[s], y);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&empty_cnt[s], 1u) == kWarpsPerCta - 1) {   // last warp out of stage s
+        empty_cnt[s] = 0;
+        const uint32_t y = atomicExch(&acc_y[s], 0u);
+        issue(s, it + kStages);                                  // refill first
+        if (f != cur_f) {
+          if (cur_n) flush(cur_f, cur_sum, cur_n);
+          cur_f = f;
+          cur_sum = 0;
+          cur_n = 0;
+        }
+        cur_sum += y;
+        cur_n += 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && cur_n) flush(cur_f, cur_sum, cur_n);
+  if (tid == 0) tl_mark(a.call, kTlSeg, 1);
+}
+
 // The words queued by the fused kernel (a pixel outside the envelope): a pair
 // of lanes per word re-reads its 32 pixels and their envelope and applies R1
 // per byte and R2 & R3 through the colour table.  Words of frames that get
@@ -792,7 +949,14 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
     const uint32_t pgrid = grid_env ? grid_env : (uint32_t)c.sms * per_sm / 2u;
     a.persist = pgrid > 0 && items > pgrid;
     const uint32_t grid = a.persist ? pgrid : items;
-    seg_fast_kernel<3, 4><<<grid, 256, 4 * kTileBytes, st>>>(a);   // 3 CTAs/SM x 4-deep ring
+    if (ng == n && n > 1) {
+      // one frame per same-stream group (multi-stream call): the envelope
+      // streams with the frame through the TMA ring
+      a.persist = true;
+      seg_multi_kernel<kMultiStages, 1><<<c.sms, 256, kMultiStages * 3 * kTileBytes, st>>>(a);
+    } else {
+      seg_fast_kernel<3, 4><<<grid, 256, 4 * kTileBytes, st>>>(a);   // 3 CTAs/SM x 4-deep ring
+    }
   } else {
     luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(c.call, c.N, f0,
                                                                                 c.luma);
@@ -843,6 +1007,9 @@ cudaError_t init_segment(Ctx& c) {
   (void)c;
   cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<3, 4>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTileBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(seg_multi_kernel<kMultiStages, 1>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMultiStages * 3 * kTileBytes);
   const char* ps = getenv("FIZI_SEG_PERSIST");          // experiment switch
   c.seg_persist = ps ? 2u * (uint32_t)atoi(ps) : 5u;      // in half CTAs per SM
   if (e == cudaSuccess)
