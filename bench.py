@@ -11,6 +11,11 @@ of the tiny per-frame records, then fizi_track (a8) over the gathered
 records in frame order.  Rank r takes batch b
 when b % N == r (weak scaling: 64 frames per rank per step).
 
+--config 5 (BASELINE.json configs[4], 256 camera streams): stream s lives on
+rank s mod N with its own envelope and tracker; a step is the current frame of
+every stream (each rank: fizi_process_frames over its 256/N streams, then one
+NCCL all_gather of the step's records for a global view; strong scaling).
+
 Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle instead
 (the reference arm for this tier).
 """
@@ -240,47 +245,53 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
 
     S = cfg.streams
-    # C5: each call takes the current frame of every stream (256 per call;
-    # 32 per call is 1.9x slower: scripts/gpu_c5_batch.sh)
-    B = args.batch or (S if S > 1 else cfg.batch)
-    if S > 1 and sharded:
-        raise SystemExit("bench: the multi-stream config (C5) is measured at N = 1 only")
     from paper_1907_04393_b200 import shard
-    # round r: rank takes batch r*world + rank (weak scaling, B frames per rank
-    # per step); the resident rounds are cycled if warmup + steps exceeds them
-    need = min(shard.n_rounds(cfg.n_proc, B, world), args.warmup + args.steps)
     frames_by_round = []
     if S > 1:
-        # C5: round r = frame k = r // G of the streams of group g = r % G
-        # (G groups of B consecutive streams): every call holds B streams,
-        # one frame each, with per-stream envelopes and per-stream folds
-        G5 = -(-S // B)
+        # C5: camera streams are sharded, stream s on rank s mod N with its
+        # own envelope and tracker (local id = index in the rank's shard);
+        # each call takes the current frame of B of the rank's streams
+        # (default: all of them; 32 per call is 1.9x slower at N = 1,
+        # scripts/gpu_c5_batch.sh), round r = frame k = r // G5 of group
+        # g = r % G5 of the rank's streams
+        sids_r = shard.stream_shard(S, world, rank)
+        S_r = len(sids_r)
+        B = min(args.batch or S_r, S_r) if not sharded else S_r
+        G5 = -(-S_r // B)
         need = min(G5 * cfg.n_proc, args.warmup + args.steps)
-    for rnd in range(need if S > 1 else 0):
-        g, k = rnd % G5, rnd // G5
-        sids = list(range(g * B, min(S, (g + 1) * B)))
-        fr = torch.empty((len(sids), cfg.H, cfg.W, 3), dtype=torch.uint8, device=dev)
-        for j, sid in enumerate(sids):
-            synth.frames_dev(cfg, sid, [k], out=fr[j:j + 1], device=dev)
-        frames_by_round.append((sids, fr, np.full(len(sids), synth.t_ms(k), np.int64)))
-    for rnd in range(need if S == 1 else 0):
-        b = shard.round_batch(cfg.n_proc, B, world, rank, rnd)
-        if b is None:
-            frames_by_round.append(None)
-            continue
-        ks = list(range(b.k0, b.k1))
-        t_base = np.asarray([synth.t_ms(k) for k in ks], np.int64)
-        if args.diag_no_hand:
-            pf = synth.frame_params(cfg, 0, ks)
-            pf[:, 4] = 0
-            fr = synth.gen_dev(cfg.W, cfg.H, cfg.seed, 0, pf, synth.clutter(cfg, 0), device=dev)
-        else:
-            fr = synth.frames_dev(cfg, 0, ks, device=dev)
-        frames_by_round.append((ks, fr, t_base))
-    fz = Fizi(cfg.W, cfg.H, n_streams=S, max_batch=B, device=local)
-    for sid in range(S):
+        for rnd in range(need):
+            g, k = rnd % G5, rnd // G5
+            loc = list(range(g * B, min(S_r, (g + 1) * B)))
+            fr = torch.empty((len(loc), cfg.H, cfg.W, 3), dtype=torch.uint8, device=dev)
+            for j, l in enumerate(loc):
+                synth.frames_dev(cfg, sids_r[l], [k], out=fr[j:j + 1], device=dev)
+            frames_by_round.append((loc, fr, np.full(len(loc), synth.t_ms(k), np.int64)))
+    else:
+        S_r = 1
+        B = args.batch or cfg.batch
+        # round r: rank takes batch r*world + rank (weak scaling, B frames per
+        # rank per step); the resident rounds are cycled if warmup + steps
+        # exceeds them
+        need = min(shard.n_rounds(cfg.n_proc, B, world), args.warmup + args.steps)
+        for rnd in range(need):
+            b = shard.round_batch(cfg.n_proc, B, world, rank, rnd)
+            if b is None:
+                frames_by_round.append(None)
+                continue
+            ks = list(range(b.k0, b.k1))
+            t_base = np.asarray([synth.t_ms(k) for k in ks], np.int64)
+            if args.diag_no_hand:
+                pf = synth.frame_params(cfg, 0, ks)
+                pf[:, 4] = 0
+                fr = synth.gen_dev(cfg.W, cfg.H, cfg.seed, 0, pf, synth.clutter(cfg, 0), device=dev)
+            else:
+                fr = synth.frames_dev(cfg, 0, ks, device=dev)
+            frames_by_round.append((ks, fr, t_base))
+    fz = Fizi(cfg.W, cfg.H, n_streams=S_r, max_batch=B, device=local)
+    for loc in range(S_r):
+        sid = sids_r[loc] if S > 1 else 0
         learn = synth.frames_dev(cfg, sid, range(cfg.n_learn), learning=True, device=dev)
-        fz.learn_background(learn, stream=sid, margin=synth.MARGIN)
+        fz.learn_background(learn, stream=loc, margin=synth.MARGIN)
     # N = 1: pipelined calls (a call's tail overlaps the next calls'
     # segmentation), so outputs rotate over CALL_SLOTS buffers and the timed
     # region ends with fz.flush() (N > 1: segment_frames, windowed gather + fold)
@@ -290,8 +301,9 @@ def main():
     # a fold stream (one NCCL all_gather per window), while the next window's
     # calls run; the folds of every rank cover every frame, in frame order
     G = max(1, args.gather_every) if sharded else 1
-    resw = torch.empty((G, B, RESULT_BYTES), dtype=torch.uint8, device=dev)
-    gathered_w = torch.empty((world * G * B, RESULT_BYTES), dtype=torch.uint8, device=dev)
+    Bg = shard.streams_per_rank(S, world) if S > 1 else B   # rows per rank and step in the gather
+    resw = torch.zeros((G, Bg, RESULT_BYTES), dtype=torch.uint8, device=dev)
+    gathered_w = torch.empty((world * G * Bg, RESULT_BYTES), dtype=torch.uint8, device=dev)
     fold_stream = torch.cuda.Stream(device=dev)
     window = []
     NBUF = CALL_SLOTS                    # = the context's call slots (include/fizi.h)
@@ -322,7 +334,10 @@ def main():
             if not sharded:            # the whole path in one call (fold fused into labelling)
                 fz.process_frames(fr_n, streams=sids, t_ms=t, masks=mk, results=res_n)
                 return n
-            fz.segment_frames(fr_n, t_ms=t, masks=mk, results=resw[len(window)][:n])
+            if S > 1:                  # streams are rank-local: the whole path, folds included
+                fz.process_frames(fr_n, streams=sids, t_ms=t, masks=mk, results=resw[len(window)][:n])
+            else:                      # one stream across ranks: stateless part, fold after the gather
+                fz.segment_frames(fr_n, t_ms=t, masks=mk, results=resw[len(window)][:n])
         window.append(rnd)
         if len(window) == G:
             drain()
@@ -340,8 +355,9 @@ def main():
             dist.all_gather_into_tensor(gathered_w, resw)
             gathered_ev = torch.cuda.Event()
             gathered_ev.record(fold_stream)
-            for o, cnt in shard.window_slices(cfg.n_proc, B, world, window, G):
-                fz.track(gathered_w[o: o + cnt])
+            if S == 1:                      # (C5: records already folded per stream, on their rank)
+                for o, cnt in shard.window_slices(cfg.n_proc, B, world, window, G):
+                    fz.track(gathered_w[o: o + cnt])
         main.wait_event(gathered_ev)        # resw is free for the next window
         window.clear()
 
@@ -451,20 +467,23 @@ def main():
         "mpix_per_s": value * N / 1e6, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
         "host_enqueue_ms_per_step": host_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "scaling": "weak" if S == 1 else "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
         "config": {"workload": (f"C{cfg.cid}: {cfg.W}x{cfg.H} stream, {cfg.n_proc} frames, "
                                 f"batches of {B} per launch (BASELINE.json configs[{cfg.cid - 1}])"
                                 if S == 1 else
                                 f"C{cfg.cid}: {S} streams of {cfg.W}x{cfg.H}, {cfg.n_proc} frames "
-                                f"each, per-stream envelopes; batches of one frame from each of "
-                                f"{B} streams (BASELINE.json configs[{cfg.cid - 1}])"),
+                                f"each, per-stream envelopes, stream s on rank s mod {world}; "
+                                f"each call takes the current frame of {B} of the rank's "
+                                f"{S_r} streams (BASELINE.json configs[{cfg.cid - 1}])"),
                    "frames_per_step_per_gpu": B, "pipelined_calls": pipelined,
                    "sharded_path": sharded, "resident_batches_per_gpu": need,
                    "l2": (f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step"
                           if B * 3 * N > 126e6 else
                           f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step, "
                           f"cycled over {need} resident batches ({need * B * 3 * N / 1e9:.1f} GB)"),
-                   "parallelism": f"frames sharded by batch, dp{world}"},
+                   "parallelism": (f"frames sharded by batch, dp{world}" if S == 1 else
+                                   f"camera streams sharded (s mod {world}), dp{world}")},
         "gpu_launches": launches,
         "roofline": roofline,
         "clocks": clk.summary(),

@@ -70,3 +70,39 @@ def window_slices(n_frames: int, batch: int, world: int, rounds, window: int):
             r = off // batch
             out.append((r * window * batch + j * batch, n))
     return out
+
+
+# ------------------------------------------------ camera-stream sharding (C5)
+# Many independent camera streams (BASELINE.json configs[4]): stream s lives
+# on rank s mod world with its own envelope and tracker state, so no exchange
+# is needed for correctness; each step the ranks all-gather the step's
+# records (one per stream) for a global view.
+
+def stream_shard(n_streams: int, world: int, rank: int) -> list[int]:
+    """Global ids of the streams rank `rank` owns (s mod world == rank), in order;
+    a stream's local id on its rank is its index in this list."""
+    return list(range(rank, n_streams, world))
+
+
+def streams_per_rank(n_streams: int, world: int) -> int:
+    """Records each rank contributes per step to the gather (the largest shard;
+    smaller shards pad)."""
+    return math.ceil(n_streams / world)
+
+
+def gathered_stream_ids(n_streams: int, world: int) -> list[int]:
+    """Global stream id of every row of a gathered step buffer (world blocks of
+    streams_per_rank rows, rank r's block first), -1 for padding rows."""
+    per = streams_per_rank(n_streams, world)
+    out = []
+    for r in range(world):
+        mine = stream_shard(n_streams, world, r)
+        out.extend(mine + [-1] * (per - len(mine)))
+    return out
+
+
+def stream_order(n_streams: int, world: int) -> list[int]:
+    """Row of the gathered step buffer holding global stream s, for s = 0..n-1."""
+    ids = gathered_stream_ids(n_streams, world)
+    pos = {s: i for i, s in enumerate(ids) if s >= 0}
+    return [pos[s] for s in range(n_streams)]

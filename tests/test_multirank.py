@@ -188,3 +188,84 @@ def test_two_ranks_match_single_process(cid, n_frames, batch):
     ref = _fold(p, _to_result_bytes(recs, range(n_frames)).view(RESULT_DTYPE).reshape(-1))
     for r in range(world):
         assert results[r] == ref
+
+
+# ------------------------------------------------ camera-stream sharding (C5)
+def test_stream_shard_partition():
+    for S, world in [(256, 1), (256, 2), (256, 8), (6, 4), (5, 2), (3, 8)]:
+        owned = [shard.stream_shard(S, world, r) for r in range(world)]
+        flat = sorted(s for o in owned for s in o)
+        assert flat == list(range(S))
+        assert all(s % world == r for r, o in enumerate(owned) for s in o)
+        ids = shard.gathered_stream_ids(S, world)
+        assert len(ids) == world * shard.streams_per_rank(S, world)
+        order = shard.stream_order(S, world)
+        assert [ids[i] for i in order] == list(range(S))
+
+
+def _stream_worker(rank, world, port, n_streams, n_steps, q):
+    """bench.py's sharded C5 path with the oracle in place of the GPU: rank r
+    owns streams s mod world == r (their envelopes and trackers), processes
+    the current frame of each per step, and the step's records are
+    all-gathered into a global view."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.CONFIGS[5]
+    p = oracle.make_params(cfg.W, cfg.H)
+    mine = shard.stream_shard(n_streams, world, rank)
+    per = shard.streams_per_rank(n_streams, world)
+    envs = {s: oracle.learn(synth.learning_frames_host(cfg, s), synth.MARGIN) for s in mine}
+    trackers = {s: oracle.Tracker(p) for s in mine}
+    order = shard.stream_order(n_streams, world)
+    views = []
+    for k in range(n_steps):
+        buf = torch.zeros(per, RESULT_BYTES, dtype=torch.uint8)
+        rows = np.zeros(per, RESULT_DTYPE)
+        for j, s in enumerate(mine):
+            rec, _ = oracle.segment(p, synth.frames_host(cfg, s, [k])[0], *envs[s],
+                                    t_ms=synth.t_ms(k), stages=False)
+            trackers[s].update(rec)
+            rows[j]["t_ms"] = rec.t_ms
+            rows[j]["stream"] = s
+            rows[j]["blob_area"] = rec.blob_area
+            rows[j]["cx"], rows[j]["cy"] = rec.cx, rec.cy
+            rows[j]["visible"], rows[j]["px"], rows[j]["py"] = rec.visible, rec.px, rec.py
+        buf[:] = torch.from_numpy(rows.view(np.uint8).reshape(per, RESULT_BYTES))
+        parts = [torch.zeros(per, RESULT_BYTES, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(parts, buf)
+        g = torch.cat(parts).numpy().view(RESULT_DTYPE).reshape(-1)[order]
+        views.append([(int(r["stream"]), int(r["t_ms"]), int(r["blob_area"]), float(r["px"]),
+                       float(r["py"]), int(r["visible"])) for r in g])
+    q.put((rank, views))
+    dist.destroy_process_group()
+
+
+def test_two_ranks_stream_sharding_matches_single_process():
+    world, n_streams, n_steps = 2, 5, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stream_worker, args=(r, world, port, n_streams, n_steps, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = dict(q.get(timeout=600) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    # reference: one process, every stream with its own envelope and tracker
+    cfg = synth.CONFIGS[5]
+    p = oracle.make_params(cfg.W, cfg.H)
+    ref = []
+    trackers = [oracle.Tracker(p) for _ in range(n_streams)]
+    envs = [oracle.learn(synth.learning_frames_host(cfg, s), synth.MARGIN) for s in range(n_streams)]
+    for k in range(n_steps):
+        step = []
+        for s in range(n_streams):
+            rec, _ = oracle.segment(p, synth.frames_host(cfg, s, [k])[0], *envs[s],
+                                    t_ms=synth.t_ms(k), stages=False)
+            trackers[s].update(rec)
+            step.append((s, rec.t_ms, rec.blob_area, rec.px, rec.py, rec.visible))
+        ref.append(step)
+    for r in range(world):
+        assert results[r] == ref
