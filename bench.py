@@ -302,7 +302,13 @@ def main():
     # calls run; the folds of every rank cover every frame, in frame order
     G = max(1, args.gather_every) if sharded else 1
     Bg = shard.streams_per_rank(S, world) if S > 1 else B   # rows per rank and step in the gather
-    resw = torch.zeros((G, Bg, RESULT_BYTES), dtype=torch.uint8, device=dev)
+    # windows rotate over NWIN record buffers: a window's calls wait only for
+    # the gather of the window NWIN back (not for the previous window's tails)
+    NWIN = 4
+    resw_ring = [torch.zeros((G, Bg, RESULT_BYTES), dtype=torch.uint8, device=dev)
+                 for _ in range(NWIN)]
+    ev_ring = [None] * NWIN
+    win_no = [0]
     gathered_w = torch.empty((world * G * Bg, RESULT_BYTES), dtype=torch.uint8, device=dev)
     fold_stream = torch.cuda.Stream(device=dev)
     window = []
@@ -335,13 +341,20 @@ def main():
                 fz.process_frames(fr_n, streams=sids, t_ms=t, masks=mk, results=res_n)
                 return n
             if S > 1:                  # streams are rank-local: the whole path, folds included
-                fz.process_frames(fr_n, streams=sids, t_ms=t, masks=mk, results=resw[len(window)][:n])
+                fz.process_frames(fr_n, streams=sids, t_ms=t, masks=mk, results=cur_resw()[len(window)][:n])
             else:                      # one stream across ranks: stateless part, fold after the gather
-                fz.segment_frames(fr_n, t_ms=t, masks=mk, results=resw[len(window)][:n])
+                fz.segment_frames(fr_n, t_ms=t, masks=mk, results=cur_resw()[len(window)][:n])
         window.append(rnd)
         if len(window) == G:
             drain()
         return n
+
+    def cur_resw():
+        w = win_no[0] % NWIN
+        if not window and ev_ring[w] is not None:
+            torch.cuda.current_stream(dev).wait_event(ev_ring[w])   # its previous gather is done
+            ev_ring[w] = None
+        return resw_ring[w]
 
     def drain():
         # a8 across ranks: gather the window's records (frame order = step
@@ -352,13 +365,22 @@ def main():
         fold_stream.wait_stream(main)
         with torch.cuda.stream(fold_stream):
             fz.flush()                      # the window's tails, joined into the fold stream
-            dist.all_gather_into_tensor(gathered_w, resw)
+            dist.all_gather_into_tensor(gathered_w, resw_ring[win_no[0] % NWIN])
             gathered_ev = torch.cuda.Event()
             gathered_ev.record(fold_stream)
+            ev_ring[win_no[0] % NWIN] = gathered_ev
             if S == 1:                      # (C5: records already folded per stream, on their rank)
+                # the window's records in frame order: runs of rows of
+                # the rank blocks (step-major, then rank)
+                runs = []
                 for o, cnt in shard.window_slices(cfg.n_proc, B, world, window, G):
-                    fz.track(gathered_w[o: o + cnt])
-        main.wait_event(gathered_ev)        # resw is free for the next window
+                    if runs and runs[-1][0] + runs[-1][1] == o:
+                        runs[-1][1] += cnt
+                    else:
+                        runs.append([o, cnt])
+                for i in range(0, len(runs), 256):  # the window's folds in one launch
+                    fz.track_runs(gathered_w, runs[i:i + 256])
+        win_no[0] += 1
         window.clear()
 
     def finish():

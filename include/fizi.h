@@ -150,6 +150,15 @@ int fizi_segment_frames(fizi_ctx *ctx, const uint32_t *stream_of_frame_host,
 int fizi_track(fizi_ctx *ctx, uint32_t stream, fizi_result *results_dev, uint32_t n,
                fizi_stream_t cuda_stream);
 
+/* a8 over records gathered from several ranks: folds, through stream
+ * `stream`'s tracker state, the n_runs (<= 256) runs of consecutive records
+ * results_dev[run_off[k] .. run_off[k] + run_len[k]) for k = 0 .. n_runs-1, in
+ * that order (run_off / run_len: host arrays); = fizi_track on the
+ * concatenation of the runs, in one launch.  FIZI_E_ARG if n_runs > 256. */
+int fizi_track_runs(fizi_ctx *ctx, uint32_t stream, fizi_result *results_dev,
+                    const uint32_t *run_off_host, const uint32_t *run_len_host, uint32_t n_runs,
+                    fizi_stream_t cuda_stream);
+
 /* End-to-end variant of fizi_process_frames on HOST buffers: copies frames
  * (n*W*H*3 bytes) host->device, runs the path, copies masks (may be NULL) and
  * results back device->host, all on cuda_stream; returns after the stream has

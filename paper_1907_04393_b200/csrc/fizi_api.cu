@@ -874,6 +874,26 @@ int fizi_track(fizi_ctx* ctx, uint32_t stream, fizi_result* results_dev, uint32_
   return FIZI_OK;
 }
 
+int fizi_track_runs(fizi_ctx* ctx, uint32_t stream, fizi_result* results_dev,
+                    const uint32_t* run_off, const uint32_t* run_len, uint32_t n_runs,
+                    fizi_stream_t cuda_stream) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (n_runs > fizi::kMaxTrackRuns) return fail(c, FIZI_E_ARG, "n_runs must be <= 256");
+  if (n_runs == 0) return FIZI_OK;
+  if (!results_dev || !run_off || !run_len) return fail(c, FIZI_E_ARG, "NULL pointer argument");
+  DeviceGuard guard(c.device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  cudaError_t e = join_tail(c, st);                   // fold order after pipelined tails
+  prof_begin(c, st);
+  if (e == cudaSuccess) e = fizi::launch_track_runs(c, stream, results_dev, run_off, run_len, n_runs, st);
+  prof_end(c, FIZI_PROF_TRACK, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "track runs");
+  return FIZI_OK;
+}
+
 int fizi_process_frames_host(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* frames_host,
                              uint32_t n, uint32_t width, uint32_t height, const int64_t* t_ms,
                              uint8_t* masks_host, fizi_result* results_host,

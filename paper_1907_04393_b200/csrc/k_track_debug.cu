@@ -43,45 +43,44 @@ constexpr int kTrackChunk = 512;
 __global__ void __launch_bounds__(256) track_stream_kernel(fizi_params p, uint32_t n,
                                                            fizi_result* __restrict__ res,
                                                            TrackState* __restrict__ ts) {
-  __shared__ int64_t t_s[kTrackChunk], dw_s[kTrackChunk];
+  __shared__ int64_t t_s[kTrackChunk];
   __shared__ double cx_s[kTrackChunk], cy_s[kTrackChunk];
-  __shared__ uint32_t area_s[kTrackChunk];
-  __shared__ uint8_t vis_s[kTrackChunk], clk_s[kTrackChunk];
+  __shared__ uint32_t ar_s[kTrackChunk];
+  __shared__ int64_t dw_o[kTrackChunk];
+  __shared__ double px_o[kTrackChunk], py_o[kTrackChunk];
+  __shared__ uint8_t vc_o[kTrackChunk];
   TrackState st;
   if (threadIdx.x == 0) st = *ts;
   for (uint32_t base = 0; base < n; base += kTrackChunk) {
     const uint32_t m = min((uint32_t)kTrackChunk, n - base);
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
       const fizi_result& r = res[base + i];
-      t_s[i] = r.t_ms;
-      area_s[i] = r.blob_area;
-      cx_s[i] = r.cx;
-      cy_s[i] = r.cy;
+      t_s[i] = r.t_ms; ar_s[i] = r.blob_area; cx_s[i] = r.cx; cy_s[i] = r.cy;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+      // the next record's inputs are loaded before the current fold step
+      // (separate output arrays: no aliasing between the two)
+      int64_t t_n = t_s[0];
+      uint32_t a_n = ar_s[0];
+      double x_n = cx_s[0], y_n = cy_s[0];
       for (uint32_t i = 0; i < m; i++) {
         fizi_result r;
-        r.t_ms = t_s[i];
-        r.blob_area = area_s[i];
-        r.cx = cx_s[i];
-        r.cy = cy_s[i];
+        r.t_ms = t_n; r.blob_area = a_n; r.cx = x_n; r.cy = y_n;
+        if (i + 1 < m) { t_n = t_s[i + 1]; a_n = ar_s[i + 1]; x_n = cx_s[i + 1]; y_n = cy_s[i + 1]; }
         track_one(p, st, r);
-        vis_s[i] = r.visible;
-        clk_s[i] = r.clicked;
-        cx_s[i] = r.px;                        // reuse the centroid slots for the pointer
-        cy_s[i] = r.py;
-        dw_s[i] = r.dwell_ms;
+        dw_o[i] = r.dwell_ms; px_o[i] = r.px; py_o[i] = r.py;
+        vc_o[i] = (uint8_t)(r.visible | (r.clicked << 1));
       }
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
       fizi_result& r = res[base + i];
-      r.visible = vis_s[i];
-      r.clicked = clk_s[i];
-      r.px = cx_s[i];
-      r.py = cy_s[i];
-      r.dwell_ms = dw_s[i];
+      r.visible = vc_o[i] & 1u;
+      r.clicked = vc_o[i] >> 1;
+      r.px = px_o[i];
+      r.py = py_o[i];
+      r.dwell_ms = dw_o[i];
     }
     __syncthreads();
   }
@@ -384,6 +383,75 @@ cudaError_t launch_track_batch(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res
 cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,
                                 cudaStream_t st) {
   track_stream_kernel<<<1, 256, 0, st>>>(c.p, n, res, reinterpret_cast<TrackState*>(c.tstate) + stream);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
+// fizi_track_runs: the records of up to kMaxRuns runs of consecutive rows,
+// folded run after run (rows of a window gathered from several ranks, in
+// frame order).  Inputs are staged run by run through the same chunked
+// shared-memory scheme as track_stream_kernel; the fold order is the
+// concatenation of the runs.
+struct TrackRuns {
+  uint32_t n_runs;
+  uint32_t off[kMaxTrackRuns], len[kMaxTrackRuns];
+};
+
+__global__ void __launch_bounds__(256) track_runs_kernel(fizi_params p, TrackRuns runs,
+                                                         fizi_result* __restrict__ res,
+                                                         TrackState* __restrict__ ts) {
+  __shared__ int64_t t_s[kTrackChunk];
+  __shared__ double cx_s[kTrackChunk], cy_s[kTrackChunk];
+  __shared__ uint32_t ar_s[kTrackChunk];
+  __shared__ int64_t dw_o[kTrackChunk];
+  __shared__ double px_o[kTrackChunk], py_o[kTrackChunk];
+  __shared__ uint8_t vc_o[kTrackChunk];
+  TrackState st;
+  if (threadIdx.x == 0) st = *ts;
+  for (uint32_t k = 0; k < runs.n_runs; k++) {
+    fizi_result* rr = res + runs.off[k];
+    const uint32_t n = runs.len[k];
+    for (uint32_t base = 0; base < n; base += kTrackChunk) {
+      const uint32_t m = min((uint32_t)kTrackChunk, n - base);
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const fizi_result& r = rr[base + i];
+        t_s[i] = r.t_ms; ar_s[i] = r.blob_area; cx_s[i] = r.cx; cy_s[i] = r.cy;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int64_t t_n = t_s[0];
+        uint32_t a_n = ar_s[0];
+        double x_n = cx_s[0], y_n = cy_s[0];
+        for (uint32_t i = 0; i < m; i++) {
+          fizi_result r;
+          r.t_ms = t_n; r.blob_area = a_n; r.cx = x_n; r.cy = y_n;
+          if (i + 1 < m) { t_n = t_s[i + 1]; a_n = ar_s[i + 1]; x_n = cx_s[i + 1]; y_n = cy_s[i + 1]; }
+          track_one(p, st, r);
+          dw_o[i] = r.dwell_ms; px_o[i] = r.px; py_o[i] = r.py;
+          vc_o[i] = (uint8_t)(r.visible | (r.clicked << 1));
+        }
+      }
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        fizi_result& r = rr[base + i];
+        r.visible = vc_o[i] & 1u;
+        r.clicked = vc_o[i] >> 1;
+        r.px = px_o[i];
+        r.py = py_o[i];
+        r.dwell_ms = dw_o[i];
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) *ts = st;
+}
+
+cudaError_t launch_track_runs(Ctx& c, uint32_t stream, fizi_result* res, const uint32_t* off,
+                              const uint32_t* len, uint32_t n_runs, cudaStream_t st) {
+  TrackRuns r;
+  r.n_runs = n_runs;
+  for (uint32_t k = 0; k < n_runs; k++) { r.off[k] = off[k]; r.len[k] = len[k]; }
+  track_runs_kernel<<<1, 256, 0, st>>>(c.p, r, res, reinterpret_cast<TrackState*>(c.tstate) + stream);
   c.launches += 1;
   return cudaGetLastError();
 }

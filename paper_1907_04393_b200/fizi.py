@@ -103,6 +103,7 @@ def lib() -> ctypes.CDLL:
         for fn in (L.fizi_process_frames, L.fizi_segment_frames, L.fizi_process_frames_host):
             fn.argtypes = [vp, vp, vp, u32, u32, u32, vp, vp, vp, vp]
         L.fizi_track.argtypes = [vp, u32, vp, u32, vp]
+        L.fizi_track_runs.argtypes = [vp, u32, vp, vp, vp, u32, vp]
         L.fizi_reset_tracker.argtypes = [vp, u32, vp]
         L.fizi_debug_stage.argtypes = [vp, i32, u32, vp, vp]
         L.fizi_get_background.argtypes = [vp, u32, vp, vp, vp]
@@ -132,7 +133,7 @@ def lib() -> ctypes.CDLL:
         for name in ("fizi_set_pipeline", "fizi_flush", "fizi_wheel_default", "fizi_set_wheel",
                      "fizi_drive", "fizi_drive_throttle", "fizi_relearn_flags", "fizi_set_zones", "fizi_hit_test", "fizi_params_default", "fizi_create", "fizi_learn_background",
                      "fizi_process_frames", "fizi_segment_frames", "fizi_process_frames_host",
-                     "fizi_track", "fizi_reset_tracker", "fizi_debug_stage",
+                     "fizi_track", "fizi_track_runs", "fizi_reset_tracker", "fizi_debug_stage",
                      "fizi_get_background", "fizi_set_background", "fizi_get_lut_table"):
             getattr(L, name).restype = i32
         _lib = L
@@ -151,6 +152,9 @@ def default_params(width: int, height: int, **kw) -> Params:
 
 def _stream_handle(device) -> int:
     import torch
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:                         # the current stream's handle, without a Stream object
+        return raw(device.index if hasattr(device, "index") else int(device))
     return torch.cuda.current_stream(device).cuda_stream
 
 
@@ -177,6 +181,7 @@ class Fizi:
         self._zeros_u32 = np.zeros(self.max_batch, np.uint32)
         self._zeros_i64 = np.zeros(self.max_batch, np.int64)
         self.device = torch.device("cuda", device)
+        self._dev_index = int(device)
         self.params = default_params(self.W, self.H, **params)
         self._h = ctypes.c_void_p()
         rc = lib().fizi_create(ctypes.byref(self.params), device, self.n_streams,
@@ -200,7 +205,7 @@ class Fizi:
             frames = frames.unsqueeze(0)
         if frames.dim() != 4 or frames.shape[3] != 3:
             raise ValueError("frames must have shape (n, H, W, 3)")
-        if frames.device != self.device:
+        if frames.get_device() != self._dev_index:
             raise ValueError(f"frames are on {frames.device}, the context on {self.device}")
         return frames
 
@@ -210,7 +215,7 @@ class Fizi:
         import torch
         if not (isinstance(t, torch.Tensor) and t.is_cuda):
             raise TypeError(f"{what} must be a CUDA tensor")
-        if t.device != self.device:
+        if t.get_device() != self._dev_index:
             raise ValueError(f"{what} is on {t.device}, the context on {self.device}")
         if not t.is_contiguous():
             raise ValueError(f"{what} must be contiguous")
@@ -253,7 +258,8 @@ class Fizi:
         n = frames.shape[0]
         if streams is None:
             streams = self._zeros_u32[:n] if n <= self.max_batch else np.zeros(n, np.uint32)
-        else:
+        elif not (isinstance(streams, np.ndarray) and streams.dtype == np.uint32
+                  and streams.shape == (n,) and streams.flags.c_contiguous):
             streams = _u32(np.broadcast_to(np.asarray(streams, np.uint32), (n,)))
         if t_ms is None:
             t = self._zeros_i64[:n] if n <= self.max_batch else np.zeros(n, np.int64)
@@ -295,6 +301,21 @@ class Fizi:
         self._dev_buf(results, n * RESULT_BYTES, "results")
         self._check(lib().fizi_track(self._h, stream, results.data_ptr(), n,
                                      _stream_handle(self.device)), "fizi_track")
+        return results
+
+    def track_runs(self, results, runs, stream: int = 0):
+        """Fold the rows results[o:o+n] for (o, n) in runs, in that order, through
+        stream's tracker (one launch; records gathered from several ranks)."""
+        runs = list(runs)
+        n_all = results.shape[0]
+        self._dev_buf(results, n_all * RESULT_BYTES, "results")
+        off = _u32([o for o, _ in runs])
+        ln = _u32([n for _, n in runs])
+        if any(o + n > n_all for o, n in runs):
+            raise ValueError("a run exceeds the results buffer")
+        self._check(lib().fizi_track_runs(self._h, stream, results.data_ptr(), off.ctypes.data,
+                                          ln.ctypes.data, len(runs), _stream_handle(self.device)),
+                    "fizi_track_runs")
         return results
 
     def process_frames_host(self, frames: np.ndarray, streams=None, t_ms=None,

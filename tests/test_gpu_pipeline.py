@@ -129,3 +129,48 @@ def test_reset_tracker_ordered_after_pipelined_fold():
     a, b = results_numpy(r1), results_numpy(r2)
     assert a.tobytes() == b.tobytes()
     fz.close()
+
+
+def test_track_runs_equals_track_of_concatenation():
+    """fizi_track_runs (the sharded path's window fold: rows of several rank
+    blocks, in frame order, one launch) equals fizi_track over the
+    concatenated records, and the oracle fold."""
+    cfg = synth.CONFIGS[3]
+    ks = list(range(95, 95 + 24))                       # a dwell pause starts at frame 100
+    learn = synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True, device=DEV)
+    frames = synth.frames_dev(cfg, 0, ks, device=DEV)
+    t = np.array([synth.t_ms(k) for k in ks], np.int64)
+    seg = Fizi(cfg.W, cfg.H, max_batch=24)
+    seg.learn_background(learn, margin=synth.MARGIN)
+    _, rec = seg.segment_frames(frames, t_ms=t, masks=None)
+    # a "gathered" buffer: 2 rank blocks of 2 steps x 6 rows, frames laid out
+    # step-major, then rank (rank r's step j = frames (2j + r) * 6 ..)
+    G, B, world = 2, 6, 2
+    gathered = torch.empty((world * G * B, RESULT_BYTES), dtype=torch.uint8, device=DEV)
+    runs = []
+    for j in range(G):
+        for r in range(world):
+            src = (j * world + r) * B
+            dst = r * G * B + j * B
+            gathered[dst: dst + B] = rec[src: src + B]
+            runs.append((dst, B))
+    ref = rec[: world * G * B].clone()
+    a = Fizi(cfg.W, cfg.H, max_batch=24)
+    b = Fizi(cfg.W, cfg.H, max_batch=24)
+    a.track(ref)
+    b.track_runs(gathered, runs)
+    torch.cuda.synchronize()
+    got = torch.cat([gathered[o: o + n] for o, n in runs])
+    assert torch.equal(got, ref)
+    p = oracle.make_params(cfg.W, cfg.H)
+    tr = oracle.Tracker(p)
+    rows = results_numpy(ref)
+    for i, row in enumerate(rows):
+        o = oracle.record_from_blob(int(row["t_ms"]), int(row["blob_area"]), float(row["cx"]),
+                                    float(row["cy"]))
+        tr.update(o)
+        assert (int(row["visible"]), int(row["clicked"]), int(row["dwell_ms"])) == (
+            o.visible, o.clicked, o.dwell_ms), i
+        assert abs(float(row["px"]) - o.px) <= 1e-3 and abs(float(row["py"]) - o.py) <= 1e-3
+    for fz in (seg, a, b):
+        fz.close()
