@@ -28,10 +28,14 @@ def _obj(src: str) -> str:
     return os.path.join(OBJ_DIR, os.path.basename(src)[:-3] + ".o")
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+CHECKED_LIB = os.path.join(HERE, "libfizi_checked.so")
+CHECKED_FLAGS = ["-DFIZI_DEVICE_CHECKS"]
+
+
+def needs_build(lib_path: str = LIB) -> bool:
+    if not os.path.exists(lib_path):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib_path)
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
@@ -40,15 +44,16 @@ def build(force: bool = False, nvcc: str = "nvcc", verbose: bool = False,
     """Compile (changed) objects in parallel and link `out` (default libfizi.so).
     extra_flags (e.g. -DFIZI_...) force a full rebuild into a separate object dir."""
     lib_path = out or LIB
-    if not force and not extra_flags and lib_path == LIB and not needs_build():
+    if not force and not needs_build(lib_path):
         return lib_path
-    obj_dir = OBJ_DIR if not extra_flags else OBJ_DIR + "_" + str(abs(hash(tuple(extra_flags))))
+    obj_dir = OBJ_DIR if not extra_flags else OBJ_DIR + "_" + "_".join(
+        f.lstrip("-").replace("=", "_") for f in extra_flags)
     os.makedirs(obj_dir, exist_ok=True)
     hdr_t = max(os.path.getmtime(h) for h in HEADERS)
 
     def compile_one(src: str):
         obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
-        if (not force and not extra_flags and os.path.exists(obj)
+        if (not force and os.path.exists(obj)
                 and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t)):
             return src, ""
         cmd = [nvcc, *NVCC_FLAGS, *(extra_flags or []), "-I", os.path.join(ROOT, "include"),
@@ -89,5 +94,13 @@ def build(force: bool = False, nvcc: str = "nvcc", verbose: bool = False,
     return lib_path
 
 
+def build_checked(force: bool = False) -> str:
+    """libfizi_checked.so: the same sources with the device-side invariant
+    checks compiled in (FIZI_DCHECK, dev_util.cuh); selected at run time with
+    FIZI_LIB=checked (the sanitizer substitute on this pool)."""
+    return build(force=force, extra_flags=CHECKED_FLAGS, out=CHECKED_LIB)
+
+
 if __name__ == "__main__":
     print(build(force=True))
+    print(build_checked(force=True))

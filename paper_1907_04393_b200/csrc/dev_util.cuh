@@ -3,6 +3,26 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
+
+// Device-side invariant checks (bounds of every queue / run / list index the
+// kernels compute).  Compiled in only for the checked build
+// (-DFIZI_DEVICE_CHECKS, libfizi_checked.so): a violated check traps, which
+// surfaces as a sticky CUDA error in the calling test.
+#ifdef FIZI_DEVICE_CHECKS
+#define FIZI_DCHECK(cond)                                                              \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("FIZI_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define FIZI_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
 
 namespace fizi {
 

@@ -468,6 +468,7 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
   extern __shared__ __align__(16) uint8_t smc[];
   const uint32_t f = a.f0 + blockIdx.x;
   const uint32_t T = a.frame_runs[f];
+  FIZI_DCHECK(T <= a.cap_runs && f < a.call->n);
   __shared__ long long t_mark[10];
   if (a.trace && threadIdx.x == 0) t_mark[9] = clock64();
   if (T <= kCclSmemRuns) {

@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(256) morph_runs_kernel(MorphArgs a) {
     uint32_t base = 0;
     if (tx == 0) {
       if (cnt) base = atomicAdd(a.frame_runs + f, cnt);
+      FIZI_DCHECK(base + cnt <= a.cap_runs);
       a.row_cnt[(uint64_t)f * H + gy] = cnt;
       a.row_base[(uint64_t)f * H + gy] = base;
     }
@@ -396,6 +397,7 @@ struct MorphPipe {
     if (lane == 0 && total) base = atomicAdd(a.frame_runs + f, total);
     base = __shfl_sync(0xFFFFFFFFu, base, 0);
     const uint32_t row_base = base + incl - my_cnt;
+    FIZI_DCHECK(base + total <= a.cap_runs);
     if (lane < y_end - y0) {
       a.row_cnt[(uint64_t)f * H + y0 + lane] = my_cnt;
       a.row_base[(uint64_t)f * H + y0 + lane] = my_cnt ? row_base : 0u;

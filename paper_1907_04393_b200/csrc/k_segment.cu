@@ -88,6 +88,7 @@ __device__ __forceinline__ void finalize_frame(const SegArgs& a, uint32_t f,
   a.call->res[f] = r;
   if (r.corrected) {             // the LUT re-test rewrites every word of the frame
     const uint32_t pos = atomicAdd(&fix[0], 1u);
+    FIZI_DCHECK(pos < a.n);
     fix[1 + pos] = f;
   }
   (void)fg;
@@ -486,11 +487,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
           if (lane == 0) base = atomicAdd(&q_tail, (uint32_t)__popc(slow_words));
           base = __shfl_sync(0xFFFFFFFFu, base, 0);
           if (!(lane & 1)) {
-            if ((slow_words >> lane) & 1u)
-              q_item[base + __popc(slow_words & ((1u << lane) - 1u))] =
-                  (uint16_t)((i << 7) | (warp << 4) | (lane >> 1));
-            else if (valid)
+            const uint32_t qpos = base + __popc(slow_words & ((1u << lane) - 1u));
+            if ((slow_words >> lane) & 1u) {
+              FIZI_DCHECK(qpos < kFrameGroup * kWarpsPerCta * 16);
+              q_item[qpos] = (uint16_t)((i << 7) | (warp << 4) | (lane >> 1));
+            } else if (valid) {
               a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
+            }
           }
         } else if (a.write_zero && !(lane & 1) && valid) {
           a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
@@ -509,6 +512,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
         const uint32_t it = q_item[q];
         const uint32_t i = it >> 7, w = (it >> 4) & 7u, k = it & 15u;
         const uint32_t f = a.group_frames[f_begin + i];
+        FIZI_DCHECK(qb + q < a.n * a.nchunks * 16u && i < nf);
         a.slow_items[qb + q] = ((unsigned long long)f << 32) | ((tile * kWarpsPerCta + w) * 16u + k);
       }
     }
@@ -645,9 +649,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_multi_kernel(SegArgs a) {
         if (lane == 0) base = atomicAdd(a.slow_count, (uint32_t)__popc(slow_words));
         base = __shfl_sync(0xFFFFFFFFu, base, 0);
         if (!(lane & 1)) {
-          if ((slow_words >> lane) & 1u)
+          if ((slow_words >> lane) & 1u) {
+            FIZI_DCHECK(base + __popc(slow_words & ((1u << lane) - 1u)) < a.n * a.nchunks * 16u);
             a.slow_items[base + __popc(slow_words & ((1u << lane) - 1u))] =
                 ((unsigned long long)f << 32) | (c * 16u + (lane >> 1));
+          }
           else if (valid)
             a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
         }
@@ -713,6 +719,7 @@ __global__ void FIZI_SLOW_BOUNDS slow_words_kernel(SegArgs a) {
     const unsigned long long it = act ? a.slow_items[qi] : 0ull;
     const uint32_t f = (uint32_t)(it >> 32), wd = (uint32_t)it;
     const uint32_t cq = wd >> 4, k = wd & 15u;
+    FIZI_DCHECK(!act || (f < a.call->n && cq < a.nchunks));
     if (act && any_fix) {
       const uint64_t mean = (a.luma[f] + 500ull * a.N) / (1000ull * a.N);
       act = a.ctab[mean] == 0;
@@ -771,6 +778,7 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
   const uint8_t* frames = a.call->frames;
   for (uint64_t it = blockIdx.x; it < items; it += gridDim.x, phase ^= 1u) {
     const uint32_t f = a.fix[1 + it / a.tiles];
+    FIZI_DCHECK(f < a.call->n);
     const uint32_t tile = (uint32_t)(it % a.tiles);
     const uint64_t tile_off = (uint64_t)tile * kTileBytes;
     const uint64_t rem = a.frame_bytes - tile_off;
@@ -891,6 +899,7 @@ __global__ void finalize_kernel(uint32_t f0, uint32_t n, uint64_t N,
   call->res[f] = r;
   if (r.corrected) {
     const uint32_t pos = atomicAdd(&fix[0], 1u);
+    FIZI_DCHECK(pos < n);
     fix[1 + pos] = f;
     fg[f] = 0;
   }
