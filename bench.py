@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-pipeline", action="store_true",
                     help="N=1: join every call's tail into the stream (no cross-call overlap)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-spot-check", action="store_true")
     ap.add_argument("--cpu-sample-frames", type=int, default=0)
     ap.add_argument("--diag-no-masks", action="store_true",
                     help="diagnostic only: do not request the u8 masks (masks_dev = NULL)")
@@ -182,37 +183,114 @@ def run_reference(args, cfg, rank, world):
         "config": {"workload": f"C{cfg.cid} {cfg.W}x{cfg.H} stream, oracle sample of {per_step} "
                                f"frames per step", "frames_per_step": per_step},
         "cpu_baseline": {"value": v, "unit": "frames/s", "cores": cores, "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": f"{per_step} frames x {args.steps} steps of C{cfg.cid}"},
         "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
 
 
-def cpu_baseline(cfg, n_frames=0, target_s=10.0):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _oracle_pass(cfg, p, frames, envs, sids, nthreads, tracker):
+    """One pass of the oracle over the sample: frames of one stream in one
+    frame-parallel batch (+ the sequential fold), or one frame per stream
+    (C5: per-stream envelopes) over a thread pool."""
+    import oracle
+    if envs is None:
+        lo, hi = tracker[1]
+        recs, _ = oracle.segment_batch(p, frames, lo, hi, nthreads=nthreads, want_masks=True)
+        for r in recs:
+            tracker[0].update(r)
+        return
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(j):
+        lo, hi = envs[j]
+        recs, _ = oracle.segment_batch(p, frames[j:j + 1], lo, hi, nthreads=1, want_masks=True)
+        return recs[0]
+    with ThreadPoolExecutor(max_workers=nthreads) as ex:
+        recs = list(ex.map(one, range(len(frames))))
+    for j, r in enumerate(recs):
+        tracker[2][sids[j]].update(r)
+
+
+def cpu_baseline(cfg, n_frames=0, target_s=8.0, single_s=4.0):
+    """The oracle as it stands on the host cores: frame-parallel
+    over all cores (the reported value) and single-core, each a bounded sample
+    of passes over the first frames of the workload (C5: the first frame of
+    the first streams, each with its own envelope)."""
     import oracle
     import synth
     cores = os.cpu_count() or 1
     n = n_frames or max(8, min(64, 2 * cores))
-    learn = synth.learning_frames_host(cfg)
-    lo, hi = oracle.learn(learn, synth.MARGIN)
-    frames = synth.frames_host(cfg, 0, range(n))
     p = oracle.make_params(cfg.W, cfg.H)
-    # passes over the same n frames until ~10 s of CPU work (bounded sample)
-    passes, done, t0 = 0, 0, time.perf_counter()
-    tr = oracle.Tracker(p)
-    while True:
-        recs, _ = oracle.segment_batch(p, frames, lo, hi, nthreads=cores, want_masks=True)
-        for r in recs:
-            tr.update(r)
-        passes += 1
-        done += n
-        dt = time.perf_counter() - t0
-        if dt >= target_s or passes >= 200:
-            break
-    return {"value": done / dt, "unit": "frames/s", "cores": cores, "kind": "oracle",
-            "sample": f"{passes} passes over the first {n} frames of C{cfg.cid} ({cfg.W}x{cfg.H}) "
-                      f"= {done} frames, frame-parallel oracle (masks + records + fold) over "
-                      f"{cores} host threads, {dt:.1f} s"}
+    if cfg.streams == 1:
+        lo, hi = oracle.learn(synth.learning_frames_host(cfg), synth.MARGIN)
+        frames = synth.frames_host(cfg, 0, range(n))
+        envs, sids = None, None
+        what = f"the first {n} frames of C{cfg.cid} ({cfg.W}x{cfg.H})"
+    else:
+        n = min(n, cfg.streams)
+        sids = list(range(n))
+        envs = [oracle.learn(synth.learning_frames_host(cfg, s), synth.MARGIN) for s in sids]
+        frames = __import__("numpy").stack([synth.frames_host(cfg, s, [0])[0] for s in sids])
+        lo = hi = None
+        what = (f"frame 0 of streams 0..{n - 1} of C{cfg.cid} ({cfg.W}x{cfg.H}, per-stream "
+                f"envelopes)")
+
+    def timed(nthreads, budget):
+        tracker = (oracle.Tracker(p), (lo, hi), [oracle.Tracker(p) for _ in range(n)])
+        passes, done, t0 = 0, 0, time.perf_counter()
+        while True:
+            _oracle_pass(cfg, p, frames, envs, sids, nthreads, tracker)
+            passes += 1
+            done += n
+            dt = time.perf_counter() - t0
+            if dt >= budget or passes >= 200:
+                return done / dt, passes, done, dt
+
+    v, passes, done, dt = timed(cores, target_s)
+    v1, passes1, done1, dt1 = timed(1, single_s)
+    return {"value": v, "unit": "frames/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"{passes} passes over {what} = {done} frames, frame-parallel oracle "
+                      f"(masks + records + fold) over {cores} host threads, {dt:.1f} s",
+            "single_core": {"value": v1, "unit": "frames/s", "cores": 1,
+                            "sample": f"{passes1} passes = {done1} frames on one thread, {dt1:.1f} s"}}
+
+
+def spot_check(cfg, frames_dev, masks_dev, res_dev, sids, idx):
+    """Bench-side parity spot check of frames `idx` of the last timed call:
+    the final mask and the stateless record fields (a2-a7) against the oracle
+    (the fold state depends on every earlier frame, so it is not checked here)."""
+    import oracle
+    import synth
+    from paper_1907_04393_b200 import results_numpy
+    p = oracle.make_params(cfg.W, cfg.H)
+    res = results_numpy(res_dev)
+    checked = []
+    for i in idx:
+        s = int(sids[i]) if sids is not None else 0
+        lo, hi = oracle.learn(synth.learning_frames_host(cfg, s), synth.MARGIN)
+        rec, st = oracle.segment(p, frames_dev[i].cpu().numpy(), lo, hi)
+        ok = bool(masks_dev is None or (masks_dev[i].cpu().numpy() == st["final_mask"]).all())
+        for f in ("mean_luma", "corrected", "fg_merged", "fg_final", "n_comp_total", "n_comp_kept",
+                  "blob_area", "blob_label", "sum_x", "sum_y"):
+            ok = ok and int(res[i][f]) == int(getattr(rec, f))
+        ok = ok and abs(float(res[i]["cx"]) - rec.cx) <= 1e-3 and abs(float(res[i]["cy"]) - rec.cy) <= 1e-3
+        checked.append({"frame_in_call": int(i), "stream": s, "match": ok})
+    return {"frames": checked, "all_match": all(c["match"] for c in checked)}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -417,6 +495,16 @@ def main():
         dist.barrier()
     launches = fz.kernel_launches() - launches0
     ms = e0.elapsed_time(e1)
+    spot = None
+    if rank == 0 and not sharded and not args.no_spot_check:
+        # the last timed call's outputs, checked against the oracle (untimed)
+        i_last = args.warmup + args.steps - 1
+        v = views[i_last % need]
+        if v is not None:
+            n_l, fr_l, mks_l, ress_l, _, sids_l = v
+            mk_l = mks_l[i_last % NBUF]
+            spot = spot_check(cfg, fr_l, mk_l, ress_l[i_last % NBUF],
+                              sids_l if S > 1 else None, sorted({0, n_l - 1}))
     # the fused kernel's launch duration: a second pass of the same K steps
     # with CUDA events around that kernel on its launching stream (direct
     # launches: events cannot be accumulated across graph replays)
@@ -474,7 +562,7 @@ def main():
         "kernel_ms_per_step": seg_ms / max(args.steps, 1),
         "kernel_timing": "CUDA events around every fused-kernel launch on its stream, "
                          "second pass of the same K steps with direct launches",
-        "graph_replay": True,
+        "graph_replay": {"timed_region": True, "kernel_timing_pass": False},
         "step": {"achieved": step_bytes / (step_ms / 1e3) / 1e9,
                  "frac": step_bytes / (step_ms / 1e3) / 1e9 / hbm,
                  "algorithmic_bytes_per_step": step_bytes},
@@ -507,6 +595,7 @@ def main():
                    "parallelism": (f"frames sharded by batch, dp{world}" if S == 1 else
                                    f"camera streams sharded (s mod {world}), dp{world}")},
         "gpu_launches": launches,
+        "spot_check": spot,
         "roofline": roofline,
         "clocks": clk.summary(),
     }
@@ -556,7 +645,7 @@ def main():
                       "steps": k2, "api": "fizi_process_frames_host (pinned host buffers)"}
         fe.close()
 
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and S == 1:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample_frames)
     if rank == 0:
         print(json.dumps(out), flush=True)
