@@ -40,3 +40,100 @@ def test_device_flags_match_oracle_on_drift_stream():
     assert flags == ref
     assert any(ref)                               # the drift stream has exposure steps
     fz.close()
+
+
+# ---------------------------------------------- in-stream relearning (oracle)
+def _step_scene(n_before, n_after, gain_after, hand=False, seed=7):
+    """A static textured scene (C1 geometry), a lighting step of gain
+    `gain_after` (Q10) from frame n_before on; optionally the C1 disc hand."""
+    import synth
+    cfg = synth.CONFIGS[1]
+    n = n_before + n_after
+    pf = synth.frame_params(cfg, 0, range(n))
+    pf[:, 1] = [1024] * n_before + [gain_after] * n_after
+    if not hand:
+        pf[:, 4] = 0
+    # skin-hued static clutter baked into the background (C4's kind): inside
+    # the learned envelope until the lighting changes
+    ell = np.array([[80, 60, 40, 30], [240, 170, 50, 35]], np.int32)
+    frames = synth.gen_host(cfg.W, cfg.H, cfg.seed, 0, pf, ell)
+    lpf = synth.frame_params(cfg, 0, range(cfg.n_learn), learning=True)
+    learn = synth.gen_host(cfg.W, cfg.H, cfg.seed, 0, lpf, ell)
+    return cfg, frames, learn
+
+
+def test_relearn_never_triggered_equals_plain_path():
+    import oracle
+    import synth
+    from oracle.relearn import run_stream_relearn
+    cfg, frames, learn = _step_scene(4, 4, 1400, hand=True)
+    lo, hi = oracle.learn(learn, synth.MARGIN)
+    p = oracle.make_params(cfg.W, cfg.H)
+    t = np.arange(len(frames)) * 33
+    recs, masks, flags, swaps = run_stream_relearn(p, frames, t, lo, hi, 255, 3, synth.MARGIN)
+    tr = oracle.Tracker(p)
+    assert flags == [0] * len(frames) and swaps == []
+    for k in range(len(frames)):
+        rec, st = oracle.segment(p, frames[k], lo, hi, t_ms=int(t[k]))
+        tr.update(rec)
+        assert rec.as_dict() == recs[k].as_dict()
+        assert np.array_equal(st["final_mask"], masks[k])
+
+
+def test_relearn_after_lighting_step_relearns_the_new_background():
+    """Static background, exposure x1.25 from frame 3: frame 3 triggers (it is
+    segmented with the old model, which now sees the brighter background as
+    foreground), frames 4..4+F-1 are learning frames, the model learned from
+    them makes the later frames exactly empty again (noise a = 4 <= margin/2,
+    the c3 'learn' pin), and the swap's model is learn(those F frames)."""
+    import oracle
+    import synth
+    from oracle.relearn import RELEARN_LEARN, RELEARN_SWAP, RELEARN_TRIGGER, run_stream_relearn
+    F = 5
+    cfg, frames, learn = _step_scene(3, 12, 1280)
+    lo, hi = oracle.learn(learn, synth.MARGIN)
+    p = oracle.make_params(cfg.W, cfg.H, min_blob_ppm=0)
+    t = np.arange(len(frames)) * 33
+    recs, masks, flags, swaps = run_stream_relearn(p, frames, t, lo, hi, 20, F, synth.MARGIN)
+    m = [oracle.mean_luma(f)[0] for f in frames]
+    assert m[3] - m[2] > 20 and all(abs(m[k] - m[k - 1]) <= 20 for k in range(4, len(m)))
+    assert flags == [0, 0, 0, RELEARN_TRIGGER] + [RELEARN_LEARN] * (F - 1) + \
+        [RELEARN_LEARN | RELEARN_SWAP] + [0] * (len(frames) - 4 - F)
+    assert [k for k, _, _ in swaps] == [3 + F]
+    nlo, nhi = oracle.learn(frames[4:4 + F], synth.MARGIN)
+    assert np.array_equal(swaps[0][1], nlo) and np.array_equal(swaps[0][2], nhi)
+    assert recs[3].fg_merged > 1000                      # the old model fails on the step frame
+    assert recs[3].blob_area > 0                         # (the brightened clutter is a "hand")
+    for k in range(4, 4 + F):                            # learning: not segmented, not tracked
+        assert masks[k].sum() == 0 and recs[k].fg_merged == 0 and recs[k].visible == 0
+        assert recs[k].mean_luma == m[k]
+    for k in range(4 + F, len(frames)):                  # the relearned model: exactly empty
+        assert masks[k].sum() == 0 and recs[k].fg_merged == 0
+
+
+def test_relearn_ignores_triggers_while_learning_and_resets_the_tracker():
+    """Two steps 2 frames apart: the second falls inside the learning window
+    and does not restart it; with the hand present the tracker is paused while
+    learning and snaps to the centroid (reset) on the first frame after the swap."""
+    import oracle
+    import synth
+    from oracle.relearn import RELEARN_LEARN, RELEARN_TRIGGER, run_stream_relearn
+    import synth as sy
+    cfg = sy.CONFIGS[1]
+    n = 14
+    pf = sy.frame_params(cfg, 0, range(n))
+    pf[:, 1] = [1024] * 3 + [1300] * 2 + [900] * (n - 5)
+    frames = sy.gen_host(cfg.W, cfg.H, cfg.seed, 0, pf, sy.clutter(cfg, 0))
+    lo, hi = oracle.learn(sy.learning_frames_host(cfg), sy.MARGIN)
+    p = oracle.make_params(cfg.W, cfg.H)
+    t = np.arange(n) * 33
+    F = 4
+    recs, masks, flags, swaps = run_stream_relearn(p, frames, t, lo, hi, 20, F, sy.MARGIN)
+    assert flags[3] == RELEARN_TRIGGER
+    assert all(flags[k] & RELEARN_LEARN for k in range(4, 4 + F))   # frame 5's step ignored
+    assert not any(flags[k] & RELEARN_TRIGGER for k in range(4, 4 + F))
+    assert len(swaps) == 1 and swaps[0][0] == 3 + F
+    k = 4 + F
+    assert recs[k].blob_area > 0 and recs[k].visible == 1
+    assert recs[k].px == recs[k].cx and recs[k].py == recs[k].cy    # snapped: tracker reset
+    assert recs[k].dwell_ms == 0
