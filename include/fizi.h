@@ -84,13 +84,16 @@ typedef struct fizi_result {
     uint32_t blob_area;            /* a7: largest kept component (0 if none)               */
     uint32_t blob_label;           /*     its label = 1 + min raster index y*W+x (L15)     */
     uint32_t bbox[4];              /*     x_min, y_min, x_max, y_max                       */
-    uint32_t _pad;
+    uint32_t relearn;              /* NEXT-1 flags (fizi_set_relearn): 1 learning frame,    */
+                                   /* 2 model swapped after it, 4 trigger; 0 otherwise      */
     uint64_t sum_x, sum_y;         /*     exact moments: sum of x (column), sum of y (row) */
     double   gamma;                /* a2: 1.0 when not corrected                           */
     double   cx, cy;               /* a7: centroid sum/area (L17); 0 if no blob            */
     double   px, py;               /* a8: smoothed pointer                                 */
     int64_t  dwell_ms;             /* a8: dwell time at the anchor                         */
 } fizi_result;
+
+enum { FIZI_RELEARN_LEARN = 1, FIZI_RELEARN_SWAP = 2, FIZI_RELEARN_TRIGGER = 4 };
 
 /* Stages for fizi_debug_stage (SPEC S:265 stage dumps). */
 typedef enum {
@@ -184,6 +187,24 @@ int fizi_reset_tracker(fizi_ctx *ctx, uint32_t stream, fizi_stream_t cuda_stream
  * resets this state).  threshold <= 255. */
 int fizi_relearn_flags(fizi_ctx *ctx, uint32_t stream, const fizi_result *results_dev, uint32_t n,
                        uint32_t threshold, uint8_t *flags_dev, fizi_stream_t cuda_stream);
+
+/* ---- NEXT-1, in-stream relearning (§3.3; SPEC S:153-161, S:170
+ * "on trigger, runtime pauses tracking and relearns", "Relearning swaps
+ * the model atomically between frames"; reading L37).  With
+ * n_frames > 0, every later call folds stream `stream`'s frames in order
+ * through a relearn state: a frame whose a2 mean luma differs from the
+ * previous frame's by more than `threshold` (strict) is processed normally
+ * and flagged FIZI_RELEARN_TRIGGER; the stream's next n_frames frames are
+ * learning frames (FIZI_RELEARN_LEARN: empty mask, a3-a7 fields 0, tracker
+ * paused: visible = clicked = 0, px = py = 0, dwell 0); after the last one
+ * (FIZI_RELEARN_SWAP) the stream's model becomes the a1 envelope of those raw
+ * frames with `margin`, and the tracker restarts.  Triggers are ignored while
+ * learning; learning may span calls.  Results do not depend on how frames are
+ * batched.  Calls holding a relearning stream run joined even in pipelined
+ * mode.  n_frames = 0 disables (and frees the model pool); threshold <= 255.
+ * fizi_learn_background / fizi_set_background restart the relearn state. */
+int fizi_set_relearn(fizi_ctx *ctx, uint32_t stream, uint32_t threshold, uint32_t n_frames,
+                     uint8_t margin);
 
 /* ---- NEXT-3: interface hit-test ("determines the interface zone
  * activated by the pointer").  Zones of a stream's layout

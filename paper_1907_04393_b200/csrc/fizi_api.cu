@@ -146,7 +146,11 @@ void free_all(Ctx& c) {
       if (q) cudaFree(q);
     if (c.calls[i]) cudaFree(c.calls[i]);
   }
+  for (uint8_t* q : c.rl_mem)
+    if (q) cudaFree(q);
+  c.rl_mem.clear();
   void* ptrs[] = {c.env, c.lut, c.gamma_tab, c.corr_tab, c.skin_tab, c.bitOC,
+                  c.rstate, c.rl_role, c.rl_pair, c.rl_env, c.rl_list, c.rl_pairs, c.rl_counts,
                   c.parent, c.stats, c.tl, c.dstate,
                   c.prev_mean, c.hstate,
                   c.tstate, c.stage_frames, c.stage_masks, c.stage_results};
@@ -273,6 +277,7 @@ struct CallPlan {
   std::vector<SubBatch> subs;
   int fold = -2;               // -2 no fold, -1 per-stream end fold, >= 0 single-stream fold
   bool fused_mask = false;     // the labelling kernel writes the u8 mask (pre-zeroed)
+  bool relearn = false;        // NEXT-1: a stream of the call relearns (joined, one sub-batch)
   bool premask = false;        // u8 mask: zeroed beside the segmentation, kept runs by labelling
   bool morphmask = false;      // u8 mask: rows of O by the morphology, dropped runs cleared
   uint8_t* masks = nullptr;    // caller's u8 masks (expand path only)
@@ -299,6 +304,7 @@ int enqueue_tail(Ctx& c, const CallPlan& pl, const SubBatch& b, uint32_t k, cuda
   cudaError_t e = cudaSuccess;
   if (with_fix) {
     e = fizi::launch_seg_fix(c, b.f0, b.n, k, sd);
+    if (e == cudaSuccess && c.rl_active) e = fizi::launch_relearn_reseg(c, b.n, sd);
     if (e != cudaSuccess) return cuda_fail(c, e, "fixup");
   }
   prof_begin(c, sd);
@@ -408,6 +414,8 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
   for (size_t k = 0; k < pl.subs.size(); k++) {
     const SubBatch& b = pl.subs[k];
     e = fizi::launch_seg_main(c, b.f0, b.n, b.g0, b.ng, (uint32_t)k, st);
+    // NEXT-1: roles and models from the means before any per-pixel word
+    if (e == cudaSuccess && c.rl_active && c.fast) e = fizi::launch_relearn_plan(c, b.n, st);
     if (e == cudaSuccess && c.fast) e = fizi::launch_slow_words(c, b.f0, b.n, (uint32_t)k, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "segment");
     e = cudaEventRecord(c.ev_seg[k], st);
@@ -415,6 +423,10 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(c, e, "event");
     rc = enqueue_tail(c, pl, b, (uint32_t)k, sd, nullptr, true);
     if (rc) return rc;
+  }
+  if (c.rl_active) {                                    // NEXT-1: install the newest models
+    e = fizi::launch_relearn_commit(c, sd);
+    if (e != cudaSuccess) return cuda_fail(c, e, "relearn commit");
   }
   e = cudaEventRecord(c.ev_join, sd);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c.ev_join, 0);
@@ -435,7 +447,7 @@ int run_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
   const bool graph = c.use_graphs && !c.prof && !(pl.masks && !pl.fused_mask);
   if (!graph) return enqueue_part(c, pl, part, st);
   std::vector<uint32_t> key = {(uint32_t)part, pl.n, (uint32_t)(pl.fold + 2), (uint32_t)pl.premask,
-                               (uint32_t)pl.fused_mask, (uint32_t)pl.morphmask};
+                               (uint32_t)pl.fused_mask, (uint32_t)pl.morphmask, (uint32_t)pl.relearn};
   for (const SubBatch& b : pl.subs) {
     key.push_back(b.n);
     key.push_back(b.g0);
@@ -513,7 +525,13 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   pl.premask = masks && pl.fused_mask && !c.mask_by_morph;
   pl.morphmask = masks && pl.fused_mask && c.mask_by_morph;
   pl.masks = masks;
-  const bool pipelined = c.pipeline && !c.p.debug;
+  // NEXT-1: a call with a relearning stream runs joined (the model swap
+  // orders the next call's segmentation after this call's relearning)
+  c.rl_active = false;
+  if (!c.rl_enabled.empty())
+    for (uint32_t i = 0; i < n && !c.rl_active; i++) c.rl_active = c.rl_enabled[sof[i]] != 0;
+  pl.relearn = c.rl_active;
+  const bool pipelined = c.pipeline && !c.p.debug && !pl.relearn;
   pl.slot = c.pinned_next;
   c.pinned_next = (c.pinned_next + 1) % fizi::kSlots;
   const auto h0 = std::chrono::steady_clock::now();
@@ -524,7 +542,7 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   fizi::CallPtrs cp{frames, pl.fused_mask ? masks : nullptr, res, n,
                     single ? (int64_t)sof[0] : -1, c.call_counter++, c.tl};
   const uint32_t sub_frames = c.sub_frames;
-  if (pipelined) c.sub_frames = 65535;                 // one sub-batch: the tail is the overlap
+  if (pipelined || pl.relearn) c.sub_frames = 65535;  // one sub-batch (the tail is the overlap / the relearn plan sees every frame)
   fill_call(c, pl.slot, cp, sof, t, n, pl.subs);
   c.sub_frames = sub_frames;
   select_slot(c, pl.slot);
@@ -709,6 +727,13 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   A(dalloc(&c.tstate, (uint64_t)n_streams * sizeof(fizi::TrackState)));
   A(dalloc(&c.dstate, (uint64_t)n_streams * sizeof(fizi::DriveState)));
   A(dalloc(&c.prev_mean, (uint64_t)n_streams * sizeof(int32_t)));
+  A(dalloc(&c.rstate, (uint64_t)n_streams * sizeof(fizi::RelearnState)));
+  A(dalloc(&c.rl_role, mb * 4));
+  A(dalloc(&c.rl_pair, mb * 4));
+  A(dalloc(&c.rl_env, mb * 8));
+  A(dalloc(&c.rl_list, (mb + 1) * 4));
+  A(dalloc(&c.rl_pairs, mb * 16));
+  A(dalloc(&c.rl_counts, (2 + 2 * (uint64_t)n_streams) * 4));
   A(dalloc(&c.hstate, (uint64_t)n_streams * sizeof(fizi::HitState)));
   for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++) {
     e = cudaMallocHost(reinterpret_cast<void**>(&c.pinned[i]), table_bytes);
@@ -786,6 +811,9 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
   if (e == cudaSuccess) e = fizi::init_ccl(c);
   if (e == cudaSuccess) e = cudaMemset(c.env, 0, (uint64_t)n_streams * 2 * c.env_plane);
   if (e == cudaSuccess) e = cudaMemset(c.dstate, 0, (uint64_t)n_streams * sizeof(fizi::DriveState));
+  if (e == cudaSuccess) e = cudaMemset(c.rstate, 0, (uint64_t)n_streams * sizeof(fizi::RelearnState));
+  c.rl_enabled.assign(n_streams, 0);
+  c.rl_mem.assign(n_streams, nullptr);
   if (e == cudaSuccess) e = fizi::launch_relearn_reset(c, 0, n_streams, 0);
   if (e == cudaSuccess) e = fizi::launch_lut_table(c, 0);
   if (e == cudaSuccess) e = fizi::launch_skin_table(c, 0);
@@ -821,6 +849,8 @@ int fizi_learn_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* frames_
   if (e != cudaSuccess) return cuda_fail(c, e, "learn");
   e = fizi::launch_tstate_reset(c, stream, 1, st);
   if (e == cudaSuccess) e = fizi::launch_relearn_reset(c, stream, 1, st);
+  if (e == cudaSuccess && c.rl_enabled[stream])          // a new model: relearning starts over
+    e = fizi::launch_relearn_state(c, stream, c.rl_state_host[stream], st);
   if (e != cudaSuccess) return cuda_fail(c, e, "tracker reset");
   c.env_valid[stream] = 1;
   c.has_t[stream] = 0;
@@ -1067,6 +1097,8 @@ int fizi_set_background(fizi_ctx* ctx, uint32_t stream, const uint8_t* lo_dev,
   cudaError_t e = join_tail(c, st);
   if (e == cudaSuccess) e = fizi::launch_env_export(c, stream, nullptr, nullptr, true, lo_dev, hi_dev, st);
   if (e == cudaSuccess) e = fizi::launch_tstate_reset(c, stream, 1, st);
+  if (e == cudaSuccess && c.rl_enabled[stream])          // a new model: relearning starts over
+    e = fizi::launch_relearn_state(c, stream, c.rl_state_host[stream], st);
   if (e != cudaSuccess) return cuda_fail(c, e, "set_background");
   c.env_valid[stream] = 1;
   c.has_t[stream] = 0;
@@ -1141,6 +1173,56 @@ int fizi_relearn_flags(fizi_ctx* ctx, uint32_t stream, const fizi_result* result
   cudaError_t e = join_tail(c, st);
   if (e == cudaSuccess) e = fizi::launch_relearn_flags(c, stream, results_dev, n, threshold, flags_dev, st);
   if (e != cudaSuccess) return cuda_fail(c, e, "relearn flags");
+  return FIZI_OK;
+}
+
+int fizi_set_relearn(fizi_ctx* ctx, uint32_t stream, uint32_t threshold, uint32_t n_frames,
+                     uint8_t margin) {
+  if (!ctx) return FIZI_E_ARG;
+  Ctx& c = ctx->c;
+  if (c.sticky) return fail(c, FIZI_E_CUDA, "context has a sticky CUDA error: " + c.err);
+  if (stream >= c.n_streams) return fail(c, FIZI_E_CAPACITY, "stream id >= n_streams");
+  if (threshold > 255) return fail(c, FIZI_E_ARG, "threshold must be <= 255");
+  DeviceGuard guard(c.device);
+  cudaError_t e = cudaDeviceSynchronize();              // no call of this stream in flight
+  if (e != cudaSuccess) return cuda_fail(c, e, "set_relearn");
+  if (c.rl_mem[stream]) {
+    cudaFree(c.rl_mem[stream]);
+    c.rl_mem[stream] = nullptr;
+  }
+  fizi::RelearnState v{};
+  v.prev_mean = -1;
+  if (n_frames > 0) {
+    // models one call can complete: every one but a continued one needs a
+    // trigger frame + n_frames learning frames of the call
+    const uint32_t slots = (c.max_batch + n_frames) / (n_frames + 1) + 1;
+    uint8_t* mem = nullptr;
+    e = cudaMalloc(reinterpret_cast<void**>(&mem), (uint64_t)(slots + 1) * 2 * c.env_plane);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, FIZI_E_OOM, "relearn model pool allocation failed");
+    }
+    c.rl_mem[stream] = mem;
+    v.enabled = 1;
+    v.threshold = threshold;
+    v.frames = n_frames;
+    v.margin = margin;
+    v.pool_slots = slots;
+    v.pool = reinterpret_cast<uint64_t>(mem);
+    v.acc = reinterpret_cast<uint64_t>(mem + (uint64_t)slots * 2 * c.env_plane);
+  }
+  e = fizi::launch_relearn_state(c, stream, v, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(c, e, "set_relearn");
+  c.rl_enabled[stream] = v.enabled ? 1 : 0;
+  c.rl_state_host.resize(c.n_streams);
+  c.rl_state_host[stream] = v;
+  uint32_t pairs = 0, commits = 0;
+  for (uint32_t s = 0; s < c.n_streams; s++)
+    if (c.rl_enabled[s]) { pairs += c.rl_state_host[s].pool_slots; commits++; }
+  c.rl_max_pairs = std::max(1u, std::min(pairs, c.max_batch));
+  c.rl_max_commits = std::max(1u, commits);
+  destroy_graphs(c);                                     // captured calls carry the launch grids
   return FIZI_OK;
 }
 

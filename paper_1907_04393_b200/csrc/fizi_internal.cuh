@@ -71,6 +71,15 @@ struct RootStats {                       // per component (indexed by its root r
   unsigned long long sx, sy;
 };
 
+struct RelearnState {                    // NEXT-1 in-stream relearning, per stream (k_relearn.cu)
+  int32_t prev_mean;                     // a2 mean of the stream's previous frame, -1 = none
+  uint32_t remaining;                    // learning frames still to come (0: segmenting)
+  uint32_t continuing;                   // the current learning began in an earlier call
+  uint32_t enabled, threshold, frames, margin, pool_slots;
+  uint64_t pool;                         // device: pool_slots models (2 planes each)
+  uint64_t acc;                          // device: carried min / max (2 planes)
+};
+
 struct Ctx {
   fizi_params p{};
   int device = 0;
@@ -145,6 +154,19 @@ struct Ctx {
   uint8_t* tstate = nullptr;             // n_streams tracker states
   uint8_t* dstate = nullptr;             // n_streams drive states (NEXT-2)
   int32_t* prev_mean = nullptr;          // n_streams relearn-trigger states (NEXT-1), -1 = none
+  // NEXT-1 in-stream relearning (fizi_set_relearn)
+  uint8_t* rstate = nullptr;             // n_streams RelearnState
+  bool rl_active = false;                // the current call has a relearning stream (joined)
+  uint32_t* rl_role = nullptr;           // max_batch: 0 / 1 learning / 2 re-segmented with rl_env
+  uint32_t* rl_pair = nullptr;           // max_batch: version a learning frame belongs to
+  uint64_t* rl_env = nullptr;            // max_batch: model of a role-2 frame
+  uint32_t* rl_list = nullptr;           // 1 + max_batch: count, frames with a non-zero role
+  uint32_t* rl_pairs = nullptr;          // max_batch x 4: versions of the call
+  uint32_t* rl_counts = nullptr;         // versions, commits, commits x (stream, slot)
+  uint32_t rl_max_pairs = 1, rl_max_commits = 1;
+  std::vector<uint8_t> rl_enabled;       // host copy of RelearnState::enabled
+  std::vector<uint8_t*> rl_mem;          // per stream: pool + accumulator allocation
+  std::vector<RelearnState> rl_state_host;   // per stream: the configured initial state
   uint8_t* hstate = nullptr;             // n_streams hit-test states (NEXT-3)
   cudaStream_t side = nullptr;           // tail: LUT re-test + morphology (joined: whole tail)
   cudaStream_t cclst = nullptr;          // pipelined tail: labelling + u8 mask + fold, call order
@@ -284,6 +306,13 @@ cudaError_t launch_track_call(Ctx& c, int fold, cudaStream_t st);
 cudaError_t launch_relearn_flags(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
                                  uint32_t threshold, uint8_t* flags, cudaStream_t st);
 cudaError_t launch_relearn_reset(Ctx& c, uint32_t first, uint32_t count, cudaStream_t st);
+// NEXT-1 in-stream relearning: roles + models of the call (after the means),
+// re-segmentation of role-2 frames / emptying of learning frames (fast path),
+// model commit at the end of the call, per-stream state upload
+cudaError_t launch_relearn_plan(Ctx& c, uint32_t n, cudaStream_t st);
+cudaError_t launch_relearn_reseg(Ctx& c, uint32_t n, cudaStream_t st);
+cudaError_t launch_relearn_commit(Ctx& c, cudaStream_t st);
+cudaError_t launch_relearn_state(Ctx& c, uint32_t stream, const RelearnState& v, cudaStream_t st);
 // NEXT-3: hit-test of a stream's records against its layout (state in c.hstate)
 cudaError_t launch_hit_test(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
                             fizi_zone_event* out, cudaStream_t st);

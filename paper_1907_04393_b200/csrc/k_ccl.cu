@@ -401,6 +401,7 @@ __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
     double* cx_s = reinterpret_cast<double*>(t_s + kChunk);       // in: cx, out: px
     double* cy_s = cx_s + kChunk;                                 // in: cy, out: py
     uint32_t* ar_s = reinterpret_cast<uint32_t*>(cy_s + kChunk);  // in: area, out: vis | clk<<1
+    uint32_t* fl_s = ar_s + kChunk;                                // in: relearn flags
     TrackState st;
     if (threadIdx.x == 0) st = a.tstate[a.track_stream];
     for (uint32_t base = 0; base < n; base += kChunk) {
@@ -409,6 +410,7 @@ __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
         const fizi_result& r = a.call->res[f0 + base + i];
         t_s[i] = __ldcg(&r.t_ms);
         ar_s[i] = __ldcg(&r.blob_area);
+        fl_s[i] = __ldcg(&r.relearn);
         cx_s[i] = __ldcg(&r.cx);
         cy_s[i] = __ldcg(&r.cy);
       }
@@ -416,7 +418,7 @@ __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
       if (threadIdx.x == 0) {
         for (uint32_t i = 0; i < m; i++) {
           fizi_result r;
-          r.t_ms = t_s[i]; r.blob_area = ar_s[i]; r.cx = cx_s[i]; r.cy = cy_s[i];
+          r.t_ms = t_s[i]; r.blob_area = ar_s[i]; r.cx = cx_s[i]; r.cy = cy_s[i]; r.relearn = fl_s[i];
           track_one(a.p, st, r);
           t_s[i] = r.dwell_ms; cx_s[i] = r.px; cy_s[i] = r.py;
           ar_s[i] = (uint32_t)r.visible | ((uint32_t)r.clicked << 1);
@@ -441,6 +443,7 @@ __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
         fizi_result r;
         r.t_ms = __ldcg(&a.call->res[f].t_ms); r.blob_area = __ldcg(&a.call->res[f].blob_area);
         r.cx = __ldcg(&a.call->res[f].cx); r.cy = __ldcg(&a.call->res[f].cy);
+        r.relearn = __ldcg(&a.call->res[f].relearn);
         track_one(a.p, st, r);
         fizi_result& o = a.call->res[f];
         o.visible = r.visible; o.clicked = r.clicked;
@@ -505,6 +508,7 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
     double* cx_s = reinterpret_cast<double*>(t_s + 1024);
     double* cy_s = cx_s + 1024;
     uint32_t* ar_s = reinterpret_cast<uint32_t*>(cy_s + 1024);
+    uint32_t* fl_s = ar_s + 1024;
     while (true) {
       if (threadIdx.x == 0) {
         s_own = atomicCAS(a.fold_sync, 0u, 1u) == 0u;
@@ -528,6 +532,7 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
         const fizi_result& r = a.call->res[a.f0 + i];
         t_s[threadIdx.x] = __ldcg(&r.t_ms);
         ar_s[threadIdx.x] = __ldcg(&r.blob_area);
+        fl_s[threadIdx.x] = __ldcg(&r.relearn);
         cx_s[threadIdx.x] = __ldcg(&r.cx);
         cy_s[threadIdx.x] = __ldcg(&r.cy);
       }
@@ -536,7 +541,7 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
         TrackState st = a.tstate[a.track_stream];
         for (uint32_t k = 0; k < cnt; k++) {
           fizi_result q;
-          q.t_ms = t_s[k]; q.blob_area = ar_s[k]; q.cx = cx_s[k]; q.cy = cy_s[k];
+          q.t_ms = t_s[k]; q.blob_area = ar_s[k]; q.cx = cx_s[k]; q.cy = cy_s[k]; q.relearn = fl_s[k];
           track_one(a.p, st, q);
           t_s[k] = q.dwell_ms; cx_s[k] = q.px; cy_s[k] = q.py;
           ar_s[k] = (uint32_t)q.visible | ((uint32_t)q.clicked << 1);
@@ -579,7 +584,7 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
 }
 
 constexpr size_t kCclSmem = (sizeof(Run) + 2 * sizeof(uint32_t)) * kCclSmemRuns;
-static_assert(kCclSmem >= 512 * 28, "fold staging fits the labelling shared memory");
+static_assert(kCclSmem >= 1024 * 32, "fold staging fits the labelling shared memory");
 
 cudaError_t init_ccl(Ctx& c) {
   (void)c;

@@ -67,6 +67,15 @@ struct SegArgs {
   const double* gtab;
   const uint8_t* ctab;
   const int64_t* frame_t;
+  // NEXT-1 relearning (nullptr when no frame of the call is of a relearning
+  // stream): per frame 0 = segmented with the stream's model, 1 = learning
+  // frame (not segmented), 2 = segmented with a model learned in this call
+  // (rl_env[f]); frames with a non-zero role are skipped by the per-pixel and
+  // LUT re-test kernels and re-segmented by the reseg launch (reseg = true:
+  // list = fix, envelope = rl_env[f])
+  const uint32_t* rl_role;
+  const uint64_t* rl_env;
+  bool reseg;
 };
 
 __device__ __forceinline__ bool valid_chunk(const SegArgs& a, uint32_t c) { return c < a.nchunks; }
@@ -724,6 +733,7 @@ __global__ void FIZI_SLOW_BOUNDS slow_words_kernel(SegArgs a) {
       const uint64_t mean = (a.luma[f] + 500ull * a.N) / (1000ull * a.N);
       act = a.ctab[mean] == 0;
     }
+    if (act && a.rl_role) act = a.rl_role[f] == 0;       // relearn: learning / re-segmented
     const uint32_t L = 2 * k + (lane & 1);                   // lane of the chunk
     const uint64_t coff = (uint64_t)cq * kChunkBytes;
     const bool valid = act && coff + 48u * L < a.frame_bytes;
@@ -776,9 +786,10 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
   __syncthreads();
   uint32_t phase = 0;
   const uint8_t* frames = a.call->frames;
-  for (uint64_t it = blockIdx.x; it < items; it += gridDim.x, phase ^= 1u) {
+  for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const uint32_t f = a.fix[1 + it / a.tiles];
     FIZI_DCHECK(f < a.call->n);
+    if (!a.reseg && a.rl_role && a.rl_role[f] != 0) continue;   // re-segmented by the reseg launch
     const uint32_t tile = (uint32_t)(it % a.tiles);
     const uint64_t tile_off = (uint64_t)tile * kTileBytes;
     const uint64_t rem = a.frame_bytes - tile_off;
@@ -796,7 +807,9 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
     const uint32_t stream = a.frame_stream[f];
     EnvRegs e;
     if (valid) {
-      const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + (uint64_t)c * kChunkBytes + 16 * lane;
+      const uint8_t* env = (a.reseg && a.rl_role[f] == 2) ? reinterpret_cast<const uint8_t*>(a.rl_env[f])
+                                                          : a.env + (uint64_t)stream * 2 * a.env_plane;
+      const uint8_t* elo = env + (uint64_t)c * kChunkBytes + 16 * lane;
       load_env(e, elo, elo + a.env_plane);
     } else {
       zero_env(e);
@@ -805,8 +818,9 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
     mbar_wait(&bar, phase);
     uint32_t y = 0;
     bool slow = false;
-    const uint32_t bits = seg16<true>(sm + warp * kChunkBytes + 48 * lane, e, valid, lut_s,
-                                      a.skin, y, slow);
+    const bool learning = a.reseg && a.rl_role[f] == 1;       // NEXT-1 learning frame: empty
+    const uint32_t bits = learning ? 0u : seg16<true>(sm + warp * kChunkBytes + 48 * lane, e, valid,
+                                                      lut_s, a.skin, y, slow);
     const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
     uint32_t pc = 0;
     if (!(lane & 1) && valid) {
@@ -825,6 +839,7 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
       if (sf) atomicAdd(&a.fg[f], sf);
     }
     __syncthreads();                          // smem tile + LUT reused next item
+    phase ^= 1u;
   }
   if (tid == 0) tl_mark(a.call, kTlFix, 1);
 }
@@ -862,12 +877,15 @@ __global__ void mask_generic_kernel(SegArgs a, uint32_t W, uint32_t H, uint32_t 
     const uint64_t q = (uint64_t)yrow * W + x;
     const uint8_t* p = a.call->frames + ((uint64_t)f * a.N + q) * 3;
     const uint32_t stream = a.frame_stream[f];
-    const uint8_t* lo = a.env + (uint64_t)stream * 2 * a.env_plane + q * 3;
+    const uint32_t role = a.rl_role ? a.rl_role[f] : 0u;
+    const uint8_t* env = role == 2 ? reinterpret_cast<const uint8_t*>(a.rl_env[f])
+                                   : a.env + (uint64_t)stream * 2 * a.env_plane;
+    const uint8_t* lo = env + q * 3;
     const uint8_t* hi = lo + a.env_plane;
     const int r = L[p[0]], g = L[p[1]], b = L[p[2]];
     const bool inside = r >= lo[0] && r <= hi[0] && g >= lo[1] && g <= hi[1] && b >= lo[2] &&
                         b <= hi[2];
-    bit = (uint32_t)!inside & gray_and_skin(r, g, b, (int)a.S, (int)a.a1, (int)a.a2);
+    bit = role == 1 ? 0u : (uint32_t)!inside & gray_and_skin(r, g, b, (int)a.S, (int)a.a1, (int)a.a2);
   }
   const uint32_t word = __ballot_sync(0xFFFFFFFFu, bit);
   if (lane == 0) {
@@ -938,6 +956,9 @@ static SegArgs seg_args(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32_t s
   a.gtab = c.gamma_tab;
   a.ctab = c.corr_tab;
   a.frame_t = c.frame_t;
+  a.rl_role = c.rl_active ? c.rl_role : nullptr;
+  a.rl_env = c.rl_env;
+  a.reseg = false;
   return a;
 }
 
@@ -993,6 +1014,19 @@ cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cud
 
 // a2 finalisation (mean -> gamma, record header) and the LUT re-test of the
 // sub-batch's corrected frames (fast path) / the branch tests (generic path).
+// NEXT-1: the frames segmented with a model learned in this call (role 2),
+// recomputed with their LUT against that model (fast path; the generic path
+// handles roles inside mask_generic_kernel)
+cudaError_t launch_relearn_reseg(Ctx& c, uint32_t n, cudaStream_t st) {
+  if (!c.fast) return cudaSuccess;
+  SegArgs a = seg_args(c, 0, n, 0, 0);
+  a.fix = c.rl_list;
+  a.reseg = true;
+  fix_fast_kernel<<<c.sms, 256, kTileBytes, st>>>(a);
+  c.launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_seg_fix(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st) {
   SegArgs a = seg_args(c, f0, n, 0, sub);
   prof_begin(c, st);
@@ -1004,6 +1038,10 @@ cudaError_t launch_seg_fix(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaSt
     finalize_kernel<<<fin_blocks, 256, 0, st>>>(f0, n, c.N, c.luma, c.fg, c.gamma_tab, c.corr_tab,
                                                  c.frame_stream, c.frame_t, c.call,
                                                  const_cast<uint32_t*>(a.fix));
+    if (c.rl_active) {               // roles need the means (NEXT-1)
+      cudaError_t e = launch_relearn_plan(c, n, st);
+      if (e != cudaSuccess) return e;
+    }
     const uint64_t warps = (uint64_t)c.H * c.P * n;
     mask_generic_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a, c.W, c.H, c.P, n);
     c.launches += 2;

@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(256) track_stream_kernel(fizi_params p, uint32
   __shared__ int64_t t_s[kTrackChunk];
   __shared__ double cx_s[kTrackChunk], cy_s[kTrackChunk];
   __shared__ uint32_t ar_s[kTrackChunk];
+  __shared__ uint32_t fl_s[kTrackChunk];
   __shared__ int64_t dw_o[kTrackChunk];
   __shared__ double px_o[kTrackChunk], py_o[kTrackChunk];
   __shared__ uint8_t vc_o[kTrackChunk];
@@ -55,19 +56,21 @@ __global__ void __launch_bounds__(256) track_stream_kernel(fizi_params p, uint32
     const uint32_t m = min((uint32_t)kTrackChunk, n - base);
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
       const fizi_result& r = res[base + i];
-      t_s[i] = r.t_ms; ar_s[i] = r.blob_area; cx_s[i] = r.cx; cy_s[i] = r.cy;
+      t_s[i] = r.t_ms; ar_s[i] = r.blob_area; cx_s[i] = r.cx; cy_s[i] = r.cy; fl_s[i] = r.relearn;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       // the next record's inputs are loaded before the current fold step
       // (separate output arrays: no aliasing between the two)
       int64_t t_n = t_s[0];
-      uint32_t a_n = ar_s[0];
+      uint32_t a_n = ar_s[0], l_n = fl_s[0];
       double x_n = cx_s[0], y_n = cy_s[0];
       for (uint32_t i = 0; i < m; i++) {
         fizi_result r;
-        r.t_ms = t_n; r.blob_area = a_n; r.cx = x_n; r.cy = y_n;
-        if (i + 1 < m) { t_n = t_s[i + 1]; a_n = ar_s[i + 1]; x_n = cx_s[i + 1]; y_n = cy_s[i + 1]; }
+        r.t_ms = t_n; r.blob_area = a_n; r.cx = x_n; r.cy = y_n; r.relearn = l_n;
+        if (i + 1 < m) {
+          t_n = t_s[i + 1]; a_n = ar_s[i + 1]; x_n = cx_s[i + 1]; y_n = cy_s[i + 1]; l_n = fl_s[i + 1];
+        }
         track_one(p, st, r);
         dw_o[i] = r.dwell_ms; px_o[i] = r.px; py_o[i] = r.py;
         vc_o[i] = (uint8_t)(r.visible | (r.clicked << 1));
@@ -110,6 +113,7 @@ __global__ void __launch_bounds__(256) track_call_kernel(fizi_params p, const Ca
         if (!any) { st = ts[s]; any = true; }
         fizi_result r;
         r.t_ms = res[f].t_ms; r.blob_area = res[f].blob_area; r.cx = res[f].cx; r.cy = res[f].cy;
+        r.relearn = res[f].relearn;
         track_one(p, st, r);
         res[f].visible = r.visible; res[f].clicked = r.clicked;
         res[f].px = r.px; res[f].py = r.py; res[f].dwell_ms = r.dwell_ms;
@@ -121,6 +125,7 @@ __global__ void __launch_bounds__(256) track_call_kernel(fizi_params p, const Ca
   __shared__ int64_t t_s[kTrackChunk];
   __shared__ double cx_s[kTrackChunk], cy_s[kTrackChunk];
   __shared__ uint32_t ar_s[kTrackChunk];
+  __shared__ uint32_t fl_s[kTrackChunk];
   __shared__ int64_t dw_o[kTrackChunk];
   __shared__ double px_o[kTrackChunk], py_o[kTrackChunk];
   __shared__ uint8_t vc_o[kTrackChunk];
@@ -130,19 +135,21 @@ __global__ void __launch_bounds__(256) track_call_kernel(fizi_params p, const Ca
     const uint32_t m = min((uint32_t)kTrackChunk, n - base);
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
       const fizi_result& r = res[base + i];
-      t_s[i] = r.t_ms; ar_s[i] = r.blob_area; cx_s[i] = r.cx; cy_s[i] = r.cy;
+      t_s[i] = r.t_ms; ar_s[i] = r.blob_area; cx_s[i] = r.cx; cy_s[i] = r.cy; fl_s[i] = r.relearn;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       // the next record's inputs are loaded before the current fold step
       // (separate output arrays: no aliasing between the two)
       int64_t t_n = t_s[0];
-      uint32_t a_n = ar_s[0];
+      uint32_t a_n = ar_s[0], l_n = fl_s[0];
       double x_n = cx_s[0], y_n = cy_s[0];
       for (uint32_t i = 0; i < m; i++) {
         fizi_result r;
-        r.t_ms = t_n; r.blob_area = a_n; r.cx = x_n; r.cy = y_n;
-        if (i + 1 < m) { t_n = t_s[i + 1]; a_n = ar_s[i + 1]; x_n = cx_s[i + 1]; y_n = cy_s[i + 1]; }
+        r.t_ms = t_n; r.blob_area = a_n; r.cx = x_n; r.cy = y_n; r.relearn = l_n;
+        if (i + 1 < m) {
+          t_n = t_s[i + 1]; a_n = ar_s[i + 1]; x_n = cx_s[i + 1]; y_n = cy_s[i + 1]; l_n = fl_s[i + 1];
+        }
         track_one(p, st, r);
         dw_o[i] = r.dwell_ms; px_o[i] = r.px; py_o[i] = r.py;
         vc_o[i] = (uint8_t)(r.visible | (r.clicked << 1));
@@ -403,6 +410,7 @@ __global__ void __launch_bounds__(256) track_runs_kernel(fizi_params p, TrackRun
   __shared__ int64_t t_s[kTrackChunk];
   __shared__ double cx_s[kTrackChunk], cy_s[kTrackChunk];
   __shared__ uint32_t ar_s[kTrackChunk];
+  __shared__ uint32_t fl_s[kTrackChunk];
   __shared__ int64_t dw_o[kTrackChunk];
   __shared__ double px_o[kTrackChunk], py_o[kTrackChunk];
   __shared__ uint8_t vc_o[kTrackChunk];
@@ -415,17 +423,19 @@ __global__ void __launch_bounds__(256) track_runs_kernel(fizi_params p, TrackRun
       const uint32_t m = min((uint32_t)kTrackChunk, n - base);
       for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
         const fizi_result& r = rr[base + i];
-        t_s[i] = r.t_ms; ar_s[i] = r.blob_area; cx_s[i] = r.cx; cy_s[i] = r.cy;
+        t_s[i] = r.t_ms; ar_s[i] = r.blob_area; cx_s[i] = r.cx; cy_s[i] = r.cy; fl_s[i] = r.relearn;
       }
       __syncthreads();
       if (threadIdx.x == 0) {
         int64_t t_n = t_s[0];
-        uint32_t a_n = ar_s[0];
+        uint32_t a_n = ar_s[0], l_n = fl_s[0];
         double x_n = cx_s[0], y_n = cy_s[0];
         for (uint32_t i = 0; i < m; i++) {
           fizi_result r;
-          r.t_ms = t_n; r.blob_area = a_n; r.cx = x_n; r.cy = y_n;
-          if (i + 1 < m) { t_n = t_s[i + 1]; a_n = ar_s[i + 1]; x_n = cx_s[i + 1]; y_n = cy_s[i + 1]; }
+          r.t_ms = t_n; r.blob_area = a_n; r.cx = x_n; r.cy = y_n; r.relearn = l_n;
+          if (i + 1 < m) {
+          t_n = t_s[i + 1]; a_n = ar_s[i + 1]; x_n = cx_s[i + 1]; y_n = cy_s[i + 1]; l_n = fl_s[i + 1];
+        }
           track_one(p, st, r);
           dw_o[i] = r.dwell_ms; px_o[i] = r.px; py_o[i] = r.py;
           vc_o[i] = (uint8_t)(r.visible | (r.clicked << 1));

@@ -12,7 +12,22 @@
 
 namespace fizi {
 
+__device__ __forceinline__ void track_reset(TrackState& s) {
+  s.vis = 0; s.fired = 0;
+  s.px = s.py = s.ax = s.ay = 0.0;
+  s.last_t = s.anchor_t = s.dwell = 0;
+}
+
+// r.relearn (NEXT-1, reading L37): a learning frame is not tracked (the state
+// is untouched, the pointer outputs are zero); after the last learning frame
+// (the model swap) the state restarts from its initial value.
 __device__ __forceinline__ void track_one(const fizi_params& p, TrackState& s, fizi_result& r) {
+  if (r.relearn & FIZI_RELEARN_LEARN) {
+    r.visible = 0; r.clicked = 0;
+    r.px = 0.0; r.py = 0.0; r.dwell_ms = 0;
+    if (r.relearn & FIZI_RELEARN_SWAP) track_reset(s);
+    return;
+  }
   const int64_t t = r.t_ms;
   if (r.blob_area > 0) {
     if (s.vis) {

@@ -48,14 +48,16 @@ class Params(ctypes.Structure):
 RESULT_DTYPE = np.dtype({
     "names": ["t_ms", "stream", "frame_idx", "mean_luma", "corrected", "visible", "clicked",
               "fg_merged", "fg_final", "n_comp_total", "n_comp_kept", "blob_area", "blob_label",
-              "bbox", "sum_x", "sum_y", "gamma", "cx", "cy", "px", "py", "dwell_ms"],
+              "bbox", "relearn", "sum_x", "sum_y", "gamma", "cx", "cy", "px", "py", "dwell_ms"],
     "formats": ["<i8", "<u4", "<u4", "u1", "u1", "u1", "u1", "<u4", "<u4", "<u4", "<u4", "<u4",
-                "<u4", ("<u4", (4,)), "<u8", "<u8", "<f8", "<f8", "<f8", "<f8", "<f8", "<i8"],
-    "offsets": [0, 8, 12, 16, 17, 18, 19, 20, 24, 28, 32, 36, 40, 44, 64, 72, 80, 88, 96, 104,
-                112, 120],
+                "<u4", ("<u4", (4,)), "<u4", "<u8", "<u8", "<f8", "<f8", "<f8", "<f8", "<f8",
+                "<i8"],
+    "offsets": [0, 8, 12, 16, 17, 18, 19, 20, 24, 28, 32, 36, 40, 44, 60, 64, 72, 80, 88, 96,
+                104, 112, 120],
     "itemsize": 128,
 })
 RESULT_BYTES = 128
+RELEARN_LEARN, RELEARN_SWAP, RELEARN_TRIGGER = 1, 2, 4   # fizi_result.relearn flags (NEXT-1)
 CALL_SLOTS = 4          # FIZI_CALL_SLOTS (include/fizi.h): output buffers a pipelined caller may rotate
 
 
@@ -128,12 +130,13 @@ def lib() -> ctypes.CDLL:
         L.fizi_drive.argtypes = [vp, u32, vp, u32, vp, vp]
         L.fizi_drive_throttle.argtypes = [vp, u32, vp, u32, vp, u32, u32, vp, vp]
         L.fizi_relearn_flags.argtypes = [vp, u32, vp, u32, u32, vp, vp]
+        L.fizi_set_relearn.argtypes = [vp, u32, u32, u32, u8]
         L.fizi_set_zones.argtypes = [vp, u32, vp, u32]
         L.fizi_hit_test.argtypes = [vp, u32, vp, u32, vp, vp]
         L.fizi_flush.argtypes = [vp, vp]
         L.fizi_get_lut_table.argtypes = [vp, vp, vp, vp, vp]
         for name in ("fizi_set_pipeline", "fizi_flush", "fizi_wheel_default", "fizi_set_wheel",
-                     "fizi_drive", "fizi_drive_throttle", "fizi_relearn_flags", "fizi_set_zones", "fizi_hit_test", "fizi_params_default", "fizi_create", "fizi_learn_background",
+                     "fizi_drive", "fizi_drive_throttle", "fizi_relearn_flags", "fizi_set_relearn", "fizi_set_zones", "fizi_hit_test", "fizi_params_default", "fizi_create", "fizi_learn_background",
                      "fizi_process_frames", "fizi_segment_frames", "fizi_process_frames_host",
                      "fizi_track", "fizi_track_runs", "fizi_reset_tracker", "fizi_debug_stage",
                      "fizi_get_background", "fizi_set_background", "fizi_get_lut_table"):
@@ -428,6 +431,13 @@ class Fizi:
                                              flags.data_ptr(), _stream_handle(self.device)),
                     "fizi_relearn_flags")
         return flags
+
+    def set_relearn(self, stream: int = 0, threshold: int = 40, n_frames: int = 30,
+                    margin: int = 10):
+        """NEXT-1 in-stream relearning of `stream` (fizi_set_relearn); n_frames=0 disables.
+        Records carry the RELEARN_* flags in their `relearn` field."""
+        self._check(lib().fizi_set_relearn(self._h, stream, threshold, n_frames, margin),
+                    "fizi_set_relearn")
 
     def set_zones(self, zones, stream: int = 0):
         """NEXT-3: install a layout (sequence of Zone) for `stream`."""

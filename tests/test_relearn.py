@@ -137,3 +137,98 @@ def test_relearn_ignores_triggers_while_learning_and_resets_the_tracker():
     assert recs[k].blob_area > 0 and recs[k].visible == 1
     assert recs[k].px == recs[k].cx and recs[k].py == recs[k].cy    # snapped: tracker reset
     assert recs[k].dwell_ms == 0
+
+
+# ------------------------------------------ in-stream relearning (GPU vs oracle)
+def _gpu_relearn_case(W, H, frames, learn, t, threshold, F, batches, params=None):
+    """Run the stream through the device in calls of the given sizes with
+    relearning enabled; compare every record (flags, tracker) and mask with
+    the oracle composition."""
+    import torch
+    import oracle
+    import synth
+    from oracle.relearn import run_stream_relearn
+    from paper_1907_04393_b200 import Fizi, results_numpy
+    from tests.gpu_common import compare_record
+    params = params or {}
+    p = oracle.make_params(W, H, **params)
+    lo, hi = oracle.learn(learn, synth.MARGIN)
+    recs, masks, flags, swaps = run_stream_relearn(p, frames, t, lo, hi, threshold, F, synth.MARGIN)
+    fz = Fizi(W, H, max_batch=max(batches), **params)
+    fz.learn_background(torch.from_numpy(learn).cuda(), margin=synth.MARGIN)
+    fz.set_relearn(threshold=threshold, n_frames=F, margin=synth.MARGIN)
+    k0 = 0
+    for b in batches:
+        if k0 >= len(frames):
+            break
+        sl = slice(k0, min(len(frames), k0 + b))
+        m, r = fz.process_frames(torch.from_numpy(frames[sl]).cuda(), t_ms=t[sl])
+        r, m = results_numpy(r), m.cpu().numpy()
+        for i, k in enumerate(range(sl.start, sl.stop)):
+            assert int(r[i]["relearn"]) == flags[k], (k, int(r[i]["relearn"]), flags[k])
+            compare_record(r[i], recs[k], k, track=True)
+            assert np.array_equal(m[i], masks[k]), k
+        k0 = sl.stop
+    # the stream's model after the run = the oracle's last swap model
+    if swaps:
+        glo, ghi = fz.get_background()
+        assert np.array_equal(glo.cpu().numpy(), swaps[-1][1])
+        assert np.array_equal(ghi.cpu().numpy(), swaps[-1][2])
+    fz.close()
+    return flags
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batches", [[15], [4] * 4, [1] * 15, [2, 7, 6]])
+def test_gpu_relearn_lighting_step_any_batching(batches):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    cfg, frames, learn = _step_scene(3, 12, 1280)
+    t = np.arange(len(frames), dtype=np.int64) * 33
+    flags = _gpu_relearn_case(cfg.W, cfg.H, frames, learn, t, 20, 5, batches,
+                              dict(min_blob_ppm=0))
+    assert flags.count(0) < len(flags)
+
+
+@pytest.mark.gpu
+def test_gpu_relearn_generic_path_and_two_swaps_in_one_call():
+    """W % 32 != 0 (generic path); two lighting steps far enough apart that two
+    models are learned and swapped inside one call (F = 2)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import synth
+    cfg = synth.CONFIGS[1]
+    W, H, n = 100, 60, 16
+    pf = synth.frame_params(cfg, 0, range(n))
+    pf[:, 2] = 50
+    pf[:, 3] = 30
+    pf[:, 4] = 12
+    pf[:, 1] = [1024] * 3 + [1300] * 6 + [800] * 7
+    ell = np.array([[20, 15, 10, 8], [80, 45, 12, 9]], np.int32)
+    frames = synth.gen_host(W, H, cfg.seed, 0, pf, ell)
+    lpf = synth.frame_params(cfg, 0, range(cfg.n_learn), learning=True)
+    learn = synth.gen_host(W, H, cfg.seed, 0, lpf, ell)
+    t = np.arange(n, dtype=np.int64) * 33
+    flags = _gpu_relearn_case(W, H, frames, learn, t, 20, 2, [16], dict(min_blob_ppm=0))
+    from oracle.relearn import RELEARN_SWAP
+    assert sum(1 for f in flags if f & RELEARN_SWAP) == 2
+
+
+@pytest.mark.gpu
+def test_gpu_relearn_c2_drift_stream():
+    """C2's lighting drift (exposure steps, over-exposure ramp) with relearning
+    (threshold 20, F = 10) over 320 frames in calls of 64."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import synth
+    cfg = synth.CONFIGS[2]
+    ks = list(range(0, 320))
+    frames = synth.frames_host(cfg, 0, ks)
+    learn = synth.learning_frames_host(cfg)
+    t = np.array([synth.t_ms(k) for k in ks], np.int64)
+    flags = _gpu_relearn_case(cfg.W, cfg.H, frames, learn, t, 20, 10, [64] * 5)
+    from oracle.relearn import RELEARN_SWAP
+    assert any(f & RELEARN_SWAP for f in flags)
