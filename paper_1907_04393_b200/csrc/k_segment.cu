@@ -305,6 +305,40 @@ __device__ __forceinline__ bool all_inside_sad(const uint32_t (&fr)[12], const E
   return e.ordered && acc[0] + acc[1] == e.W;
 }
 
+// Per-pixel R1 & R2 & R3 of the thread's 16 pixels (bit p = pixel p) from the
+// raw envelope bytes: per byte lo <= v <= hi (two byte-SIMD compares; lo > hi
+// is never inside, L2), the three byte flags of each pixel gathered into R,
+// G and B planes by byte permutes (a pixel is background iff all three are
+// inside, L3), and one colour-table lookup (R2 & R3) per pixel outside.
+__device__ __forceinline__ uint32_t slow_bits16_raw(const uint32_t (&fr)[12], const uint32_t (&lo)[12],
+                                                    const uint32_t (&hi)[12],
+                                                    const uint32_t* __restrict__ skin) {
+  uint32_t m[12];
+#pragma unroll
+  for (int i = 0; i < 12; i++) m[i] = __vcmpgeu4(fr[i], lo[i]) & __vcmpleu4(fr[i], hi[i]);
+  uint32_t outm = 0;                                   // bit p: pixel p has a byte outside
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint32_t w0 = m[3 * q], w1 = m[3 * q + 1], w2 = m[3 * q + 2];
+    const uint32_t R = __byte_perm(__byte_perm(w0, w1, 0x0630), w2, 0x5210);
+    const uint32_t G = __byte_perm(__byte_perm(w0, w1, 0x0741), w2, 0x6210);
+    const uint32_t B = __byte_perm(__byte_perm(w0, w1, 0x0052), w2, 0x7410);
+    outm |= (((((~(R & G & B)) >> 7) & 0x01010101u) * 0x01020408u) >> 24) << (4 * q);
+  }
+  uint32_t bits = 0;
+#pragma unroll
+  for (int p = 0; p < 16; p++) {
+    const int b0 = 3 * p;
+    const uint32_t wl = fr[b0 >> 2], wh = fr[(b0 >> 2) + ((b0 & 3) > 1 ? 1 : 0)];
+    const uint32_t o = b0 & 3;
+    const uint32_t sel = ((o + 2) & 0x7) | (((o + 1) & 0x7) << 4) | ((o & 0x7) << 8) | 0x4000u;
+    const uint32_t idx = __byte_perm(wl, wh, sel) & 0x00FFFFFFu;
+    const uint32_t t = ((outm >> p) & 1u) ? (__ldg(skin + (idx >> 5)) >> (idx & 31)) & 1u : 0u;
+    bits |= t << p;
+  }
+  return bits;
+}
+
 // Per-pixel R1 & R2 & R3 of the thread's 16 pixels (bit p = pixel p):
 // R1 per byte from the envelope lanes, R2 & R3 from the colour table.
 __device__ __forceinline__ uint32_t slow_bits16(const uint32_t (&fr)[12], const EnvRegs& e,
@@ -332,30 +366,6 @@ __device__ __forceinline__ uint32_t slow_bits16(const uint32_t (&fr)[12], const 
   uint32_t bits = 0;
 #pragma unroll
   for (int p = 0; p < 16; p++) bits |= tw[p] << p;
-  return bits;
-}
-
-// The same per-pixel result with R2 & R3 evaluated arithmetically
-// (gray_and_skin, the definition the colour table is built from) instead of
-// looked up: no dependent memory round trip in the per-pixel kernel.
-__device__ __forceinline__ uint32_t slow_bits16_alu(const uint32_t (&fr)[12], const EnvRegs& e,
-                                                    int S, int a1, int a2) {
-  uint64_t inside = 0;
-#pragma unroll
-  for (int i = 0; i < 12; i++) {
-    uint32_t tE, tO;
-    r1_lanes(fr[i], e, i, tE, tO);
-    const uint32_t f4 = ((tE >> 15) & 1u) | ((tO >> 14) & 2u) | ((tE >> 29) & 4u) | ((tO >> 28) & 8u);
-    inside |= (uint64_t)f4 << (4 * i);
-  }
-  uint32_t bits = 0;
-#pragma unroll
-  for (int p = 0; p < 16; p++) {
-    const int b0 = 3 * p;
-    const int r = (int)byte_of(fr, b0), g = (int)byte_of(fr, b0 + 1), b = (int)byte_of(fr, b0 + 2);
-    const uint32_t bit = ((inside >> b0) & 7u) == 7u ? 0u : gray_and_skin(r, g, b, S, a1, a2);
-    bits |= bit << p;
-  }
   return bits;
 }
 
@@ -708,7 +718,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_multi_kernel(SegArgs a) {
 #else
 #define FIZI_SLOW_BOUNDS __launch_bounds__(256)
 #endif
-template <bool kAluSkin>
 __global__ void FIZI_SLOW_BOUNDS slow_words_kernel(SegArgs a) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) tl_mark(a.call, kTlSlow, 0);
@@ -737,15 +746,22 @@ __global__ void FIZI_SLOW_BOUNDS slow_words_kernel(SegArgs a) {
     const uint32_t L = 2 * k + (lane & 1);                   // lane of the chunk
     const uint64_t coff = (uint64_t)cq * kChunkBytes;
     const bool valid = act && coff + 48u * L < a.frame_bytes;
-    EnvRegs e;
     const uint32_t stream = single >= 0 ? (uint32_t)single : (act ? a.frame_stream[f] : 0u);
     const uint8_t* elo = a.env + (uint64_t)stream * 2 * a.env_plane + coff + 16 * L;
-    if (valid) load_env(e, elo, elo + a.env_plane);
-    else zero_env(e);
+    uint32_t lo[12], hi[12];
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      uint4 l = make_uint4(0, 0, 0, 0), h = make_uint4(~0u, ~0u, ~0u, ~0u);
+      if (valid) {
+        l = __ldg(reinterpret_cast<const uint4*>(elo + 512 * k));
+        h = __ldg(reinterpret_cast<const uint4*>(elo + a.env_plane + 512 * k));
+      }
+      lo[4 * k] = l.x; lo[4 * k + 1] = l.y; lo[4 * k + 2] = l.z; lo[4 * k + 3] = l.w;
+      hi[4 * k] = h.x; hi[4 * k + 1] = h.y; hi[4 * k + 2] = h.z; hi[4 * k + 3] = h.w;
+    }
     uint32_t fr[12];
     load48(frames + (uint64_t)f * a.frame_bytes + coff + 48 * L, valid, fr);
-    uint32_t bits = kAluSkin ? slow_bits16_alu(fr, e, (int)a.S, (int)a.a1, (int)a.a2)
-                             : slow_bits16(fr, e, a.skin);
+    uint32_t bits = slow_bits16_raw(fr, lo, hi, a.skin);
     bits = valid ? bits : 0u;
     const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
     const bool writer = !(lane & 1) && valid;
@@ -999,14 +1015,9 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
 cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st) {
   SegArgs a = seg_args(c, f0, n, 0, sub);
   prof_begin(c, st);
-  // colour-table test by default: the ALU test keeps the ALU pipe 83 % busy
-  // on C4 (profiles/r01_slow_words_c4_ncu.txt); the table is 223 vs 290 us
-  // per C4 call and 19 vs 21 us per C3 call (gpurun_out A/B)
-#ifdef FIZI_SLOW_ALU
-  slow_words_kernel<true><<<c.sms * 8, 256, 0, st>>>(a);    // A/B build: arithmetic test
-#else
-  slow_words_kernel<false><<<c.sms * 8, 256, 0, st>>>(a);
-#endif
+  // colour-table test (an arithmetic R2 & R3 test kept the ALU pipe 83 %
+  // busy on C4 and was slower: 290 vs 223 us per C4 call in round 1)
+  slow_words_kernel<<<c.sms * 8, 256, 0, st>>>(a);
   prof_end(c, FIZI_PROF_SLOW, st);
   c.launches += 1;
   return cudaGetLastError();

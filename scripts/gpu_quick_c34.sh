@@ -1,0 +1,9 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_gaps.py tests/test_gpu_pipeline.py -m gpu -q -x --timeout 900 -p no:cacheprovider --deselect tests/test_gpu_gaps.py::test_exhaustive_5x5_masks_morphology_and_labelling > gpurun_out/pytest_q.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_q.log
+timeout 600 python bench.py --steps 300 --warmup 10 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3.log 2>&1
+timeout 900 python bench.py --config 4 --steps 40 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_c4.log 2>&1
+P4="python bench.py --config 4 --steps 3 --warmup 2 --no-e2e --no-cpu-baseline --no-spot-check"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv $P4 > gpurun_out/ncu_l4.log 2>&1
