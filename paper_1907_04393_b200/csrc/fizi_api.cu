@@ -176,6 +176,9 @@ void free_all(Ctx& c) {
   if (c.side2) cudaStreamDestroy(c.side2);
   if (c.side3) cudaStreamDestroy(c.side3);
   if (c.head) cudaStreamDestroy(c.head);
+  if (c.prep) cudaStreamDestroy(c.prep);
+  for (auto ev : c.ev_prep)
+    if (ev) cudaEventDestroy(ev);
   if (c.cclst) cudaStreamDestroy(c.cclst);
   if (c.morphst) cudaStreamDestroy(c.morphst);
   if (c.pinned_results) cudaFreeHost(c.pinned_results);
@@ -341,10 +344,9 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   int rc = FIZI_OK;
   if (part == kHead) {
-    // per-call table upload and counter clear, then the fused segmentation
-    // kernel beside the u8 mask clear (a branch on side2, joined back)
-    rc = enqueue_head(c, pl, st);
-    if (rc) return rc;
+    // the fused segmentation kernel beside the u8 mask clear (a branch on
+    // side2, joined back); the table upload and counter clear ran ahead on
+    // the prep stream
     if (pl.premask) {
       e = cudaEventRecord(c.ev_hfork, st);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side2, c.ev_hfork, 0);
@@ -535,7 +537,8 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
   pl.slot = c.pinned_next;
   c.pinned_next = (c.pinned_next + 1) % fizi::kSlots;
   const auto h0 = std::chrono::steady_clock::now();
-  cudaError_t e = cudaEventSynchronize(c.pinned_ev[pl.slot]);   // slot's last upload consumed
+  cudaError_t e = cudaEventSynchronize(c.slot_upload[pl.slot] ? c.slot_upload[pl.slot]
+                                                               : c.pinned_ev[pl.slot]);   // slot's last upload consumed
   const auto h1 = std::chrono::steady_clock::now();
   c.host_sync_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(h1 - h0).count();
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventSynchronize");
@@ -557,6 +560,7 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
     if (rc) return rc;
     e = cudaEventRecord(c.pinned_ev[pl.slot], st);
     if (e == cudaSuccess) e = cudaEventRecord(c.ev_tail[pl.slot], st);
+    c.slot_upload[pl.slot] = c.pinned_ev[pl.slot];
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
   } else {
     // Four graph launches per call, each on a stream that runs its stage
@@ -570,14 +574,22 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
     // tracker state are only touched by the in-order labelling stage).  st
     // itself is not joined (fizi_flush does that); st already waits for the
     // slot's previous call (above), and every stage is ordered after st.
+    // The slot's table upload and counter clear run ahead on the prep
+    // stream, as soon as the slot's previous call is done, so the
+    // segmentation starts the moment the previous one ends.
     cudaStream_t hs = c.head;
-    e = cudaEventRecord(c.ev_in[pl.slot], st);
+    e = cudaStreamWaitEvent(c.prep, c.ev_tail[pl.slot], 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "prep");
+    rc = enqueue_head(c, pl, c.prep);
+    if (rc) return rc;
+    e = cudaEventRecord(c.ev_prep[pl.slot], c.prep);   // (also: the pinned table consumed)
+    if (e == cudaSuccess) e = cudaEventRecord(c.ev_in[pl.slot], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, c.ev_in[pl.slot], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, c.ev_prep[pl.slot], 0);
     if (e != cudaSuccess) return cuda_fail(c, e, "fork");
     rc = run_part(c, pl, kHead, hs);
     if (rc) return rc;
     e = cudaEventRecord(c.ev_head[pl.slot], hs);
-    if (e == cudaSuccess) e = cudaEventRecord(c.pinned_ev[pl.slot], hs);   // table consumed
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side, c.ev_head[pl.slot], 0);
     if (e != cudaSuccess) return cuda_fail(c, e, "fork");
     rc = run_part(c, pl, kTail, c.side);
@@ -594,6 +606,7 @@ int run_call(Ctx& c, const uint32_t* sof, const uint8_t* frames, uint32_t n, con
     if (rc) return rc;
     e = cudaEventRecord(c.ev_tail[pl.slot], c.cclst);
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
+    c.slot_upload[pl.slot] = c.ev_prep[pl.slot];
   }
   c.tail_pending = true;
   c.host_call_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
@@ -766,6 +779,9 @@ int fizi_create(const fizi_params* params, int cuda_device, uint32_t n_streams,
       e = cudaStreamCreateWithPriority(&c.head, cudaStreamNonBlocking,
                                        (hp && atoi(hp) == 0) ? lo_prio : hi_prio);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.cclst, cudaStreamNonBlocking, side_prio);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.prep, cudaStreamNonBlocking, hi_prio);
+    for (uint32_t i = 0; i < fizi::kSlots && e == cudaSuccess; i++)
+      e = cudaEventCreateWithFlags(&c.ev_prep[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.morphst, cudaStreamNonBlocking, side_prio);
     for (cudaEvent_t* ev : {&c.ev_zfork, &c.ev_zjoin, &c.ev_hfork, &c.ev_hjoin})
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);

@@ -173,7 +173,9 @@ struct Ctx {
   cudaStream_t morphst = nullptr;        // pipelined tail: morphology, call order
   cudaStream_t side2 = nullptr;          // head branch: u8 mask zeroing
   cudaStream_t side3 = nullptr;          // tail branch: LUT re-test
-  cudaStream_t head = nullptr;           // pipelined head: upload, clear, segmentation (call order)
+  cudaStream_t head = nullptr;           // pipelined head: segmentation (call order)
+  cudaStream_t prep = nullptr;           // pipelined: the slot's table upload + counter clear, ahead
+  cudaEvent_t ev_prep[kSlots] = {};      // pipelined: slot's table uploaded and counters cleared
   cudaEvent_t ev_hfork = nullptr, ev_hjoin = nullptr;   // head: u8 mask clear branch
   cudaStream_t h2d = nullptr, d2h = nullptr;   // fizi_process_frames_host copy streams
   std::vector<cudaEvent_t> host_ev;            // fizi_process_frames_host chunk events
@@ -205,6 +207,7 @@ struct Ctx {
   uint8_t* pinned[kSlots] = {};               // staging for the per-call upload (one per slot)
   size_t pinned_bytes = 0;
   cudaEvent_t pinned_ev[kSlots] = {};
+  cudaEvent_t slot_upload[kSlots] = {};  // the event that marks the slot's last table upload done
   uint32_t pinned_next = 0;
   // captured launch sequences, one per call shape and pinned slot
   struct GraphEntry {
