@@ -65,19 +65,21 @@ def parse():
     return ap.parse_args()
 
 
-def ncu_traffic(seg_bytes):
-    """DRAM bytes per launch of the fused kernel from the latest committed
-    ncu --set full capture (profiles/r*_seg_fast_traffic.json), if it was
-    taken on the same per-launch workload."""
+def ncu_traffic(seg_bytes, kernel):
+    """DRAM bytes per launch of the fused kernel from the latest committed ncu
+    --set full capture of that kernel on the same per-launch workload
+    (profiles/r*_*_traffic.json)."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_seg_fast_traffic.json")))
-    if not files:
-        return None, None
-    with open(files[-1]) as f:
-        d = json.load(f)
-    if abs(d.get("algorithmic_bytes_per_launch", 0) - seg_bytes) > 1:
-        return None, None
-    return d["dram_bytes_per_launch"], os.path.relpath(files[-1], ROOT)
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json"))):
+        with open(path) as f:
+            d = json.load(f)
+        if d.get("kernel", "seg_fast_kernel") != kernel:
+            continue
+        if abs(d.get("algorithmic_bytes_per_launch", 0) - seg_bytes) > 1:
+            continue
+        best = (d["dram_bytes_per_launch"], os.path.relpath(path, ROOT))
+    return best if best else (None, None)
 
 
 def peaks():
@@ -550,9 +552,10 @@ def main():
     seg_gbs = seg_bytes * args.steps / (seg_ms / 1e3) / 1e9 if seg_n else None
     step_bytes = B * (3 * N + N) + 6 * N * min(S, B)   # whole-path algorithmic bytes per step
     step_ms = ms_max / args.steps
-    traffic, traffic_src = ncu_traffic(seg_bytes) if launches_per_step == 1 else (None, None)
+    kname = "seg_multi_kernel" if (S > 1 and B > 1) else "seg_fast_kernel"
+    traffic, traffic_src = ncu_traffic(seg_bytes, kname) if launches_per_step == 1 else (None, None)
     roofline = {
-        "bound": "hbm", "kernel": "seg_fast_kernel (fused luma + R1/R2/R3, a2+a3)",
+        "bound": "hbm", "kernel": f"{kname} (fused luma + R1/R2/R3, a2+a3)",
         "achieved": seg_gbs, "peak": hbm, "unit": "GB/s",
         "frac": (seg_gbs / hbm) if seg_gbs else None, "traffic": traffic,
         "traffic_source": traffic_src,
