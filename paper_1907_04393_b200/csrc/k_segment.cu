@@ -32,7 +32,7 @@
 namespace fizi {
 
 #ifndef FIZI_MULTI_STAGES
-#define FIZI_MULTI_STAGES 4
+#define FIZI_MULTI_STAGES 2
 #endif
 constexpr int kMultiStages = FIZI_MULTI_STAGES;   // ring depth of the multi-stream kernel
 
@@ -999,7 +999,15 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
       // one frame per same-stream group (multi-stream call): the envelope
       // streams with the frame through the TMA ring
       a.persist = true;
-      seg_multi_kernel<kMultiStages, 1><<<c.sms, 256, kMultiStages * 3 * kTileBytes, st>>>(a);
+      // two CTAs per SM, each a 2-deep ring of 36 KiB stages (measured on
+      // C5: 1.69M frames/s, vs 1.54M with one CTA per SM and a 4-deep ring,
+      // 1.61M with 2 x 3-deep, 1.58M with 3 x 2-deep; FIZI_MULTI_CFG=1
+      // selects the 1 x 4-deep variant)
+      static const int cfg = getenv("FIZI_MULTI_CFG") ? atoi(getenv("FIZI_MULTI_CFG")) : 0;
+      if (cfg == 1)
+        seg_multi_kernel<4, 1><<<c.sms, 256, 4 * 3 * kTileBytes, st>>>(a);
+      else
+        seg_multi_kernel<kMultiStages, 2><<<2 * c.sms, 256, kMultiStages * 3 * kTileBytes, st>>>(a);
     } else {
       seg_fast_kernel<3, 4><<<grid, 256, 4 * kTileBytes, st>>>(a);   // 3 CTAs/SM x 4-deep ring
     }
@@ -1066,8 +1074,11 @@ cudaError_t init_segment(Ctx& c) {
   cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<3, 4>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTileBytes);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(seg_multi_kernel<kMultiStages, 1>,
+    e = cudaFuncSetAttribute(seg_multi_kernel<kMultiStages, 2>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, kMultiStages * 3 * kTileBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(seg_multi_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             4 * 3 * kTileBytes);
   const char* ps = getenv("FIZI_SEG_PERSIST");          // experiment switch
   c.seg_persist = ps ? 2u * (uint32_t)atoi(ps) : 5u;      // in half CTAs per SM
   if (e == cudaSuccess)
