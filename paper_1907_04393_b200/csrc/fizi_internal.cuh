@@ -94,6 +94,7 @@ struct Ctx {
   uint32_t seg_persist = 5;              // persistent fused kernel: half-CTAs per SM (0: off)
   uint32_t group_max = kFrameGroup;      // frames per same-stream group (fused-kernel item)
   bool use_dirty = false;                // clean chunks of A are not written (dirty bitmap)
+  bool inline_words = false;             // per-pixel words evaluated inside the fused kernel (A/B)
   bool mask_by_morph = true;             // u8 mask rows written by the morphology (else zero + kept runs)
   uint32_t morph_tr = 0;                 // output rows per morphology CTA
   uint64_t launches = 0;

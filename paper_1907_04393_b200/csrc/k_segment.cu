@@ -99,8 +99,8 @@ __device__ __forceinline__ void finalize_frame(const SegArgs& a, uint32_t f,
     const uint32_t pos = atomicAdd(&fix[0], 1u);
     FIZI_DCHECK(pos < a.n);
     fix[1 + pos] = f;
+    fg[f] = 0;                   // the LUT re-test recounts the frame's merged pixels
   }
-  (void)fg;
 }
 
 // Rec.601 weights split so every dp4a weight fits a byte:
@@ -399,7 +399,7 @@ __device__ __forceinline__ uint32_t seg16(const uint8_t* px48, const EnvRegs& e,
 // of every SM for its whole duration and the pipelined tail kernels of the
 // previous call run beside it in the rest.  The ring's stage / parity run on
 // across items (g0 counts the frames this CTA has streamed so far).
-template <int kMinBlocks, int kStages>
+template <int kMinBlocks, int kStages, bool kInline>
 __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   static_assert(kStages >= 2 && kStages <= kFrameGroup, "ring depth");
   extern __shared__ __align__(128) uint8_t sm[];          // kStages x 12 KiB tiles
@@ -407,6 +407,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
   __shared__ uint32_t empty_cnt[kStages];
   // per-frame partial luma sums of the CTA: <= 8 warps * 512 px * 255000 < 2^32
   __shared__ uint32_t acc_y[kFrameGroup];
+  __shared__ uint32_t acc_fg[kFrameGroup];                  // kInline: merged pixels per frame
   __shared__ uint32_t s_item;
   // words queued for the per-pixel kernel, staged per work item: (frame
   // index in the group, warp, word); moved to the global queue at the end of
@@ -443,7 +444,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     const uint32_t tbytes = trem < (uint64_t)kTileBytes ? (uint32_t)trem : (uint32_t)kTileBytes;
     const uint32_t n_active = min((uint32_t)kWarpsPerCta, a.nchunks - tile * kWarpsPerCta);
     const uint8_t* src0 = frames + toff;
-    if (tid < kFrameGroup) acc_y[tid] = 0;
+    if (tid < kFrameGroup) { acc_y[tid] = 0; acc_fg[tid] = 0; }
     if (tid == 0) q_tail = 0;
     __syncthreads();
     uint64_t pol = 0;
@@ -473,6 +474,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
       if (warp != 0) pol = policy_evict_first();
       const uint8_t* my = sm + warp * kChunkBytes + 48 * lane;
       uint32_t luma_lane = 0;                                // lane i: this warp's luma of frame i
+      uint32_t fg_lane = 0;                                  // kInline: lane i: merged pixels of frame i
       for (uint32_t i = 0; i < nf; i++) {
         const uint32_t gi = g0 + i;
         const uint32_t s = gi % kStages;
@@ -500,7 +502,20 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
         // marked).  In a chunk touching the foreground, the words with a pixel
         // outside the envelope are queued for the per-pixel kernel (one item
         // each) and the others written as 0.
-        if (out_lanes) {
+        if (kInline && out_lanes) {
+          // per-pixel R1 & R2 & R3 right here, from the registers (A/B
+          // variant: no queue, no re-read, but the CTA's ring advances at
+          // the pace of its slowest warp)
+          const uint32_t bits = inside ? 0u : slow_bits16_raw(fr, e.lo, e.hi, a.skin);
+          const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
+          const bool writer = !(lane & 1) && valid;
+          const uint32_t pc = warp_sum_u32(writer ? __popc(word) : 0u);
+          if ((uint32_t)lane == i) fg_lane += pc;
+          if ((pc || a.write_zero) && writer)
+            a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = word;
+          if (pc && lane == 0)
+            atomicOr(a.dirty + (uint64_t)f * a.dirty_words + (c >> 5), 1u << (c & 31));
+        } else if (out_lanes) {
           const uint32_t slow_words = (out_lanes | (out_lanes >> 1)) & 0x55555555u;   // bit 2k
           uint32_t base = 0;
           if (lane == 0) base = atomicAdd(&q_tail, (uint32_t)__popc(slow_words));
@@ -518,7 +533,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
           a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = 0u;
         }
       }
-      if ((uint32_t)lane < nf) atomicAdd(&acc_y[lane], luma_lane);
+      if ((uint32_t)lane < nf) {
+        atomicAdd(&acc_y[lane], luma_lane);
+        if (kInline && fg_lane) atomicAdd(&acc_fg[lane], fg_lane);
+      }
     }
     g0 += nf;
     __syncthreads();                                         // flush the CTA's sums and queue
@@ -538,6 +556,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_fast_kernel(SegArgs a) {
     if (tid < (int)nf) {
       const uint32_t f = a.group_frames[f_begin + tid];
       atomicAdd(&a.luma[f], (unsigned long long)acc_y[tid]);
+      if (kInline && acc_fg[tid]) atomicAdd(&a.fg[f], acc_fg[tid]);
       __threadfence();
       if (atomicAdd(&a.frame_done[f], 1u) == a.tiles - 1) {   // last CTA of frame f
         __threadfence();
@@ -1009,7 +1028,9 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
       else
         seg_multi_kernel<kMultiStages, 2><<<2 * c.sms, 256, kMultiStages * 3 * kTileBytes, st>>>(a);
     } else {
-      seg_fast_kernel<3, 4><<<grid, 256, 4 * kTileBytes, st>>>(a);   // 3 CTAs/SM x 4-deep ring
+      // 3 CTAs/SM x 4-deep ring; FIZI_INLINE=1: per-pixel words inside (A/B)
+      if (c.inline_words) seg_fast_kernel<3, 4, true><<<grid, 256, 4 * kTileBytes, st>>>(a);
+      else seg_fast_kernel<3, 4, false><<<grid, 256, 4 * kTileBytes, st>>>(a);
     }
   } else {
     luma_generic_kernel<<<dim3((unsigned)((c.N + 255) / 256), n), 256, 0, st>>>(c.call, c.N, f0,
@@ -1071,8 +1092,12 @@ cudaError_t launch_seg_fix(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaSt
 
 cudaError_t init_segment(Ctx& c) {
   (void)c;
-  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<3, 4>,
+  cudaError_t e = cudaFuncSetAttribute(seg_fast_kernel<3, 4, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTileBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(seg_fast_kernel<3, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             4 * kTileBytes);
+  c.inline_words = getenv("FIZI_INLINE") != nullptr && atoi(getenv("FIZI_INLINE")) == 1;
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(seg_multi_kernel<kMultiStages, 2>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, kMultiStages * 3 * kTileBytes);

@@ -538,3 +538,36 @@ def test_error_codes():
         Fizi(320, 240, se_radius=0)
     assert e.value.status == F.E_ARG
     fz.close()
+
+
+def test_binding_validates_output_buffers():
+    """The binding checks every caller-supplied buffer before the C call
+    (ADVICE r01): too small, wrong dtype, non-contiguous or host buffers raise
+    instead of reaching the library."""
+    cfg = synth.CONFIGS[1]
+    fz = _ctx(cfg.W, cfg.H, max_batch=4)
+    fz.learn_background(_t(synth.learning_frames_host(cfg)))
+    frames = _t(synth.frames_host(cfg, 0, range(2)))
+    t = np.array([0, 33], np.int64)
+    ok_res = torch.empty((2, 128), dtype=torch.uint8, device=DEV)
+    with pytest.raises(ValueError):
+        fz.process_frames(frames, t_ms=t, results=torch.empty((1, 128), dtype=torch.uint8, device=DEV))
+    with pytest.raises(ValueError):
+        fz.process_frames(frames, t_ms=t, results=ok_res,
+                          masks=torch.empty((1, cfg.H, cfg.W), dtype=torch.uint8, device=DEV))
+    with pytest.raises(TypeError):
+        fz.process_frames(frames, t_ms=t, results=ok_res,
+                          masks=torch.empty((2, cfg.H, cfg.W), dtype=torch.float32, device=DEV))
+    with pytest.raises(TypeError):
+        fz.process_frames(frames, t_ms=t, results=torch.empty((2, 128), dtype=torch.uint8))
+    with pytest.raises(ValueError):
+        fz.process_frames(frames, t_ms=t, results=torch.empty((128, 4), dtype=torch.uint8,
+                                                              device=DEV).t())
+    with pytest.raises(ValueError):
+        fz.track(torch.empty((2, 64), dtype=torch.uint8, device=DEV))
+    with pytest.raises(TypeError):
+        fz.process_frames_host(synth.frames_host(cfg, 0, range(2)), t_ms=t,
+                               results=np.zeros(2, np.float64))
+    m, r = fz.process_frames(frames, t_ms=t, results=ok_res)
+    assert r.data_ptr() == ok_res.data_ptr()
+    fz.close()
