@@ -879,6 +879,138 @@ __global__ void __launch_bounds__(256, 2) fix_fast_kernel(SegArgs a) {
   if (tid == 0) tl_mark(a.call, kTlFix, 1);
 }
 
+// The LUT re-test of corrected frames (and NEXT-1's re-segmented / learning
+// frames, reseg = true) as a streaming kernel: work item = one 12 KiB tile of
+// a listed frame; a 2-deep ring of stages per CTA, two CTAs per SM, each
+// stage holding the frame tile, its two envelope tiles and the frame's
+// 256-byte LUT row, all four filled by TMA bulk copies on one mbarrier; each
+// CTA owns a contiguous range of the (frames x tiles) items.  Every word of a
+// listed frame is rewritten (the fused kernel's identity-LUT words are void
+// for it); words whose 16-pixel lanes are all inside are written as 0
+// without the per-pixel test.  Items of frames another launch handles arrive
+// on their stage without data and are skipped.
+constexpr int kFixStages = 2;
+constexpr uint32_t kFixStageBytes = 3 * kTileBytes + 256;
+__global__ void __launch_bounds__(256, 2) fix_ring_kernel(SegArgs a) {
+  extern __shared__ __align__(128) uint8_t sm[];           // kFixStages x (tile, lo, hi, LUT)
+  __shared__ __align__(8) uint64_t full[kFixStages];
+  __shared__ uint32_t empty_cnt[kFixStages];
+  __shared__ uint32_t st_skip[kFixStages];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) tl_mark(a.call, kTlFix, 0);
+  const uint32_t count = a.fix[0];
+  const uint32_t n_items = count * a.tiles;
+  const uint32_t per = (n_items + gridDim.x - 1) / gridDim.x;
+  const uint32_t it0 = min(n_items, blockIdx.x * per), it1 = min(n_items, it0 + per);
+  if (it0 >= it1) {
+    if (tid == 0) tl_mark(a.call, kTlFix, 1);
+    return;
+  }
+  if (tid < kFixStages) { empty_cnt[tid] = 0; st_skip[tid] = 0; }
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kFixStages; s++) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint8_t* frames = a.call->frames;
+  auto frame_of = [&](uint32_t it) { return a.fix[1 + it / a.tiles]; };
+  auto skip_of = [&](uint32_t f) {
+    return a.reseg ? a.rl_role[f] == 1u : (a.rl_role != nullptr && a.rl_role[f] != 0u);
+  };
+  auto issue = [&](uint32_t s, uint32_t it) {
+    if (it >= it1) { mbar_arrive(&full[s]); return; }
+    const uint32_t f = frame_of(it);
+    if (skip_of(f)) {                           // nothing to load (skipped or emptied below)
+      st_skip[s] = 1;
+      mbar_arrive(&full[s]);
+      return;
+    }
+    st_skip[s] = 0;
+    const uint32_t tile = it % a.tiles;
+    const uint64_t toff = (uint64_t)tile * kTileBytes;
+    const uint64_t trem = a.frame_bytes - toff;
+    const uint32_t tbytes = trem < (uint64_t)kTileBytes ? (uint32_t)trem : (uint32_t)kTileBytes;
+    const uint32_t ebytes = min((uint32_t)kWarpsPerCta, a.nchunks - tile * kWarpsPerCta) * kChunkBytes;
+    const uint8_t* env = (a.reseg && a.rl_role[f] == 2u)
+                             ? reinterpret_cast<const uint8_t*>(a.rl_env[f])
+                             : a.env + (uint64_t)a.frame_stream[f] * 2 * a.env_plane;
+    const uint64_t mean = (a.luma[f] + 500ull * a.N) / (1000ull * a.N);
+    const uint64_t pol = policy_evict_first();
+    uint8_t* dst = sm + s * kFixStageBytes;
+    mbar_arrive_expect_tx(&full[s], tbytes + 2 * ebytes + 256);
+    bulk_g2s(dst, frames + (uint64_t)f * a.frame_bytes + toff, tbytes, &full[s], pol);
+    bulk_g2s(dst + kTileBytes, env + toff, ebytes, &full[s], pol);
+    bulk_g2s(dst + 2 * kTileBytes, env + a.env_plane + toff, ebytes, &full[s], pol);
+    bulk_g2s(dst + 3 * kTileBytes, a.lut_table + mean * 256, 256, &full[s], pol);
+  };
+  if (tid == 0)
+    for (int s = 0; s < kFixStages; s++) issue(s, it0 + s);
+  for (uint32_t k = 0;; k++) {
+    const uint32_t s = k % kFixStages;
+    const uint32_t it = it0 + k;
+    mbar_wait(&full[s], (k / kFixStages) & 1u);
+    if (it >= it1) break;
+    const uint32_t f = frame_of(it);
+    const uint32_t tile = it % a.tiles;
+    const uint32_t c = tile * kWarpsPerCta + warp;
+    const bool skipped = *reinterpret_cast<volatile uint32_t*>(&st_skip[s]) != 0u;
+    if (c < a.nchunks && (!skipped || a.reseg)) {
+      const uint64_t coff = (uint64_t)c * kChunkBytes;
+      const bool valid = coff + 48u * lane < a.frame_bytes;
+      uint32_t bits = 0;
+      if (!skipped) {                           // (a skipped reseg item is a learning frame: empty)
+        const uint8_t* st0 = sm + s * kFixStageBytes + warp * kChunkBytes;
+        const uint8_t* lut_s = sm + s * kFixStageBytes + 3 * kTileBytes;
+        uint32_t fr[12];
+        load48(st0 + 48 * lane, valid, fr);
+        apply_lut(fr, lut_s);
+        EnvRaw e;
+        if (valid) {
+#pragma unroll
+          for (int q = 0; q < 3; q++) {
+            const uint4 l = *reinterpret_cast<const uint4*>(st0 + kTileBytes + 512 * q + 16 * lane);
+            const uint4 h = *reinterpret_cast<const uint4*>(st0 + 2 * kTileBytes + 512 * q + 16 * lane);
+            e.lo[4 * q + 0] = l.x; e.lo[4 * q + 1] = l.y; e.lo[4 * q + 2] = l.z; e.lo[4 * q + 3] = l.w;
+            e.hi[4 * q + 0] = h.x; e.hi[4 * q + 1] = h.y; e.hi[4 * q + 2] = h.z; e.hi[4 * q + 3] = h.w;
+          }
+          uint32_t w = 0, slo = 0, shi = 0;
+#pragma unroll
+          for (int i = 0; i < 12; i++) {
+            w = sad4(e.lo[i], e.hi[i], w);
+            slo = sad4(e.lo[i], 0u, slo);
+            shi = sad4(e.hi[i], 0u, shi);
+          }
+          e.W = w;
+          e.ordered = w == shi - slo;
+        } else {
+          full_env_raw(e);
+        }
+        const bool inside = all_inside_sad(fr, e) || !valid;
+        if (__any_sync(0xFFFFFFFFu, !inside))
+          bits = inside ? 0u : slow_bits16_raw(fr, e.lo, e.hi, a.skin);
+      }
+      const uint32_t word = bits | (__shfl_down_sync(0xFFFFFFFFu, bits, 1) << 16);
+      const bool writer = !(lane & 1) && valid;
+      if (writer) a.bitA[(uint64_t)f * a.words_per_frame + (uint64_t)c * 16 + (lane >> 1)] = word;
+      const uint32_t pc = warp_sum_u32(writer ? __popc(word) : 0u);
+      if (pc && lane == 0) {
+        atomicAdd(&a.fg[f], pc);
+        atomicOr(a.dirty + (uint64_t)f * a.dirty_words + (c >> 5), 1u << (c & 31));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&empty_cnt[s], 1u) == kWarpsPerCta - 1) {   // last warp out of stage s
+        empty_cnt[s] = 0;
+        issue(s, it + kFixStages);
+      }
+    }
+  }
+  if (tid == 0) tl_mark(a.call, kTlFix, 1);
+}
+
 // ------------------------------------------------------------- generic path
 // Any width: thread per pixel for the luma sum, warp per 32-pixel word of a
 // bit-mask row for the branch tests (ballot), after the means are known.
@@ -1063,7 +1195,7 @@ cudaError_t launch_relearn_reseg(Ctx& c, uint32_t n, cudaStream_t st) {
   SegArgs a = seg_args(c, 0, n, 0, 0);
   a.fix = c.rl_list;
   a.reseg = true;
-  fix_fast_kernel<<<c.sms, 256, kTileBytes, st>>>(a);
+  fix_ring_kernel<<<2 * c.sms, 256, kFixStages * kFixStageBytes, st>>>(a);
   c.launches += 1;
   return cudaGetLastError();
 }
@@ -1072,7 +1204,9 @@ cudaError_t launch_seg_fix(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaSt
   SegArgs a = seg_args(c, f0, n, 0, sub);
   prof_begin(c, st);
   if (c.fast) {                      // finalisation already done by the fused kernel
-    fix_fast_kernel<<<c.sms, 256, kTileBytes, st>>>(a);
+    static const bool old_fix = getenv("FIZI_FIX_OLD") != nullptr;   // A/B: round-1 kernel
+    if (old_fix) fix_fast_kernel<<<c.sms, 256, kTileBytes, st>>>(a);
+    else fix_ring_kernel<<<2 * c.sms, 256, kFixStages * kFixStageBytes, st>>>(a);
     c.launches += 1;
   } else {
     const unsigned fin_blocks = (n + 255) / 256;
@@ -1110,6 +1244,9 @@ cudaError_t init_segment(Ctx& c) {
   c.seg_persist = ps ? 2u * (uint32_t)atoi(ps) : 5u;      // in half CTAs per SM
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(fix_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fix_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kFixStages * kFixStageBytes);
   return e;
 }
 
