@@ -298,14 +298,11 @@ cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, bool masks
                        int track_stream, cudaStream_t st);
 cudaError_t launch_zero_masks(Ctx& c, uint32_t n, cudaStream_t st);
 cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st);
-cudaError_t launch_track_batch(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st);
 cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,
                                 cudaStream_t st);
 constexpr uint32_t kMaxTrackRuns = 256;
 cudaError_t launch_track_runs(Ctx& c, uint32_t stream, fizi_result* res, const uint32_t* off,
                               const uint32_t* len, uint32_t n_runs, cudaStream_t st);
-// a8 fold of the current call's records (c.call) on st; fold >= 0: one stream
-cudaError_t launch_track_call(Ctx& c, int fold, cudaStream_t st);
 // NEXT-1: relearn-trigger flags of a stream's records / reset of the state
 cudaError_t launch_relearn_flags(Ctx& c, uint32_t stream, const fizi_result* res, uint32_t n,
                                  uint32_t threshold, uint8_t* flags, cudaStream_t st);

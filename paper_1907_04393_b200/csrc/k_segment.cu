@@ -728,16 +728,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_multi_kernel(SegArgs a) {
 // per byte and R2 & R3 through the colour table.  Words of frames that get
 // the LUT re-test are skipped (that kernel rewrites the whole frame).
 // Grid-stride over the queue, foreground counts aggregated per frame.
-// FIZI_SLOW_MINB (A/B builds only): minimum resident CTAs per SM.  Default
-// (unset, 77 registers) and 4 (64 registers, small spill) measured equal on
-// C3 and C4; an explicit 1 lets ptxas take 88 registers and is 16 % slower
-// on C4 (scripts/gpu_minb_ab.sh).
-#ifdef FIZI_SLOW_MINB
-#define FIZI_SLOW_BOUNDS __launch_bounds__(256, FIZI_SLOW_MINB)
-#else
-#define FIZI_SLOW_BOUNDS __launch_bounds__(256)
-#endif
-__global__ void FIZI_SLOW_BOUNDS slow_words_kernel(SegArgs a) {
+__global__ void __launch_bounds__(256) slow_words_kernel(SegArgs a) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) tl_mark(a.call, kTlSlow, 0);
   struct TlEnd {

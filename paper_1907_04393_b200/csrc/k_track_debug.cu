@@ -13,29 +13,6 @@
 
 namespace fizi {
 
-// One thread per stream; frames of the batch in index order.
-__global__ void track_batch_kernel(fizi_params p, uint32_t f0, uint32_t n, uint32_t n_streams,
-                                   const uint32_t* __restrict__ frame_stream,
-                                   fizi_result* __restrict__ res, TrackState* __restrict__ ts) {
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_streams;
-       s += gridDim.x * blockDim.x) {
-    bool any = false;
-    TrackState st;
-    for (uint32_t f = f0; f < f0 + n; f++) {
-      if (frame_stream[f] != s) continue;
-      if (!any) { st = ts[s]; any = true; }
-      fizi_result r = res[f];
-      track_one(p, st, r);
-      res[f].visible = r.visible;
-      res[f].clicked = r.clicked;
-      res[f].px = r.px;
-      res[f].py = r.py;
-      res[f].dwell_ms = r.dwell_ms;
-    }
-    if (any) ts[s] = st;
-  }
-}
-
 // One stream: the inputs of up to kTrackChunk records are staged in shared
 // memory by the whole block, one thread folds them, the block writes back.
 constexpr int kTrackChunk = 512;
@@ -88,89 +65,6 @@ __global__ void __launch_bounds__(256) track_stream_kernel(fizi_params p, uint32
     __syncthreads();
   }
   if (threadIdx.x == 0) *ts = st;
-}
-
-// Fold of one call's records (pointers from the uploaded call table): a
-// single stream (fold >= 0) staged through shared memory, else one thread
-// per stream.  Runs on its own stream after the labelling in pipelined mode.
-__global__ void __launch_bounds__(256) track_call_kernel(fizi_params p, const CallPtrs* call,
-                                                         int fold, uint32_t n_streams,
-                                                         const uint32_t* __restrict__ frame_stream,
-                                                         TrackState* __restrict__ ts) {
-  if (threadIdx.x == 0) tl_mark(call, kTlFold, 0);
-  struct TlEnd {
-    const CallPtrs* call;
-    __device__ ~TlEnd() { if (threadIdx.x == 0) tl_mark(call, kTlFold, 1); }
-  } tl_end{call};
-  fizi_result* res = call->res;
-  const uint32_t n = (uint32_t)call->n;
-  if (fold < 0) {
-    for (uint32_t s = threadIdx.x; s < n_streams; s += blockDim.x) {
-      bool any = false;
-      TrackState st;
-      for (uint32_t f = 0; f < n; f++) {
-        if (frame_stream[f] != s) continue;
-        if (!any) { st = ts[s]; any = true; }
-        fizi_result r;
-        r.t_ms = res[f].t_ms; r.blob_area = res[f].blob_area; r.cx = res[f].cx; r.cy = res[f].cy;
-        r.relearn = res[f].relearn;
-        track_one(p, st, r);
-        res[f].visible = r.visible; res[f].clicked = r.clicked;
-        res[f].px = r.px; res[f].py = r.py; res[f].dwell_ms = r.dwell_ms;
-      }
-      if (any) ts[s] = st;
-    }
-    return;
-  }
-  __shared__ int64_t t_s[kTrackChunk];
-  __shared__ double cx_s[kTrackChunk], cy_s[kTrackChunk];
-  __shared__ uint32_t ar_s[kTrackChunk];
-  __shared__ uint32_t fl_s[kTrackChunk];
-  __shared__ int64_t dw_o[kTrackChunk];
-  __shared__ double px_o[kTrackChunk], py_o[kTrackChunk];
-  __shared__ uint8_t vc_o[kTrackChunk];
-  TrackState st;
-  if (threadIdx.x == 0) st = ts[fold];
-  for (uint32_t base = 0; base < n; base += kTrackChunk) {
-    const uint32_t m = min((uint32_t)kTrackChunk, n - base);
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-      const fizi_result& r = res[base + i];
-      t_s[i] = r.t_ms; ar_s[i] = r.blob_area; cx_s[i] = r.cx; cy_s[i] = r.cy; fl_s[i] = r.relearn;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      // the next record's inputs are loaded before the current fold step
-      // (separate output arrays: no aliasing between the two)
-      int64_t t_n = t_s[0];
-      uint32_t a_n = ar_s[0], l_n = fl_s[0];
-      double x_n = cx_s[0], y_n = cy_s[0];
-      for (uint32_t i = 0; i < m; i++) {
-        fizi_result r;
-        r.t_ms = t_n; r.blob_area = a_n; r.cx = x_n; r.cy = y_n; r.relearn = l_n;
-        if (i + 1 < m) {
-          t_n = t_s[i + 1]; a_n = ar_s[i + 1]; x_n = cx_s[i + 1]; y_n = cy_s[i + 1]; l_n = fl_s[i + 1];
-        }
-        track_one(p, st, r);
-        dw_o[i] = r.dwell_ms; px_o[i] = r.px; py_o[i] = r.py;
-        vc_o[i] = (uint8_t)(r.visible | (r.clicked << 1));
-      }
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-      fizi_result& r = res[base + i];
-      r.visible = (uint8_t)(vc_o[i] & 1u); r.clicked = (uint8_t)(vc_o[i] >> 1);
-      r.px = px_o[i]; r.py = py_o[i]; r.dwell_ms = dw_o[i];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) ts[fold] = st;
-}
-
-cudaError_t launch_track_call(Ctx& c, int fold, cudaStream_t st) {
-  track_call_kernel<<<1, 256, 0, st>>>(c.p, c.call, fold, c.n_streams, c.frame_stream,
-                                       reinterpret_cast<TrackState*>(c.tstate));
-  c.launches += 1;
-  return cudaGetLastError();
 }
 
 // ----------------------------------------------------- NEXT-1 relearn trigger
@@ -378,14 +272,6 @@ __global__ void tstate_reset_kernel(TrackState* ts, uint32_t count) {
   }
 }
 
-cudaError_t launch_track_batch(Ctx& c, uint32_t f0, uint32_t n, fizi_result* res, cudaStream_t st) {
-  const uint32_t threads = c.n_streams < 256 ? ((c.n_streams + 31) / 32) * 32 : 256;
-  const uint32_t blocks = (c.n_streams + threads - 1) / threads;
-  track_batch_kernel<<<blocks, threads, 0, st>>>(c.p, f0, n, c.n_streams, c.frame_stream, res,
-                                                  reinterpret_cast<TrackState*>(c.tstate));
-  c.launches += 1;
-  return cudaGetLastError();
-}
 
 cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,
                                 cudaStream_t st) {
