@@ -232,3 +232,58 @@ def test_gpu_relearn_c2_drift_stream():
     flags = _gpu_relearn_case(cfg.W, cfg.H, frames, learn, t, 20, 10, [64] * 5)
     from oracle.relearn import RELEARN_SWAP
     assert any(f & RELEARN_SWAP for f in flags)
+
+
+@pytest.mark.gpu
+def test_gpu_relearn_multistream_pipelined_context():
+    """Two streams in interleaved calls on a pipelined context: stream 1
+    relearns (its calls run joined), stream 0 does not; each stream's records
+    and masks equal its own oracle run (the oracle composition for stream 1,
+    the plain path for stream 0)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import oracle
+    import synth
+    from oracle.relearn import run_stream_relearn
+    from paper_1907_04393_b200 import Fizi, results_numpy
+    from tests.gpu_common import compare_record
+    cfg, step_frames, step_learn = _step_scene(3, 9, 1280)       # stream 1: lighting step
+    plain = synth.frames_host(cfg, 0, range(12))                  # stream 0: C1 orbit
+    plain_learn = synth.learning_frames_host(cfg)
+    p = oracle.make_params(cfg.W, cfg.H, min_blob_ppm=0)
+    t = np.arange(12, dtype=np.int64) * 33
+    lo0, hi0 = oracle.learn(plain_learn, synth.MARGIN)
+    lo1, hi1 = oracle.learn(step_learn, synth.MARGIN)
+    r1, m1, f1, _ = run_stream_relearn(p, step_frames, t, lo1, hi1, 20, 4, synth.MARGIN)
+    fz = Fizi(cfg.W, cfg.H, n_streams=2, max_batch=8, min_blob_ppm=0)
+    fz.learn_background(torch.from_numpy(plain_learn).cuda(), stream=0, margin=synth.MARGIN)
+    fz.learn_background(torch.from_numpy(step_learn).cuda(), stream=1, margin=synth.MARGIN)
+    fz.set_relearn(stream=1, threshold=20, n_frames=4, margin=synth.MARGIN)
+    fz.set_pipeline(True)
+    tr0 = oracle.Tracker(p)
+    outs = []
+    for k0 in range(0, 12, 3):                                    # calls of 3 + 3 frames, interleaved
+        ks = list(range(k0, k0 + 3))
+        fr = np.concatenate([plain[ks], step_frames[ks]])
+        sof = np.array([0, 0, 0, 1, 1, 1], np.uint32)
+        tt = np.concatenate([t[ks], t[ks]])
+        mk = torch.empty((6, cfg.H, cfg.W), dtype=torch.uint8, device="cuda")
+        rs = torch.empty((6, 128), dtype=torch.uint8, device="cuda")
+        fz.process_frames(torch.from_numpy(fr).cuda(), streams=sof, t_ms=tt, masks=mk, results=rs)
+        outs.append((ks, mk, rs))
+    fz.flush()
+    torch.cuda.synchronize()
+    for ks, mk, rs in outs:
+        rr, mm = results_numpy(rs), mk.cpu().numpy()
+        for i, k in enumerate(ks):
+            rec0, st0 = oracle.segment(p, plain[k], lo0, hi0, t_ms=int(t[k]))
+            tr0.update(rec0)
+            compare_record(rr[i], rec0, ("s0", k), track=True)
+            assert int(rr[i]["relearn"]) == 0
+            assert np.array_equal(mm[i], st0["final_mask"])
+            compare_record(rr[3 + i], r1[k], ("s1", k), track=True)
+            assert int(rr[3 + i]["relearn"]) == f1[k]
+            assert np.array_equal(mm[3 + i], m1[k])
+    assert any(f1)
+    fz.close()
