@@ -5,7 +5,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth
 from paper_1907_04393_b200 import Fizi, lib
-cfg = synth.CONFIGS[3]
+cfg = synth.CONFIGS[int(os.environ.get("CT_CONFIG", "3"))]
 dev = torch.device("cuda", 0)
 fz = Fizi(cfg.W, cfg.H, max_batch=64)
 fz.learn_background(synth.frames_dev(cfg, 0, range(30), learning=True))
