@@ -25,3 +25,5 @@ full c5_seg seg_multi $P5
 $P4 > gpurun_out/ncu_plain4.log 2>&1
 full c4_seg seg_fast $P4
 full c4_slow slow_words $P4
+full c4_ccl ccl_kernel $P4
+full c4_morph morph_rows $P4

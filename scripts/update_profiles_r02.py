@@ -26,6 +26,9 @@ CAPTURES = {  # name: (kernel, config, command)
     "c4_seg": ("seg_fast_kernel", "C4 3840x2160, 64 frames", "bench.py --config 4 --steps 3 --warmup 2"),
     "c4_slow": ("slow_words_kernel", "C4 3840x2160, 64 frames",
                 "bench.py --config 4 --steps 3 --warmup 2"),
+    "c4_ccl": ("ccl_kernel", "C4 3840x2160, 64 frames", "bench.py --config 4 --steps 3 --warmup 2"),
+    "c4_morph": ("morph_rows_kernel", "C4 3840x2160, 64 frames",
+                 "bench.py --config 4 --steps 3 --warmup 2"),
 }
 ALG = {  # algorithmic bytes per launch of the fused kernels
     "c3_seg": 64 * (3 + 1 / 8) * 1920 * 1080 + 6 * 1920 * 1080,
