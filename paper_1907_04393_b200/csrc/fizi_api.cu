@@ -972,7 +972,8 @@ int fizi_process_frames_host(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* 
   // and the path overlap.  Chunks are processed in order on st, so the
   // tracker sees the frames in index order.
   const uint64_t fb = c.N * 3;
-  const uint32_t m = std::max<uint32_t>(1u, std::min<uint64_t>(n, (32ull << 20) / fb));
+  static const uint64_t chunk_mb = getenv("FIZI_HOST_CHUNK_MB") ? (uint64_t)atoi(getenv("FIZI_HOST_CHUNK_MB")) : 32;
+  const uint32_t m = std::max<uint32_t>(1u, std::min<uint64_t>(n, (chunk_mb << 20) / fb));
   const uint32_t nchunk = (n + m - 1) / m;
   if (!c.h2d) {
     e = cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking);
@@ -999,9 +1000,19 @@ int fizi_process_frames_host(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* 
   if (e == cudaSuccess) e = cudaStreamWaitEvent(c.h2d, c.host_ev[2 * nchunk], 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(c.d2h, c.host_ev[2 * nchunk], 0);
   if (e != cudaSuccess) return cuda_fail(c, e, "fork");
+  // the chunks run as pipelined calls (each chunk's tail overlaps the next
+  // chunk's segmentation; outputs are complete when this entry returns), and
+  // each chunk's read-back waits for that chunk's last stage only
+  const bool pipeline_saved = c.pipeline;
+  c.pipeline = true;
+  struct Restore {
+    Ctx& c;
+    bool v;
+    ~Restore() { c.pipeline = v; }
+  } restore{c, pipeline_saved};
   for (uint32_t j = 0; j < nchunk; j++) {
     const uint32_t j0 = j * m, mj = std::min(m, n - j0);
-    cudaEvent_t ev_in = c.host_ev[2 * j], ev_out = c.host_ev[2 * j + 1];
+    cudaEvent_t ev_in = c.host_ev[2 * j];
     e = cudaMemcpyAsync(c.stage_frames + (uint64_t)j0 * fb, frames_host + (uint64_t)j0 * fb,
                         (size_t)mj * fb, cudaMemcpyHostToDevice, c.h2d);
     if (e == cudaSuccess) e = cudaEventRecord(ev_in, c.h2d);
@@ -1012,9 +1023,7 @@ int fizi_process_frames_host(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* 
                                  masks_host ? c.stage_masks + (uint64_t)j0 * c.N : nullptr,
                                  c.stage_results + j0, cuda_stream);
     if (rc) return rc;
-    e = join_tail(c, st);
-    if (e == cudaSuccess) e = cudaEventRecord(ev_out, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.d2h, ev_out, 0);
+    e = cudaStreamWaitEvent(c.d2h, c.ev_tail[c.last_slot], 0);   // this chunk's outputs
     if (e != cudaSuccess) return cuda_fail(c, e, "join");
     if (masks_pinned) {
       e = cudaMemcpyAsync(masks_host + (uint64_t)j0 * c.N, c.stage_masks + (uint64_t)j0 * c.N,
@@ -1031,7 +1040,8 @@ int fizi_process_frames_host(fizi_ctx* ctx, const uint32_t* sof, const uint8_t* 
     e = cudaMemcpyAsync(masks_host, c.stage_masks, (size_t)n * c.N, cudaMemcpyDeviceToHost, c.d2h);
     if (e != cudaSuccess) return cuda_fail(c, e, "D2H masks");
   }
-  e = cudaStreamSynchronize(c.d2h);
+  e = join_tail(c, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c.d2h);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamSynchronize");
   memcpy(results_host, c.pinned_results, (size_t)n * sizeof(fizi_result));
