@@ -113,6 +113,11 @@ __device__ __forceinline__ void unite(uint32_t* par, const Run* R, uint32_t W, u
 
 #define CCL_MARK(k) if (a.trace && threadIdx.x == 0) t_mark[k] = clock64();
 
+// above this many 4-row blocks the block boundaries are merged in
+// log2(blocks) tree rounds instead of one pass (C3: 270 blocks, one pass
+// 2.2 us vs 9 rounds 7.8 us; C4: 540 blocks, one pass 21.5 us vs 12.2 us)
+constexpr uint32_t kCclTreeBlocks = 384;
+
 template <bool kShared>
 __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, uint32_t* s_area,
                           uint32_t T, long long* t_mark) {
@@ -173,8 +178,21 @@ __device__ void ccl_frame(const CclArgs& a, uint32_t f, Run* R, uint32_t* par, u
     for (uint32_t y = blk * kRowBlock + 1; y < y1; y++) unite_rows(y);
   }
   __syncthreads();
-  for (uint32_t blk = tid + 1; blk * kRowBlock < H; blk += nthr) unite_rows(blk * kRowBlock);
-  __syncthreads();
+  const uint32_t nblk = (H + kRowBlock - 1) / kRowBlock;
+  if (nblk <= kCclTreeBlocks) {
+    // all block boundaries at once (a tall component links its block roots
+    // into a chain, walked with path halving: cheap for a few hundred blocks)
+    for (uint32_t blk = tid + 1; blk < nblk; blk += nthr) unite_rows(blk * kRowBlock);
+    __syncthreads();
+  } else {
+    // tall frames: boundaries merged as a tree, in round s the boundary at
+    // block (2k+1)s joins two merged groups of s blocks, so trees grow by at
+    // most one level per round (C4: the union phase 21.5 -> 12.2 us per frame)
+    for (uint32_t sd = 1; sd < nblk; sd <<= 1) {
+      for (uint32_t k = tid; (2 * k + 1) * sd < nblk; k += nthr) unite_rows((2 * k + 1) * sd * kRowBlock);
+      __syncthreads();
+    }
+  }
 
   CCL_MARK(2)
   // 2. flatten: every run walks to its root, halving the path as it goes

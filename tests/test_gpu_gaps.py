@@ -154,3 +154,31 @@ def test_exhaustive_5x5_masks_morphology_and_labelling():
         assert np.abs(gr["cx"] - recs["cx"]).max() <= 1e-3
         assert np.abs(gr["cy"] - recs["cy"]).max() <= 1e-3
     fz.close()
+
+
+def test_tall_frames_tree_ordered_block_merging():
+    """Frames taller than 384 four-row blocks take the labelling's tree-ordered
+    boundary merging (k_ccl.cu, kCclTreeBlocks): random masks, a tall snake
+    component spanning the whole height, and vertical stripes, against the
+    oracle's labels and records."""
+    W, H = 64, 2048
+    rng = np.random.default_rng(2048)
+    masks = np.zeros((3, H, W), np.uint8)
+    masks[0] = rng.random((H, W)) < 0.45
+    masks[1][:, 30:34] = 1                                  # one tall component
+    masks[1][::7, 5:60] = 1
+    masks[2][:, ::3] = 1                                    # many tall thin stripes (removed by the opening)
+    masks[2][:, 40:50] = 1
+    frames, lo, hi = mask_frames(masks)
+    fz = Fizi(W, H, max_batch=3, min_blob_ppm=0, debug=1)
+    fz.set_background(_t(lo), _t(hi))
+    gm, gr = fz.segment_frames(_t(frames))
+    gm, gr = gm.cpu().numpy(), results_numpy(gr)
+    p = oracle.make_params(W, H, min_blob_ppm=0)
+    for k in range(3):
+        rec, st = oracle.segment(p, frames[k], lo, hi)
+        compare_record(gr[k], rec, k)
+        assert np.array_equal(gm[k], st["final_mask"]), k
+        lab = fz.debug_stage("labels", k).cpu().numpy().view(np.uint32)
+        assert np.array_equal(lab, st["labels"]), k
+    fz.close()
