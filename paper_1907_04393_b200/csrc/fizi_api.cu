@@ -251,24 +251,40 @@ void fill_call(Ctx& c, uint32_t slot, const fizi::CallPtrs& cp, const uint32_t* 
   uint32_t sb = c.sub_frames;
   if ((n + sb - 1) / sb > fizi::kMaxSub) sb = (n + fizi::kMaxSub - 1) / fizi::kMaxSub;
   subs.clear();
-  std::vector<uint8_t> seen(c.n_streams, 0);
+  // per sub-batch: the frames bucketed by stream (streams in order of first
+  // appearance, frames in index order; a counting sort, O(frames + streams)),
+  // each bucket cut into groups of at most group_max frames
+  if (c.fc_slot.size() != c.n_streams) c.fc_slot.assign(c.n_streams, -1);
+  std::vector<uint32_t>& order = c.fc_order;     // streams of the sub-batch, first appearance
+  std::vector<uint32_t>& start = c.fc_start;     // bucket offsets
   uint32_t pos = 0, g = 0;
   for (uint32_t f0 = 0; f0 < n; f0 += sb) {
     const uint32_t f1 = std::min(n, f0 + sb);
     SubBatch b{f0, f1 - f0, g, 0};
-    for (uint32_t i = f0; i < f1; i++) seen[sof[i]] = 0;
+    order.clear();
+    start.clear();
     for (uint32_t i = f0; i < f1; i++) {
-      const uint32_t s = sof[i];
-      if (seen[s]) continue;
-      seen[s] = 1;
-      uint32_t in_group = 0;
-      for (uint32_t j = i; j < f1; j++) {
-        if (sof[j] != s) continue;
-        if (in_group == 0) ho[g++] = pos;
-        hg[pos++] = j;
-        if (++in_group == c.group_max) in_group = 0;
+      int& k = c.fc_slot[sof[i]];
+      if (k < 0) {
+        k = (int)order.size();
+        order.push_back(sof[i]);
+        start.push_back(0);
       }
+      start[k]++;
     }
+    uint32_t acc = pos;
+    for (uint32_t& v : start) {                  // counts -> bucket starts
+      const uint32_t cnt = v;
+      v = acc;
+      acc += cnt;
+    }
+    for (size_t k = 0; k < order.size(); k++) {  // group starts, group_max frames each
+      const uint32_t b0 = start[k], b1 = k + 1 < order.size() ? start[k + 1] : acc;
+      for (uint32_t q = b0; q < b1; q += c.group_max) ho[g++] = q;
+    }
+    for (uint32_t i = f0; i < f1; i++) hg[start[c.fc_slot[sof[i]]]++] = i;
+    for (uint32_t st : order) c.fc_slot[st] = -1;
+    pos = acc;
     b.ng = g - b.g0;
     subs.push_back(b);
   }
@@ -325,7 +341,7 @@ int enqueue_tail(Ctx& c, const CallPlan& pl, const SubBatch& b, uint32_t k, cuda
     if (e != cudaSuccess) return cuda_fail(c, e, "join");
   }
   prof_begin(c, sd);
-  e = fizi::launch_ccl(c, b.f0, b.n, k, pl.premask, pl.fold, sd);
+  e = fizi::launch_ccl(c, b.f0, b.n, k, b.g0, b.ng, pl.premask, pl.fold, sd);
   prof_end(c, FIZI_PROF_CCL, sd);
   if (e != cudaSuccess) return cuda_fail(c, e, "ccl");
   if (pl.masks && !pl.fused_mask) {
@@ -389,7 +405,7 @@ int enqueue_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
   }
   if (part == kTailCcl) {                  // a5-a7 + u8 mask + a8 fold (fused)
     prof_begin(c, st);
-    e = fizi::launch_ccl(c, 0, pl.n, 0, pl.premask, pl.fold, st);
+    e = fizi::launch_ccl(c, 0, pl.n, 0, pl.subs[0].g0, pl.subs[0].ng, pl.premask, pl.fold, st);
     prof_end(c, FIZI_PROF_CCL, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "ccl");
     if (pl.masks && !pl.fused_mask) {

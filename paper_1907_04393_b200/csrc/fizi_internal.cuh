@@ -204,6 +204,8 @@ struct Ctx {
   std::vector<uint32_t> n_zones;         // NEXT-3: zones per stream (0: no layout)
   std::vector<uint64_t> slider_zones;    // NEXT-3: bit k set iff zone k of the stream is a slider
   std::vector<int64_t> last_t;
+  std::vector<int> fc_slot;               // fill_call scratch: stream -> bucket (-1: none)
+  std::vector<uint32_t> fc_order, fc_start;
   std::vector<uint8_t> has_t;
   uint8_t* pinned[kSlots] = {};               // staging for the per-call upload (one per slot)
   size_t pinned_bytes = 0;
@@ -294,8 +296,9 @@ cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, bool write_masks, cuda
 // masks_zeroed: c.call->masks (if any) was zeroed by launch_zero_masks (the
 // labelling writes the kept runs), else it holds O (the labelling clears the
 // dropped runs)
-cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, bool masks_zeroed,
-                       int track_stream, cudaStream_t st);
+// g0 / ng: the sub-batch's same-stream groups (the per-stream fold walks them)
+cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, uint32_t g0, uint32_t ng,
+                       bool masks_zeroed, int track_stream, cudaStream_t st);
 cudaError_t launch_zero_masks(Ctx& c, uint32_t n, cudaStream_t st);
 cudaError_t launch_expand(Ctx& c, uint32_t f0, uint32_t n, uint8_t* masks, cudaStream_t st);
 cudaError_t launch_track_stream(Ctx& c, uint32_t stream, fizi_result* res, uint32_t n,

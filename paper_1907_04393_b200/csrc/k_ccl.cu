@@ -58,6 +58,9 @@ struct CclArgs {
   int trace;                    // diagnostics: block 0 prints phase clocks
   uint32_t n_streams;
   const uint32_t* frame_stream;
+  const uint32_t* group_frames;            // the sub-batch's same-stream groups (frames in order)
+  const uint32_t* group_off;
+  uint32_t n_groups;
   TrackState* tstate;
   fizi_params p;
 };
@@ -452,22 +455,29 @@ __device__ void fold_records(const CclArgs& a, uint8_t* smem) {
     }
     if (threadIdx.x == 0) a.tstate[a.track_stream] = st;
   } else {
-    for (uint32_t s = threadIdx.x; s < a.n_streams; s += blockDim.x) {
-      bool any = false;
-      TrackState st;
-      for (uint32_t f = f0; f < f0 + n; f++) {
-        if (a.frame_stream[f] != s) continue;
-        if (!any) { st = a.tstate[s]; any = true; }
-        fizi_result r;
-        r.t_ms = __ldcg(&a.call->res[f].t_ms); r.blob_area = __ldcg(&a.call->res[f].blob_area);
-        r.cx = __ldcg(&a.call->res[f].cx); r.cy = __ldcg(&a.call->res[f].cy);
-        r.relearn = __ldcg(&a.call->res[f].relearn);
-        track_one(a.p, st, r);
-        fizi_result& o = a.call->res[f];
-        o.visible = r.visible; o.clicked = r.clicked;
-        o.px = r.px; o.py = r.py; o.dwell_ms = r.dwell_ms;
+    // one thread per stream: a stream's groups are consecutive in the group
+    // list and hold its frames in index order (fill_call), so the thread that
+    // owns a stream's first group folds the stream's frames in order
+    for (uint32_t g = threadIdx.x; g < a.n_groups; g += blockDim.x) {
+      const uint32_t s = a.frame_stream[a.group_frames[a.group_off[g]]];
+      if (g > 0 && a.frame_stream[a.group_frames[a.group_off[g - 1]]] == s) continue;
+      TrackState st = a.tstate[s];
+      for (uint32_t gg = g; gg < a.n_groups; gg++) {
+        const uint32_t q0 = a.group_off[gg], q1 = a.group_off[gg + 1];
+        if (a.frame_stream[a.group_frames[q0]] != s) break;
+        for (uint32_t q = q0; q < q1; q++) {
+          const uint32_t f = a.group_frames[q];
+          fizi_result r;
+          r.t_ms = __ldcg(&a.call->res[f].t_ms); r.blob_area = __ldcg(&a.call->res[f].blob_area);
+          r.cx = __ldcg(&a.call->res[f].cx); r.cy = __ldcg(&a.call->res[f].cy);
+          r.relearn = __ldcg(&a.call->res[f].relearn);
+          track_one(a.p, st, r);
+          fizi_result& o = a.call->res[f];
+          o.visible = r.visible; o.clicked = r.clicked;
+          o.px = r.px; o.py = r.py; o.dwell_ms = r.dwell_ms;
+        }
       }
-      if (any) a.tstate[s] = st;
+      a.tstate[s] = st;
     }
   }
 }
@@ -610,8 +620,8 @@ cudaError_t init_ccl(Ctx& c) {
                               (int)kCclSmem);
 }
 
-cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, bool masks_zeroed,
-                       int track_stream, cudaStream_t st) {
+cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, uint32_t g0, uint32_t ng,
+                       bool masks_zeroed, int track_stream, cudaStream_t st) {
   CclArgs a;
   a.f0 = f0;
   a.call = c.call;
@@ -622,6 +632,9 @@ cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, bool masks
   a.track_stream = track_stream;
   a.n_streams = c.n_streams;
   a.frame_stream = c.frame_stream;
+  a.group_frames = c.group_frames;
+  a.group_off = c.group_off + g0;
+  a.n_groups = ng;
   a.tstate = reinterpret_cast<TrackState*>(c.tstate);
   a.p = c.p;
   static const int trace = getenv("FIZI_CCL_TRACE") ? atoi(getenv("FIZI_CCL_TRACE")) : 0;

@@ -15,11 +15,24 @@ B = int(os.environ.get("TL_BATCH", "64"))
 pipelined = os.environ.get("TL_PIPELINE", "1") == "1"
 cfg = synth.CONFIGS[cid]
 dev = torch.device("cuda", 0)
-fz = Fizi(cfg.W, cfg.H, max_batch=B)
-fz.learn_background(synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True), margin=synth.MARGIN)
+multi = cfg.streams > 1 and os.environ.get("TL_MULTI") == "1"   # C5: one frame of each of B streams
+fz = Fizi(cfg.W, cfg.H, n_streams=B if multi else 1, max_batch=B)
+for sid in range(B if multi else 1):
+    fz.learn_background(synth.frames_dev(cfg, sid, range(cfg.n_learn), learning=True), stream=sid,
+                        margin=synth.MARGIN)
 fz.set_pipeline(pipelined)
 nb = 4
-frames = [synth.frames_dev(cfg, 0, range(b * B, (b + 1) * B)) for b in range(nb)]
+if multi:
+    frames = []
+    for b in range(nb):
+        fr = torch.empty((B, cfg.H, cfg.W, 3), dtype=torch.uint8, device=dev)
+        for sid in range(B):
+            synth.frames_dev(cfg, sid, [b], out=fr[sid:sid + 1])
+        frames.append(fr)
+    sids = np.arange(B, dtype=np.uint32)
+else:
+    frames = [synth.frames_dev(cfg, 0, range(b * B, (b + 1) * B)) for b in range(nb)]
+    sids = None
 masks = [torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=dev) for _ in range(4)]
 res = [torch.empty((B, 128), dtype=torch.uint8, device=dev) for _ in range(4)]
 ncalls = 48
@@ -31,8 +44,8 @@ L0.fizi_diag_host_ns(fz._h, ctypes.byref(hc), ctypes.byref(hsync))
 c0, s0 = hc.value, hsync.value
 tp0 = time.perf_counter()
 for i in range(ncalls):
-    t = np.arange(B, dtype=np.int64) * 33 + i * B * 33
-    fz.process_frames(frames[i % nb], t_ms=t,
+    t = (np.full(B, i * 33, np.int64) if multi else np.arange(B, dtype=np.int64) * 33 + i * B * 33)
+    fz.process_frames(frames[i % nb], streams=sids, t_ms=t,
                       masks=None if os.environ.get("TL_NOMASK") else masks[i % 4], results=res[i % 4])
 tp1 = time.perf_counter()
 L0.fizi_diag_host_ns(fz._h, ctypes.byref(hc), ctypes.byref(hsync))
