@@ -313,17 +313,21 @@ int fizi_set_background(fizi_ctx *ctx, uint32_t stream, const uint8_t *lo_dev,
 
 /* Pipelined mode (enable = 1; default 0).  By default every output of a
  * fizi_process_frames / fizi_segment_frames call is complete in cuda_stream
- * order when the call returns.  In pipelined mode a call's tail (LUT
- * re-test, a4-a7, the u8 mask, the a8 fold) runs on the context's internal
- * stream and is NOT joined into cuda_stream, so that it overlaps the next
- * call's segmentation; per-call state is multi-buffered inside the context.
- * The context keeps FIZI_CALL_SLOTS call slots: every write of call
- * k+FIZI_CALL_SLOTS is ordered after the tail of call k, so a caller may
- * rotate FIZI_CALL_SLOTS output buffers across calls without waiting.  Outputs of a pipelined call are complete in a stream's
- * order after fizi_flush on that stream; until then the caller must not read
- * them, nor overwrite the call's frames.  Every other entry point
- * that touches the tail's state (learn / set_background / track / debug /
- * host entry) joins the outstanding tails into its stream itself. */
+ * order when the call returns.  In pipelined mode a call runs as four stages
+ * on the context's internal streams (segmentation; per-pixel words + LUT
+ * re-test; a4 + the u8 mask; a5-a7 + the a8 fold), each stage in call order,
+ * and is NOT joined into cuda_stream, so that the stages of consecutive calls
+ * overlap; per-call state is multi-buffered inside the context.  A call's
+ * stages start after the caller's earlier work on cuda_stream.  The context
+ * keeps FIZI_CALL_SLOTS call slots: every write of call k+FIZI_CALL_SLOTS is
+ * ordered after the last stage of call k, so a caller may rotate
+ * FIZI_CALL_SLOTS output buffers across calls without waiting.  Outputs of a
+ * pipelined call are complete in a stream's order after fizi_flush on that
+ * stream; until then the caller must not read them, nor overwrite the call's
+ * frames.  Every other entry point that touches the stages' state (learn /
+ * set_background / track / reset_tracker / relearn / drive / hit test / debug
+ * / host entry) joins the outstanding stages into its stream itself.  Calls
+ * holding a relearning stream (fizi_set_relearn) always run joined. */
 #define FIZI_CALL_SLOTS 4
 int fizi_set_pipeline(fizi_ctx *ctx, int enable);
 
