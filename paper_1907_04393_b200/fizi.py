@@ -13,9 +13,11 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# FIZI_LIB=checked selects the build with device-side invariant checks
-LIB_PATH = os.path.join(HERE, "libfizi_checked.so" if os.environ.get("FIZI_LIB") == "checked"
-                        else "libfizi.so")
+# FIZI_LIB=checked selects the build with device-side invariant checks;
+# FIZI_LIB=<file>.so an alternative in-tree build (A/B experiments)
+_lib_env = os.environ.get("FIZI_LIB", "")
+LIB_PATH = os.path.join(HERE, "libfizi_checked.so" if _lib_env == "checked"
+                        else _lib_env if _lib_env.endswith(".so") else "libfizi.so")
 
 # fizi_status
 OK, E_ARG, E_EMPTY, E_DIMS, E_NOMODEL, E_TIME, E_CUDA, E_OOM, E_CAPACITY = 0, -1, -2, -3, -4, -5, -6, -7, -8
