@@ -22,6 +22,7 @@ Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle instead
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -286,6 +287,17 @@ def cpu_baseline(cfg, n_frames=0, target_s=8.0, single_s=4.0):
                             "sample": f"{passes1} passes = {done1} frames on one thread, {dt1:.1f} s"}}
 
 
+def host_gaps(hts):
+    """Host time per step call inside the timed region (diagnostics: the
+    calls are asynchronous, so a long gap is the host waiting for a call slot
+    or being descheduled)."""
+    d = np.diff(np.asarray(hts)) * 1e6
+    if d.size == 0:
+        return None
+    return {"median_us": float(np.median(d)), "max_us": float(d.max()),
+            "over_1ms": int((d > 1000).sum()), "sum_over_1ms_ms": float(d[d > 1000].sum() / 1e3)}
+
+
 def spot_check(cfg, frames_dev, masks_dev, res_dev, sids, idx):
     """Bench-side parity spot check of frames `idx` of the last timed call:
     the final mask and the stateless record fields (a2-a7) against the oracle
@@ -483,6 +495,18 @@ def main():
         torch.cuda.current_stream(dev).wait_stream(fold_stream)
         fz.flush()
 
+    # a round of another size (the last, partial batch) is run once before the
+    # warm-up, with earlier timestamps, so that its call shape is captured
+    # outside the timed region (the library captures a new shape for all slots)
+    if not sharded:
+        common = views[0][0] if views and views[0] else None
+        for v in views:
+            if v is not None and v[0] != common:
+                n_v, fr_v, mks_v, ress_v, tb_v, sids_v = v
+                fz.process_frames(fr_v, streams=sids_v, t_ms=tb_v - 10**12, masks=mks_v[0],
+                                  results=ress_v[0])
+                fz.flush()
+                break
     for i in range(args.warmup):
         step(i)
     finish()
@@ -498,15 +522,22 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # no cyclic-GC pause inside the timed region (a full collection over the
+    # interpreter's objects takes milliseconds; the step loop allocates little)
+    gc.collect()
+    gc.disable()
     with ClockSampler(torch.cuda.current_device()) as clk:
         e0.record(st)
         h0 = time.perf_counter()
+        hts = [time.perf_counter()]
         for i in range(args.steps):
             frames_done += step(args.warmup + i)
+            hts.append(time.perf_counter())
         finish()                         # every tail (and fold) of the timed calls is inside
         host_ms = (time.perf_counter() - h0) * 1e3
         e1.record(st)
         torch.cuda.synchronize()
+    gc.enable()
     if world > 1:
         dist.barrier()
     launches = fz.kernel_launches() - launches0
@@ -613,6 +644,7 @@ def main():
                    "parallelism": (f"frames sharded by batch, dp{world}" if S == 1 else
                                    f"camera streams sharded (s mod {world}), dp{world}")},
         "gpu_launches": launches,
+        "host_step_gaps": host_gaps(hts),
         "spot_check": spot,
         "roofline": roofline,
         "clocks": clk.summary(),

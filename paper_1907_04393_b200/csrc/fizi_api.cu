@@ -490,22 +490,31 @@ int run_part(Ctx& c, const CallPlan& pl, int part, cudaStream_t st) {
   }
   ent->used = ++c.graph_clock;
   if (!ent->exec[pl.slot]) {
-    const uint64_t l0 = c.launches;
-    cudaError_t e = cudaStreamBeginCapture(c.cap, cudaStreamCaptureModeThreadLocal);
-    if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamBeginCapture");
-    const int rc = enqueue_part(c, pl, part, c.cap);
-    cudaGraph_t g = nullptr;
-    e = cudaStreamEndCapture(c.cap, &g);
-    if (rc) {
+    // a new call shape: capture it for every slot now (the slots' pointers
+    // differ), so that later calls of this shape never stall on a capture
+    for (uint32_t s = 0; s < fizi::kSlots; s++) {
+      if (ent->exec[s]) continue;
+      select_slot(c, s);
+      CallPlan ps = pl;
+      ps.slot = s;
+      const uint64_t l0 = c.launches;
+      cudaError_t e = cudaStreamBeginCapture(c.cap, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) { select_slot(c, pl.slot); return cuda_fail(c, e, "cudaStreamBeginCapture"); }
+      const int rc = enqueue_part(c, ps, part, c.cap);
+      cudaGraph_t g = nullptr;
+      e = cudaStreamEndCapture(c.cap, &g);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        select_slot(c, pl.slot);
+        return rc;
+      }
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&ent->exec[s], g, 0);
       if (g) cudaGraphDestroy(g);
-      return rc;
+      ent->kernels = c.launches - l0;
+      c.launches = l0;
+      if (e != cudaSuccess) { select_slot(c, pl.slot); return cuda_fail(c, e, "graph capture"); }
     }
-    if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamEndCapture");
-    e = cudaGraphInstantiate(&ent->exec[pl.slot], g, 0);
-    cudaGraphDestroy(g);
-    if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
-    ent->kernels = c.launches - l0;
-    c.launches = l0;
+    select_slot(c, pl.slot);
   }
   cudaError_t e = cudaGraphLaunch(ent->exec[pl.slot], st);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphLaunch");
