@@ -107,11 +107,15 @@ def peaks():
 
 
 class ClockSampler:
-    """NVML SM clock + throttle reasons, sampled in a thread during the timed region."""
+    """NVML SM clock + throttle reasons, sampled in a thread; only the samples
+    taken while `active` is set (the timed region) are kept.  The thread is
+    started before the warm-up, so its start-up and NVML initialisation do not
+    compete with the timed calls for the GIL or the host caches."""
 
     def __init__(self, index: int):
         self.samples, self.reasons, self.ok = [], set(), False
         self.max_mhz = None
+        self.active = False
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -133,36 +137,76 @@ class ClockSampler:
             "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
         }
         while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            if self.active:
                 try:
-                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                except AttributeError:
-                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-                for k, bit in names.items():
-                    if r & bit:
-                        self.reasons.add(k)
-            except Exception:
-                pass
+                    mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                    try:
+                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    except AttributeError:
+                        r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                    if self.active:
+                        self.samples.append(mhz)
+                        for k, bit in names.items():
+                            if r & bit:
+                                self.reasons.add(k)
+                except Exception:
+                    pass
             time.sleep(0.002)
 
-    def __enter__(self):
+    def start(self):
         if self.ok:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
 
-    def __exit__(self, *a):
+    def stop(self):
+        self.active = False
         if self.ok:
             self._stop.set()
             self.t.join()
+            self.in_region = len(self.samples)
+            if not self.samples:          # a timed region shorter than one sample period
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
 
     def summary(self):
         if not self.ok:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+                "samples": len(self.samples),
+                "samples_in_timed_region": getattr(self, "in_region", len(self.samples))}
+
+
+def workload_config(cfg, args, world):
+    """The `config` object of the JSON line; the reference arm prints the same
+    one (its per-step oracle sample is described in its `cpu_baseline`)."""
+    from paper_1907_04393_b200 import shard
+    sharded = world > 1 or args.force_gather
+    pipelined = not args.no_pipeline
+    S = cfg.streams
+    N = cfg.W * cfg.H
+    if S > 1:
+        S_r = len(shard.stream_shard(S, world, 0))
+        B = min(args.batch or S_r, S_r) if not sharded else S_r
+        need = min(-(-S_r // B) * cfg.n_proc, args.warmup + args.steps)
+        workload = (f"C{cfg.cid}: {S} streams of {cfg.W}x{cfg.H}, {cfg.n_proc} frames "
+                    f"each, per-stream envelopes, stream s on rank s mod {world}; "
+                    f"each call takes the current frame of {B} of the rank's "
+                    f"{S_r} streams (BASELINE.json configs[{cfg.cid - 1}])")
+    else:
+        B = args.batch or cfg.batch
+        need = min(shard.n_rounds(cfg.n_proc, B, world), args.warmup + args.steps)
+        workload = (f"C{cfg.cid}: {cfg.W}x{cfg.H} stream, {cfg.n_proc} frames, "
+                    f"batches of {B} per launch (BASELINE.json configs[{cfg.cid - 1}])")
+    return {"workload": workload,
+            "frames_per_step_per_gpu": B, "pipelined_calls": pipelined,
+            "sharded_path": sharded, "resident_batches_per_gpu": need,
+            "l2": (f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step"
+                   if B * 3 * N > 126e6 else
+                   f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step, "
+                   f"cycled over {need} resident batches ({need * B * 3 * N / 1e9:.1f} GB)"),
+            "parallelism": (f"frames sharded by batch, dp{world}" if S == 1 else
+                            f"camera streams sharded (s mod {world}), dp{world}")}
 
 
 # ------------------------------------------------------------- reference arm
@@ -197,11 +241,13 @@ def run_reference(args, cfg, rank, world):
         "mpix_per_s": v * cfg.npx / 1e6, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"C{cfg.cid} {cfg.W}x{cfg.H} stream, oracle sample of {per_step} "
-                               f"frames per step", "frames_per_step": per_step},
+        "config": workload_config(cfg, args, world),
         "cpu_baseline": {"value": v, "unit": "frames/s", "cores": cores, "kind": "oracle",
                          "cpu_model": cpu_model(),
-                         "sample": f"{per_step} frames x {args.steps} steps of C{cfg.cid}"},
+                         "sample": f"each step: {per_step} frames of C{cfg.cid} "
+                                   f"({cfg.W}x{cfg.H}) through the oracle (masks + records "
+                                   f"+ fold), frame-parallel over {cores} host threads; "
+                                   f"{args.steps} steps"},
         "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -295,6 +341,7 @@ def host_gaps(hts):
     if d.size == 0:
         return None
     return {"median_us": float(np.median(d)), "max_us": float(d.max()),
+            "first_us": [round(float(x), 1) for x in d[:3]],
             "over_1ms": int((d > 1000).sum()), "sum_over_1ms_ms": float(d[d > 1000].sum() / 1e3)}
 
 
@@ -507,6 +554,14 @@ def main():
                                   results=ress_v[0])
                 fz.flush()
                 break
+    # no cyclic-GC pause inside the timed region (a full collection over the
+    # interpreter's objects takes milliseconds; the step loop allocates little).
+    # The collection runs before the warm-up: right before the timed region it
+    # leaves the host caches cold, and the first timed call then takes ~190 us
+    # of host time instead of ~35 (scripts/first_call.py)
+    clk = ClockSampler(torch.cuda.current_device()).start()
+    gc.collect()
+    gc.disable()
     for i in range(args.warmup):
         step(i)
     finish()
@@ -522,21 +577,18 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # no cyclic-GC pause inside the timed region (a full collection over the
-    # interpreter's objects takes milliseconds; the step loop allocates little)
-    gc.collect()
-    gc.disable()
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        e0.record(st)
-        h0 = time.perf_counter()
-        hts = [time.perf_counter()]
-        for i in range(args.steps):
-            frames_done += step(args.warmup + i)
-            hts.append(time.perf_counter())
-        finish()                         # every tail (and fold) of the timed calls is inside
-        host_ms = (time.perf_counter() - h0) * 1e3
-        e1.record(st)
-        torch.cuda.synchronize()
+    clk.active = True
+    e0.record(st)
+    h0 = time.perf_counter()
+    hts = [time.perf_counter()]
+    for i in range(args.steps):
+        frames_done += step(args.warmup + i)
+        hts.append(time.perf_counter())
+    finish()                         # every tail (and fold) of the timed calls is inside
+    host_ms = (time.perf_counter() - h0) * 1e3
+    e1.record(st)
+    torch.cuda.synchronize()
+    clk.stop()
     gc.enable()
     if world > 1:
         dist.barrier()
@@ -628,21 +680,7 @@ def main():
         "host_enqueue_ms_per_step": host_ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if S == 1 else "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": (f"C{cfg.cid}: {cfg.W}x{cfg.H} stream, {cfg.n_proc} frames, "
-                                f"batches of {B} per launch (BASELINE.json configs[{cfg.cid - 1}])"
-                                if S == 1 else
-                                f"C{cfg.cid}: {S} streams of {cfg.W}x{cfg.H}, {cfg.n_proc} frames "
-                                f"each, per-stream envelopes, stream s on rank s mod {world}; "
-                                f"each call takes the current frame of {B} of the rank's "
-                                f"{S_r} streams (BASELINE.json configs[{cfg.cid - 1}])"),
-                   "frames_per_step_per_gpu": B, "pipelined_calls": pipelined,
-                   "sharded_path": sharded, "resident_batches_per_gpu": need,
-                   "l2": (f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step"
-                          if B * 3 * N > 126e6 else
-                          f"inputs larger than L2: {B * 3 * N / 1e6:.0f} MB of frames per step, "
-                          f"cycled over {need} resident batches ({need * B * 3 * N / 1e9:.1f} GB)"),
-                   "parallelism": (f"frames sharded by batch, dp{world}" if S == 1 else
-                                   f"camera streams sharded (s mod {world}), dp{world}")},
+        "config": workload_config(cfg, args, world),
         "gpu_launches": launches,
         "host_step_gaps": host_gaps(hts),
         "spot_check": spot,

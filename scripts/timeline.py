@@ -35,11 +35,17 @@ else:
     sids = None
 masks = [torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=dev) for _ in range(4)]
 res = [torch.empty((B, 128), dtype=torch.uint8, device=dev) for _ in range(4)]
-ncalls = 48
+ncalls = int(os.environ.get("TL_NCALLS", "48"))
+nwarm = int(os.environ.get("TL_WARM", "0"))
 import time
 L0 = lib()
 L0.fizi_diag_host_ns.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 hc, hsync = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+for i in range(nwarm):          # untimed calls, then an idle pipeline (as bench.py's warm-up)
+    fz.process_frames(frames[i % nb], t_ms=np.arange(B, dtype=np.int64) * 33 + (i - nwarm) * B * 33,
+                      masks=masks[i % 4], results=res[i % 4])
+fz.flush()
+torch.cuda.synchronize()
 L0.fizi_diag_host_ns(fz._h, ctypes.byref(hc), ctypes.byref(hsync))
 c0, s0 = hc.value, hsync.value
 tp0 = time.perf_counter()
@@ -63,7 +69,8 @@ en = buf[8 * 256:].reshape(8, 256).astype(np.float64)
 names = ["seg", "slow", "fix", "zero", "morph", "ccl", "fold"]
 print("pipelined" if pipelined else "joined", "C%d B=%d" % (cid, B))
 print("call " + " ".join("%15s" % n for n in names) + "   period")
-for k in range(ncalls - 12, ncalls):
+rows = range(nwarm + ncalls) if nwarm else range(ncalls - 12, ncalls)
+for k in rows:
     t0 = st[0, k]
     cells = []
     kinds = {"seg": 0, "fix": 1, "zero": 2, "morph": 3, "ccl": 4, "fold": 5, "slow": 6}
@@ -75,5 +82,10 @@ for k in range(ncalls - 12, ncalls):
             cells.append("%6.1f..%6.1f" % ((st[j, k] - t0) / 1e3, (en[j, k] - t0) / 1e3))
     per = (st[0, k] - st[0, k - 1]) / 1e3
     print("%4d " % k + " ".join(cells) + "   %6.1f" % per)
+if nwarm:
+    k0, k1 = nwarm, nwarm + ncalls - 1
+    span = (max(en[j, k1] for j in range(7) if en[j, k1] < 1e19 and st[j, k1] < 1e19) - st[0, k0]) / 1e3
+    print("timed calls %d..%d: first seg start -> last end %.1f us = %.1f us/call -> %.0f frames/s"
+          % (k0, k1, span, span / ncalls, B * ncalls / span * 1e6))
 per = (st[0, ncalls - 1] - st[0, 8]) / 1e3 / (ncalls - 9)
 print("mean period %.1f us -> %.0f frames/s" % (per, B / per * 1e6))
