@@ -382,7 +382,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_1907_04393_b200 import CALL_SLOTS, RESULT_BYTES, Fizi
+    from paper_1907_04393_b200 import RESULT_BYTES, Fizi
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -465,7 +465,7 @@ def main():
     gathered_w = torch.empty((world * G * Bg, RESULT_BYTES), dtype=torch.uint8, device=dev)
     fold_stream = torch.cuda.Stream(device=dev)
     window = []
-    NBUF = CALL_SLOTS                    # = the context's call slots (include/fizi.h)
+    NBUF = fz.call_slots                 # = the context's call slots (include/fizi.h)
     masks2 = [torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
     res2 = [torch.empty((B, RESULT_BYTES), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
     del learn

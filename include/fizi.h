@@ -328,8 +328,15 @@ int fizi_set_background(fizi_ctx *ctx, uint32_t stream, const uint8_t *lo_dev,
  * set_background / track / reset_tracker / relearn / drive / hit test / debug
  * / host entry) joins the outstanding stages into its stream itself.  Calls
  * holding a relearning stream (fizi_set_relearn) always run joined. */
+#ifndef FIZI_CALL_SLOTS
 #define FIZI_CALL_SLOTS 4
+#endif
 int fizi_set_pipeline(fizi_ctx *ctx, int enable);
+
+/* FIZI_CALL_SLOTS as this library was built with (a build may override the
+ * header default with -DFIZI_CALL_SLOTS=k; callers size their output rotation
+ * from this value). */
+uint32_t fizi_call_slots(void);
 
 /* Make cuda_stream wait for the tails of all previous calls (no-op when
  * nothing is outstanding).  Enqueues only; does not block the host. */

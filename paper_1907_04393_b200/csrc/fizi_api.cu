@@ -1394,6 +1394,8 @@ int fizi_profile_read(fizi_ctx* ctx, double* ms_out, uint64_t* count_out, int re
 
 uint64_t fizi_kernel_launches(const fizi_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
+uint32_t fizi_call_slots(void) { return fizi::kSlots; }
+
 const char* fizi_last_error(const fizi_ctx* ctx) {
   if (!ctx) return "NULL context";
   return ctx->c.err.c_str();

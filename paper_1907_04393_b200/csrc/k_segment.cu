@@ -25,6 +25,7 @@
 // envelope evaluate R1/R2/R3 per pixel in exact integer arithmetic (the hue is
 // compared by cross-multiplication, reading L8).
 #include <cstdlib>
+#include <cstring>
 
 #include "dev_util.cuh"
 #include "fizi_internal.cuh"
@@ -1166,6 +1167,10 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
 }
 
 cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st) {
+  // diagnostics only (wrong results): FIZI_DIAG_SKIP=slow measures the
+  // pipeline without this stage, an upper bound for speeding it up
+  static const bool skip = getenv("FIZI_DIAG_SKIP") && strstr(getenv("FIZI_DIAG_SKIP"), "slow");
+  if (skip) return cudaSuccess;
   SegArgs a = seg_args(c, f0, n, 0, sub);
   prof_begin(c, st);
   // colour-table test (an arithmetic R2 & R3 test kept the ALU pipe 83 %

@@ -60,7 +60,7 @@ RESULT_DTYPE = np.dtype({
 })
 RESULT_BYTES = 128
 RELEARN_LEARN, RELEARN_SWAP, RELEARN_TRIGGER = 1, 2, 4   # fizi_result.relearn flags (NEXT-1)
-CALL_SLOTS = 4          # FIZI_CALL_SLOTS (include/fizi.h): output buffers a pipelined caller may rotate
+CALL_SLOTS = 4          # FIZI_CALL_SLOTS default (include/fizi.h); Fizi.call_slots = the loaded build's
 
 
 class Wheel(ctypes.Structure):
@@ -120,6 +120,8 @@ def lib() -> ctypes.CDLL:
         L.fizi_profile_read.restype = i32
         L.fizi_kernel_launches.argtypes = [vp]
         L.fizi_kernel_launches.restype = ctypes.c_uint64
+        L.fizi_call_slots.argtypes = []
+        L.fizi_call_slots.restype = ctypes.c_uint32
         L.fizi_last_error.argtypes = [vp]
         L.fizi_last_error.restype = ctypes.c_char_p
         L.fizi_status_string.argtypes = [i32]
@@ -516,6 +518,12 @@ class Fizi:
 
     def kernel_launches(self) -> int:
         return int(lib().fizi_kernel_launches(self._h))
+
+    @property
+    def call_slots(self) -> int:
+        """FIZI_CALL_SLOTS of the loaded library (output buffers a pipelined
+        caller may rotate)."""
+        return int(lib().fizi_call_slots())
 
 
 def results_numpy(results) -> np.ndarray:
