@@ -729,7 +729,19 @@ __global__ void __launch_bounds__(256, kMinBlocks) seg_multi_kernel(SegArgs a) {
 // per byte and R2 & R3 through the colour table.  Words of frames that get
 // the LUT re-test are skipped (that kernel rewrites the whole frame).
 // Grid-stride over the queue, foreground counts aggregated per frame.
-__global__ void __launch_bounds__(256) slow_words_kernel(SegArgs a) {
+// FIZI_SLOW_THREADS / FIZI_SLOW_MINB: CTA size and minimum resident CTAs per
+// SM.  5 x 256 caps the kernel at 48 registers (no spill), so more of it
+// co-resides with the persistent fused kernel: C4 116.8k -> 119.6k, C3 624k
+// -> 636k frames/s; 128-thread CTAs at 48 / 56 registers were no better and a
+// 40-register cap spills (profiles/r02_slow_words_occupancy.txt)
+#ifndef FIZI_SLOW_THREADS
+#define FIZI_SLOW_THREADS 256
+#endif
+#ifndef FIZI_SLOW_MINB
+#define FIZI_SLOW_MINB 5
+#endif
+#define FIZI_SLOW_BOUNDS __launch_bounds__(FIZI_SLOW_THREADS, FIZI_SLOW_MINB)
+__global__ void FIZI_SLOW_BOUNDS slow_words_kernel(SegArgs a) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) tl_mark(a.call, kTlSlow, 0);
   struct TlEnd {
@@ -1175,7 +1187,7 @@ cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cud
   prof_begin(c, st);
   // colour-table test (an arithmetic R2 & R3 test kept the ALU pipe 83 %
   // busy on C4 and was slower: 290 vs 223 us per C4 call in round 1)
-  slow_words_kernel<<<c.sms * 8, 256, 0, st>>>(a);
+  slow_words_kernel<<<c.sms * 8 * (256 / FIZI_SLOW_THREADS), FIZI_SLOW_THREADS, 0, st>>>(a);
   prof_end(c, FIZI_PROF_SLOW, st);
   c.launches += 1;
   return cudaGetLastError();

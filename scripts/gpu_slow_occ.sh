@@ -1,0 +1,11 @@
+#!/bin/bash
+# A/B: per-pixel words kernel CTA size / register cap (co-residency beside the fused kernel)
+mkdir -p gpurun_out
+out=gpurun_out/slow_occ.log; : > $out
+for lib in libfizi.so libfizi_t128m8.so libfizi_t128m10.so libfizi_t128m12.so libfizi_t256m5.so; do
+  for cfg in 4 2 3; do
+    st=100; [ $cfg = 4 ] && st=40
+    echo "== $lib C$cfg" >> $out
+    FIZI_LIB=$lib timeout 300 python bench.py --config $cfg --steps $st --warmup 5 --no-e2e --no-cpu-baseline --no-spot-check 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['ms_per_step']*1e3,1), 'slow', round(d['roofline']['stage_ms_per_step']['slow']*1e3,1))" >> $out 2>&1
+  done
+done
