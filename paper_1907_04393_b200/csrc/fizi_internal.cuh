@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "fizi.h"
@@ -327,5 +328,13 @@ cudaError_t launch_drive(Ctx& c, uint32_t stream, const fizi_result* res, uint32
                          cudaStream_t st);
 cudaError_t launch_tstate_reset(Ctx& c, uint32_t first, uint32_t count, cudaStream_t st);
 cudaError_t launch_debug_stage(Ctx& c, int stage, uint32_t frame, void* out, cudaStream_t st);
+
+// Experiment switch FIZI_CARVEOUT=<0..100>: the preferred shared-memory
+// carveout of the per-call kernels (unset: the driver's choice per launch).
+inline cudaError_t set_carveout(const void* fn) {
+  static const int pct = getenv("FIZI_CARVEOUT") ? atoi(getenv("FIZI_CARVEOUT")) : -1;
+  if (pct < 0) return cudaSuccess;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
 
 }  // namespace fizi

@@ -614,10 +614,15 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
 constexpr size_t kCclSmem = (sizeof(Run) + 2 * sizeof(uint32_t)) * kCclSmemRuns;
 static_assert(kCclSmem >= 1024 * 32, "fold staging fits the labelling shared memory");
 
+__global__ void __launch_bounds__(512) zero_masks_kernel(const CallPtrs* call, uint64_t N);
+
 cudaError_t init_ccl(Ctx& c) {
   (void)c;
-  return cudaFuncSetAttribute(ccl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)kCclSmem);
+  cudaError_t e = cudaFuncSetAttribute(ccl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kCclSmem);
+  if (e == cudaSuccess) e = set_carveout((const void*)ccl_kernel);
+  if (e == cudaSuccess) e = set_carveout((const void*)zero_masks_kernel);
+  return e;
 }
 
 cudaError_t launch_ccl(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, uint32_t g0, uint32_t ng,

@@ -670,6 +670,9 @@ cudaError_t init_morph(Ctx& c) {
   set((const void*)morph_runs_kernel<6>);
   set((const void*)morph_runs_kernel<7>);
   set((const void*)morph_runs_kernel<8>);
+  for (const void* fn : {(const void*)morph_rows_kernel<1, 1, 4>, (const void*)morph_rows_kernel<1, 2, 4>,
+                         (const void*)morph_rows_kernel<1, 4, 4>})
+    if (e == cudaSuccess) e = set_carveout(fn);
   return e;
 }
 

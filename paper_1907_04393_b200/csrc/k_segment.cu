@@ -1255,6 +1255,10 @@ cudaError_t init_segment(Ctx& c) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(fix_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kFixStages * kFixStageBytes);
+  for (const void* fn : {(const void*)seg_fast_kernel<3, 4, false>, (const void*)seg_fast_kernel<3, 4, true>,
+                         (const void*)seg_multi_kernel<kMultiStages, 2>, (const void*)seg_multi_kernel<4, 1>,
+                         (const void*)fix_ring_kernel, (const void*)slow_words_kernel})
+    if (e == cudaSuccess) e = set_carveout(fn);
   return e;
 }
 
