@@ -24,11 +24,12 @@ def _t(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
 
 
-def test_pipelined_c3_six_calls_in_flight():
-    """C3 (1920x1080), 6 pipelined calls of 32 frames back to back, no flush
-    until the end, each call with its own output buffers."""
+@pytest.mark.parametrize("B,ncalls", [(32, 6), (64, 4)])
+def test_pipelined_c3_calls_in_flight(B, ncalls):
+    """C3 (1920x1080), pipelined calls back to back (64 frames per call =
+    bench.py's launch configuration), no flush until the end, each call with
+    its own output buffers."""
     cfg = synth.CONFIGS[3]
-    B, ncalls = 32, 6
     learn = synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True, device=DEV)
     ks = list(range(80, 80 + B * ncalls))          # includes a dwell pause (frames 100-139)
     frames = synth.frames_dev(cfg, 0, ks, device=DEV)
@@ -64,6 +65,84 @@ def test_pipelined_c3_six_calls_in_flight():
                 assert np.array_equal(outs[j][0][i].cpu().numpy(), st["final_mask"])
     pip.close()
     ref.close()
+
+
+def test_pipelined_c4_two_calls_of_64_in_flight():
+    """C4 (3840x2160) in bench.py's launch configuration: pipelined calls of
+    64 frames, two in flight, one flush; every mask and record of all 128
+    frames against the oracle (frame-parallel over the host cores) and the
+    fold over them, in order."""
+    import os
+    cfg = synth.CONFIGS[4]
+    B, ncalls = 64, 2
+    learn = synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True, device=DEV)
+    ks = list(range(64, 64 + B * ncalls))          # hand present, a dwell pause at 100-139
+    frames = synth.frames_dev(cfg, 0, ks, device=DEV)
+    t = np.array([synth.t_ms(k) for k in ks], np.int64)
+    fz = Fizi(cfg.W, cfg.H, max_batch=B)
+    fz.learn_background(learn, margin=synth.MARGIN)
+    fz.set_pipeline(True)
+    outs = [(torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=DEV),
+             torch.empty((B, RESULT_BYTES), dtype=torch.uint8, device=DEV)) for _ in range(ncalls)]
+    for j in range(ncalls):
+        sl = slice(j * B, (j + 1) * B)
+        fz.process_frames(frames[sl], t_ms=t[sl], masks=outs[j][0], results=outs[j][1])
+    fz.flush()
+    torch.cuda.synchronize()
+    lo, hi = oracle.learn(learn.cpu().numpy(), synth.MARGIN)
+    p = oracle.make_params(cfg.W, cfg.H)
+    tr = oracle.Tracker(p)
+    nthreads = max(1, min(32, os.cpu_count() or 1))
+    for j in range(ncalls):
+        sl = slice(j * B, (j + 1) * B)
+        recs, om = oracle.segment_batch(p, frames[sl].cpu().numpy(), lo, hi, t_ms=t[sl],
+                                        nthreads=nthreads)
+        rp = results_numpy(outs[j][1])
+        got = outs[j][0].cpu().numpy()
+        for i in range(B):
+            tr.update(recs[i])
+            compare_record(rp[i], recs[i], ks[j * B + i], track=True)
+            assert np.array_equal(got[i], om[i]), ks[j * B + i]
+    fz.close()
+
+
+def test_pipelined_c2_drift_four_calls_in_flight():
+    """C2 (640x480, lighting drift) in bench.py's launch configuration: four
+    pipelined calls of 64 frames in flight over frames 0-255, which hold the
+    over-exposure ramp (LUT re-test frames, every gamma regime) and a dwell
+    pause; every mask and record against the oracle, the fold in order."""
+    cfg = synth.CONFIGS[2]
+    B, ncalls = 64, 4
+    learn = synth.frames_dev(cfg, 0, range(cfg.n_learn), learning=True, device=DEV)
+    ks = list(range(B * ncalls))
+    frames = synth.frames_dev(cfg, 0, ks, device=DEV)
+    t = np.array([synth.t_ms(k) for k in ks], np.int64)
+    fz = Fizi(cfg.W, cfg.H, max_batch=B)
+    fz.learn_background(learn, margin=synth.MARGIN)
+    fz.set_pipeline(True)
+    outs = [(torch.empty((B, cfg.H, cfg.W), dtype=torch.uint8, device=DEV),
+             torch.empty((B, RESULT_BYTES), dtype=torch.uint8, device=DEV)) for _ in range(ncalls)]
+    for j in range(ncalls):
+        sl = slice(j * B, (j + 1) * B)
+        fz.process_frames(frames[sl], t_ms=t[sl], masks=outs[j][0], results=outs[j][1])
+    fz.flush()
+    torch.cuda.synchronize()
+    lo, hi = oracle.learn(learn.cpu().numpy(), synth.MARGIN)
+    p = oracle.make_params(cfg.W, cfg.H)
+    tr = oracle.Tracker(p)
+    corrected = 0
+    for j in range(ncalls):
+        sl = slice(j * B, (j + 1) * B)
+        recs, om = oracle.segment_batch(p, frames[sl].cpu().numpy(), lo, hi, t_ms=t[sl], nthreads=8)
+        rp = results_numpy(outs[j][1])
+        got = outs[j][0].cpu().numpy()
+        for i in range(B):
+            tr.update(recs[i])
+            compare_record(rp[i], recs[i], ks[j * B + i], track=True)
+            assert np.array_equal(got[i], om[i]), ks[j * B + i]
+            corrected += recs[i].corrected
+    assert corrected > 50
+    fz.close()
 
 
 def test_pipelined_c5_all_streams_four_calls_in_flight():
