@@ -122,36 +122,44 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            nv = pynvml
+            self.names = {
+                "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+                "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+            }
             self.ok = True
         except Exception:
             self.ok = False
         self._stop = threading.Event()
 
     def _run(self):
-        nv = self.nv
-        names = {
-            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
-            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
-            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
-            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
-            "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
-        }
         while not self._stop.is_set():
             if self.active:
-                try:
-                    mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                    try:
-                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                    except AttributeError:
-                        r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-                    if self.active:
-                        self.samples.append(mhz)
-                        for k, bit in names.items():
-                            if r & bit:
-                                self.reasons.add(k)
-                except Exception:
-                    pass
+                self.sample_now()
             time.sleep(0.002)
+
+    def sample_now(self):
+        """One sample (also called by the main thread right after the timed
+        region's end event is recorded, while the GPU still runs its queued
+        work: a short timed region may see no thread sample)."""
+        if not self.ok or not self.active:
+            return
+        nv = self.nv
+        try:
+            mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            try:
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except AttributeError:
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+            self.samples.append(mhz)
+            for k, bit in self.names.items():
+                if r & bit:
+                    self.reasons.add(k)
+        except Exception:
+            pass
 
     def start(self):
         if self.ok:
@@ -587,6 +595,9 @@ def main():
     finish()                         # every tail (and fold) of the timed calls is inside
     host_ms = (time.perf_counter() - h0) * 1e3
     e1.record(st)
+    gpu_busy = not e1.query()            # the GPU is still inside the timed region
+    if gpu_busy:
+        clk.sample_now()
     torch.cuda.synchronize()
     clk.stop()
     gc.enable()

@@ -1,4 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-TL_CONFIG=4 TL_WARM=3 TL_NCALLS=10 timeout 300 python scripts/timeline.py > gpurun_out/tl_c4.log 2>&1
-TL_CONFIG=2 TL_WARM=3 TL_NCALLS=12 timeout 300 python scripts/timeline.py > gpurun_out/tl_c2.log 2>&1
+: > gpurun_out/drain_bench.log
+for i in 1 2 3; do
+  timeout 300 python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu-baseline --no-spot-check 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), d['clocks'], d['host_step_gaps']['first_us'])" >> gpurun_out/drain_bench.log
+done
+timeout 300 python bench.py --steps 300 --warmup 10 --no-e2e --no-cpu-baseline --no-spot-check 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), d['clocks'])" >> gpurun_out/drain_bench.log
