@@ -1187,7 +1187,12 @@ cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cud
   prof_begin(c, st);
   // colour-table test (an arithmetic R2 & R3 test kept the ALU pipe 83 %
   // busy on C4 and was slower: 290 vs 223 us per C4 call in round 1)
-  slow_words_kernel<<<c.sms * 8 * (256 / FIZI_SLOW_THREADS), FIZI_SLOW_THREADS, 0, st>>>(a);
+  // grid-stride over the queue with 16 CTAs per SM (5 resident alone; the
+  // rest fill in beside the fused kernel): 8 / 16 / 32 per SM measured C4
+  // 119.6k / 121.2k / 120.6k, C2 713k / 728k / 731k, C3 633k / 633k / 630k
+  // (FIZI_SLOW_GRID, profiles/r02_slow_words_grid.txt)
+  static const uint32_t per_sm = getenv("FIZI_SLOW_GRID") ? (uint32_t)atoi(getenv("FIZI_SLOW_GRID")) : 16u;
+  slow_words_kernel<<<c.sms * per_sm * (256 / FIZI_SLOW_THREADS), FIZI_SLOW_THREADS, 0, st>>>(a);
   prof_end(c, FIZI_PROF_SLOW, st);
   c.launches += 1;
   return cudaGetLastError();
