@@ -116,6 +116,40 @@ def test_random_frames_all_stages(W, H):
         _run_stages_case(W, H, frames, lo, hi, params)
 
 
+@pytest.mark.parametrize("W,H,params", [(4160, 40, dict()),                 # P = 130 words > 128
+                                         (96, 64, dict(se_radius=5)),       # r > 4
+                                         (4128, 24, dict(se_radius=6, min_blob_ppm=0))])
+def test_generic_morphology_path(W, H, params):
+    """Rows wider than 4096 pixels or structuring elements with r > 4 take
+    the shared-memory morphology kernel (morph_runs_kernel) beside the fused
+    segmentation; masks and records against the oracle, with and without the
+    debug stages."""
+    rng = np.random.default_rng(W + H)
+    n = 4
+    frames = rng.integers(0, 256, (n, H, W, 3), dtype=np.uint8)
+    for k in range(n):
+        yy, xx = np.mgrid[0:H, 0:W]
+        cx, cy, r = rng.integers(0, W), rng.integers(0, H), rng.integers(8, 30)
+        m = ((xx - cx) ** 2 + (yy - cy) ** 2 < r * r) | (rng.random((H, W)) < 0.05)
+        frames[k][m] = (210, 120, 110)
+    lo = rng.integers(0, 140, (H, W, 3)).astype(np.uint8)
+    hi = np.minimum(255, lo.astype(int) + rng.integers(0, 120, (H, W, 3))).astype(np.uint8)
+    _run_stages_case(W, H, frames, lo, hi, params)
+    t = np.arange(n, dtype=np.int64) * 33
+    fz = _ctx(W, H, max_batch=n, **params)
+    fz.set_background(_t(lo), _t(hi))
+    masks, res = fz.process_frames(_t(frames), t_ms=t)
+    res, masks = results_numpy(res), masks.cpu().numpy()
+    p = oracle.make_params(W, H, **params)
+    tr = oracle.Tracker(p)
+    for k in range(n):
+        rec, st = oracle.segment(p, frames[k], lo, hi, t_ms=int(t[k]))
+        tr.update(rec)
+        compare_record(res[k], rec, k, track=True)
+        assert np.array_equal(masks[k], st["final_mask"]), k
+    fz.close()
+
+
 def test_brightness_regimes_all_means():
     # uniform-ish frames at every mean luma -> every LUT regime, fast path
     W, H = 64, 32
