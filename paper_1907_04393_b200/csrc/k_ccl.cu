@@ -537,6 +537,10 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
     double* cy_s = cx_s + 1024;
     uint32_t* ar_s = reinterpret_cast<uint32_t*>(cy_s + 1024);
     uint32_t* fl_s = ar_s + 1024;
+    int64_t* od_s = reinterpret_cast<int64_t*>(fl_s + 1024);     // out: dwell
+    double* opx_s = reinterpret_cast<double*>(od_s + 1024);      // out: px
+    double* opy_s = opx_s + 1024;                                 // out: py
+    uint32_t* ov_s = reinterpret_cast<uint32_t*>(opy_s + 1024);  // out: vis | clk<<1
     while (true) {
       if (threadIdx.x == 0) {
         s_own = atomicCAS(a.fold_sync, 0u, 1u) == 0u;
@@ -566,21 +570,30 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
       }
       __syncthreads();
       if (threadIdx.x == 0) {
+        // one thread folds in order; the next record's inputs are read from
+        // shared memory before the current one is folded (outputs go to
+        // separate arrays), so the loads overlap the FP64 chain
         TrackState st = a.tstate[a.track_stream];
+        int64_t nt = cnt ? t_s[0] : 0;
+        uint32_t na = cnt ? ar_s[0] : 0u, nfl = cnt ? fl_s[0] : 0u;
+        double nx = cnt ? cx_s[0] : 0.0, ny = cnt ? cy_s[0] : 0.0;
         for (uint32_t k = 0; k < cnt; k++) {
           fizi_result q;
-          q.t_ms = t_s[k]; q.blob_area = ar_s[k]; q.cx = cx_s[k]; q.cy = cy_s[k]; q.relearn = fl_s[k];
+          q.t_ms = nt; q.blob_area = na; q.cx = nx; q.cy = ny; q.relearn = nfl;
+          if (k + 1 < cnt) {
+            nt = t_s[k + 1]; na = ar_s[k + 1]; nfl = fl_s[k + 1]; nx = cx_s[k + 1]; ny = cy_s[k + 1];
+          }
           track_one(a.p, st, q);
-          t_s[k] = q.dwell_ms; cx_s[k] = q.px; cy_s[k] = q.py;
-          ar_s[k] = (uint32_t)q.visible | ((uint32_t)q.clicked << 1);
+          od_s[k] = q.dwell_ms; opx_s[k] = q.px; opy_s[k] = q.py;
+          ov_s[k] = (uint32_t)q.visible | ((uint32_t)q.clicked << 1);
         }
         a.tstate[a.track_stream] = st;
       }
       __syncthreads();
       if (threadIdx.x < cnt) {
         fizi_result& o = a.call->res[a.f0 + i];
-        o.visible = (uint8_t)(ar_s[threadIdx.x] & 1u); o.clicked = (uint8_t)(ar_s[threadIdx.x] >> 1);
-        o.px = cx_s[threadIdx.x]; o.py = cy_s[threadIdx.x]; o.dwell_ms = t_s[threadIdx.x];
+        o.visible = (uint8_t)(ov_s[threadIdx.x] & 1u); o.clicked = (uint8_t)(ov_s[threadIdx.x] >> 1);
+        o.px = opx_s[threadIdx.x]; o.py = opy_s[threadIdx.x]; o.dwell_ms = od_s[threadIdx.x];
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -612,7 +625,7 @@ __global__ void __launch_bounds__(1024) ccl_kernel(CclArgs a) {
 }
 
 constexpr size_t kCclSmem = (sizeof(Run) + 2 * sizeof(uint32_t)) * kCclSmemRuns;
-static_assert(kCclSmem >= 1024 * 32, "fold staging fits the labelling shared memory");
+static_assert(kCclSmem >= 1024 * 60, "fold staging fits the labelling shared memory");
 
 __global__ void __launch_bounds__(512) zero_masks_kernel(const CallPtrs* call, uint64_t N);
 
