@@ -15,7 +15,9 @@
 #include <string>
 #include <vector>
 
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include "fizi.h"
@@ -335,6 +337,20 @@ inline cudaError_t set_carveout(const void* fn) {
   static const int pct = getenv("FIZI_CARVEOUT") ? atoi(getenv("FIZI_CARVEOUT")) : -1;
   if (pct < 0) return cudaSuccess;
   return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
+// Diagnostics only: FIZI_DIAG_SKIP=<stage>[,<stage>] skips a pipeline stage
+// (the outputs are then wrong) to measure what that stage costs; announced
+// once on stderr so that it cannot pass unnoticed.
+inline bool diag_skip(const char* stage) {
+  const char* v = getenv("FIZI_DIAG_SKIP");
+  if (!v || !strstr(v, stage)) return false;
+  static bool warned = false;
+  if (!warned) {
+    fprintf(stderr, "libfizi: FIZI_DIAG_SKIP=%s is set: stages are skipped, outputs are NOT valid\n", v);
+    warned = true;
+  }
+  return true;
 }
 
 }  // namespace fizi

@@ -592,7 +592,7 @@ static void launch_r(const MorphArgs& a, uint32_t n, size_t smem, cudaStream_t s
 
 cudaError_t launch_morph(Ctx& c, uint32_t f0, uint32_t n, bool write_masks, cudaStream_t st) {
   // diagnostics only (wrong results): FIZI_DIAG_SKIP=morph, see launch_slow_words
-  static const bool skip = getenv("FIZI_DIAG_SKIP") && strstr(getenv("FIZI_DIAG_SKIP"), "morph");
+  static const bool skip = diag_skip("morph");
   if (skip) return cudaSuccess;
   MorphArgs a;
   a.f0 = f0;

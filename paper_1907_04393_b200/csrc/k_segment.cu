@@ -1181,7 +1181,7 @@ cudaError_t launch_seg_main(Ctx& c, uint32_t f0, uint32_t n, uint32_t g0, uint32
 cudaError_t launch_slow_words(Ctx& c, uint32_t f0, uint32_t n, uint32_t sub, cudaStream_t st) {
   // diagnostics only (wrong results): FIZI_DIAG_SKIP=slow measures the
   // pipeline without this stage, an upper bound for speeding it up
-  static const bool skip = getenv("FIZI_DIAG_SKIP") && strstr(getenv("FIZI_DIAG_SKIP"), "slow");
+  static const bool skip = diag_skip("slow");
   if (skip) return cudaSuccess;
   SegArgs a = seg_args(c, f0, n, 0, sub);
   prof_begin(c, st);
