@@ -52,5 +52,8 @@ txt = f"""# r02 sanitizer substitute (compute-sanitizer is closed on this GPU po
 {tail("final_pytest")}
 {tail("final_smoke")}
 """
+if os.path.exists(os.path.join(G, "race_stress50.log")):
+    txt += ("\n## 3b. race stress with 50 repetitions (REPS=50 scripts/race_stress.py, same code)\n"
+            + open(os.path.join(G, "race_stress50.log")).read().strip() + "\n")
 open(os.path.join(P, "r02_checks.txt"), "w").write(txt)
 print("ok")
