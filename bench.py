@@ -50,8 +50,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="frames per launch (default: config's)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps (capped)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--gather-every", type=int, default=16,
-                    help="sharded path: steps per record gather + fold window")
+    ap.add_argument("--gather-every", type=int, default=0,
+                    help="sharded path: steps per record gather + fold window "
+                         "(0: max(1, 16 // N), so that the last window's fold stays short)")
     ap.add_argument("--force-gather", action="store_true",
                     help="N=1: run the sharded path (segment + NCCL gather + fold) on a one-rank group")
     ap.add_argument("--no-pipeline", action="store_true",
@@ -461,7 +462,11 @@ def main():
     # sharded path: the records of G steps are gathered and folded together on
     # a fold stream (one NCCL all_gather per window), while the next window's
     # calls run; the folds of every rank cover every frame, in frame order
-    G = max(1, args.gather_every) if sharded else 1
+    # one window's fold costs ~0.15 us per record in one thread (every rank
+    # folds every rank's records): N x 64 x G records per window, so the
+    # window shrinks with N to keep the fold of the last window (the only one
+    # not hidden behind later calls) short
+    G = (max(1, args.gather_every) if args.gather_every else max(1, 16 // world)) if sharded else 1
     Bg = shard.streams_per_rank(S, world) if S > 1 else B   # rows per rank and step in the gather
     # windows rotate over NWIN record buffers: a window's calls wait only for
     # the gather of the window NWIN back (not for the previous window's tails)
@@ -693,6 +698,7 @@ def main():
         "data": "synthetic",
         "config": workload_config(cfg, args, world),
         "gpu_launches": launches,
+        "gather_window_steps": G if sharded else None,
         "host_step_gaps": host_gaps(hts),
         "spot_check": spot,
         "roofline": roofline,
